@@ -1,0 +1,235 @@
+/*
+ * sfi_b200.h — C ABI of the B200-native SFI decode-attention hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, int status codes,
+ * no C++ or torch types. Every entry point is stream-ordered on the caller's
+ * cudaStream_t (passed as void*), never synchronizes the host, and replaces a
+ * reference CPU function (paths relative to /root/reference/proj):
+ *
+ *   sfi_ring_append     KvStore::append_layer            attention.cpp:136-152
+ *                       + the recent window slide         scheduler.cpp:45-51
+ *   sfi_dense_decode    attention_kernel_dense + the slow-step logit capture
+ *                       attention.cpp:502-523, 80-113, 367-409
+ *   sfi_selector        run_selector + stats_for_layer    selector.cpp:254-299,
+ *                                                         scheduler.cpp:150-180
+ *   sfi_compact_build   KvStore::reorganize               attention.cpp:186-217
+ *   sfi_sparse_decode   attention_kernel_sparse           attention.cpp:525-550
+ *
+ * Data layout (all device memory, caller-owned):
+ *   k_cache, v_cache : bf16 [n_layers][batch][n_kv_heads][max_positions][head_dim]
+ *                      row p-1 holds position p (1-based, distribution.hpp:23-26)
+ *   key_norms        : fp64 [n_layers][batch][n_kv_heads][max_positions]
+ *   ck, cv (compact) : bf16 [n_layers][batch][n_kv_heads][compact_rows][head_dim]
+ *                      compact_rows = n_recent + n_sink + k_budget:
+ *                      rows [0, n_recent)            recent ring, slot (p-1) % n_recent
+ *                      rows [n_recent, +n_sink_b)    sink positions 1..n_sink_b
+ *                      rows [.., +n_sel)             selected positions, ascending
+ *   sel              : int32 [n_layers][batch][n_kv_heads][k_budget] (1-based, ascending)
+ *   n_sel            : int32 [n_layers][batch][n_kv_heads]
+ *   prefix_len       : int32 [batch]  L_b = positions 1..L_b live, current token included
+ *   n_sink_b         : int32 [batch]  min(n_sink, prompt length) (scheduler.cpp:69)
+ *   recent_len       : int32 [batch]  recent window length rl_b <= n_recent
+ *   error_flags      : uint32 [1]     bit (1 << code) set by kernels on a contract
+ *                                     violation; read with sfi_read_errors
+ * The allowed set of a slow step is the contiguous range
+ * J_b = [n_sink_b + 1, L_b - rl_b] with rl_b = recent_len[b], normally
+ * clamp(L_b - n_sink_b, 0, n_recent) (scheduler.cpp:45-51, 81-91). Pooled logits are fp32 [batch][n_kv_heads][max_positions],
+ * entry (b, h, p - (n_sink_b + 1)) for p in J_b.
+ */
+#ifndef SFI_B200_H
+#define SFI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SFI_API __attribute__((visibility("default")))
+#else
+#define SFI_API
+#endif
+
+/* 0 = success; 1..10 = 1 + sfi::ErrorCode (error.hpp:23-34); >= 100 ABI-level. */
+typedef enum {
+  SFI_OK = 0,
+  SFI_ERR_CONFIG = 1,
+  SFI_ERR_EMPTY_SUPPORT = 2,
+  SFI_ERR_SUPPORT_MISMATCH = 3,
+  SFI_ERR_NON_FINITE_INPUT = 4,
+  SFI_ERR_OVERLAP_VIOLATION = 5,
+  SFI_ERR_STALE_COMPACT = 6,
+  SFI_ERR_OUT_OF_RANGE = 7,
+  SFI_ERR_BAD_WEIGHT_FILE = 8,
+  SFI_ERR_CONTEXT_OVERFLOW = 9,
+  SFI_ERR_IO = 10,
+  SFI_ERR_CUDA = 100,
+  SFI_ERR_UNSUPPORTED = 101,
+  SFI_ERR_INVALID_ARGUMENT = 102
+} sfi_status;
+
+typedef enum { SFI_POOL_MEAN = 0, SFI_POOL_MAX = 1 } sfi_pool_mode; /* config.hpp:28 */
+
+/* Static shape of one device cache (ModelSpec attention.hpp:31-44 + CacheLimits config.hpp:62-68). */
+typedef struct {
+  int32_t n_layers;
+  int32_t batch;
+  int32_t n_kv_heads;    /* H */
+  int32_t n_q_heads;     /* Hq, multiple of H; group G = Hq / H in {1,2,4,8,16} */
+  int32_t head_dim;      /* d in {64, 128} */
+  int32_t max_positions; /* per-(layer, b, head) paged capacity */
+  int32_t n_sink;        /* CacheLimits::n_sink */
+  int32_t k_budget;      /* CacheLimits::k_budget == SelectorConfig::k_budget */
+  int32_t n_recent;      /* CacheLimits::n_recent (ring capacity) */
+} sfi_shape;
+
+/* Device buffers of one cache (layout in the header comment). */
+typedef struct {
+  void* k_cache;
+  void* v_cache;
+  double* key_norms;
+  void* ck;
+  void* cv;
+  int32_t* sel;
+  int32_t* n_sel;
+  int32_t* prefix_len;
+  int32_t* n_sink_b;
+  int32_t* recent_len; /* [batch] recent window length; sfi_step_advance keeps it at
+                          clamp(L_b - n_sink_b, 0, n_recent) (scheduler.cpp:45-51) */
+  uint32_t* error_flags;
+  void* workspace; /* >= sfi_workspace_bytes(shape); must be zeroed once at allocation */
+  size_t workspace_bytes;
+} sfi_cache;
+
+/* Selector hyperparameters (SelectorConfig, config.hpp:31-47). k_budget comes from sfi_shape. */
+typedef struct {
+  double alpha, gamma, beta, p_curve, eta, lambda_clip, alpha_soft, alpha_cross,
+      temperature, epsilon;
+  int32_t nms_radius;
+  int32_t pool; /* sfi_pool_mode; selects the pooling used by sfi_dense_decode */
+} sfi_selector_params;
+
+/* Byte sizes of every buffer for a shape (for the caller's allocator). */
+typedef struct {
+  size_t kv_cache;   /* each of k_cache, v_cache */
+  size_t key_norms;
+  size_t compact;    /* each of ck, cv */
+  size_t sel;
+  size_t n_sel;
+  size_t per_batch;  /* prefix_len, n_sink_b */
+  size_t workspace;
+  size_t pooled_logits; /* fp32 [batch][n_kv][max_positions] */
+} sfi_sizes;
+
+SFI_API const char* sfi_version(void);
+/* Thread-local message of the last non-OK status returned on this thread. */
+SFI_API const char* sfi_last_error(void);
+SFI_API int sfi_shape_validate(const sfi_shape* shape);
+SFI_API int sfi_buffer_sizes(const sfi_shape* shape, sfi_sizes* out);
+SFI_API void sfi_default_selector_params(sfi_selector_params* out);
+
+/* Host-side recent window / allowed range for one request (scheduler.cpp:45-51, 81-91). */
+SFI_API void sfi_recent_window(int32_t prefix_len, int32_t n_sink_b, int32_t n_recent,
+                               int32_t* recent_start, int32_t* recent_len);
+
+/* Host -> device per-request lengths: prefix_len[b], n_sink_b[b] and
+ * recent_len[b] (NULL recent_len: the SFI rule clamp(L - n_sink_b, 0, n_recent)). */
+SFI_API int sfi_set_lengths(const sfi_shape* shape, const sfi_cache* cache,
+                            const int32_t* prefix_len_host, const int32_t* n_sink_host,
+                            const int32_t* recent_len_host, void* stream);
+
+/* prefix_len[b] += 1 for every request: opens the next decode step
+ * (KvStore::begin_token attention.cpp:128-134; fast/slow_step_update
+ * scheduler.cpp:101-131) and slides recent_len[b] by the SFI rule. Sets
+ * SFI_ERR_CONTEXT_OVERFLOW past max_positions. */
+SFI_API int sfi_step_advance(const sfi_shape* shape, const sfi_cache* cache, void* stream);
+
+/* Appends the current token (row prefix_len[b]-1) of `layer`:
+ * k_new, v_new bf16 [batch][n_kv_heads][head_dim] -> paged cache, recent ring
+ * slot (L_b-1) % n_recent, and the fp64 key norm sqrt(sum_c k_c^2) summed in
+ * c order (attention.cpp:143-150). */
+SFI_API int sfi_ring_append(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                            const void* k_new, const void* v_new, void* stream);
+
+/* Same for `count` consecutive positions starting at row prefix_len[b] (prefill;
+ * does not move prefix_len): k, v bf16 [batch][n_kv_heads][count][head_dim]. */
+SFI_API int sfi_append_block(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                             int32_t count, const void* k, const void* v, void* stream);
+
+/* Slow step, one layer: o = softmax(q K^T / sqrt(d)) V over positions
+ * 1..L_b for every q head (fp32 accumulation over bf16 KV); when
+ * pooled_logits != NULL also emits the raw logits q.k/sqrt(d) over J_b
+ * pooled across each GQA group (mean or max, attention.cpp:394-409).
+ * q, out: fp32 [batch][n_q_heads][head_dim]. */
+SFI_API int sfi_dense_decode(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                             const float* q, float* out, float* pooled_logits,
+                             int32_t pool_mode, void* stream);
+
+/* Fast step, one layer: attention over the compact cache only (ring + sink +
+ * selected rows; S = recent_len + n_sink_b + n_sel per (b, head)). */
+SFI_API int sfi_sparse_decode(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                              const float* q, float* out, void* stream);
+
+/* Selector, one layer: pooled logits over J_b (+ cached key norms) ->
+ * sel/n_sel of `layer`, indices bit-exact with run_selector given identical
+ * logits (fp64 arithmetic, (score desc, position asc) tie rule). */
+SFI_API int sfi_selector(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                         const float* pooled_logits, const sfi_selector_params* params,
+                         void* stream);
+
+/* run_selector on explicit device arrays (the reference-facing form,
+ * selector.cpp:254-299): H heads, a W x n window per head over an arbitrary
+ * ascending allowed list. logits fp64 [H][W][n], norms fp64 [H][n] (CacheStats
+ * key norms), allowed int32 [n]; scratch >= sfi_selector_explicit_scratch_bytes;
+ * outputs sel int32 [H][k_budget] ascending, n_sel int32 [H]; contract
+ * violations set bits in err (uint32 device word). W <= 16, H <= 16. */
+SFI_API size_t sfi_selector_explicit_scratch_bytes(int32_t H, int32_t n);
+SFI_API int sfi_selector_explicit(int32_t H, int32_t W, int32_t n, int32_t k_budget,
+                                  const double* logits, const double* norms,
+                                  const int32_t* allowed, const sfi_selector_params* params,
+                                  void* scratch, int32_t* sel, int32_t* n_sel, uint32_t* err,
+                                  void* stream);
+
+/* select_top_k (selector.cpp:232-252) on device arrays: rows independent score
+ * rows fp64 [rows][n] over allowed int32 [n]; sel int32 [rows][k], n_sel [rows]. */
+SFI_API int sfi_select_top_k(int32_t rows, int32_t n, int32_t k, const double* scores,
+                             const int32_t* allowed, int32_t* sel, int32_t* n_sel, void* stream);
+
+/* Debug: after sfi_selector, copies the fp64 stage arrays z_base and z_adj
+ * (selector.cpp:270-297) of request b into host buffers [n_kv_heads][n_J]. */
+SFI_API int sfi_selector_stages(const sfi_shape* shape, const sfi_cache* cache, int32_t b,
+                                double* z_base, double* z_adj, int32_t n_j, void* stream);
+
+/* Compact-cache builder, one layer: gathers sink rows and selected rows
+ * (sel/n_sel of `layer`) into the compact buffer; with rebuild_ring also
+ * refills the recent ring from the paged cache. Validates strictly ascending
+ * merged positions within [1, L_b] (kOverlapViolation / kOutOfRange). */
+SFI_API int sfi_compact_build(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                              int32_t rebuild_ring, void* stream);
+
+/* Host-supplied selection for one layer (KvStore::reorganize semantics):
+ * sel_host int32 [batch][n_kv_heads][k_budget], counts [batch][n_kv_heads];
+ * copied to the device, then sfi_compact_build. Synchronous on `stream`. */
+SFI_API int sfi_set_selection(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                              const int32_t* sel_host, const int32_t* counts_host,
+                              void* stream);
+
+/* Reads (and clears) the device error word; synchronizes `stream`. Returns
+ * the lowest set code as the status (SFI_OK when clean). */
+SFI_API int sfi_read_errors(const sfi_cache* cache, uint32_t* flags_out, void* stream);
+
+/* Deterministic synthetic bf16 N(0,~1) fill of the paged cache rows [0, len)
+ * of every (layer, b, head) plus their key norms (bench / tests only). */
+SFI_API int sfi_fill_synthetic(const sfi_shape* shape, const sfi_cache* cache, uint64_t seed,
+                               int32_t len, void* stream);
+
+/* Number of kernels the last call on this thread enqueued (launch accounting). */
+SFI_API int32_t sfi_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFI_B200_H */

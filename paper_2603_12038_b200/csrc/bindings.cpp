@@ -1,0 +1,327 @@
+// bindings.cpp — pybind11 module `_sfi_b200`: the reference's `_sfi` names
+// (proj/bindings/module.cpp:29-247, python/sfi/__init__.py) for the hot-path
+// operators, backed by the B200 host API, plus the batched device API (the
+// C ABI one-to-one, taking raw device pointers and a cudaStream_t handle).
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cstdint>
+
+#include "sfi_b200.h"
+#include "sfi_b200.hpp"
+
+namespace py = pybind11;
+using namespace sfi_b200;
+
+namespace {
+
+void* vp(std::uintptr_t p) { return reinterpret_cast<void*>(p); }
+
+py::dict sizes_dict(const sfi_sizes& z) {
+  py::dict d;
+  d["kv_cache"] = z.kv_cache;
+  d["key_norms"] = z.key_norms;
+  d["compact"] = z.compact;
+  d["sel"] = z.sel;
+  d["n_sel"] = z.n_sel;
+  d["per_batch"] = z.per_batch;
+  d["workspace"] = z.workspace;
+  d["pooled_logits"] = z.pooled_logits;
+  return d;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_sfi_b200, m) {
+  m.doc() = "B200-native SFI decode-attention hot path (sm_100a)";
+
+  static py::exception<Error> exc(m, "SfiError");
+  py::register_exception_translator([](std::exception_ptr p) {
+    try {
+      if (p) std::rethrow_exception(p);
+    } catch (const Error& e) {
+      py::object type = py::reinterpret_borrow<py::object>(exc);
+      py::object err = type(std::string("[") + error_code_name(e.code()) + "] " + e.what());
+      err.attr("code") = error_code_name(e.code());
+      PyErr_SetObject(exc.ptr(), err.ptr());
+    }
+  });
+
+  py::enum_<PoolMode>(m, "PoolMode").value("mean", PoolMode::kMean).value("max", PoolMode::kMax);
+
+  py::class_<SelectorConfig>(m, "SelectorConfig")
+      .def(py::init<>())
+      .def_readwrite("alpha", &SelectorConfig::alpha)
+      .def_readwrite("gamma", &SelectorConfig::gamma)
+      .def_readwrite("beta", &SelectorConfig::beta)
+      .def_readwrite("p_curve", &SelectorConfig::p_curve)
+      .def_readwrite("eta", &SelectorConfig::eta)
+      .def_readwrite("lambda_clip", &SelectorConfig::lambda_clip)
+      .def_readwrite("alpha_soft", &SelectorConfig::alpha_soft)
+      .def_readwrite("alpha_cross", &SelectorConfig::alpha_cross)
+      .def_readwrite("temperature", &SelectorConfig::temperature)
+      .def_readwrite("nms_radius", &SelectorConfig::nms_radius)
+      .def_readwrite("epsilon", &SelectorConfig::epsilon)
+      .def_readwrite("k_budget", &SelectorConfig::k_budget)
+      .def_readwrite("pool", &SelectorConfig::pool)
+      .def("validate", &SelectorConfig::validate);
+
+  py::class_<TriggerConfig>(m, "TriggerConfig")
+      .def(py::init<>())
+      .def_readwrite("trigger_tokens", &TriggerConfig::trigger_tokens)
+      .def_readwrite("t_max", &TriggerConfig::t_max)
+      .def_readwrite("window_decode", &TriggerConfig::window_decode)
+      .def_readwrite("window_prefill", &TriggerConfig::window_prefill)
+      .def("is_trigger", &TriggerConfig::is_trigger);
+
+  py::class_<CacheLimits>(m, "CacheLimits")
+      .def(py::init<>())
+      .def_readwrite("n_sink", &CacheLimits::n_sink)
+      .def_readwrite("n_recent", &CacheLimits::n_recent)
+      .def_readwrite("k_budget", &CacheLimits::k_budget)
+      .def("validate", &CacheLimits::validate);
+
+  py::class_<Config>(m, "Config")
+      .def(py::init<>())
+      .def_readwrite("selector", &Config::selector)
+      .def_readwrite("trigger", &Config::trigger)
+      .def_readwrite("limits", &Config::limits)
+      .def("validate", &Config::validate);
+  m.def("default_config", &default_config);
+
+  py::class_<LogitWindow>(m, "LogitWindow")
+      .def(py::init<>())
+      .def_readwrite("width", &LogitWindow::width)
+      .def_readwrite("allowed", &LogitWindow::allowed)
+      .def_readwrite("values", &LogitWindow::values);
+
+  py::class_<CacheStats>(m, "CacheStats")
+      .def(py::init<>())
+      .def_readwrite("key_norms", &CacheStats::key_norms)
+      .def_readwrite("j_min", &CacheStats::j_min)
+      .def_readwrite("j_max", &CacheStats::j_max)
+      .def_readwrite("normalized_pos", &CacheStats::normalized_pos);
+  m.def("make_cache_stats", &make_cache_stats, py::arg("key_norms"), py::arg("allowed"),
+        py::arg("epsilon") = 1e-8);
+
+  py::class_<SelectorStages>(m, "SelectorStages")
+      .def(py::init<>())
+      .def_readonly("base", &SelectorStages::base)
+      .def_readonly("after_cross", &SelectorStages::after_cross);
+
+  m.def("select_top_k", &select_top_k, py::arg("scores"), py::arg("allowed"), py::arg("k"));
+  m.def(
+      "run_selector",
+      [](const LogitWindow& w, const CacheStats& stats, const SelectorConfig& cfg) {
+        return run_selector(w, stats, cfg);
+      },
+      py::arg("window"), py::arg("stats"), py::arg("config"));
+  m.def(
+      "run_selector_stages",
+      [](const LogitWindow& w, const CacheStats& stats, const SelectorConfig& cfg) {
+        SelectorStages st;
+        auto sel = run_selector(w, stats, cfg, &st);
+        return py::make_tuple(sel, st);
+      },
+      py::arg("window"), py::arg("stats"), py::arg("config"));
+
+  py::class_<ModelSpec>(m, "ModelSpec")
+      .def(py::init<>())
+      .def_readwrite("n_layers", &ModelSpec::n_layers)
+      .def_readwrite("n_query_heads", &ModelSpec::n_query_heads)
+      .def_readwrite("n_kv_heads", &ModelSpec::n_kv_heads)
+      .def_readwrite("head_dim", &ModelSpec::head_dim)
+      .def_readwrite("vocab_size", &ModelSpec::vocab_size)
+      .def_readwrite("max_positions", &ModelSpec::max_positions)
+      .def_readwrite("rope_base", &ModelSpec::rope_base)
+      .def("group_size", &ModelSpec::group_size)
+      .def("validate", &ModelSpec::validate);
+
+  py::class_<SupportSet>(m, "SupportSet")
+      .def(py::init<>())
+      .def_readwrite("sink", &SupportSet::sink)
+      .def_readwrite("selected", &SupportSet::selected)
+      .def_readwrite("recent_start", &SupportSet::recent_start)
+      .def_readwrite("recent_len", &SupportSet::recent_len)
+      .def("size_for_head", &SupportSet::size_for_head);
+
+  py::class_<KernelStats>(m, "KernelStats")
+      .def(py::init<>())
+      .def_readwrite("flops", &KernelStats::flops)
+      .def_readwrite("reads", &KernelStats::reads);
+
+  py::class_<KvStore::CompactSegment>(m, "CompactSegment")
+      .def_readonly("positions", &KvStore::CompactSegment::positions)
+      .def_readonly("k", &KvStore::CompactSegment::k)
+      .def_readonly("v", &KvStore::CompactSegment::v);
+
+  py::class_<KvStore>(m, "KvStore")
+      .def(py::init<const ModelSpec&, const CacheLimits&>(), py::arg("spec"),
+           py::arg("limits") = CacheLimits{})
+      .def("size", &KvStore::size)
+      .def_property_readonly("spec", &KvStore::spec)
+      .def("begin_token", &KvStore::begin_token)
+      .def("append_layer",
+           [](KvStore& s, int layer, const std::vector<float>& k, const std::vector<float>& v) {
+             const size_t hd = static_cast<size_t>(s.spec().n_kv_heads) * s.spec().head_dim;
+             if (k.size() != hd || v.size() != hd)
+               fail(ErrorCode::kSupportMismatch, "append_layer: k/v must hold n_kv_heads * head_dim values");
+             s.append_layer(layer, k.data(), v.data());
+           })
+      .def("end_token", &KvStore::end_token)
+      .def("append_tokens",
+           [](KvStore& s, int count, std::uintptr_t k, std::uintptr_t v) {
+             s.append_tokens(count, reinterpret_cast<const float*>(k), reinterpret_cast<const float*>(v));
+           },
+           "host fp32 pointers [n_layers][count][H*d]")
+      .def("key_row", &KvStore::key_row)
+      .def("value_row", &KvStore::value_row)
+      .def("key_norm", &KvStore::key_norm)
+      .def("reorganize", &KvStore::reorganize)
+      .def("compact_valid", &KvStore::compact_valid)
+      .def("compact_matches", &KvStore::compact_matches)
+      .def("compact", &KvStore::compact)
+      .def("recent_tail", &KvStore::recent_tail);
+
+  m.def("attention_kernel_dense",
+        [](const KvStore& s, int layer, const std::vector<double>& q, KernelStats* stats) {
+          return attention_kernel_dense(s, layer, q, stats);
+        },
+        py::arg("store"), py::arg("layer"), py::arg("q"), py::arg("stats") = nullptr);
+  m.def("attention_kernel_sparse",
+        [](const KvStore& s, int layer, const std::vector<double>& q, const SupportSet& sup,
+           KernelStats* stats) { return attention_kernel_sparse(s, layer, q, sup, stats); },
+        py::arg("store"), py::arg("layer"), py::arg("q"), py::arg("support"), py::arg("stats") = nullptr);
+  py::class_<DenseCapture>(m, "DenseCapture")
+      .def_readonly("context", &DenseCapture::context)
+      .def_readonly("window", &DenseCapture::window);
+  m.def("dense_capture", &dense_capture, py::arg("store"), py::arg("layer"), py::arg("q"),
+        py::arg("allowed"), py::arg("pool") = PoolMode::kMean);
+
+  py::class_<SparseState>(m, "SparseState")
+      .def(py::init<>())
+      .def_readwrite("layer", &SparseState::layer)
+      .def_readwrite("sink", &SparseState::sink)
+      .def_readwrite("recent_start", &SparseState::recent_start)
+      .def_readwrite("recent_len", &SparseState::recent_len)
+      .def_readwrite("selected", &SparseState::selected)
+      .def("recent", &SparseState::recent)
+      .def("support", &SparseState::support);
+  py::class_<DecodeState>(m, "DecodeState")
+      .def(py::init<>())
+      .def_readwrite("t", &DecodeState::t)
+      .def_readwrite("prefix_len", &DecodeState::prefix_len)
+      .def_readwrite("g", &DecodeState::g)
+      .def_readwrite("steps_since_slow", &DecodeState::steps_since_slow)
+      .def_readwrite("last_token", &DecodeState::last_token)
+      .def_readwrite("per_layer", &DecodeState::per_layer);
+  m.def("init_decode_state", &init_decode_state, py::arg("prompt_len"), py::arg("n_layers"),
+        py::arg("n_kv_heads"), py::arg("limits"));
+  m.def("compute_allowed", &compute_allowed, py::arg("state"), py::arg("prefix_len"));
+  m.def("next_step_type", &next_step_type, py::arg("state"), py::arg("trigger"));
+  m.def("fast_step_update", &fast_step_update, py::arg("state"), py::arg("limits"));
+  m.def("slow_step_update", &slow_step_update, py::arg("state"), py::arg("selected_per_layer"),
+        py::arg("limits"));
+  m.def("flop_model", &flop_model, py::arg("prefix_len"), py::arg("support"), py::arg("slow_fraction"));
+
+  // ---- batched device API: the C ABI one-to-one --------------------------
+  py::class_<sfi_shape>(m, "Shape")
+      .def(py::init<>())
+      .def_readwrite("n_layers", &sfi_shape::n_layers)
+      .def_readwrite("batch", &sfi_shape::batch)
+      .def_readwrite("n_kv_heads", &sfi_shape::n_kv_heads)
+      .def_readwrite("n_q_heads", &sfi_shape::n_q_heads)
+      .def_readwrite("head_dim", &sfi_shape::head_dim)
+      .def_readwrite("max_positions", &sfi_shape::max_positions)
+      .def_readwrite("n_sink", &sfi_shape::n_sink)
+      .def_readwrite("k_budget", &sfi_shape::k_budget)
+      .def_readwrite("n_recent", &sfi_shape::n_recent);
+
+#define PTR_FIELD(name, type)                                                          \
+  def_property(                                                                        \
+      #name, [](const sfi_cache& c) { return reinterpret_cast<std::uintptr_t>(c.name); }, \
+      [](sfi_cache& c, std::uintptr_t p) { c.name = reinterpret_cast<type>(p); })
+  py::class_<sfi_cache>(m, "Cache")
+      .def(py::init([]() { return sfi_cache{}; }))
+      .PTR_FIELD(k_cache, void*)
+      .PTR_FIELD(v_cache, void*)
+      .PTR_FIELD(key_norms, double*)
+      .PTR_FIELD(ck, void*)
+      .PTR_FIELD(cv, void*)
+      .PTR_FIELD(sel, int32_t*)
+      .PTR_FIELD(n_sel, int32_t*)
+      .PTR_FIELD(prefix_len, int32_t*)
+      .PTR_FIELD(n_sink_b, int32_t*)
+      .PTR_FIELD(recent_len, int32_t*)
+      .PTR_FIELD(error_flags, uint32_t*)
+      .PTR_FIELD(workspace, void*)
+      .def_readwrite("workspace_bytes", &sfi_cache::workspace_bytes);
+#undef PTR_FIELD
+
+  py::class_<sfi_selector_params>(m, "SelectorParams")
+      .def(py::init([](const SelectorConfig& c) { return c.to_params(); }), py::arg("config") = SelectorConfig{});
+
+  m.def("version", &sfi_version);
+  m.def("last_launch_count", &sfi_last_launch_count);
+  m.def("buffer_sizes", [](const sfi_shape& s) {
+    sfi_sizes z;
+    check(sfi_buffer_sizes(&s, &z));
+    return sizes_dict(z);
+  });
+  m.def("shape_validate", [](const sfi_shape& s) { check(sfi_shape_validate(&s)); });
+  m.def("set_lengths", [](const sfi_shape& s, const sfi_cache& c, const std::vector<int32_t>& L,
+                          const std::vector<int32_t>& nsb, py::object rl, std::uintptr_t stream) {
+    if ((int)L.size() != s.batch || (int)nsb.size() != s.batch)
+      fail(ErrorCode::kSupportMismatch, "set_lengths: one entry per request");
+    if (rl.is_none()) {
+      check(sfi_set_lengths(&s, &c, L.data(), nsb.data(), nullptr, vp(stream)));
+    } else {
+      auto r = rl.cast<std::vector<int32_t>>();
+      if ((int)r.size() != s.batch) fail(ErrorCode::kSupportMismatch, "set_lengths: one entry per request");
+      check(sfi_set_lengths(&s, &c, L.data(), nsb.data(), r.data(), vp(stream)));
+    }
+  });
+  m.def("step_advance", [](const sfi_shape& s, const sfi_cache& c, std::uintptr_t stream) {
+    check(sfi_step_advance(&s, &c, vp(stream)));
+  });
+  m.def("ring_append", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t k,
+                          std::uintptr_t v, std::uintptr_t stream) {
+    check(sfi_ring_append(&s, &c, layer, vp(k), vp(v), vp(stream)));
+  });
+  m.def("append_block", [](const sfi_shape& s, const sfi_cache& c, int layer, int count, std::uintptr_t k,
+                           std::uintptr_t v, std::uintptr_t stream) {
+    check(sfi_append_block(&s, &c, layer, count, vp(k), vp(v), vp(stream)));
+  });
+  m.def("dense_decode", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
+                           std::uintptr_t out, std::uintptr_t logits, int pool, std::uintptr_t stream) {
+    check(sfi_dense_decode(&s, &c, layer, static_cast<const float*>(vp(q)), static_cast<float*>(vp(out)),
+                           static_cast<float*>(vp(logits)), pool, vp(stream)));
+  });
+  m.def("sparse_decode", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
+                            std::uintptr_t out, std::uintptr_t stream) {
+    check(sfi_sparse_decode(&s, &c, layer, static_cast<const float*>(vp(q)), static_cast<float*>(vp(out)),
+                            vp(stream)));
+  });
+  m.def("selector", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
+                       const sfi_selector_params& prm, std::uintptr_t stream) {
+    check(sfi_selector(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm, vp(stream)));
+  });
+  m.def("compact_build", [](const sfi_shape& s, const sfi_cache& c, int layer, int rebuild_ring,
+                            std::uintptr_t stream) {
+    check(sfi_compact_build(&s, &c, layer, rebuild_ring, vp(stream)));
+  });
+  m.def("read_errors", [](const sfi_cache& c, std::uintptr_t stream) {
+    uint32_t flags = 0;
+    const int rc = sfi_read_errors(&c, &flags, vp(stream));
+    return py::make_tuple(rc, flags, std::string(rc ? sfi_last_error() : ""));
+  });
+  m.def("fill_synthetic", [](const sfi_shape& s, const sfi_cache& c, std::uint64_t seed, int len,
+                             std::uintptr_t stream) {
+    check(sfi_fill_synthetic(&s, &c, seed, len, vp(stream)));
+  });
+  m.def("selector_stages", [](const sfi_shape& s, const sfi_cache& c, int b, int n_j, std::uintptr_t stream) {
+    std::vector<double> zb(static_cast<size_t>(s.n_kv_heads) * n_j), za(zb.size());
+    check(sfi_selector_stages(&s, &c, b, zb.data(), za.data(), n_j, vp(stream)));
+    return py::make_tuple(zb, za);
+  });
+}

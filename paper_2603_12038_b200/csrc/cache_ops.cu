@@ -1,0 +1,295 @@
+// cache_ops.cu — K3: recent-ring append (every step) and the compact-cache
+// builder (slow steps), plus step advance and the synthetic cache fill.
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   KvStore::append_layer   attention.cpp:136-152  row p-1 <- k, v; key norm
+//                           sqrt(sum_c (double)k_c^2) in c order
+//   slide_recent            scheduler.cpp:45-51    recent window = last
+//                           clamp(L - n_sink, 0, n_recent) positions
+//   KvStore::reorganize     attention.cpp:186-217  merge(sink, selected),
+//                           strictly ascending, 1 <= p <= len, bit-exact copy
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sfi_impl {
+
+using namespace sfi_dev;
+
+namespace {
+
+// prefix_len += advance; recent_len = clamp(L - n_sink_b, 0, R) (slide_recent)
+__global__ void advance_kernel(int32_t* prefix_len, const int32_t* n_sink_b, int32_t* recent_len,
+                               int B, int Lmax, int R, int advance, uint32_t* err) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int L = prefix_len[b];
+  if (L + advance > Lmax) {
+    raise_error(err, SFI_ERR_CONTEXT_OVERFLOW);
+  } else {
+    L += advance;
+    prefix_len[b] = L;
+  }
+  int rl = L - n_sink_b[b];
+  recent_len[b] = rl < 0 ? 0 : (rl > R ? R : rl);
+}
+
+struct AppendParams {
+  const __nv_bfloat16* k;  // [B][H][count][D]
+  const __nv_bfloat16* v;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  __nv_bfloat16* ck;
+  __nv_bfloat16* cv;
+  double* norms;
+  const int32_t* prefix_len;
+  uint32_t* err;
+  int layer, B, H, D, Lmax, crows, R, count;
+  int block_mode;  // 0: current token (row L-1); 1: rows L .. L+count-1
+};
+
+// One CTA per (token, b, head); D threads. The norm is summed by one thread in
+// c order with explicit round-to-nearest ops (no FMA contraction) so it is
+// bit-identical to the reference's sequential fp64 loop.
+__global__ void append_kernel(const AppendParams p) {
+  __shared__ float xs[128];
+  const int i = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int b = bh / p.H;
+  const int c = threadIdx.x;
+  const int L = p.prefix_len[b];
+  const int row = p.block_mode ? (L + i) : (L - 1);
+  if (row < 0 || row >= p.Lmax) {
+    if (c == 0) raise_error(p.err, p.block_mode ? SFI_ERR_CONTEXT_OVERFLOW : SFI_ERR_OUT_OF_RANGE);
+    return;
+  }
+  const size_t src = ((size_t)bh * p.count + i) * p.D + c;
+  const __nv_bfloat16 kx = p.k[src];
+  const __nv_bfloat16 vx = p.v[src];
+  const size_t slice = (size_t)(p.layer * p.B) * p.H + bh;
+  const size_t dst = (slice * p.Lmax + row) * p.D + c;
+  p.kc[dst] = kx;
+  p.vc[dst] = vx;
+  // ring slot of position row+1 is row % R; in block mode only the last R rows land
+  if (!p.block_mode || i >= p.count - p.R) {
+    const size_t rd = (slice * p.crows + (row % p.R)) * p.D + c;
+    p.ck[rd] = kx;
+    p.cv[rd] = vx;
+  }
+  xs[c] = __bfloat162float(kx);
+  __syncthreads();
+  if (c == 0) {
+    double acc = 0.0;
+    for (int j = 0; j < p.D; ++j) {
+      const double x = (double)xs[j];
+      acc = __dadd_rn(acc, __dmul_rn(x, x));
+    }
+    p.norms[slice * p.Lmax + row] = __dsqrt_rn(acc);
+  }
+}
+
+struct CompactParams {
+  const __nv_bfloat16* kc;
+  const __nv_bfloat16* vc;
+  __nv_bfloat16* ck;
+  __nv_bfloat16* cv;
+  const int32_t* sel;    // [layers][B][H][K]
+  const int32_t* n_sel;  // [layers][B][H]
+  const int32_t* prefix_len;
+  const int32_t* n_sink_b;
+  const int32_t* recent_len;
+  uint32_t* err;
+  int layer, B, H, D, Lmax, crows, R, K;
+  int rebuild_ring;
+};
+
+// One warp per compact row: lanes 0-15 move the K row, lanes 16-31 the V row.
+__global__ void compact_kernel(const CompactParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bh = blockIdx.y;
+  const int b = bh / p.H;
+  const int i = blockIdx.x * (blockDim.x >> 5) + warp;
+  const size_t slice = (size_t)(p.layer * p.B) * p.H + bh;
+  const int L = p.prefix_len[b];
+  const int nsb = p.n_sink_b[b];
+  const int nsel = p.n_sel[slice];
+  const int rl = p.recent_len[b];
+  if (nsb > p.crows - p.R - p.K || nsel > p.K || rl > p.R) {
+    if (i == 0 && lane == 0) raise_error(p.err, SFI_ERR_CONFIG);
+    return;
+  }
+  const int total = nsb + nsel + (p.rebuild_ring ? rl : 0);
+  if (i >= total) return;
+  int pos, dst;
+  if (i < nsb) {
+    pos = i + 1;
+    dst = p.R + i;
+  } else if (i < nsb + nsel) {
+    const int k = i - nsb;
+    const int32_t* s = p.sel + slice * p.K;
+    pos = s[k];
+    dst = p.R + i;
+    if (lane == 0) {
+      if (pos <= nsb || (k > 0 && s[k - 1] >= pos)) raise_error(p.err, SFI_ERR_OVERLAP_VIOLATION);
+      if (pos < 1 || pos > L) raise_error(p.err, SFI_ERR_OUT_OF_RANGE);
+    }
+    if (pos < 1 || pos > L) return;
+  } else {
+    pos = (L - rl + 1) + (i - nsb - nsel);
+    dst = (pos - 1) % p.R;
+  }
+  const size_t srow = (slice * p.Lmax + (pos - 1)) * p.D;
+  const size_t drow = (slice * p.crows + dst) * p.D;
+  const int half = lane >> 4, l16 = lane & 15;
+  const __nv_bfloat16* s = (half ? p.vc : p.kc) + srow;
+  __nv_bfloat16* d = (half ? p.cv : p.ck) + drow;
+  if (p.D == 128) {
+    reinterpret_cast<uint4*>(d)[l16] = reinterpret_cast<const uint4*>(s)[l16];
+  } else {
+    reinterpret_cast<uint2*>(d)[l16] = reinterpret_cast<const uint2*>(s)[l16];
+  }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// bf16 of an Irwin-Hall(4) approximation of N(0, 1.155^2); exact in fp32.
+__device__ __forceinline__ __nv_bfloat16 synth(uint64_t seed, uint64_t slice, int row, int c, int kv) {
+  const uint64_t u = splitmix64(seed ^ (((slice << 32) | (uint64_t)row) * 0x100000001B3ull) ^
+                                ((uint64_t)(c * 2 + kv) << 52));
+  const int s = (int)(u & 0xFFFF) + (int)((u >> 16) & 0xFFFF) + (int)((u >> 32) & 0xFFFF) +
+                (int)(u >> 48) - 131070;
+  return __float2bfloat16_rn((float)s * (1.0f / 32768.0f));
+}
+
+struct FillParams {
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  double* norms;
+  uint64_t seed;
+  int slices, D, Lmax, len;
+};
+
+__global__ void fill_kernel(const FillParams p) {
+  const size_t n = (size_t)p.slices * p.len * p.D;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx % p.D);
+    const size_t rr = idx / p.D;
+    const int row = (int)(rr % p.len);
+    const size_t slice = rr / p.len;
+    const size_t dst = (slice * p.Lmax + row) * p.D + c;
+    p.kc[dst] = synth(p.seed, slice, row, c, 0);
+    p.vc[dst] = synth(p.seed, slice, row, c, 1);
+  }
+}
+
+__global__ void fill_norms_kernel(const FillParams p) {
+  const size_t n = (size_t)p.slices * p.len;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(idx % p.len);
+    const size_t slice = idx / p.len;
+    double acc = 0.0;
+    for (int c = 0; c < p.D; ++c) {
+      const double x = (double)__bfloat162float(synth(p.seed, slice, row, c, 0));
+      acc = __dadd_rn(acc, __dmul_rn(x, x));
+    }
+    p.norms[slice * p.Lmax + row] = __dsqrt_rn(acc);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_step_advance(const sfi_shape& s, const sfi_cache& c, cudaStream_t st) {
+  advance_kernel<<<(s.batch + 127) / 128, 128, 0, st>>>(c.prefix_len, c.n_sink_b, c.recent_len,
+                                                         s.batch, s.max_positions, s.n_recent, 1,
+                                                         c.error_flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_recent_rule(const sfi_shape& s, const sfi_cache& c, cudaStream_t st) {
+  advance_kernel<<<(s.batch + 127) / 128, 128, 0, st>>>(c.prefix_len, c.n_sink_b, c.recent_len,
+                                                         s.batch, s.max_positions, s.n_recent, 0,
+                                                         c.error_flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_append(const sfi_shape& s, const sfi_cache& c, int layer, int count, const void* k,
+                          const void* v, int block_mode, cudaStream_t st) {
+  AppendParams p;
+  p.k = static_cast<const __nv_bfloat16*>(k);
+  p.v = static_cast<const __nv_bfloat16*>(v);
+  p.kc = static_cast<__nv_bfloat16*>(c.k_cache);
+  p.vc = static_cast<__nv_bfloat16*>(c.v_cache);
+  p.ck = static_cast<__nv_bfloat16*>(c.ck);
+  p.cv = static_cast<__nv_bfloat16*>(c.cv);
+  p.norms = c.key_norms;
+  p.prefix_len = c.prefix_len;
+  p.err = c.error_flags;
+  p.layer = layer;
+  p.B = s.batch;
+  p.H = s.n_kv_heads;
+  p.D = s.head_dim;
+  p.Lmax = s.max_positions;
+  p.crows = s.n_recent + s.n_sink + s.k_budget;
+  p.R = s.n_recent;
+  p.count = count;
+  p.block_mode = block_mode;
+  dim3 grid(count, s.batch * s.n_kv_heads);
+  append_kernel<<<grid, s.head_dim, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_build(const sfi_shape& s, const sfi_cache& c, int layer, int rebuild_ring,
+                                 cudaStream_t st) {
+  CompactParams p;
+  p.kc = static_cast<const __nv_bfloat16*>(c.k_cache);
+  p.vc = static_cast<const __nv_bfloat16*>(c.v_cache);
+  p.ck = static_cast<__nv_bfloat16*>(c.ck);
+  p.cv = static_cast<__nv_bfloat16*>(c.cv);
+  p.sel = c.sel;
+  p.n_sel = c.n_sel;
+  p.prefix_len = c.prefix_len;
+  p.n_sink_b = c.n_sink_b;
+  p.recent_len = c.recent_len;
+  p.err = c.error_flags;
+  p.layer = layer;
+  p.B = s.batch;
+  p.H = s.n_kv_heads;
+  p.D = s.head_dim;
+  p.Lmax = s.max_positions;
+  p.crows = s.n_recent + s.n_sink + s.k_budget;
+  p.R = s.n_recent;
+  p.K = s.k_budget;
+  p.rebuild_ring = rebuild_ring;
+  const int rows = s.n_sink + s.k_budget + (rebuild_ring ? s.n_recent : 0);
+  constexpr int kWarps = 8;
+  dim3 grid((rows + kWarps - 1) / kWarps, s.batch * s.n_kv_heads);
+  if (rows == 0) return cudaSuccess;
+  compact_kernel<<<grid, kWarps * 32, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_synthetic(const sfi_shape& s, const sfi_cache& c, uint64_t seed, int len,
+                                  cudaStream_t st) {
+  FillParams p;
+  p.kc = static_cast<__nv_bfloat16*>(c.k_cache);
+  p.vc = static_cast<__nv_bfloat16*>(c.v_cache);
+  p.norms = c.key_norms;
+  p.seed = seed;
+  p.slices = s.n_layers * s.batch * s.n_kv_heads;
+  p.D = s.head_dim;
+  p.Lmax = s.max_positions;
+  p.len = len;
+  if (len <= 0) return cudaSuccess;
+  fill_kernel<<<4096, 256, 0, st>>>(p);
+  fill_norms_kernel<<<2048, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace sfi_impl

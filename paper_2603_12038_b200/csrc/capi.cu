@@ -1,0 +1,479 @@
+// capi.cu — the extern "C" boundary (include/sfi_b200.h): argument
+// validation, TMA descriptor encoding, workspace carve-up, kernel launches,
+// status codes and a thread-local error message. No exceptions cross it.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "sfi_b200.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int32_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SFI_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define SFI_CUDA(call, where)                      \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+int group_of(const sfi_shape& s) { return s.n_q_heads / s.n_kv_heads; }
+int compact_rows(const sfi_shape& s) { return s.n_recent + s.n_sink + s.k_budget; }
+
+int validate(const sfi_shape* s) {
+  if (!s) return fail(SFI_ERR_INVALID_ARGUMENT, "shape is null");
+  if (s->n_layers < 1 || s->batch < 1 || s->n_kv_heads < 1 || s->n_q_heads < 1)
+    return fail(SFI_ERR_CONFIG, "shape: n_layers, batch and head counts must be >= 1");
+  if (s->n_q_heads % s->n_kv_heads != 0)
+    return fail(SFI_ERR_CONFIG, "shape: n_q_heads must be a multiple of n_kv_heads");
+  const int G = group_of(*s);
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return fail(SFI_ERR_UNSUPPORTED, "shape: GQA group size must be 1, 2, 4 or 8");
+  if (s->head_dim != 64 && s->head_dim != 128)
+    return fail(SFI_ERR_UNSUPPORTED, "shape: head_dim must be 64 or 128");
+  if (s->n_kv_heads > 16) return fail(SFI_ERR_UNSUPPORTED, "shape: at most 16 KV heads");
+  if (s->max_positions < 1) return fail(SFI_ERR_CONFIG, "shape: max_positions must be >= 1");
+  if (s->n_sink < 0 || s->k_budget < 0 || s->n_recent < 1)
+    return fail(SFI_ERR_CONFIG, "shape: n_sink >= 0, k_budget >= 0, n_recent >= 1 required");
+  const double rows = double(s->n_layers) * s->batch * s->n_kv_heads *
+                      std::max(s->max_positions, compact_rows(*s));
+  if (rows >= 2147483647.0)
+    return fail(SFI_ERR_UNSUPPORTED, "shape: more than 2^31 cache rows (TMA coordinate range)");
+  return SFI_OK;
+}
+
+int check_layer(const sfi_shape* s, int layer) {
+  if (layer < 0 || layer >= s->n_layers) return fail(SFI_ERR_OUT_OF_RANGE, "layer out of range");
+  return SFI_OK;
+}
+
+int check_cache(const sfi_shape* s, const sfi_cache* c) {
+  if (!c || !c->k_cache || !c->v_cache || !c->key_norms || !c->ck || !c->cv || !c->sel ||
+      !c->n_sel || !c->prefix_len || !c->n_sink_b || !c->recent_len || !c->error_flags || !c->workspace)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "cache: null buffer");
+  if (c->workspace_bytes < sfi_impl::workspace_bytes(*s))
+    return fail(SFI_ERR_INVALID_ARGUMENT, "cache: workspace too small");
+  return SFI_OK;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2D bf16 view [rows][D] with 64-column x 64-row boxes, 128-byte swizzle.
+int make_tmap(CUtensorMap* m, void* base, uint64_t rows, int D) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(SFI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)D, rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SFI_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return SFI_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* q, float* out,
+                  float* logits, int pool, bool sparse, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc) return rc;
+  if ((rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!q || !out) return fail(SFI_ERR_INVALID_ARGUMENT, "decode: q/out null");
+  if (pool != SFI_POOL_MEAN && pool != SFI_POOL_MAX) return fail(SFI_ERR_CONFIG, "decode: bad pool mode");
+  const int D = s->head_dim;
+  const uint64_t slices = (uint64_t)s->n_layers * s->batch * s->n_kv_heads;
+  const uint64_t rows_per = sparse ? (uint64_t)compact_rows(*s) : (uint64_t)s->max_positions;
+  CUtensorMap tk, tv;
+  if ((rc = make_tmap(&tk, sparse ? c->ck : c->k_cache, slices * rows_per, D))) return rc;
+  if ((rc = make_tmap(&tv, sparse ? c->cv : c->v_cache, slices * rows_per, D))) return rc;
+  sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
+  sfi_impl::DecodeParams p;
+  p.q = q;
+  p.out = out;
+  p.logits = sparse ? nullptr : logits;
+  p.pool = pool;
+  p.layer = layer;
+  p.B = s->batch;
+  p.H = s->n_kv_heads;
+  p.Hq = s->n_q_heads;
+  p.Lmax = s->max_positions;
+  p.crows = compact_rows(*s);
+  p.R = s->n_recent;
+  p.sparse = sparse ? 1 : 0;
+  p.prefix_len = c->prefix_len;
+  p.n_sink_b = c->n_sink_b;
+  p.recent_len = c->recent_len;
+  p.n_sel = c->n_sel;
+  p.max_chunks = sfi_impl::kMaxChunks;
+  p.part_o = ws.part_o;
+  p.part_ml = ws.part_ml;
+  p.counters = ws.counters;
+  p.err = c->error_flags;
+  p.inv_sqrt_d = (float)(1.0 / std::sqrt((double)D));
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  const int tiles = sparse ? (s->n_recent + 63) / 64 + 1 + (s->n_sink + s->k_budget + 63) / 64
+                           : (s->max_positions + 63) / 64;
+  const int chunks = sfi_impl::choose_chunks(s->batch * s->n_kv_heads, tiles, num_sms());
+  SFI_CUDA(sfi_impl::launch_decode(p, tk, tv, D, group_of(*s), chunks, (cudaStream_t)stream),
+           sparse ? "sfi_sparse_decode" : "sfi_dense_decode");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+}  // namespace
+
+namespace sfi_impl {
+
+size_t workspace_bytes(const sfi_shape& s) {
+  const size_t slices = (size_t)s.batch * s.n_kv_heads;
+  const int G = s.n_q_heads / s.n_kv_heads;
+  size_t b = 0;
+  b += align_up(slices * kMaxChunks * G * s.head_dim * sizeof(float));
+  b += align_up(slices * kMaxChunks * 2 * 8 * sizeof(float));
+  b += align_up(slices * sizeof(int32_t));
+  b += 2 * align_up(slices * (size_t)s.max_positions * sizeof(double));
+  return b;
+}
+
+Workspace carve_workspace(const sfi_shape& s, void* base) {
+  const size_t slices = (size_t)s.batch * s.n_kv_heads;
+  const int G = s.n_q_heads / s.n_kv_heads;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  Workspace w;
+  w.part_o = reinterpret_cast<float*>(p);
+  p += align_up(slices * kMaxChunks * G * s.head_dim * sizeof(float));
+  w.part_ml = reinterpret_cast<float*>(p);
+  p += align_up(slices * kMaxChunks * 2 * 8 * sizeof(float));
+  w.counters = reinterpret_cast<int32_t*>(p);
+  p += align_up(slices * sizeof(int32_t));
+  w.sel.a = reinterpret_cast<double*>(p);
+  p += align_up(slices * (size_t)s.max_positions * sizeof(double));
+  w.sel.b = reinterpret_cast<double*>(p);
+  return w;
+}
+
+}  // namespace sfi_impl
+
+extern "C" {
+
+SFI_API const char* sfi_version(void) { return "sfi_b200 0.1 (sm_100a)"; }
+SFI_API const char* sfi_last_error(void) { return g_err.c_str(); }
+SFI_API int32_t sfi_last_launch_count(void) { return g_launches; }
+
+SFI_API int sfi_shape_validate(const sfi_shape* shape) { return validate(shape); }
+
+SFI_API int sfi_buffer_sizes(const sfi_shape* s, sfi_sizes* out) {
+  int rc = validate(s);
+  if (rc) return rc;
+  if (!out) return fail(SFI_ERR_INVALID_ARGUMENT, "sizes: out is null");
+  const size_t slices = (size_t)s->n_layers * s->batch * s->n_kv_heads;
+  out->kv_cache = slices * s->max_positions * s->head_dim * 2;
+  out->key_norms = slices * s->max_positions * sizeof(double);
+  out->compact = slices * compact_rows(*s) * s->head_dim * 2;
+  out->sel = slices * (size_t)std::max(1, s->k_budget) * sizeof(int32_t);
+  out->n_sel = slices * sizeof(int32_t);
+  out->per_batch = (size_t)s->batch * sizeof(int32_t);
+  out->workspace = sfi_impl::workspace_bytes(*s);
+  out->pooled_logits = (size_t)s->batch * s->n_kv_heads * s->max_positions * sizeof(float);
+  return SFI_OK;
+}
+
+SFI_API void sfi_default_selector_params(sfi_selector_params* o) {
+  // SelectorConfig defaults, config.hpp:31-47
+  o->alpha = 1.0;
+  o->gamma = 1.0;
+  o->beta = 1.0;
+  o->p_curve = 2.0;
+  o->eta = 0.5;
+  o->lambda_clip = 0.02;
+  o->alpha_soft = 0.5;
+  o->alpha_cross = 0.35;
+  o->temperature = 1.0;
+  o->epsilon = 1e-8;
+  o->nms_radius = 2;
+  o->pool = SFI_POOL_MEAN;
+}
+
+SFI_API void sfi_recent_window(int32_t prefix_len, int32_t n_sink_b, int32_t n_recent,
+                               int32_t* recent_start, int32_t* recent_len) {
+  int rl = prefix_len - n_sink_b;
+  rl = rl < 0 ? 0 : (rl > n_recent ? n_recent : rl);
+  if (recent_len) *recent_len = rl;
+  if (recent_start) *recent_start = prefix_len - rl + 1;
+}
+
+SFI_API int sfi_set_lengths(const sfi_shape* s, const sfi_cache* c, const int32_t* prefix_len_host,
+                            const int32_t* n_sink_host, const int32_t* recent_len_host, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c))) return rc;
+  if (!prefix_len_host || !n_sink_host) return fail(SFI_ERR_INVALID_ARGUMENT, "set_lengths: null argument");
+  for (int b = 0; b < s->batch; ++b) {
+    if (prefix_len_host[b] < 0 || prefix_len_host[b] > s->max_positions)
+      return fail(SFI_ERR_CONTEXT_OVERFLOW, "set_lengths: prefix length exceeds max_positions");
+    // n_sink_b <= n_sink and recent_len <= n_recent are required by the compact
+    // layout (checked on the device by sfi_compact_build / sfi_sparse_decode);
+    // a dense capture may use any window inside [0, L].
+    if (n_sink_host[b] < 0 || n_sink_host[b] > prefix_len_host[b])
+      return fail(SFI_ERR_CONFIG, "set_lengths: n_sink_b must be in [0, L]");
+    if (recent_len_host && (recent_len_host[b] < 0 || recent_len_host[b] > prefix_len_host[b]))
+      return fail(SFI_ERR_OUT_OF_RANGE, "set_lengths: recent_len must be in [0, L]");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t nb = (size_t)s->batch * sizeof(int32_t);
+  SFI_CUDA(cudaMemcpyAsync(c->prefix_len, prefix_len_host, nb, cudaMemcpyHostToDevice, st), "set_lengths");
+  SFI_CUDA(cudaMemcpyAsync(c->n_sink_b, n_sink_host, nb, cudaMemcpyHostToDevice, st), "set_lengths");
+  if (recent_len_host) {
+    SFI_CUDA(cudaMemcpyAsync(c->recent_len, recent_len_host, nb, cudaMemcpyHostToDevice, st), "set_lengths");
+  } else {
+    SFI_CUDA(sfi_impl::launch_set_recent_rule(*s, *c, st), "set_lengths");
+    g_launches = 1;
+  }
+  SFI_CUDA(cudaStreamSynchronize(st), "set_lengths");
+  return SFI_OK;
+}
+
+SFI_API int sfi_step_advance(const sfi_shape* s, const sfi_cache* c, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c))) return rc;
+  SFI_CUDA(sfi_impl::launch_step_advance(*s, *c, (cudaStream_t)stream), "sfi_step_advance");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_ring_append(const sfi_shape* s, const sfi_cache* c, int32_t layer, const void* k_new,
+                            const void* v_new, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!k_new || !v_new) return fail(SFI_ERR_INVALID_ARGUMENT, "ring_append: k/v null");
+  SFI_CUDA(sfi_impl::launch_append(*s, *c, layer, 1, k_new, v_new, 0, (cudaStream_t)stream),
+           "sfi_ring_append");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_append_block(const sfi_shape* s, const sfi_cache* c, int32_t layer, int32_t count,
+                             const void* k, const void* v, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (count < 0) return fail(SFI_ERR_OUT_OF_RANGE, "append_block: negative count");
+  if (count == 0) return SFI_OK;
+  if (!k || !v) return fail(SFI_ERR_INVALID_ARGUMENT, "append_block: k/v null");
+  SFI_CUDA(sfi_impl::launch_append(*s, *c, layer, count, k, v, 1, (cudaStream_t)stream),
+           "sfi_append_block");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_dense_decode(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q,
+                             float* out, float* pooled_logits, int32_t pool_mode, void* stream) {
+  return decode_common(s, c, layer, q, out, pooled_logits, pool_mode, false, stream);
+}
+
+SFI_API int sfi_sparse_decode(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q,
+                              float* out, void* stream) {
+  return decode_common(s, c, layer, q, out, nullptr, SFI_POOL_MEAN, true, stream);
+}
+
+SFI_API int sfi_selector(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                         const float* pooled_logits, const sfi_selector_params* prm, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!pooled_logits || !prm) return fail(SFI_ERR_INVALID_ARGUMENT, "selector: null argument");
+  // SelectorConfig::validate (config.cpp:68-87)
+  const bool ok = prm->alpha > 0.0 && prm->alpha <= 1.0 && prm->gamma >= 0.0 && prm->beta >= 0.0 &&
+                  prm->p_curve >= 1.0 && prm->eta >= 0.0 && prm->lambda_clip >= 0.0 &&
+                  prm->lambda_clip <= 1.0 && prm->alpha_soft >= 0.0 && prm->alpha_cross >= 0.0 &&
+                  prm->temperature > 0.0 && prm->nms_radius >= 0 && prm->epsilon > 0.0 &&
+                  std::isfinite(prm->alpha) && std::isfinite(prm->gamma) && std::isfinite(prm->beta) &&
+                  std::isfinite(prm->p_curve) && std::isfinite(prm->eta) &&
+                  std::isfinite(prm->alpha_soft) && std::isfinite(prm->alpha_cross) &&
+                  std::isfinite(prm->temperature) && std::isfinite(prm->epsilon);
+  if (!ok) return fail(SFI_ERR_CONFIG, "selector: invalid SelectorConfig");
+  sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
+  int n = 0;
+  SFI_CUDA(sfi_impl::launch_selector(*s, *c, layer, pooled_logits, *prm, ws.sel, (cudaStream_t)stream, &n),
+           "sfi_selector");
+  g_launches = n;
+  return SFI_OK;
+}
+
+SFI_API size_t sfi_selector_explicit_scratch_bytes(int32_t H, int32_t n) {
+  return 2 * (size_t)std::max(0, H) * (size_t)std::max(0, n) * sizeof(double);
+}
+
+SFI_API int sfi_selector_explicit(int32_t H, int32_t W, int32_t n, int32_t k_budget,
+                                  const double* logits, const double* norms, const int32_t* allowed,
+                                  const sfi_selector_params* prm, void* scratch, int32_t* sel,
+                                  int32_t* n_sel, uint32_t* err, void* stream) {
+  g_launches = 0;
+  if (H < 1 || H > 16) return fail(SFI_ERR_UNSUPPORTED, "selector: 1..16 heads");
+  if (W < 1) return fail(SFI_ERR_OUT_OF_RANGE, "evidence_from_window: window width must be >= 1");
+  if (W > 16) return fail(SFI_ERR_UNSUPPORTED, "selector: window width <= 16");
+  if (n < 1) return fail(SFI_ERR_EMPTY_SUPPORT, "make_cache_stats: empty allowed set");
+  if (k_budget < 0) return fail(SFI_ERR_OUT_OF_RANGE, "select_top_k: negative budget");
+  if (!logits || !norms || !allowed || !prm || !scratch || !sel || !n_sel)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "selector: null argument");
+  double* sa = static_cast<double*>(scratch);
+  double* sb = sa + (size_t)H * n;
+  int nl = 0;
+  SFI_CUDA(sfi_impl::launch_selector_explicit(H, W, n, k_budget, logits, norms, allowed, *prm, sa, sb, sel,
+                                              n_sel, err, (cudaStream_t)stream, &nl),
+           "sfi_selector_explicit");
+  g_launches = nl;
+  return SFI_OK;
+}
+
+SFI_API int sfi_select_top_k(int32_t rows, int32_t n, int32_t k, const double* scores,
+                             const int32_t* allowed, int32_t* sel, int32_t* n_sel, void* stream) {
+  g_launches = 0;
+  if (k < 0) return fail(SFI_ERR_OUT_OF_RANGE, "select_top_k: negative budget");
+  if (rows < 1 || n < 0) return fail(SFI_ERR_INVALID_ARGUMENT, "select_top_k: bad shape");
+  if (n > 0 && (!scores || !allowed)) return fail(SFI_ERR_INVALID_ARGUMENT, "select_top_k: null argument");
+  int nl = 0;
+  SFI_CUDA(sfi_impl::launch_topk_explicit(rows, n, k, scores, allowed, sel, n_sel, (cudaStream_t)stream, &nl),
+           "sfi_select_top_k");
+  g_launches = nl;
+  return SFI_OK;
+}
+
+SFI_API int sfi_selector_stages(const sfi_shape* s, const sfi_cache* c, int32_t b, double* z_base,
+                                double* z_adj, int32_t n_j, void* stream) {
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c))) return rc;
+  if (b < 0 || b >= s->batch || n_j < 0 || n_j > s->max_positions)
+    return fail(SFI_ERR_OUT_OF_RANGE, "selector_stages: bad request index or length");
+  sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int h = 0; h < s->n_kv_heads; ++h) {
+    const size_t off = ((size_t)b * s->n_kv_heads + h) * s->max_positions;
+    if (z_base)
+      SFI_CUDA(cudaMemcpyAsync(z_base + (size_t)h * n_j, ws.sel.a + off, n_j * sizeof(double),
+                               cudaMemcpyDeviceToHost, st), "selector_stages");
+    if (z_adj)
+      SFI_CUDA(cudaMemcpyAsync(z_adj + (size_t)h * n_j, ws.sel.b + off, n_j * sizeof(double),
+                               cudaMemcpyDeviceToHost, st), "selector_stages");
+  }
+  SFI_CUDA(cudaStreamSynchronize(st), "selector_stages");
+  return SFI_OK;
+}
+
+SFI_API int sfi_compact_build(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                              int32_t rebuild_ring, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  SFI_CUDA(sfi_impl::launch_compact_build(*s, *c, layer, rebuild_ring, (cudaStream_t)stream),
+           "sfi_compact_build");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_set_selection(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                              const int32_t* sel_host, const int32_t* counts_host, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!counts_host || (!sel_host && s->k_budget > 0))
+    return fail(SFI_ERR_INVALID_ARGUMENT, "set_selection: null argument");
+  const size_t slices = (size_t)s->batch * s->n_kv_heads;
+  for (size_t i = 0; i < slices; ++i)
+    if (counts_host[i] < 0 || counts_host[i] > s->k_budget)
+      return fail(SFI_ERR_OUT_OF_RANGE, "set_selection: selected set exceeds k_budget");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (s->k_budget > 0)
+    SFI_CUDA(cudaMemcpyAsync(c->sel + (size_t)layer * slices * s->k_budget, sel_host,
+                             slices * s->k_budget * sizeof(int32_t), cudaMemcpyHostToDevice, st),
+             "set_selection");
+  SFI_CUDA(cudaMemcpyAsync(c->n_sel + (size_t)layer * slices, counts_host, slices * sizeof(int32_t),
+                           cudaMemcpyHostToDevice, st),
+           "set_selection");
+  SFI_CUDA(sfi_impl::launch_compact_build(*s, *c, layer, 0, st), "set_selection");
+  SFI_CUDA(cudaStreamSynchronize(st), "set_selection");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_read_errors(const sfi_cache* c, uint32_t* flags_out, void* stream) {
+  if (!c || !c->error_flags) return fail(SFI_ERR_INVALID_ARGUMENT, "read_errors: null cache");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t f = 0;
+  SFI_CUDA(cudaMemcpyAsync(&f, c->error_flags, sizeof(f), cudaMemcpyDeviceToHost, st), "read_errors");
+  SFI_CUDA(cudaStreamSynchronize(st), "read_errors");
+  if (f) SFI_CUDA(cudaMemsetAsync(c->error_flags, 0, sizeof(uint32_t), st), "read_errors");
+  SFI_CUDA(cudaStreamSynchronize(st), "read_errors");
+  if (flags_out) *flags_out = f;
+  if (!f) return SFI_OK;
+  for (int code = 1; code < 32; ++code)
+    if (f & (1u << code)) {
+      static const char* names[] = {"ok", "config", "empty_support", "support_mismatch",
+                                    "non_finite_input", "overlap_violation", "stale_compact",
+                                    "out_of_range", "bad_weight_file", "context_overflow", "io"};
+      return fail(code, std::string("device contract violation: ") + (code <= 10 ? names[code] : "?"));
+    }
+  return SFI_OK;
+}
+
+SFI_API int sfi_fill_synthetic(const sfi_shape* s, const sfi_cache* c, uint64_t seed, int32_t len,
+                               void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c))) return rc;
+  if (len < 0 || len > s->max_positions) return fail(SFI_ERR_OUT_OF_RANGE, "fill_synthetic: bad length");
+  SFI_CUDA(sfi_impl::launch_fill_synthetic(*s, *c, seed, len, (cudaStream_t)stream), "sfi_fill_synthetic");
+  g_launches = 2;
+  return SFI_OK;
+}
+
+}  // extern "C"

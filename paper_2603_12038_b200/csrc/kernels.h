@@ -1,0 +1,78 @@
+// kernels.h — internal launch interface between the C-ABI (capi.cu) and the
+// kernel translation units. Not part of the public boundary.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sfi_b200.h"
+
+namespace sfi_impl {
+
+constexpr int kMaxChunks = 64;  // split-KV chunks per (b, head) slice
+
+struct DecodeParams {
+  const float* q;      // [B][Hq][D]
+  float* out;          // [B][Hq][D]
+  float* logits;       // [B][H][Lmax] pooled logits over J (dense only) or null
+  int pool;
+  int layer, B, H, Hq, Lmax, crows, R;
+  int sparse;
+  const int32_t* prefix_len;
+  const int32_t* n_sink_b;
+  const int32_t* recent_len;
+  const int32_t* n_sel;  // [layers][B][H]
+  int max_chunks;
+  float* part_o;         // [B*H][kMaxChunks][G][D]
+  float* part_ml;        // [B*H][kMaxChunks][2][8]
+  int32_t* counters;     // [B*H], zero between launches
+  uint32_t* err;
+  float scale_log2;      // log2(e) / sqrt(d)
+  float inv_sqrt_d;
+};
+
+int decode_smem_bytes(int D);
+int choose_chunks(int slices, int tiles_per_slice, int num_sms);
+cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv,
+                          int D, int G, int chunks, cudaStream_t stream);
+
+// cache_ops.cu
+cudaError_t launch_step_advance(const sfi_shape& s, const sfi_cache& c, cudaStream_t st);
+cudaError_t launch_set_recent_rule(const sfi_shape& s, const sfi_cache& c, cudaStream_t st);
+cudaError_t launch_append(const sfi_shape& s, const sfi_cache& c, int layer, int count,
+                          const void* k, const void* v, int advance_ring_only_current,
+                          cudaStream_t st);
+cudaError_t launch_compact_build(const sfi_shape& s, const sfi_cache& c, int layer,
+                                 int rebuild_ring, cudaStream_t st);
+cudaError_t launch_fill_synthetic(const sfi_shape& s, const sfi_cache& c, uint64_t seed, int len,
+                                  cudaStream_t st);
+
+// selector.cu
+struct SelectorScratch {
+  double* a;  // [B*H][Lmax]  p -> weights -> f -> z_base
+  double* b;  // [B*H][Lmax]  w -> r -> z_adj
+};
+cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
+                            const sfi_selector_params& prm, const SelectorScratch& scr,
+                            cudaStream_t st, int* launches);
+
+cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* logits,
+                                     const double* norms, const int32_t* allowed,
+                                     const sfi_selector_params& prm, double* sa, double* sb,
+                                     int32_t* sel, int32_t* n_sel, uint32_t* err, cudaStream_t st,
+                                     int* launches);
+cudaError_t launch_topk_explicit(int rows, int n, int K, const double* scores, const int32_t* allowed,
+                                 int32_t* sel, int32_t* n_sel, cudaStream_t st, int* launches);
+
+// workspace carve-up (capi.cu)
+struct Workspace {
+  float* part_o;
+  float* part_ml;
+  int32_t* counters;
+  SelectorScratch sel;
+};
+size_t workspace_bytes(const sfi_shape& s);
+Workspace carve_workspace(const sfi_shape& s, void* base);
+
+}  // namespace sfi_impl

@@ -1,0 +1,618 @@
+// selector.cu — K2: the SFI Selector on the device, fp64 end to end.
+//
+// Reference (paths relative to /root/reference/proj):
+//   make_cache_stats     selector.cpp:78-94    u = (j - j_min) / ((j_max - j_min) + eps)
+//   row_softmax          selector.cpp:54-74    p = exp(v - max), max from kMaskedLogit
+//   evidence_from_window selector.cpp:96-127   power mean over W rows, normalize
+//   prior_from_stats     selector.cpp:129-160  (|k|+eps)^-g exp(-b u^p) (1-u+eps)^eta
+//   normalize            distribution.cpp:41-60
+//   fuse                 selector.cpp:162-185  lambda* closed form, clip
+//   z = log(s + eps)     selector.cpp:270-276
+//   refine_soft_nms      selector.cpp:187-202
+//   refine_cross_head    selector.cpp:204-230
+//   select_top_k         selector.cpp:232-252  (score desc, position asc)
+//
+// Three kernels per call:
+//   sel_fuse_kernel   one 8-CTA cluster per (b, head) row: the chain of
+//                     dependent row reductions (max -> sums -> sum -> ff/fr/rr)
+//                     runs with deterministic block trees + DSMEM cluster
+//                     reductions; writes z_base.
+//   sel_refine_kernel one thread per (b, j): soft-NMS of every head then the
+//                     cross-head softmax in head order; writes z_adj.
+//   sel_topk_kernel   one 8-CTA cluster per row: exact K-th key by radix
+//                     refinement over order-preserving 64-bit keys (11-bit
+//                     digits, cluster-merged histograms), then an ordered
+//                     cluster scan emits the selected positions ascending with
+//                     the reference tie rule (equal scores -> lower position).
+// Inputs come either from the device cache (production: fp32 pooled logits
+// over the contiguous J_b, cached fp64 key norms) or from explicit arrays
+// (reference-facing run_selector: fp64 W x |J| windows over an arbitrary
+// ascending allowed list).
+// This file is compiled with -fmad=false: no FMA contraction, matching the
+// reference's x86-64 build. Reductions are tree-ordered (not sequential), so
+// intermediate values can differ from the reference by a few ulps; indices
+// are exact whenever the K-th/(K+1)-th score gap exceeds that.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace sfi_impl {
+
+using namespace sfi_dev;
+
+namespace {
+
+constexpr int kCS = 8;      // CTAs per cluster
+constexpr int kT = 512;     // threads per CTA
+constexpr int kWarps = kT / 32;
+constexpr int kBins = 2048; // 11-bit radix digits
+constexpr int kBinsPerCta = kBins / kCS;
+constexpr int kMaxW = 16;   // observation window rows (prefill window_prefill = 16)
+constexpr double kMaskedLogit = -1e30;  // selector.hpp:42
+
+struct SelParams {
+  // cache mode
+  const float* logits32;    // [rows][ld] fp32, W = 1
+  const double* norms_c;    // this layer's cache norms: [rows][Lmax] by position
+  const int32_t* prefix_len;
+  const int32_t* n_sink_b;
+  const int32_t* recent_len;
+  // explicit mode
+  const double* logits64;   // [rows][W][ld]
+  const double* norms_e;    // [rows][ld]
+  const int32_t* allowed;   // [n] ascending
+  int n_fixed;
+  // common
+  int W;
+  int ld;                   // row stride of scratch / explicit arrays
+  double* sa;               // [rows][ld]
+  double* sb;               // [rows][ld]
+  int32_t* sel;             // [rows][K]
+  int32_t* n_sel;           // [rows]
+  uint32_t* err;
+  int B, H, Lmax, K;
+  double alpha, gamma, beta, p_curve, eta, lambda_clip, alpha_soft, alpha_cross, temperature, eps;
+  int nms_radius;
+};
+
+// Row geometry: n = |J|, j_min, position of index j, u(j).
+template <bool kExp>
+struct Src {
+  const SelParams& p;
+  int n, j_min;
+  __device__ __forceinline__ Src(const SelParams& pp, int b) : p(pp) {
+    if (kExp) {
+      n = p.n_fixed;
+      j_min = n > 0 ? p.allowed[0] : 0;
+    } else {
+      const int L = p.prefix_len[b];
+      const int nsb = p.n_sink_b[b];
+      j_min = nsb + 1;
+      n = max(0, (L - p.recent_len[b]) - j_min + 1);
+    }
+  }
+  __device__ __forceinline__ double logit(int row, int w, int j) const {
+    if (kExp) return p.logits64[((size_t)row * p.W + w) * p.ld + j];
+    return (double)p.logits32[(size_t)row * p.ld + j];
+  }
+  __device__ __forceinline__ double norm(int row, int j) const {
+    if (kExp) return p.norms_e[(size_t)row * p.ld + j];
+    return p.norms_c[(size_t)row * p.Lmax + (j_min - 1) + j];
+  }
+  // make_cache_stats: (double)(allowed[i] - j_min) / ((double)(j_max - j_min) + eps)
+  __device__ __forceinline__ double u(int j, double denom) const {
+    if (kExp) return (double)(p.allowed[j] - j_min) / denom;
+    return (double)j / denom;
+  }
+  __device__ __forceinline__ double u_denom() const {
+    if (kExp) return (double)(p.allowed[n - 1] - j_min) + p.eps;
+    return (double)(n - 1) + p.eps;
+  }
+  __device__ __forceinline__ int pos(int j) const { return kExp ? p.allowed[j] : j_min + j; }
+};
+
+// std::max semantics (first argument on ties)
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// pow with the exponents the defaults use evaluated exactly (correctly
+// rounded), everything else through CUDA's pow.
+__device__ __forceinline__ double pow_ref(double x, double y) {
+  if (y == 1.0) return x;
+  if (y == 2.0) return x * x;
+  if (y == 0.5) return sqrt(x);
+  if (y == -1.0) return 1.0 / x;
+  if (y == 0.0) return 1.0;
+  return pow(x, y);
+}
+
+struct OpSum {
+  __device__ double operator()(double a, double b) const { return a + b; }
+};
+struct OpMax {
+  __device__ double operator()(double a, double b) const { return smax(a, b); }
+};
+struct OpMinU {
+  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const {
+    return a < b ? a : b;
+  }
+};
+struct OpMaxU {
+  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const {
+    return a < b ? b : a;
+  }
+};
+
+// Deterministic cluster-wide reduction of the first `nv` of NV values: warp
+// butterfly, warps in index order, CTAs in rank order. Every thread of the
+// cluster returns the same result.
+template <int NV, typename T, typename Op>
+__device__ __forceinline__ void cluster_reduce(T (&v)[NV], int nv, T* wbuf, T* red,
+                                               cg::cluster_group& cl, Op op) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    if (k < nv)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] = op(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      if (k < nv) wbuf[warp * NV + k] = v[k];
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    const int k = threadIdx.x;
+    T acc = wbuf[k];
+    for (int w = 1; w < kWarps; ++w) acc = op(acc, wbuf[w * NV + k]);
+    red[k] = acc;
+  }
+  cl.sync();
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    if (k < nv) {
+      T acc = *cl.map_shared_rank(&red[k], 0);
+      for (int r = 1; r < kCS; ++r) acc = op(acc, *cl.map_shared_rank(&red[k], r));
+      v[k] = acc;
+    }
+  // no CTA may overwrite `red` (or exit) before every CTA has read it
+  cl.sync();
+}
+
+template <bool kExp, int WM>
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
+    sel_fuse_kernel(const SelParams p) {
+  __shared__ double wbuf[kWarps * (WM + 1)];
+  __shared__ double red[WM + 1];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.y;
+  const int b = row / p.H;
+  const Src<kExp> src(p, b);
+  const int n = src.n;
+  if (n <= 0) return;  // uniform over the cluster
+  const int W = WM == 1 ? 1 : p.W;
+  const int chunk = (n + kCS - 1) / kCS;
+  const int lo = rank * chunk;
+  const int hi = min(n, lo + chunk);
+  double* A = p.sa + (size_t)row * p.ld;
+  double* Bw = p.sb + (size_t)row * p.ld;
+
+  // pass 1: per window row max (row_softmax: starts at kMaskedLogit), finite check
+  double mx[WM];
+#pragma unroll
+  for (int w = 0; w < WM; ++w) mx[w] = kMaskedLogit;
+  bool bad = false;
+  for (int j = lo + threadIdx.x; j < hi; j += kT) {
+#pragma unroll
+    for (int w = 0; w < WM; ++w)
+      if (w < W) {
+        const double v = src.logit(row, w, j);
+        if (!isfinite(v)) bad = true;
+        mx[w] = smax(mx[w], v);
+      }
+  }
+  if (bad) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
+  cluster_reduce<WM>(mx, W, wbuf, red, cl, OpMax());
+
+  // pass 2: sum_j exp(v - max) per window row; prior weight w and its sum
+  const double denom_u = src.u_denom();
+  double s2[WM + 1];
+#pragma unroll
+  for (int k = 0; k <= WM; ++k) s2[k] = 0.0;
+  bool badn = false;
+  for (int j = lo + threadIdx.x; j < hi; j += kT) {
+#pragma unroll
+    for (int w = 0; w < WM; ++w)
+      if (w < W) {
+        const double v = src.logit(row, w, j);
+        const double pj = (v <= kMaskedLogit) ? 0.0 : exp(v - mx[w]);
+        if (WM == 1) A[j] = pj;
+        s2[w] += pj;
+      }
+    const double norm = src.norm(row, j);
+    if (!isfinite(norm) || norm < 0.0) badn = true;
+    const double u = src.u(j, denom_u);
+    const double pi_kn = pow_ref(norm + p.eps, -p.gamma);
+    const double pi_pos = exp(-p.beta * pow_ref(u, p.p_curve)) * pow_ref(1.0 - u + p.eps, p.eta);
+    const double wr = pi_kn * pi_pos;
+    if (!isfinite(wr) || wr < 0.0) badn = true;
+    Bw[j] = wr;
+    s2[WM] += wr;
+  }
+  if (badn) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
+  // pack the prior sum right after the W row sums
+  s2[W] = s2[WM];
+  cluster_reduce<WM + 1>(s2, W + 1, wbuf, red, cl, OpSum());
+  const double sumw = s2[W];
+  if (threadIdx.x == 0 && rank == 0) {
+    for (int w = 0; w < W; ++w)
+      if (s2[w] <= 0.0) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+    if (sumw <= 0.0) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+  }
+
+  // pass 3: p /= sum; mu += pow(p, alpha) over rows; weight = pow(mu / W, 1/alpha)
+  const bool a_one = (p.alpha == 1.0);
+  const double inv_a = 1.0 / p.alpha;
+  const double inv_w = 1.0 / (double)W;
+  double s3[1] = {0.0};
+  for (int j = lo + threadIdx.x; j < hi; j += kT) {
+    double wt;
+    if (WM == 1) {
+      const double f1 = A[j] / s2[0];
+      wt = a_one ? f1 : pow_ref((0.0 + pow_ref(f1, p.alpha)) * inv_w, inv_a);
+    } else {
+      double mu = 0.0;
+      for (int w = 0; w < W; ++w) {
+        const double v = src.logit(row, w, j);
+        const double pj = ((v <= kMaskedLogit) ? 0.0 : exp(v - mx[w])) / s2[w];
+        mu += pow_ref(pj, p.alpha);
+      }
+      wt = pow_ref(mu * inv_w, inv_a);
+    }
+    A[j] = wt;
+    s3[0] += wt;
+  }
+  cluster_reduce<1>(s3, 1, wbuf, red, cl, OpSum());
+  const double sum2 = s3[0];
+  if (threadIdx.x == 0 && rank == 0 && sum2 <= 0.0) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+
+  // pass 4: f = normalize(evidence), r = normalize(prior); |f|^2, f.r, |r|^2
+  double s4[3] = {0.0, 0.0, 0.0};
+  for (int j = lo + threadIdx.x; j < hi; j += kT) {
+    const double f = A[j] / sum2;
+    const double r = Bw[j] / sumw;
+    A[j] = f;
+    Bw[j] = r;
+    s4[0] += f * f;
+    s4[1] += f * r;
+    s4[2] += r * r;
+  }
+  cluster_reduce<3>(s4, 3, wbuf, red, cl, OpSum());
+  const double ff = s4[0], fr = s4[1], rr = s4[2];
+  const double denom = ff - 2.0 * fr + rr;
+  double lambda = 0.0;
+  if (fabs(denom) >= p.eps) {
+    lambda = (ff - fr) / denom;
+    lambda = (lambda < 0.0) ? 0.0 : (p.lambda_clip < lambda) ? p.lambda_clip : lambda;
+  }
+
+  // pass 5: s = (1 - lambda) f + lambda r; z = log(s + eps)
+  for (int j = lo + threadIdx.x; j < hi; j += kT) {
+    const double s = (1.0 - lambda) * A[j] + lambda * Bw[j];
+    A[j] = log(s + p.eps);
+  }
+}
+
+// Soft-NMS per head then cross-head exclusivity, one thread per (b, j).
+template <bool kExp>
+__global__ void __launch_bounds__(256) sel_refine_kernel(const SelParams p) {
+  const int b = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const Src<kExp> src(p, b);
+  const int n = src.n;
+  if (idx >= n) return;
+  double zn[16];
+  const int lo = max(0, idx - p.nms_radius);
+  const int hi = min(n - 1, idx + p.nms_radius);
+#pragma unroll
+  for (int h = 0; h < 16; ++h) {
+    if (h < p.H) {
+      const double* z = p.sa + (size_t)(b * p.H + h) * p.ld;
+      const double zj = z[idx];
+      double m = zj;
+      for (int i = lo; i <= hi; ++i) m = smax(m, z[i]);
+      const double gap = m - zj;
+      zn[h] = zj - p.alpha_soft * gap;
+    }
+  }
+  double mxs = zn[0];
+#pragma unroll
+  for (int h = 1; h < 16; ++h)
+    if (h < p.H) mxs = smax(mxs, zn[h]);
+  double e[16];
+  double sum = 0.0;
+#pragma unroll
+  for (int h = 0; h < 16; ++h)
+    if (h < p.H) {
+      e[h] = exp((zn[h] - mxs) / p.temperature);
+      sum += e[h];
+    }
+#pragma unroll
+  for (int h = 0; h < 16; ++h)
+    if (h < p.H) {
+      const double r = e[h] / sum;
+      p.sb[(size_t)(b * p.H + h) * p.ld + idx] = zn[h] + p.alpha_cross * log(smax(r, p.eps));
+    }
+}
+
+// Order-preserving key: larger score -> larger key; -0.0 ties +0.0 as in the
+// reference comparator (selector.cpp:245 compares with != and >).
+__device__ __forceinline__ unsigned long long okey(double x) {
+  if (x == 0.0) x = 0.0;
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+template <bool kExp>
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
+    sel_topk_kernel(const SelParams p) {
+  __shared__ uint32_t hist[kBins];
+  __shared__ uint32_t bsum[kBinsPerCta];
+  __shared__ unsigned long long wbuf[kWarps * 2];
+  __shared__ unsigned long long red[2];
+  __shared__ uint32_t slice_tot;
+  __shared__ int res_tb, res_above;
+  __shared__ unsigned long long cta_tot;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.y;
+  const int b = row / p.H;
+  const Src<kExp> src(p, b);
+  const int n = src.n;
+  const int K = p.K;
+  int32_t* out = p.sel + (size_t)row * K;
+  if (n <= 0 || K == 0) {
+    if (rank == 0 && threadIdx.x == 0) p.n_sel[row] = 0;
+    return;
+  }
+  if (n <= K) {  // |J| <= k: all of J (selector.cpp:239)
+    for (int i = rank * kT + threadIdx.x; i < n; i += kCS * kT) out[i] = src.pos(i);
+    if (rank == 0 && threadIdx.x == 0) p.n_sel[row] = n;
+    return;
+  }
+  const double* z = p.sb + (size_t)row * p.ld;
+
+  // pass 0: key range
+  unsigned long long mm[1] = {~0ull}, MM[1] = {0ull};
+  for (int i = rank * kT + threadIdx.x; i < n; i += kCS * kT) {
+    const unsigned long long k = okey(z[i]);
+    mm[0] = k < mm[0] ? k : mm[0];
+    MM[0] = k > MM[0] ? k : MM[0];
+  }
+  cluster_reduce<1>(mm, 1, wbuf, red, cl, OpMinU());
+  cluster_reduce<1>(MM, 1, wbuf, red, cl, OpMaxU());
+
+  // radix refinement: invariant T in [lo, lo + 2^bits); `above` keys > range
+  unsigned long long lo = mm[0];
+  int bits = (MM[0] == mm[0]) ? 0 : 64 - __clzll((long long)(MM[0] - mm[0]));
+  int above = 0;
+  while (bits > 0) {
+    const int shift = bits > 11 ? bits - 11 : 0;
+    const int nb = 1 << (bits - shift);
+    for (int i = threadIdx.x; i < kBins; i += kT) hist[i] = 0;
+    __syncthreads();
+    for (int i = rank * kT + threadIdx.x; i < n; i += kCS * kT) {
+      const unsigned long long k = okey(z[i]);
+      if (k >= lo) {
+        const unsigned long long d = (k - lo) >> shift;
+        if (d < (unsigned long long)nb) atomicAdd(&hist[d], 1u);
+      }
+    }
+    cl.sync();
+    uint32_t mine = 0;
+    for (int bi = threadIdx.x; bi < kBinsPerCta; bi += kT) {
+      const int gb = rank * kBinsPerCta + bi;
+      uint32_t s = 0;
+      if (gb < nb)
+        for (int r = 0; r < kCS; ++r) s += cl.map_shared_rank(hist, r)[gb];
+      bsum[bi] = s;
+      mine += s;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0) wbuf[threadIdx.x >> 5] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < kWarps; ++w) t += (uint32_t)wbuf[w];
+      slice_tot = t;
+    }
+    cl.sync();
+    const int need_rem = K - above;
+    int own = 0, cum = 0;
+    for (int r = kCS - 1; r >= 0; --r) {
+      const int tr = (int)*cl.map_shared_rank(&slice_tot, r);
+      if (cum + tr >= need_rem) {
+        own = r;
+        break;
+      }
+      cum += tr;
+    }
+    if (rank == own && threadIdx.x == 0) {
+      int c2 = cum, tb = rank * kBinsPerCta;
+      for (int bi = kBinsPerCta - 1; bi >= 0; --bi) {
+        if (c2 + (int)bsum[bi] >= need_rem) {
+          tb = rank * kBinsPerCta + bi;
+          break;
+        }
+        c2 += (int)bsum[bi];
+      }
+      res_tb = tb;
+      res_above = c2;
+    }
+    cl.sync();
+    const int tb = *cl.map_shared_rank(&res_tb, own);
+    const int ab = *cl.map_shared_rank(&res_above, own);
+    above += ab;
+    lo += (unsigned long long)tb << shift;
+    bits = shift;
+    cl.sync();
+  }
+  const unsigned long long T = lo;
+  const int need = K - above;
+
+  // ordered emission: blocked ranges, packed (gt, eq) exclusive scan
+  const int chunk = (n + kCS - 1) / kCS;
+  const int c0 = rank * chunk, c1 = min(n, c0 + chunk);
+  const int len = max(0, c1 - c0);
+  const int E = (len + kT - 1) / kT;
+  const int e0 = c0 + threadIdx.x * E, e1 = min(c1, e0 + E);
+  unsigned long long cnt = 0;
+  for (int i = e0; i < e1; ++i) {
+    const unsigned long long k = okey(z[i]);
+    if (k > T) cnt += (1ull << 32);
+    else if (k == T) cnt += 1ull;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wbuf[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      const unsigned long long t = wbuf[w];
+      wbuf[w] = run;
+      run += t;
+    }
+    cta_tot = run;
+  }
+  cl.sync();
+  unsigned long long base = wbuf[warp] + (inc - cnt);
+  for (int r = 0; r < rank; ++r) base += *cl.map_shared_rank(&cta_tot, r);
+  int gt_b = (int)(base >> 32), eq_b = (int)(base & 0xffffffffu);
+  for (int i = e0; i < e1; ++i) {
+    const unsigned long long k = okey(z[i]);
+    if (k > T) {
+      out[gt_b + min(eq_b, need)] = src.pos(i);
+      ++gt_b;
+    } else if (k == T) {
+      if (eq_b < need) out[gt_b + eq_b] = src.pos(i);
+      ++eq_b;
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0) p.n_sel[row] = K;
+  cl.sync();
+}
+
+void fill_cfg(SelParams& p, const sfi_selector_params& prm) {
+  p.alpha = prm.alpha;
+  p.gamma = prm.gamma;
+  p.beta = prm.beta;
+  p.p_curve = prm.p_curve;
+  p.eta = prm.eta;
+  p.lambda_clip = prm.lambda_clip;
+  p.alpha_soft = prm.alpha_soft;
+  p.alpha_cross = prm.alpha_cross;
+  p.temperature = prm.temperature;
+  p.eps = prm.epsilon;
+  p.nms_radius = prm.nms_radius;
+}
+
+template <bool kExp>
+cudaError_t run3(const SelParams& p, int rows, int refine_blocks, int batches, cudaStream_t st,
+                 int* launches) {
+  const dim3 gc(kCS, (unsigned)rows);
+  if (p.W > 1)
+    sel_fuse_kernel<kExp, kMaxW><<<gc, kT, 0, st>>>(p);
+  else
+    sel_fuse_kernel<kExp, 1><<<gc, kT, 0, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  sel_refine_kernel<kExp><<<dim3(refine_blocks, batches), 256, 0, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  sel_topk_kernel<kExp><<<gc, kT, 0, st>>>(p);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
+                            const sfi_selector_params& prm, const SelectorScratch& scr,
+                            cudaStream_t st, int* launches) {
+  SelParams p{};
+  const size_t slices = (size_t)s.batch * s.n_kv_heads;
+  p.logits32 = logits;
+  p.norms_c = c.key_norms + (size_t)layer * slices * s.max_positions;
+  p.prefix_len = c.prefix_len;
+  p.n_sink_b = c.n_sink_b;
+  p.recent_len = c.recent_len;
+  p.W = 1;
+  p.ld = s.max_positions;
+  p.sa = scr.a;
+  p.sb = scr.b;
+  p.sel = c.sel + (size_t)layer * slices * s.k_budget;
+  p.n_sel = c.n_sel + (size_t)layer * slices;
+  p.err = c.error_flags;
+  p.B = s.batch;
+  p.H = s.n_kv_heads;
+  p.Lmax = s.max_positions;
+  p.K = s.k_budget;
+  fill_cfg(p, prm);
+  if (s.n_kv_heads > 16) return cudaErrorInvalidValue;
+  return run3<false>(p, (int)slices, (s.max_positions + 255) / 256, s.batch, st, launches);
+}
+
+cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* logits, const double* norms,
+                                     const int32_t* allowed, const sfi_selector_params& prm, double* sa,
+                                     double* sb, int32_t* sel, int32_t* n_sel, uint32_t* err,
+                                     cudaStream_t st, int* launches) {
+  SelParams p{};
+  p.logits64 = logits;
+  p.norms_e = norms;
+  p.allowed = allowed;
+  p.n_fixed = n;
+  p.W = W;
+  p.ld = n;
+  p.sa = sa;
+  p.sb = sb;
+  p.sel = sel;
+  p.n_sel = n_sel;
+  p.err = err;
+  p.B = 1;
+  p.H = H;
+  p.Lmax = n;
+  p.K = K;
+  fill_cfg(p, prm);
+  if (H > 16 || W > kMaxW || W < 1) return cudaErrorInvalidValue;
+  return run3<true>(p, H, (n + 255) / 256, 1, st, launches);
+}
+
+cudaError_t launch_topk_explicit(int rows, int n, int K, const double* scores, const int32_t* allowed,
+                                 int32_t* sel, int32_t* n_sel, cudaStream_t st, int* launches) {
+  SelParams p{};
+  p.allowed = allowed;
+  p.n_fixed = n;
+  p.W = 1;
+  p.ld = n;
+  p.sb = const_cast<double*>(scores);
+  p.sel = sel;
+  p.n_sel = n_sel;
+  p.B = rows;
+  p.H = 1;
+  p.Lmax = n;
+  p.K = K;
+  sel_topk_kernel<true><<<dim3(kCS, rows), kT, 0, st>>>(p);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace sfi_impl

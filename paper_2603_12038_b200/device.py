@@ -1,0 +1,129 @@
+"""Batched device API: one SFI cache (all layers, a batch of requests) whose
+buffers are torch tensors in HBM, driven through the C ABI on the current
+torch CUDA stream. This is the production / bench path; torch is only the
+allocator and the stream provider.
+
+Layout (include/sfi_b200.h):
+    k_cache, v_cache  bf16 [L][B][H][max_positions][d]
+    key_norms         fp64 [L][B][H][max_positions]
+    ck, cv            bf16 [L][B][H][n_recent + n_sink + k_budget][d]
+    sel               int32 [L][B][H][k_budget],  n_sel int32 [L][B][H]
+    prefix_len, n_sink_b, recent_len  int32 [B]
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _sfi_b200 as _C
+
+
+class SfiCache:
+    def __init__(self, n_layers: int, batch: int, n_kv_heads: int, n_q_heads: int,
+                 head_dim: int, max_positions: int, n_sink: int = 4, k_budget: int = 2048,
+                 n_recent: int = 256, device: str | torch.device = "cuda"):
+        s = _C.Shape()
+        s.n_layers, s.batch, s.n_kv_heads, s.n_q_heads = n_layers, batch, n_kv_heads, n_q_heads
+        s.head_dim, s.max_positions = head_dim, max_positions
+        s.n_sink, s.k_budget, s.n_recent = n_sink, k_budget, n_recent
+        _C.shape_validate(s)
+        self.shape = s
+        self.sizes = _C.buffer_sizes(s)
+        dev = torch.device(device)
+        L, B, H, d = n_layers, batch, n_kv_heads, head_dim
+        self.compact_rows = n_recent + n_sink + k_budget
+        z = torch.zeros
+        self.k_cache = z((L, B, H, max_positions, d), dtype=torch.bfloat16, device=dev)
+        self.v_cache = z((L, B, H, max_positions, d), dtype=torch.bfloat16, device=dev)
+        self.key_norms = z((L, B, H, max_positions), dtype=torch.float64, device=dev)
+        self.ck = z((L, B, H, self.compact_rows, d), dtype=torch.bfloat16, device=dev)
+        self.cv = z((L, B, H, self.compact_rows, d), dtype=torch.bfloat16, device=dev)
+        self.sel = z((L, B, H, max(1, k_budget)), dtype=torch.int32, device=dev)
+        self.n_sel = z((L, B, H), dtype=torch.int32, device=dev)
+        self.prefix_len = z((B,), dtype=torch.int32, device=dev)
+        self.n_sink_b = z((B,), dtype=torch.int32, device=dev)
+        self.recent_len = z((B,), dtype=torch.int32, device=dev)
+        self.error_flags = z((1,), dtype=torch.int32, device=dev)
+        self.workspace = z((self.sizes["workspace"],), dtype=torch.uint8, device=dev)
+        self.pooled_logits = z((B, H, max_positions), dtype=torch.float32, device=dev)
+        c = _C.Cache()
+        c.k_cache, c.v_cache = self.k_cache.data_ptr(), self.v_cache.data_ptr()
+        c.key_norms = self.key_norms.data_ptr()
+        c.ck, c.cv = self.ck.data_ptr(), self.cv.data_ptr()
+        c.sel, c.n_sel = self.sel.data_ptr(), self.n_sel.data_ptr()
+        c.prefix_len, c.n_sink_b = self.prefix_len.data_ptr(), self.n_sink_b.data_ptr()
+        c.recent_len = self.recent_len.data_ptr()
+        c.error_flags = self.error_flags.data_ptr()
+        c.workspace = self.workspace.data_ptr()
+        c.workspace_bytes = self.sizes["workspace"]
+        self.cache = c
+
+    # -- plumbing -------------------------------------------------------------
+    @staticmethod
+    def _stream(stream=None) -> int:
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        return stream.cuda_stream
+
+    @staticmethod
+    def _ptr(t: torch.Tensor | None, dtype=None) -> int:
+        if t is None:
+            return 0
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("device op arguments must be contiguous CUDA tensors")
+        if dtype is not None and t.dtype != dtype:
+            raise TypeError(f"expected {dtype}, got {t.dtype}")
+        return t.data_ptr()
+
+    # -- C ABI, one to one -----------------------------------------------------
+    def set_lengths(self, prefix_len, n_sink_b, recent_len=None, stream=None):
+        _C.set_lengths(self.shape, self.cache, list(map(int, prefix_len)), list(map(int, n_sink_b)),
+                       None if recent_len is None else list(map(int, recent_len)),
+                       self._stream(stream))
+
+    def fill_synthetic(self, seed: int, length: int, stream=None):
+        _C.fill_synthetic(self.shape, self.cache, seed, length, self._stream(stream))
+
+    def step_advance(self, stream=None):
+        _C.step_advance(self.shape, self.cache, self._stream(stream))
+
+    def ring_append(self, layer: int, k_new: torch.Tensor, v_new: torch.Tensor, stream=None):
+        _C.ring_append(self.shape, self.cache, layer, self._ptr(k_new, torch.bfloat16),
+                       self._ptr(v_new, torch.bfloat16), self._stream(stream))
+
+    def append_block(self, layer: int, k: torch.Tensor, v: torch.Tensor, stream=None):
+        """k, v: bf16 [B][H][count][d] appended at rows prefix_len[b].. (prefill)."""
+        _C.append_block(self.shape, self.cache, layer, k.shape[2], self._ptr(k, torch.bfloat16),
+                        self._ptr(v, torch.bfloat16), self._stream(stream))
+
+    def dense_decode(self, layer: int, q: torch.Tensor, out: torch.Tensor,
+                     logits: torch.Tensor | None = None, pool: int = 0, stream=None):
+        _C.dense_decode(self.shape, self.cache, layer, self._ptr(q, torch.float32),
+                        self._ptr(out, torch.float32), self._ptr(logits, torch.float32), pool,
+                        self._stream(stream))
+
+    def sparse_decode(self, layer: int, q: torch.Tensor, out: torch.Tensor, stream=None):
+        _C.sparse_decode(self.shape, self.cache, layer, self._ptr(q, torch.float32),
+                         self._ptr(out, torch.float32), self._stream(stream))
+
+    def selector(self, layer: int, logits: torch.Tensor, params=None, stream=None):
+        _C.selector(self.shape, self.cache, layer, self._ptr(logits, torch.float32),
+                    params if params is not None else _C.SelectorParams(), self._stream(stream))
+
+    def compact_build(self, layer: int, rebuild_ring: bool = False, stream=None):
+        _C.compact_build(self.shape, self.cache, layer, int(bool(rebuild_ring)), self._stream(stream))
+
+    def selector_stages(self, b: int, n_j: int, stream=None):
+        return _C.selector_stages(self.shape, self.cache, b, n_j, self._stream(stream))
+
+    def read_errors(self, stream=None):
+        """(status, flags, message); clears the device error word."""
+        return _C.read_errors(self.cache, self._stream(stream))
+
+    def check_errors(self, stream=None):
+        rc, flags, msg = self.read_errors(stream)
+        if rc:
+            raise _C.SfiError(f"device flags 0x{flags:x}: {msg}")
+
+    @staticmethod
+    def last_launch_count() -> int:
+        return _C.last_launch_count()

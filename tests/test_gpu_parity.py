@@ -1,0 +1,327 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on
+identical seeded inputs.
+
+Bars (BASELINE.json north_star): gather, ring update and Selector indices
+bit-exact; attention outputs and pooled logits within 2e-3 relative
+(max |got - want| / max |want|).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import bf16_round, oracle, rel_err, store_from_rows
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3  # north_star: attention outputs and logits within 2e-3 relative
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _cache(L=2, B=2, H=2, Hq=4, d=128, Lmax=1024, ns=4, K=64, R=32):
+    from paper_2603_12038_b200 import SfiCache
+
+    return SfiCache(L, B, H, Hq, d, Lmax, ns, K, R)
+
+
+def _rows(c, l, b, n):
+    """fp32 numpy [H][n][d] of the paged K and V rows of (layer l, request b)."""
+    k = c.k_cache[l, b, :, :n].float().cpu().numpy()
+    v = c.v_cache[l, b, :, :n].float().cpu().numpy()
+    return k, v
+
+
+def _window(c, b):
+    L = int(c.prefix_len[b])
+    nsb = int(c.n_sink_b[b])
+    rl = int(c.recent_len[b])
+    return L, nsb, rl, nsb + 1, L - rl
+
+
+@pytest.fixture(scope="module")
+def prepared():
+    """Synthetic cache, one appended decode token, random selections, compact built."""
+    torch = _torch()
+    c = _cache()
+    s = c.shape
+    lens = [700, 650]
+    c.fill_synthetic(seed=7, length=max(lens))
+    c.set_lengths(lens, [s.n_sink] * s.batch)
+    c.step_advance()  # current token = position L+1
+    g = torch.Generator().manual_seed(3)
+    new_k, new_v = [], []
+    for l in range(s.n_layers):
+        k = bf16_round(torch.randn(s.batch, s.n_kv_heads, s.head_dim, generator=g).numpy())
+        v = bf16_round(torch.randn(s.batch, s.n_kv_heads, s.head_dim, generator=g).numpy())
+        kt = torch.from_numpy(k).bfloat16().cuda().contiguous()
+        vt = torch.from_numpy(v).bfloat16().cuda().contiguous()
+        c.ring_append(l, kt, vt)
+        new_k.append(k)
+        new_v.append(v)
+    rng = np.random.default_rng(11)
+    sels = {}
+    for l in range(s.n_layers):
+        for b in range(s.batch):
+            L, nsb, rl, j0, j1 = _window(c, b)
+            for h in range(s.n_kv_heads):
+                n = int(rng.integers(0, s.k_budget + 1))
+                pos = np.sort(rng.choice(np.arange(j0, j1 + 1), size=n, replace=False)).astype(np.int32)
+                c.sel[l, b, h, :n] = torch.from_numpy(pos).cuda()
+                c.n_sel[l, b, h] = n
+                sels[(l, b, h)] = pos
+        c.compact_build(l, rebuild_ring=True)
+    torch.cuda.synchronize()
+    c.check_errors()
+    return c, new_k, new_v, sels
+
+
+def test_ring_append_writes_row_ring_and_norm(prepared):
+    torch = _torch()
+    c, new_k, new_v, _ = prepared
+    s = c.shape
+    orc = oracle()
+    for l in range(s.n_layers):
+        for b in range(s.batch):
+            L = int(c.prefix_len[b])
+            got_k = c.k_cache[l, b, :, L - 1].float().cpu().numpy()
+            assert np.array_equal(got_k, new_k[l][b])
+            assert np.array_equal(c.v_cache[l, b, :, L - 1].float().cpu().numpy(), new_v[l][b])
+            slot = (L - 1) % s.n_recent
+            assert np.array_equal(c.ck[l, b, :, slot].float().cpu().numpy(), new_k[l][b])
+            # key norm: sqrt of the sequential fp64 sum of squares (attention.cpp:143-150)
+            k, v = _rows(c, l, b, L)
+            st = store_from_rows(orc, k, v, s.n_q_heads)
+            for h in range(s.n_kv_heads):
+                for pos in (1, 2, L // 2, L - 1, L):
+                    assert c.key_norms[l, b, h, pos - 1].item() == st.key_norm(0, h, pos)
+    del torch
+
+
+def test_compact_gather_bit_exact_vs_reorganize(prepared):
+    c, _, _, sels = prepared
+    s = c.shape
+    orc = oracle()
+    R = s.n_recent
+    for l in range(s.n_layers):
+        for b in range(s.batch):
+            L, nsb, rl, j0, j1 = _window(c, b)
+            k, v = _rows(c, l, b, L)
+            st = store_from_rows(orc, k, v, s.n_q_heads)
+            sink = list(range(1, nsb + 1))
+            sel = [sels[(l, b, h)] for h in range(s.n_kv_heads)]
+            st.reorganize(0, sink, sel)
+            for h in range(s.n_kv_heads):
+                pos, rk, rv = st.compact(0, h)
+                n = len(pos)
+                got_k = c.ck[l, b, h, R:R + n].float().cpu().numpy()
+                got_v = c.cv[l, b, h, R:R + n].float().cpu().numpy()
+                assert np.array_equal(got_k, rk) and np.array_equal(got_v, rv)
+                # recent ring: slot (p-1) % R holds position p for the last rl positions
+                for p in range(L - rl + 1, L + 1):
+                    assert np.array_equal(c.ck[l, b, h, (p - 1) % R].float().cpu().numpy(), k[h, p - 1])
+                    assert np.array_equal(c.cv[l, b, h, (p - 1) % R].float().cpu().numpy(), v[h, p - 1])
+
+
+@pytest.mark.parametrize("pool", [0, 1])
+def test_dense_decode_and_pooled_logits(prepared, pool):
+    torch = _torch()
+    c, _, _, _ = prepared
+    s = c.shape
+    orc = oracle("port")
+    g = torch.Generator().manual_seed(5 + pool)
+    q = torch.randn(s.batch, s.n_q_heads, s.head_dim, generator=g)
+    out = torch.zeros_like(q).cuda()
+    logits = torch.zeros_like(c.pooled_logits)
+    for l in range(s.n_layers):
+        c.dense_decode(l, q.cuda().contiguous(), out, logits, pool)
+        torch.cuda.synchronize()
+        c.check_errors()
+        for b in range(s.batch):
+            L, nsb, rl, j0, j1 = _window(c, b)
+            k, v = _rows(c, l, b, L)
+            st = store_from_rows(orc, k, v, s.n_q_heads)
+            want_o, want_lg = st.dense_capture(0, q[b].double().numpy(), np.arange(j0, j1 + 1), pool)
+            assert rel_err(out[b].cpu().numpy().reshape(-1), want_o) < TOL
+            got_lg = logits[b, :, : j1 - j0 + 1].cpu().numpy()
+            assert rel_err(got_lg, want_lg) < TOL
+
+
+def test_sparse_decode_vs_attention_kernel_sparse(prepared):
+    torch = _torch()
+    c, _, _, sels = prepared
+    s = c.shape
+    orc = oracle()
+    g = torch.Generator().manual_seed(9)
+    q = torch.randn(s.batch, s.n_q_heads, s.head_dim, generator=g)
+    out = torch.zeros_like(q).cuda()
+    for l in range(s.n_layers):
+        c.sparse_decode(l, q.cuda().contiguous(), out)
+        torch.cuda.synchronize()
+        c.check_errors()
+        for b in range(s.batch):
+            L, nsb, rl, j0, j1 = _window(c, b)
+            k, v = _rows(c, l, b, L)
+            st = store_from_rows(orc, k, v, s.n_q_heads)
+            sink = list(range(1, nsb + 1))
+            sel = [sels[(l, b, h)] for h in range(s.n_kv_heads)]
+            st.reorganize(0, sink, sel)
+            want, reads = st.attention_sparse(0, q[b].double().numpy(), sink, sel, L - rl + 1, rl)
+            assert reads == sum(nsb + len(x) + rl for x in sel)
+            assert rel_err(out[b].cpu().numpy().reshape(-1), want) < TOL
+
+
+def _selector_case(B, H, Hq, Lmax, lens, K, ns=4, R=256, seed=1):
+    """Dense decode -> device pooled logits -> device Selector; returns the
+    cache and the fp32 logits so the reference can run on identical inputs."""
+    torch = _torch()
+    from paper_2603_12038_b200 import SelectorParams
+
+    c = _cache(L=1, B=B, H=H, Hq=Hq, d=128, Lmax=Lmax, ns=ns, K=K, R=R)
+    c.fill_synthetic(seed=seed, length=max(lens))
+    c.set_lengths(lens, [ns] * B)
+    q = torch.randn(B, Hq, 128, generator=torch.Generator().manual_seed(seed)).cuda()
+    out = torch.zeros_like(q)
+    logits = torch.zeros_like(c.pooled_logits)
+    c.dense_decode(0, q, out, logits, 0)
+    c.selector(0, logits, SelectorParams())
+    torch.cuda.synchronize()
+    c.check_errors()
+    return c, logits
+
+
+@pytest.mark.parametrize("B,H,Hq,lens,K", [
+    (2, 2, 4, [700, 650], 64),
+    (1, 8, 16, [8192], 512),        # C1 shape (Qwen3-0.6B heads), |J| = 8124
+    (2, 8, 32, [32768, 20000], 2048),  # C2 shape (Qwen3-8B heads), |J| = 32508
+])
+def test_device_selector_indices_bit_exact(B, H, Hq, lens, K):
+    c, logits = _selector_case(B, H, Hq, max(lens) + 8, lens, K)
+    orc = oracle()
+    from oracle import oracle as O
+
+    cfg = O.make_cfg(k_budget=K)
+    for b in range(B):
+        L, nsb, rl, j0, j1 = _window(c, b)
+        n = j1 - j0 + 1
+        vals = logits[b, :, :n].double().cpu().numpy()
+        norms = c.key_norms[0, b, :, j0 - 1:j1].cpu().numpy()
+        want, _ = orc.run_selector(vals, np.arange(j0, j1 + 1), norms, cfg)
+        for h in range(H):
+            ns_ = int(c.n_sel[0, b, h])
+            got = c.sel[0, b, h, :ns_].cpu().numpy()
+            assert np.array_equal(got, want[h]), (b, h, ns_, len(want[h]))
+
+
+def _explicit_case(rng, H, n, W, K, contiguous, quantize=False, masked=False):
+    if contiguous:
+        allowed = np.arange(5, 5 + n, dtype=np.int32)
+    else:
+        allowed = np.cumsum(rng.integers(1, 4, size=n)).astype(np.int32) + 4
+    vals = rng.normal(0.0, 1.5, size=(H, W * n))
+    if quantize:
+        vals = np.round(vals * 2) / 2
+    if masked and W > 1:
+        m = rng.random((H, W * n)) < 0.2
+        vals[m] = -1e30
+        vals[:, :n] = np.where(vals[:, :n] <= -1e30, 0.0, vals[:, :n])  # keep row 0 unmasked
+    norms = np.abs(rng.normal(10.0, 3.0, size=(H, n))) + 0.1
+    return allowed, vals, norms
+
+
+@pytest.mark.parametrize("H,n,W,K,contig,quant,masked", [
+    (1, 2, 1, 1, True, False, False),
+    (2, 5, 1, 3, False, False, False),
+    (3, 40, 2, 6, False, False, True),
+    (8, 4096, 1, 256, True, False, False),
+    (4, 3000, 16, 300, False, False, True),
+    (8, 5000, 1, 700, True, True, False),
+    (5, 64, 1, 100, True, False, False),   # |J| <= k: all of J
+    (2, 64, 1, 0, True, False, False),     # k = 0
+])
+def test_run_selector_api_matches_reference(H, n, W, K, contig, quant, masked):
+    import paper_2603_12038_b200 as sfi
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(H * 1000 + n + W)
+    allowed, vals, norms = _explicit_case(rng, H, n, W, K, contig, quant, masked)
+    w = sfi.LogitWindow()
+    w.width = W
+    w.allowed = allowed.tolist()
+    w.values = vals.tolist()
+    stats = sfi.make_cache_stats(norms.tolist(), allowed.tolist(), 1e-8)
+    cfg = sfi.SelectorConfig()
+    cfg.k_budget = K
+    got = sfi.run_selector(w, stats, cfg)
+    want, _ = oracle().run_selector(vals, allowed, norms, O.make_cfg(k_budget=K), width=W)
+    assert len(got) == H
+    for h in range(H):
+        assert np.array_equal(np.asarray(got[h], np.int32), want[h]), h
+
+
+def test_run_selector_nondefault_config():
+    import paper_2603_12038_b200 as sfi
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(42)
+    H, n, K = 4, 2000, 150
+    allowed, vals, norms = _explicit_case(rng, H, n, 1, K, True)
+    kw = dict(alpha=0.5, gamma=0.7, beta=2.0, p_curve=1.5, eta=0.25, lambda_clip=0.3,
+              alpha_soft=0.8, alpha_cross=0.1, temperature=0.7, nms_radius=3, k_budget=K)
+    cfg = sfi.SelectorConfig()
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    w = sfi.LogitWindow()
+    w.width, w.allowed, w.values = 1, allowed.tolist(), vals.tolist()
+    got = sfi.run_selector(w, sfi.make_cache_stats(norms.tolist(), allowed.tolist(), 1e-8), cfg)
+    want, _ = oracle().run_selector(vals, allowed, norms, O.make_cfg(**kw))
+    for h in range(H):
+        assert np.array_equal(np.asarray(got[h], np.int32), want[h]), h
+
+
+def test_select_top_k_ties_match_reference():
+    import paper_2603_12038_b200 as sfi
+
+    rng = np.random.default_rng(16)
+    orc = oracle()
+    for trial in range(60):
+        n = int(rng.integers(1, 3000))
+        k = int(rng.integers(0, n + 5))
+        pos = np.cumsum(rng.integers(1, 5, size=n)).astype(np.int32)
+        scores = rng.uniform(-1, 1, size=n)
+        if trial % 2 == 0:
+            scores = np.round(scores * 4) / 4  # force ties (oracle.cpp:548-552)
+        if trial % 7 == 0:
+            scores[rng.random(n) < 0.3] = -0.0
+        got = sfi.select_top_k(scores.tolist(), pos.tolist(), k)
+        want = orc.select_top_k(scores, pos, k)
+        assert np.array_equal(np.asarray(got, np.int32), want), trial
+    # selector.cpp:295-301 known answers
+    assert sfi.select_top_k([0.1, 0.9, 0.5, 0.9], [10, 20, 30, 40], 2) == [20, 40]
+    assert sfi.select_top_k([0.9, 0.5, 0.5], [10, 20, 30], 2) == [10, 20]
+    assert sfi.select_top_k([0.9, 0.5], [10, 20], 0) == []
+    assert sfi.select_top_k([0.1, 0.2], [10, 20], 5) == [10, 20]
+
+
+def test_selector_error_paths():
+    import paper_2603_12038_b200 as sfi
+
+    w = sfi.LogitWindow()
+    w.width = 1
+    w.allowed = [1, 2]
+    w.values = [[0.0, float("nan")]]
+    stats = sfi.make_cache_stats([[1.0, 1.0]], [1, 2], 1e-8)
+    with pytest.raises(sfi.SfiError) as e:
+        sfi.run_selector(w, stats, sfi.SelectorConfig())
+    assert e.value.code == "non_finite_input"
+    w.values = [[0.0, 1.0]]
+    bad = sfi.make_cache_stats([[1.0, -1.0]], [1, 2], 1e-8)
+    with pytest.raises(sfi.SfiError) as e:
+        sfi.run_selector(w, bad, sfi.SelectorConfig())
+    assert e.value.code == "non_finite_input"
+    with pytest.raises(sfi.SfiError):
+        sfi.select_top_k([1.0], [1], -1)
