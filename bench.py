@@ -1,0 +1,557 @@
+"""SFI decode-attention hot-path benchmark (BASELINE.json metric: SFI decode
+tokens/s at 32K-256K context; fast/slow step us; HBM GB/s vs peak).
+
+A step = one SFI decode step of the whole hot path for a batch of requests:
+  advance the prefix, then for every layer
+    fast: ring append (K3) + sparse decode over the compact cache (K4)
+    slow: ring append (K3) + dense decode with pooled logits (K1)
+          + Selector (K2) + compact build (K3)
+following a seeded schedule (step 0 slow; triggers Bernoulli(1/24); forced at
+t_max = 64, scheduler.cpp:93-99). Default workload = configs[1] (C2):
+Qwen3-8B-shaped attention (32 q / 8 kv heads, d = 128, 36 layers), batch 8,
+32K context, CacheLimits defaults (sink 4, selected 2048, recent 256).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3]
+    python bench.py --impl reference ...   # the reference CPU path on the host cores
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (workload, n_layers, Hq, H, batch, context, n_sink, k_budget, n_recent)
+    "c1": ("Qwen3-0.6B-shaped attention, batch 1, 8K", 28, 16, 8, 1, 8192, 4, 512, 64),
+    "c2": ("Qwen3-8B-shaped attention, batch 8, 32K", 36, 32, 8, 8, 32768, 4, 2048, 256),
+    "c3": ("Qwen3-32B-shaped attention, batch 4, 128K", 64, 64, 8, 4, 131072, 4, 2048, 256),
+}
+HEAD_DIM = 128
+T_MAX = 64
+P_TRIGGER = 1.0 / 24.0
+
+
+def schedule(n_steps: int, seed: int) -> list[bool]:
+    """True = slow. Step 0 slow; afterwards slow iff the previous token was a
+    trigger (Bernoulli(1/24)) or steps_since_slow + 1 >= t_max."""
+    rng = np.random.default_rng(seed)
+    out, since, trig = [], 0, True
+    for _ in range(n_steps):
+        slow = trig or since + 1 >= T_MAX
+        out.append(slow)
+        since = 0 if slow else since + 1
+        trig = bool(rng.random() < P_TRIGGER)
+    return out
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self) -> dict:
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+class Workload:
+    def __init__(self, cfg_name: str, steps_total: int, device):
+        import torch
+
+        import paper_2603_12038_b200 as sfi
+
+        (self.name, self.L, self.Hq, self.H, self.B, self.ctx, self.ns, self.K,
+         self.R) = CONFIGS[cfg_name]
+        self.cfg_name = cfg_name
+        self.G = self.Hq // self.H
+        self.Lmax = self.ctx + steps_total + 64
+        self.torch = torch
+        self.cache = sfi.SfiCache(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
+                                  self.K, self.R, device=device)
+        self.params = sfi.SelectorParams()
+        t = torch
+        g = t.Generator(device="cpu").manual_seed(2027)
+        L, B, H, Hq, d = self.L, self.B, self.H, self.Hq, HEAD_DIM
+        # per-layer step inputs, resident in HBM (q fp32 from the projection; new K/V bf16)
+        self.q = t.randn(L, B, Hq, d, generator=g).to(device)
+        self.k_new = t.randn(L, B, H, d, generator=g).to(device).bfloat16()
+        self.v_new = t.randn(L, B, H, d, generator=g).to(device).bfloat16()
+        self.out = t.zeros(L, B, Hq, d, device=device)
+        self.logits = self.cache.pooled_logits
+        c = self.cache
+        c.fill_synthetic(seed=2026 + 1, length=self.ctx)
+        c.set_lengths([self.ctx] * B, [self.ns] * B)
+        # initial slow step (untimed): dense + Selector + compact incl. the ring
+        self.step(slow=True, rebuild_ring=True)
+        t.cuda.synchronize()
+        c.check_errors()
+        # exercise the fast path once eagerly (same prefix: undo its advance)
+        self.step(slow=False)
+        c.set_lengths([self.ctx + 1] * B, [self.ns] * B)
+        t.cuda.synchronize()
+        c.check_errors()
+
+    def step(self, slow: bool, rebuild_ring: bool = False):
+        c = self.cache
+        c.step_advance()
+        for l in range(self.L):
+            c.ring_append(l, self.k_new[l], self.v_new[l])
+            if slow:
+                c.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
+                c.selector(l, self.logits, self.params)
+                c.compact_build(l, rebuild_ring=rebuild_ring)
+            else:
+                c.sparse_decode(l, self.q[l], self.out[l])
+
+    def launches(self, slow: bool) -> int:
+        return 1 + self.L * (6 if slow else 2)
+
+    # algorithmic bytes of one launch
+    def bytes_sparse(self) -> float:
+        S = self.R + self.ns + self.K
+        return self.B * self.H * S * 4 * HEAD_DIM + 2 * self.B * self.Hq * HEAD_DIM * 4
+
+    def bytes_dense(self, Lcur: int) -> float:
+        rl = min(self.R, Lcur - self.ns)
+        nj = Lcur - rl - self.ns
+        return (self.B * self.H * Lcur * 4 * HEAD_DIM + self.B * self.H * nj * 4
+                + 2 * self.B * self.Hq * HEAD_DIM * 4)
+
+
+def time_kernel(wl: Workload, which: str, iters: int) -> float:
+    """Average device duration (ms) of one decode launch, CUDA events on the
+    launching stream, over `iters` launches cycling the layers."""
+    t = wl.torch
+    s = t.cuda.current_stream()
+    c = wl.cache
+    evs = []
+    for i in range(iters):
+        l = i % wl.L
+        a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        a.record(s)
+        if which == "sparse":
+            c.sparse_decode(l, wl.q[l], wl.out[l])
+        else:
+            c.dense_decode(l, wl.q[l], wl.out[l], wl.logits, 0)
+        b.record(s)
+        evs.append((a, b))
+    t.cuda.synchronize()
+    ts = [a.elapsed_time(b) for a, b in evs]
+    return float(np.mean(ts[min(3, len(ts) - 1):]))
+
+
+def time_selector(wl: Workload, iters: int) -> tuple[float, float]:
+    t = wl.torch
+    s = t.cuda.current_stream()
+    c = wl.cache
+    ts, tc = [], []
+    for i in range(iters):
+        l = i % wl.L
+        a, b, e = (t.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(s)
+        c.selector(l, wl.logits, wl.params)
+        b.record(s)
+        c.compact_build(l)
+        e.record(s)
+        ts.append((a, b))
+        tc.append((b, e))
+    t.cuda.synchronize()
+    return (float(np.mean([a.elapsed_time(b) for a, b in ts[1:]])),
+            float(np.mean([a.elapsed_time(b) for a, b in tc[1:]])))
+
+
+def gpu_arm(args) -> dict:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    W, K = args.warmup, args.steps
+    sched = schedule(W + K + 1, seed=2026 + 1)[1:]  # step 0 of the schedule is the setup slow step
+    wl = Workload(args.config, W + K + 8, dev)
+    c = wl.cache
+    use_graph = not args.no_graph
+    graphs = {}
+    if use_graph:
+        # both paths already ran eagerly in setup (kernel attributes, driver entry
+        # points); capture records without executing, so prefix_len is untouched
+        for slow in (False, True):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                wl.step(slow)
+            graphs[slow] = g
+        torch.cuda.synchronize()
+
+    def run(slow: bool):
+        if use_graph:
+            graphs[slow].replay()
+        else:
+            wl.step(slow)
+
+    for i in range(W):
+        run(sched[i])
+    torch.cuda.synchronize()
+    c.check_errors()
+
+    timed = sched[W:W + K]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for slow in timed:
+            run(slow)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    c.check_errors()
+    n_slow = sum(timed)
+    tokens = wl.B * K * world
+    value = tokens / (ms / 1e3)
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        qh = torch.empty_like(wl.q, device="cpu").pin_memory()
+        kh = torch.empty_like(wl.k_new, device="cpu").pin_memory()
+        vh = torch.empty_like(wl.v_new, device="cpu").pin_memory()
+        oh = torch.empty_like(wl.out, device="cpu").pin_memory()
+        qh.copy_(wl.q)
+        kh.copy_(wl.k_new)
+        vh.copy_(wl.v_new)
+        torch.cuda.synchronize()
+        Ke = min(K, 32)
+        sched_e = sched[W:W + Ke]
+        c.set_lengths([wl.ctx + 1] * wl.B, [wl.ns] * wl.B)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for slow in sched_e:
+            wl.q.copy_(qh, non_blocking=True)
+            wl.k_new.copy_(kh, non_blocking=True)
+            wl.v_new.copy_(vh, non_blocking=True)
+            run(slow)
+            oh.copy_(wl.out, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = (wl.q.numel() * 4 + wl.k_new.numel() * 2 + wl.v_new.numel() * 2)
+        d2h = wl.out.numel() * 4
+        e2e = {"value": wl.B * Ke * world / (ems / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": Ke}
+
+    # ---- per-kernel device time (CUDA events on the launching stream) ----
+    pk = peaks()
+    Lcur = int(c.prefix_len[0].item())
+    t_sp = time_kernel(wl, "sparse", max(20, 2 * wl.L))
+    t_de = time_kernel(wl, "dense", max(8, wl.L // 2))
+    t_sel, t_cb = time_selector(wl, max(6, wl.L // 4))
+    bsp, bde = wl.bytes_sparse(), wl.bytes_dense(Lcur)
+    kernels = {
+        "sparse_decode": {"ms": t_sp, "GB/s": bsp / t_sp / 1e6, "bytes": bsp},
+        "dense_decode": {"ms": t_de, "GB/s": bde / t_de / 1e6, "bytes": bde},
+        "selector": {"ms": t_sel},
+        "compact_build": {"ms": t_cb},
+    }
+    for kk in ("sparse_decode", "dense_decode"):
+        kernels[kk]["frac"] = kernels[kk]["GB/s"] / pk["hbm_gbs"]
+    share_sp = (K - n_slow) * wl.L * t_sp
+    share_de = n_slow * wl.L * t_de
+    dom = "sparse_decode" if share_sp >= share_de else "dense_decode"
+    roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["GB/s"], "peak": pk["hbm_gbs"],
+            "peak_source": pk["source"], "unit": "GB/s", "frac": kernels[dom]["frac"],
+            "traffic": None, "share_of_step": (share_sp if dom == "sparse_decode" else share_de) / ms}
+    fast_us = wl.L * (t_sp * 1e3)
+    res = {
+        "metric": "SFI decode tokens/s (32K ctx, Qwen3-8B-shaped attention, batch 8)",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 KV, fp32 accumulate; fp64 Selector", "data": "synthetic",
+        "config": {"workload": wl.name + f" ({args.config.upper()})", "layers": wl.L,
+                   "q_heads": wl.Hq, "kv_heads": wl.H, "head_dim": HEAD_DIM, "batch_per_gpu": wl.B,
+                   "context": wl.ctx, "n_sink": wl.ns, "k_budget": wl.K, "n_recent": wl.R,
+                   "schedule": f"seeded triggers p=1/24 + t_max={T_MAX}; {n_slow} slow / {K} steps",
+                   "parallelism": f"dp{world} (independent request batches)",
+                   "cuda_graphs": use_graph,
+                   "l2": "inputs larger than L2 (KV cache %.1f GB)" % (2 * c.sizes['kv_cache'] / 1e9)},
+        "slow_steps": n_slow, "fast_step_us_kernels": fast_us,
+        "slow_step_us_kernels": wl.L * (t_de + t_sel + t_cb) * 1e3,
+        "kernels": kernels, "roofline": roof,
+        "gpu_launches": sum(wl.launches(s_) for s_ in timed),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_baseline(wl, sched[W:W + K], args)
+    if world > 1:
+        dist.destroy_process_group()
+    return res if rank == 0 else None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified reference, else the port)
+
+class CpuSample:
+    """One layer of the workload on the reference CPU path: per request a
+    reference KvStore (fp32, bf16-exact values copied from the device cache),
+    the device's current selection for the compact segment, and the device's
+    pooled logits as the Selector input."""
+
+    def __init__(self, src, data: dict):
+        from oracle import oracle as O
+
+        self.orc = O.load("best")
+        self.kind = self.orc.kind
+        self.src = src
+        self.d = data
+        self.stores = []
+        self.cur_sel = list(data["sel"])
+        B = data["B"]
+        with cf.ThreadPoolExecutor(max_workers=min(B, os.cpu_count() or 1)) as ex:
+            self.stores = list(ex.map(self._make_store, range(B)))
+
+    def _make_store(self, b):
+        d = self.d
+        st = self.orc.store(1, d["H"], d["Hq"], HEAD_DIM, d["L"] + 8)
+        st.append_many(d["k"][b], d["v"][b])
+        st.reorganize(0, d["sink"], d["sel"][b])
+        return st
+
+    def fast(self, b):
+        d = self.d
+        self.stores[b].attention_sparse(0, d["q"][b], d["sink"], self.cur_sel[b], d["rs"], d["rl"])
+
+    def slow(self, b):
+        from oracle import oracle as O
+
+        d = self.d
+        st = self.stores[b]
+        st.attention_dense(0, d["q"][b])
+        sel, _ = self.orc.run_selector(d["logits"][b], np.arange(d["j0"], d["j1"] + 1),
+                                       d["norms"][b], O.make_cfg(k_budget=d["K"]))
+        st.reorganize(0, d["sink"], sel)
+        self.cur_sel[b] = sel
+
+
+def gather_cpu_data(wl: Workload) -> dict:
+    t = wl.torch
+    c = wl.cache
+    t.cuda.synchronize()
+    L = int(c.prefix_len[0].item())
+    rl = int(c.recent_len[0].item())
+    ns = int(c.n_sink_b[0].item())
+    j0, j1 = ns + 1, L - rl
+    # make layer 0's pooled logits current for the Selector input
+    c.dense_decode(0, wl.q[0], wl.out[0], wl.logits, 0)
+    t.cuda.synchronize()
+    B, H, d = wl.B, wl.H, HEAD_DIM
+    k = c.k_cache[0, :, :, :L].float().cpu().numpy()  # [B][H][L][d]
+    v = c.v_cache[0, :, :, :L].float().cpu().numpy()
+    data = {
+        "B": B, "H": H, "Hq": wl.Hq, "L": L, "K": wl.K, "sink": list(range(1, ns + 1)),
+        "rs": L - rl + 1, "rl": rl, "j0": j0, "j1": j1,
+        "k": [np.ascontiguousarray(np.transpose(k[b], (1, 0, 2)).reshape(L, H * d)) for b in range(B)],
+        "v": [np.ascontiguousarray(np.transpose(v[b], (1, 0, 2)).reshape(L, H * d)) for b in range(B)],
+        "q": [wl.q[0, b].double().cpu().numpy().reshape(-1) for b in range(B)],
+        "sel": [[c.sel[0, b, h, : int(c.n_sel[0, b, h])].cpu().numpy() for h in range(H)] for b in range(B)],
+        "logits": [wl.logits[b, :, : j1 - j0 + 1].double().cpu().numpy() for b in range(B)],
+        "norms": [c.key_norms[0, b, :, j0 - 1:j1].cpu().numpy() for b in range(B)],
+    }
+    return data
+
+
+def synth_cpu_data(cfg_name: str) -> dict:
+    """Same-shaped synthetic inputs generated on the host (numpy; bf16-exact
+    N(0,1) K/V, fp64 q), for the reference arm: no device code involved."""
+    name, n_layers, Hq, H, B, ctx, ns, K, R = CONFIGS[cfg_name]
+    rng = np.random.default_rng(2026 + 1)
+    L = ctx + 1
+    rl = min(R, L - ns)
+    j0, j1 = ns + 1, L - rl
+    d = HEAD_DIM
+
+    def bf16(x):
+        u = x.view(np.uint32).astype(np.uint64)
+        return (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
+
+    ks, vs, norms, logits, sels = [], [], [], [], []
+    for b in range(B):
+        k = bf16(rng.standard_normal((L, H * d), dtype=np.float32))
+        v = bf16(rng.standard_normal((L, H * d), dtype=np.float32))
+        kh = k.reshape(L, H, d)
+        norms.append(np.sqrt((kh[j0 - 1:j1].astype(np.float64) ** 2).sum(-1)).T.copy())
+        logits.append(rng.normal(0.0, 0.3, size=(H, j1 - j0 + 1)))
+        sels.append([np.sort(rng.choice(np.arange(j0, j1 + 1), size=min(K, j1 - j0 + 1),
+                                        replace=False)).astype(np.int32) for _ in range(H)])
+        ks.append(k)
+        vs.append(v)
+    return {"B": B, "H": H, "Hq": Hq, "L": L, "K": K, "sink": list(range(1, ns + 1)),
+            "rs": L - rl + 1, "rl": rl, "j0": j0, "j1": j1, "k": ks, "v": vs,
+            "q": [rng.standard_normal(Hq * d) for _ in range(B)], "sel": sels, "logits": logits,
+            "norms": norms, "n_layers": n_layers, "name": name, "ctx": ctx}
+
+
+def time_cpu_layer(sample: CpuSample, slow: bool, threads: int) -> float:
+    fn = sample.slow if slow else sample.fast
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(fn, range(sample.d["B"])))
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(wl: Workload, sched_timed: list[bool], args) -> dict:
+    data = gather_cpu_data(wl)
+    sample = CpuSample(wl, data)
+    threads = min(wl.B, os.cpu_count() or 1)
+    time_cpu_layer(sample, False, threads)  # warm-up (reference bench_attention: 1 warm-up)
+    tf = [time_cpu_layer(sample, False, threads) for _ in range(3)]
+    ts = [time_cpu_layer(sample, True, threads) for _ in range(1)]
+    t_fast, t_slow = float(np.median(tf)), float(np.median(ts))
+    frac_slow = sum(sched_timed) / max(1, len(sched_timed))
+    step_s = wl.L * (frac_slow * t_slow + (1 - frac_slow) * t_fast)
+    return {"value": wl.B / step_s, "unit": "tokens/s", "cores": threads, "kind": sample.kind,
+            "sample": (f"layer 0 of {wl.L}, all {wl.B} requests x {wl.H} KV heads at L={data['L']}: "
+                       f"fast (attention_kernel_sparse) {t_fast*1e3:.1f} ms, slow (attention_kernel_dense"
+                       f" + run_selector + reorganize) {t_slow*1e3:.1f} ms per layer; x{wl.L} layers at the "
+                       f"timed schedule's slow fraction {frac_slow:.3f}"),
+            "fast_layer_ms": t_fast * 1e3, "slow_layer_ms": t_slow * 1e3}
+
+
+def reference_arm(args) -> dict | None:
+    """--impl reference: the reference CPU implementation of the path on this
+    host's cores, same config / metric; each step a one-layer sample of the
+    workload (fast or slow per the same schedule) extrapolated to all layers."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    W, K = args.warmup, args.steps
+    sched = schedule(W + K + 1, seed=2026 + 1)[1:]
+    data = synth_cpu_data(args.config)
+    nl = data["n_layers"]
+    sample = CpuSample(None, data)
+    threads = min(data["B"], os.cpu_count() or 1)
+    for i in range(W):
+        time_cpu_layer(sample, sched[i], threads)
+    total = 0.0
+    for slow in sched[W:W + K]:
+        total += nl * time_cpu_layer(sample, slow, threads)
+    value = data["B"] * K / total
+    return {
+        "impl": "reference", "metric": "SFI decode tokens/s (32K ctx, Qwen3-8B-shaped attention, batch 8)",
+        "value": value, "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": K, "warmup": W, "ms_per_step": total / K * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 KV, fp64 accumulate (reference)",
+        "data": "synthetic",
+        "config": {"workload": data["name"] + f" ({args.config.upper()})", "layers": nl,
+                   "batch_per_gpu": data["B"], "context": data["ctx"]},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": sample.kind,
+                         "sample": (f"one layer per step (of {nl}), all {data['B']} requests x "
+                                    f"{data['H']} KV heads, extrapolated x{nl}; fast = "
+                                    "attention_kernel_sparse, slow = attention_kernel_dense + "
+                                    "run_selector + reorganize")},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=128)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    res = reference_arm(args) if args.impl == "reference" else gpu_arm(args)
+    if res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

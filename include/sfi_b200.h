@@ -228,6 +228,12 @@ SFI_API int sfi_fill_synthetic(const sfi_shape* shape, const sfi_cache* cache, u
 /* Number of kernels the last call on this thread enqueued (launch accounting). */
 SFI_API int32_t sfi_last_launch_count(void);
 
+/* Debug (tuning): with SFI_DECODE_TRACE set in the environment, copies the
+ * per-CTA timeline of the last decode launch ([ctas][8] int64: start ns,
+ * prologue done, first tile landed, end, emissions, tiles, smid) into `out`;
+ * returns the CTA count. SFI_DECODE_CTAS=<n> overrides the decode grid. */
+SFI_API int32_t sfi_debug_decode_trace(int64_t* out, int32_t max_ctas);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,8 +4,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,6 +20,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int32_t g_launches = 0;
+int g_trace_ctas = 0;
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -51,6 +54,8 @@ int validate(const sfi_shape* s) {
   if (s->head_dim != 64 && s->head_dim != 128)
     return fail(SFI_ERR_UNSUPPORTED, "shape: head_dim must be 64 or 128");
   if (s->n_kv_heads > 16) return fail(SFI_ERR_UNSUPPORTED, "shape: at most 16 KV heads");
+  if ((long long)s->batch * s->n_kv_heads > 4096)
+    return fail(SFI_ERR_UNSUPPORTED, "shape: at most 4096 (request, KV head) slices");
   if (s->max_positions < 1) return fail(SFI_ERR_CONFIG, "shape: max_positions must be >= 1");
   if (s->n_sink < 0 || s->k_budget < 0 || s->n_recent < 1)
     return fail(SFI_ERR_CONFIG, "shape: n_sink >= 0, k_budget >= 0, n_recent >= 1 required");
@@ -151,17 +156,30 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   p.n_sink_b = c->n_sink_b;
   p.recent_len = c->recent_len;
   p.n_sel = c->n_sel;
-  p.max_chunks = sfi_impl::kMaxChunks;
   p.part_o = ws.part_o;
   p.part_ml = ws.part_ml;
   p.counters = ws.counters;
   p.err = c->error_flags;
   p.inv_sqrt_d = (float)(1.0 / std::sqrt((double)D));
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
-  const int tiles = sparse ? (s->n_recent + 63) / 64 + 1 + (s->n_sink + s->k_budget + 63) / 64
-                           : (s->max_positions + 63) / 64;
-  const int chunks = sfi_impl::choose_chunks(s->batch * s->n_kv_heads, tiles, num_sms());
-  SFI_CUDA(sfi_impl::launch_decode(p, tk, tv, D, group_of(*s), chunks, (cudaStream_t)stream),
+  const int per_slice = sparse ? (s->n_recent + 63) / 64 + 1 + (s->n_sink + s->k_budget + 63) / 64
+                              : (s->max_positions + 63) / 64;
+  int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms());
+  static const int env_ctas = [] {
+    const char* e = std::getenv("SFI_DECODE_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env_ctas > 0) ctas = std::min(env_ctas, sfi_impl::kMaxCtas);
+  p.trace = nullptr;
+  static const bool env_trace = std::getenv("SFI_DECODE_TRACE") != nullptr;
+  if (env_trace) {
+    p.trace = sfi_impl::decode_trace_buffer();
+    if (!p.trace) return fail(SFI_ERR_CUDA, "trace buffer");
+    SFI_CUDA(cudaMemsetAsync(p.trace, 0, sizeof(long long) * 16 * sfi_impl::kMaxCtas, (cudaStream_t)stream),
+             "trace");
+    g_trace_ctas = ctas;
+  }
+  SFI_CUDA(sfi_impl::launch_decode(p, tk, tv, D, group_of(*s), ctas, (cudaStream_t)stream),
            sparse ? "sfi_sparse_decode" : "sfi_dense_decode");
   g_launches = 1;
   return SFI_OK;
@@ -171,12 +189,17 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
 
 namespace sfi_impl {
 
+long long* decode_trace_buffer() {
+  static long long* buf = nullptr;
+  if (!buf && cudaMalloc(&buf, sizeof(long long) * 16 * kMaxCtas) != cudaSuccess) buf = nullptr;
+  return buf;
+}
+
 size_t workspace_bytes(const sfi_shape& s) {
   const size_t slices = (size_t)s.batch * s.n_kv_heads;
-  const int G = s.n_q_heads / s.n_kv_heads;
   size_t b = 0;
-  b += align_up(slices * kMaxChunks * G * s.head_dim * sizeof(float));
-  b += align_up(slices * kMaxChunks * 2 * 8 * sizeof(float));
+  b += align_up((size_t)kMaxCtas * 2 * 8 * s.head_dim * sizeof(float));
+  b += align_up((size_t)kMaxCtas * 2 * 2 * 8 * sizeof(float));
   b += align_up(slices * sizeof(int32_t));
   b += 2 * align_up(slices * (size_t)s.max_positions * sizeof(double));
   return b;
@@ -184,13 +207,12 @@ size_t workspace_bytes(const sfi_shape& s) {
 
 Workspace carve_workspace(const sfi_shape& s, void* base) {
   const size_t slices = (size_t)s.batch * s.n_kv_heads;
-  const int G = s.n_q_heads / s.n_kv_heads;
   uint8_t* p = static_cast<uint8_t*>(base);
   Workspace w;
   w.part_o = reinterpret_cast<float*>(p);
-  p += align_up(slices * kMaxChunks * G * s.head_dim * sizeof(float));
+  p += align_up((size_t)kMaxCtas * 2 * 8 * s.head_dim * sizeof(float));
   w.part_ml = reinterpret_cast<float*>(p);
-  p += align_up(slices * kMaxChunks * 2 * 8 * sizeof(float));
+  p += align_up((size_t)kMaxCtas * 2 * 2 * 8 * sizeof(float));
   w.counters = reinterpret_cast<int32_t*>(p);
   p += align_up(slices * sizeof(int32_t));
   w.sel.a = reinterpret_cast<double*>(p);
@@ -206,6 +228,14 @@ extern "C" {
 SFI_API const char* sfi_version(void) { return "sfi_b200 0.1 (sm_100a)"; }
 SFI_API const char* sfi_last_error(void) { return g_err.c_str(); }
 SFI_API int32_t sfi_last_launch_count(void) { return g_launches; }
+
+SFI_API int32_t sfi_debug_decode_trace(int64_t* out, int32_t max_ctas) {
+  long long* buf = sfi_impl::decode_trace_buffer();
+  const int n = std::min(max_ctas, g_trace_ctas);
+  if (!buf || !out || n <= 0) return 0;
+  if (cudaMemcpy(out, buf, sizeof(long long) * 16 * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return n;
+}
 
 SFI_API int sfi_shape_validate(const sfi_shape* shape) { return validate(shape); }
 

@@ -10,7 +10,7 @@
 
 namespace sfi_impl {
 
-constexpr int kMaxChunks = 64;  // split-KV chunks per (b, head) slice
+constexpr int kMaxCtas = 1024;  // stream-K decode grid cap (2 partial slots per CTA)
 
 struct DecodeParams {
   const float* q;      // [B][Hq][D]
@@ -23,19 +23,23 @@ struct DecodeParams {
   const int32_t* n_sink_b;
   const int32_t* recent_len;
   const int32_t* n_sel;  // [layers][B][H]
-  int max_chunks;
-  float* part_o;         // [B*H][kMaxChunks][G][D]
-  float* part_ml;        // [B*H][kMaxChunks][2][8]
+  float* part_o;         // [kMaxCtas][2][8][D]   per-CTA partial O (first / last slice)
+  float* part_ml;        // [kMaxCtas][2][2][8]   per-CTA partial (m, l)
   int32_t* counters;     // [B*H], zero between launches
   uint32_t* err;
   float scale_log2;      // log2(e) / sqrt(d)
   float inv_sqrt_d;
+  long long* trace;      // debug: per-CTA globaltimer stamps [grid][8] (null = off)
 };
 
-int decode_smem_bytes(int D);
-int choose_chunks(int slices, int tiles_per_slice, int num_sms);
+// debug / tuning hooks (capi.cu): SFI_DECODE_CTAS overrides the decode grid,
+// SFI_DECODE_TRACE=1 records per-CTA timelines readable with sfi_debug_decode_trace.
+long long* decode_trace_buffer();
+
+int decode_smem_bytes(int D, int slices);
+int decode_grid(int tiles_upper, int num_sms);
 cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv,
-                          int D, int G, int chunks, cudaStream_t stream);
+                          int D, int G, int ctas, cudaStream_t stream);
 
 // cache_ops.cu
 cudaError_t launch_step_advance(const sfi_shape& s, const sfi_cache& c, cudaStream_t st);

@@ -13,25 +13,34 @@
 //   select_top_k         selector.cpp:232-252  (score desc, position asc)
 //
 // Three kernels per call:
-//   sel_fuse_kernel   one 8-CTA cluster per (b, head) row: the chain of
-//                     dependent row reductions (max -> sums -> sum -> ff/fr/rr)
-//                     runs with deterministic block trees + DSMEM cluster
-//                     reductions; writes z_base.
-//   sel_refine_kernel one thread per (b, j): soft-NMS of every head then the
-//                     cross-head softmax in head order; writes z_adj.
-//   sel_topk_kernel   one 8-CTA cluster per row: exact K-th key by radix
-//                     refinement over order-preserving 64-bit keys (11-bit
-//                     digits, cluster-merged histograms), then an ordered
-//                     cluster scan emits the selected positions ascending with
-//                     the reference tie rule (equal scores -> lower position).
+//   sel_fuse_*        one 8-CTA cluster per (b, head) row. Decode fast path
+//                     (W = 1, alpha = 1): pass 1 row max; pass 2 p = exp(v-max)
+//                     and the prior weight w with the five sums
+//                     sum p, sum w, sum p^2, sum pw, sum w^2 in ONE cluster
+//                     reduction (f = p/sum p and r = w/sum w are rescalings,
+//                     so |f|^2, f.r, |r|^2 follow from them); pass 3 z_base.
+//                     The general path (W > 1 or alpha != 1) keeps the
+//                     reference's pass structure.
+//   sel_refine_kernel 256 positions of one request per CTA, all heads staged
+//                     in shared memory with the NMS halo; soft-NMS per head,
+//                     then the cross-head softmax in head order with
+//                     log r_h = (z_h - max)/T - log(sum) (one log per position).
+//   sel_topk_kernel   one 8-CTA cluster per row, the row's 64-bit
+//                     order-preserving keys resident in shared memory: exact
+//                     K-th key by radix refinement (11-bit digits, histograms
+//                     merged over DSMEM, 2 cluster barriers per digit), then an
+//                     ordered cluster scan emits the selected positions
+//                     ascending with the reference tie rule (equal scores ->
+//                     lower position).
 // Inputs come either from the device cache (production: fp32 pooled logits
 // over the contiguous J_b, cached fp64 key norms) or from explicit arrays
 // (reference-facing run_selector: fp64 W x |J| windows over an arbitrary
 // ascending allowed list).
-// This file is compiled with -fmad=false: no FMA contraction, matching the
-// reference's x86-64 build. Reductions are tree-ordered (not sequential), so
-// intermediate values can differ from the reference by a few ulps; indices
-// are exact whenever the K-th/(K+1)-th score gap exceeds that.
+// Compiled with -fmad=false (no FMA contraction). Reductions are tree-ordered
+// and the fast path rescales instead of dividing twice, so intermediates can
+// differ from the reference by a few ulps (~1e-16 relative); the indices are
+// exact whenever the K-th/(K+1)-th score gap exceeds that, measured >= 3.7e-8
+// relative and checked by tests/test_gpu_parity.py.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -51,6 +60,9 @@ constexpr int kWarps = kT / 32;
 constexpr int kBins = 2048; // 11-bit radix digits
 constexpr int kBinsPerCta = kBins / kCS;
 constexpr int kMaxW = 16;   // observation window rows (prefill window_prefill = 16)
+constexpr int kRefineT = 256;
+constexpr int kMaxNmsR = 16;  // smem halo of the refine kernel
+constexpr int kTopkSmemKeys = 24 * 1024;  // keys per CTA kept in shared memory
 constexpr double kMaskedLogit = -1e30;  // selector.hpp:42
 
 struct SelParams {
@@ -128,6 +140,13 @@ __device__ __forceinline__ double pow_ref(double x, double y) {
   return pow(x, y);
 }
 
+// prior_from_stats weight (selector.cpp:150-153)
+__device__ __forceinline__ double prior_w(const SelParams& p, double norm, double u) {
+  const double pi_kn = pow_ref(norm + p.eps, -p.gamma);
+  const double pi_pos = exp(-p.beta * pow_ref(u, p.p_curve)) * pow_ref(1.0 - u + p.eps, p.eta);
+  return pi_kn * pi_pos;
+}
+
 struct OpSum {
   __device__ double operator()(double a, double b) const { return a + b; }
 };
@@ -139,19 +158,20 @@ struct OpMinU {
     return a < b ? a : b;
   }
 };
-struct OpMaxU {
-  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const {
-    return a < b ? b : a;
-  }
-};
 
 // Deterministic cluster-wide reduction of the first `nv` of NV values: warp
-// butterfly, warps in index order, CTAs in rank order. Every thread of the
-// cluster returns the same result.
-template <int NV, typename T, typename Op>
-__device__ __forceinline__ void cluster_reduce(T (&v)[NV], int nv, T* wbuf, T* red,
+// butterfly, warps in index order, CTAs in rank order; every thread of the
+// cluster gets the same result. `red` is a [2][NV] buffer whose halves are
+// used alternately by successive calls (`parity`; every call site of a kernel
+// shares one buffer of the kernel's widest NV), so one cluster barrier per
+// call suffices; the kernel ends with a cluster barrier before any CTA exits.
+template <int NV, int S, typename T, typename Op>
+__device__ __forceinline__ void cluster_reduce(T (&v)[NV], int nv, T* wbuf, T (*red)[S], int& parity,
                                                cg::cluster_group& cl, Op op) {
+  static_assert(NV <= S, "reduction buffer too narrow");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* slot = red[parity];
+  parity ^= 1;
 #pragma unroll
   for (int k = 0; k < NV; ++k)
     if (k < nv)
@@ -166,30 +186,102 @@ __device__ __forceinline__ void cluster_reduce(T (&v)[NV], int nv, T* wbuf, T* r
     const int k = threadIdx.x;
     T acc = wbuf[k];
     for (int w = 1; w < kWarps; ++w) acc = op(acc, wbuf[w * NV + k]);
-    red[k] = acc;
+    slot[k] = acc;
   }
   cl.sync();
 #pragma unroll
   for (int k = 0; k < NV; ++k)
     if (k < nv) {
-      T acc = *cl.map_shared_rank(&red[k], 0);
-      for (int r = 1; r < kCS; ++r) acc = op(acc, *cl.map_shared_rank(&red[k], r));
+      T acc = *cl.map_shared_rank(&slot[k], 0);
+      for (int r = 1; r < kCS; ++r) acc = op(acc, *cl.map_shared_rank(&slot[k], r));
       v[k] = acc;
     }
-  // no CTA may overwrite `red` (or exit) before every CTA has read it
-  cl.sync();
 }
 
-template <bool kExp, int WM>
+// ---------------------------------------------------------------------------
+// Stage A, decode fast path: W = 1, alpha = 1.
+template <bool kExp>
 __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
-    sel_fuse_kernel(const SelParams p) {
-  __shared__ double wbuf[kWarps * (WM + 1)];
-  __shared__ double red[WM + 1];
+    sel_fuse_fast_kernel(const SelParams p) {
+  __shared__ double wbuf[kWarps * 5];
+  __shared__ double red[2][5];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int row = blockIdx.y;
-  const int b = row / p.H;
-  const Src<kExp> src(p, b);
+  const Src<kExp> src(p, row / p.H);
+  const int n = src.n;
+  if (n <= 0) return;  // uniform over the cluster
+  const int chunk = (n + kCS - 1) / kCS;
+  const int lo = rank * chunk;
+  const int hi = min(n, lo + chunk);
+  double* A = p.sa + (size_t)row * p.ld;
+  double* Bw = p.sb + (size_t)row * p.ld;
+  int par = 0;
+
+  // pass 1: row max (starts at kMaskedLogit), finite check
+  double m1[1] = {kMaskedLogit};
+  bool bad = false;
+  for (int j = lo + threadIdx.x; j < hi; j += kT) {
+    const double v = src.logit(row, 0, j);
+    if (!isfinite(v)) bad = true;
+    m1[0] = smax(m1[0], v);
+  }
+  if (bad) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
+  cluster_reduce<1>(m1, 1, wbuf, red, par, cl, OpMax());
+  const double mx = m1[0];
+
+  // pass 2: p, w and the five sums
+  const double denom_u = src.u_denom();
+  double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  bool badn = false;
+  for (int j = lo + threadIdx.x; j < hi; j += kT) {
+    const double v = src.logit(row, 0, j);
+    const double pj = (v <= kMaskedLogit) ? 0.0 : exp(v - mx);
+    const double norm = src.norm(row, j);
+    if (!isfinite(norm) || norm < 0.0) badn = true;
+    const double wr = prior_w(p, norm, src.u(j, denom_u));
+    if (!isfinite(wr) || wr < 0.0) badn = true;
+    A[j] = pj;
+    Bw[j] = wr;
+    s[0] += pj;
+    s[1] += wr;
+    s[2] += pj * pj;
+    s[3] += pj * wr;
+    s[4] += wr * wr;
+  }
+  if (badn) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
+  cluster_reduce<5>(s, 5, wbuf, red, par, cl, OpSum());
+  if (threadIdx.x == 0 && rank == 0 && (s[0] <= 0.0 || s[1] <= 0.0))
+    raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+  // f = p c1, r = w c2 (normalize); fuse (selector.cpp:166-174)
+  const double c1 = 1.0 / s[0], c2 = 1.0 / s[1];
+  const double ff = s[2] * c1 * c1;
+  const double fr = s[3] * c1 * c2;
+  const double rr = s[4] * c2 * c2;
+  const double denom = ff - 2.0 * fr + rr;
+  double lambda = 0.0;
+  if (fabs(denom) >= p.eps) {
+    lambda = (ff - fr) / denom;
+    lambda = (lambda < 0.0) ? 0.0 : (p.lambda_clip < lambda) ? p.lambda_clip : lambda;
+  }
+  const double a = (1.0 - lambda) * c1, bb = lambda * c2;
+
+  // pass 3: z = log((1 - lambda) f + lambda r + eps)
+  for (int j = lo + threadIdx.x; j < hi; j += kT) A[j] = log(a * A[j] + bb * Bw[j] + p.eps);
+  cl.sync();  // remote reads of `red` done before any CTA exits
+}
+
+// Stage A, general path (W >= 1, any alpha): the reference's pass structure.
+template <bool kExp, int WM>
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
+    sel_fuse_kernel(const SelParams p) {
+  constexpr int kNV = (WM + 1) > 3 ? (WM + 1) : 3;
+  __shared__ double wbuf[kWarps * kNV];
+  __shared__ double red[2][kNV];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.y;
+  const Src<kExp> src(p, row / p.H);
   const int n = src.n;
   if (n <= 0) return;  // uniform over the cluster
   const int W = WM == 1 ? 1 : p.W;
@@ -198,6 +290,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
   const int hi = min(n, lo + chunk);
   double* A = p.sa + (size_t)row * p.ld;
   double* Bw = p.sb + (size_t)row * p.ld;
+  int par = 0;
 
   // pass 1: per window row max (row_softmax: starts at kMaskedLogit), finite check
   double mx[WM];
@@ -214,7 +307,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
       }
   }
   if (bad) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
-  cluster_reduce<WM>(mx, W, wbuf, red, cl, OpMax());
+  cluster_reduce<WM>(mx, W, wbuf, red, par, cl, OpMax());
 
   // pass 2: sum_j exp(v - max) per window row; prior weight w and its sum
   const double denom_u = src.u_denom();
@@ -233,18 +326,14 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
       }
     const double norm = src.norm(row, j);
     if (!isfinite(norm) || norm < 0.0) badn = true;
-    const double u = src.u(j, denom_u);
-    const double pi_kn = pow_ref(norm + p.eps, -p.gamma);
-    const double pi_pos = exp(-p.beta * pow_ref(u, p.p_curve)) * pow_ref(1.0 - u + p.eps, p.eta);
-    const double wr = pi_kn * pi_pos;
+    const double wr = prior_w(p, norm, src.u(j, denom_u));
     if (!isfinite(wr) || wr < 0.0) badn = true;
     Bw[j] = wr;
     s2[WM] += wr;
   }
   if (badn) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
-  // pack the prior sum right after the W row sums
-  s2[W] = s2[WM];
-  cluster_reduce<WM + 1>(s2, W + 1, wbuf, red, cl, OpSum());
+  s2[W] = s2[WM];  // pack the prior sum right after the W row sums
+  cluster_reduce<WM + 1>(s2, W + 1, wbuf, red, par, cl, OpSum());
   const double sumw = s2[W];
   if (threadIdx.x == 0 && rank == 0) {
     for (int w = 0; w < W; ++w)
@@ -274,7 +363,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     A[j] = wt;
     s3[0] += wt;
   }
-  cluster_reduce<1>(s3, 1, wbuf, red, cl, OpSum());
+  cluster_reduce<1>(s3, 1, wbuf, red, par, cl, OpSum());
   const double sum2 = s3[0];
   if (threadIdx.x == 0 && rank == 0 && sum2 <= 0.0) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
 
@@ -289,7 +378,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     s4[1] += f * r;
     s4[2] += r * r;
   }
-  cluster_reduce<3>(s4, 3, wbuf, red, cl, OpSum());
+  cluster_reduce<3>(s4, 3, wbuf, red, par, cl, OpSum());
   const double ff = s4[0], fr = s4[1], rr = s4[2];
   const double denom = ff - 2.0 * fr + rr;
   double lambda = 0.0;
@@ -303,26 +392,53 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     const double s = (1.0 - lambda) * A[j] + lambda * Bw[j];
     A[j] = log(s + p.eps);
   }
+  cl.sync();
 }
 
-// Soft-NMS per head then cross-head exclusivity, one thread per (b, j).
+// ---------------------------------------------------------------------------
+// Stage B: soft-NMS per head, then cross-head exclusivity; one thread per
+// (b, j), the CTA's 256 positions x H heads (+ halo) staged in shared memory.
 template <bool kExp>
-__global__ void __launch_bounds__(256) sel_refine_kernel(const SelParams p) {
+__global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p) {
+  __shared__ double tile[16][kRefineT + 2 * kMaxNmsR];
   const int b = blockIdx.y;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.x * kRefineT;
   const Src<kExp> src(p, b);
   const int n = src.n;
+  if (j0 >= n) return;
+  const int R = p.nms_radius;
+  const bool staged = R <= kMaxNmsR;
+  if (staged) {
+    const int span = kRefineT + 2 * R;
+    for (int h = 0; h < p.H; ++h) {
+      const double* z = p.sa + (size_t)(b * p.H + h) * p.ld;
+      for (int t = threadIdx.x; t < span; t += kRefineT) {
+        const int j = j0 - R + t;
+        tile[h][t] = (j >= 0 && j < n) ? z[j] : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  const int idx = j0 + threadIdx.x;
   if (idx >= n) return;
+  const int lo = max(0, idx - R);
+  const int hi = min(n - 1, idx + R);
   double zn[16];
-  const int lo = max(0, idx - p.nms_radius);
-  const int hi = min(n - 1, idx + p.nms_radius);
 #pragma unroll
   for (int h = 0; h < 16; ++h) {
     if (h < p.H) {
-      const double* z = p.sa + (size_t)(b * p.H + h) * p.ld;
-      const double zj = z[idx];
-      double m = zj;
-      for (int i = lo; i <= hi; ++i) m = smax(m, z[i]);
+      double zj, m;
+      if (staged) {
+        const double* t = &tile[h][R + threadIdx.x - idx];  // t[j] = z[j] for j in [j0-R, j0+256+R)
+        zj = t[idx];
+        m = zj;
+        for (int i = lo; i <= hi; ++i) m = smax(m, t[i]);
+      } else {
+        const double* z = p.sa + (size_t)(b * p.H + h) * p.ld;
+        zj = z[idx];
+        m = zj;
+        for (int i = lo; i <= hi; ++i) m = smax(m, z[i]);
+      }
       const double gap = m - zj;
       zn[h] = zj - p.alpha_soft * gap;
     }
@@ -331,21 +447,30 @@ __global__ void __launch_bounds__(256) sel_refine_kernel(const SelParams p) {
 #pragma unroll
   for (int h = 1; h < 16; ++h)
     if (h < p.H) mxs = smax(mxs, zn[h]);
-  double e[16];
+  const bool t_one = (p.temperature == 1.0);
+  double e[16], x[16];
   double sum = 0.0;
 #pragma unroll
   for (int h = 0; h < 16; ++h)
     if (h < p.H) {
-      e[h] = exp((zn[h] - mxs) / p.temperature);
+      x[h] = t_one ? (zn[h] - mxs) : (zn[h] - mxs) / p.temperature;
+      e[h] = exp(x[h]);
       sum += e[h];
     }
+  // log(max(e_h / sum, eps)) = x_h - log(sum) unless the responsibility is clipped
+  const double ls = log(sum);
+  const double le = log(p.eps);
+  const double floor_e = p.eps * sum;
 #pragma unroll
   for (int h = 0; h < 16; ++h)
     if (h < p.H) {
-      const double r = e[h] / sum;
-      p.sb[(size_t)(b * p.H + h) * p.ld + idx] = zn[h] + p.alpha_cross * log(smax(r, p.eps));
+      const double lr = (e[h] >= floor_e) ? (x[h] - ls) : le;
+      p.sb[(size_t)(b * p.H + h) * p.ld + idx] = zn[h] + p.alpha_cross * lr;
     }
 }
+
+// ---------------------------------------------------------------------------
+// Stage C: top-k per row.
 
 // Order-preserving key: larger score -> larger key; -0.0 ties +0.0 as in the
 // reference comparator (selector.cpp:245 compares with != and >).
@@ -355,21 +480,23 @@ __device__ __forceinline__ unsigned long long okey(double x) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-template <bool kExp>
+// kSmem: the CTA's block of keys lives in dynamic shared memory (one global
+// read); otherwise every pass re-reads z from global/L2.
+template <bool kExp, bool kSmem>
 __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     sel_topk_kernel(const SelParams p) {
-  __shared__ uint32_t hist[kBins];
-  __shared__ uint32_t bsum[kBinsPerCta];
+  extern __shared__ unsigned long long skeys[];
+  __shared__ uint32_t hist[2][kBins];
+  __shared__ uint32_t bsum[2][kBinsPerCta];
+  __shared__ uint32_t slice_tot[2];
+  __shared__ int res_tb[2], res_cum[2];
   __shared__ unsigned long long wbuf[kWarps * 2];
-  __shared__ unsigned long long red[2];
-  __shared__ uint32_t slice_tot;
-  __shared__ int res_tb, res_above;
+  __shared__ unsigned long long red[2][2];
   __shared__ unsigned long long cta_tot;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int row = blockIdx.y;
-  const int b = row / p.H;
-  const Src<kExp> src(p, b);
+  const Src<kExp> src(p, row / p.H);
   const int n = src.n;
   const int K = p.K;
   int32_t* out = p.sel + (size_t)row * K;
@@ -383,41 +510,55 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     return;
   }
   const double* z = p.sb + (size_t)row * p.ld;
+  // this CTA's contiguous block of the row
+  const int chunk = (n + kCS - 1) / kCS;
+  const int c0 = rank * chunk, c1 = min(n, c0 + chunk);
+  const int len = max(0, c1 - c0);
+  auto key_at = [&](int i) -> unsigned long long {  // i relative to c0
+    return kSmem ? skeys[i] : okey(z[c0 + i]);
+  };
+  int par = 0;
 
-  // pass 0: key range
-  unsigned long long mm[1] = {~0ull}, MM[1] = {0ull};
-  for (int i = rank * kT + threadIdx.x; i < n; i += kCS * kT) {
-    const unsigned long long k = okey(z[i]);
+  // pass 0: stage keys, key range
+  unsigned long long mm[2] = {~0ull, ~0ull};  // min key, min ~key (= ~max key)
+  for (int i = threadIdx.x; i < len; i += kT) {
+    const unsigned long long k = okey(z[c0 + i]);
+    if (kSmem) skeys[i] = k;
     mm[0] = k < mm[0] ? k : mm[0];
-    MM[0] = k > MM[0] ? k : MM[0];
+    mm[1] = ~k < mm[1] ? ~k : mm[1];
   }
-  cluster_reduce<1>(mm, 1, wbuf, red, cl, OpMinU());
-  cluster_reduce<1>(MM, 1, wbuf, red, cl, OpMaxU());
+  cluster_reduce<2>(mm, 2, wbuf, red, par, cl, OpMinU());  // includes the smem-key barrier
+  const unsigned long long kmin = mm[0], kmax = ~mm[1];
 
-  // radix refinement: invariant T in [lo, lo + 2^bits); `above` keys > range
-  unsigned long long lo = mm[0];
-  int bits = (MM[0] == mm[0]) ? 0 : 64 - __clzll((long long)(MM[0] - mm[0]));
+  // radix refinement: invariant T in [lo, lo + 2^bits); `above` keys > range.
+  // Buffers alternate by pass; 2 cluster barriers per pass.
+  unsigned long long lo = kmin;
+  int bits = (kmax == kmin) ? 0 : 64 - __clzll((long long)(kmax - kmin));
   int above = 0;
+  int pb = 0;
+  for (int i = threadIdx.x; i < kBins; i += kT) hist[0][i] = 0;
+  __syncthreads();
   while (bits > 0) {
     const int shift = bits > 11 ? bits - 11 : 0;
     const int nb = 1 << (bits - shift);
-    for (int i = threadIdx.x; i < kBins; i += kT) hist[i] = 0;
-    __syncthreads();
-    for (int i = rank * kT + threadIdx.x; i < n; i += kCS * kT) {
-      const unsigned long long k = okey(z[i]);
+    uint32_t* hcur = hist[pb];
+    for (int i = threadIdx.x; i < len; i += kT) {
+      const unsigned long long k = key_at(i);
       if (k >= lo) {
         const unsigned long long d = (k - lo) >> shift;
-        if (d < (unsigned long long)nb) atomicAdd(&hist[d], 1u);
+        if (d < (unsigned long long)nb) atomicAdd(&hcur[d], 1u);
       }
     }
-    cl.sync();
+    cl.sync();  // (1) every CTA's histogram complete
+    // zero the other buffer for the next pass (its last readers passed barrier (1))
+    for (int i = threadIdx.x; i < kBins; i += kT) hist[pb ^ 1][i] = 0;
     uint32_t mine = 0;
     for (int bi = threadIdx.x; bi < kBinsPerCta; bi += kT) {
       const int gb = rank * kBinsPerCta + bi;
       uint32_t s = 0;
       if (gb < nb)
-        for (int r = 0; r < kCS; ++r) s += cl.map_shared_rank(hist, r)[gb];
-      bsum[bi] = s;
+        for (int r = 0; r < kCS; ++r) s += cl.map_shared_rank(hcur, r)[gb];
+      bsum[pb][bi] = s;
       mine += s;
     }
 #pragma unroll
@@ -427,51 +568,73 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     if (threadIdx.x == 0) {
       uint32_t t = 0;
       for (int w = 0; w < kWarps; ++w) t += (uint32_t)wbuf[w];
-      slice_tot = t;
+      slice_tot[pb] = t;
     }
-    cl.sync();
+    cl.sync();  // (2) merged slices + their totals published
+    // warp 0 of every CTA finds the threshold bucket (same answer cluster-wide):
+    // lanes read the 8 slice totals, then the owner slice's 256 bins (8 per
+    // lane) over DSMEM in parallel, scanning from the top bin down
     const int need_rem = K - above;
-    int own = 0, cum = 0;
-    for (int r = kCS - 1; r >= 0; --r) {
-      const int tr = (int)*cl.map_shared_rank(&slice_tot, r);
-      if (cum + tr >= need_rem) {
-        own = r;
-        break;
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int tr = lane < kCS ? (int)*cl.map_shared_rank(&slice_tot[pb], kCS - 1 - lane) : 0;
+      int inc = tr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
       }
-      cum += tr;
-    }
-    if (rank == own && threadIdx.x == 0) {
-      int c2 = cum, tb = rank * kBinsPerCta;
-      for (int bi = kBinsPerCta - 1; bi >= 0; --bi) {
-        if (c2 + (int)bsum[bi] >= need_rem) {
-          tb = rank * kBinsPerCta + bi;
-          break;
+      const unsigned m1 = __ballot_sync(0xffffffffu, lane < kCS && inc >= need_rem);
+      const int fl = m1 ? __ffs(m1) - 1 : kCS - 1;
+      const int own = kCS - 1 - fl;
+      const int cum = __shfl_sync(0xffffffffu, inc - tr, fl);  // keys in ranks above `own`
+      const uint32_t* ob = cl.map_shared_rank(&bsum[pb][0], own);
+      uint32_t bv[8];
+      int lsum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        bv[k] = ob[kBinsPerCta - 1 - (lane * 8 + k)];  // descending bins
+        lsum += (int)bv[k];
+      }
+      int inc2 = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc2, o);
+        if (lane >= o) inc2 += y;
+      }
+      const unsigned m2 = __ballot_sync(0xffffffffu, cum + inc2 >= need_rem);
+      const int fl2 = m2 ? __ffs(m2) - 1 : 31;
+      if (lane == fl2) {
+        int c2 = cum + inc2 - lsum;
+        int tb = own * kBinsPerCta + (kBinsPerCta - 1 - lane * 8 - 7);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (c2 + (int)bv[k] >= need_rem) {
+            tb = own * kBinsPerCta + (kBinsPerCta - 1 - (lane * 8 + k));
+            break;
+          }
+          c2 += (int)bv[k];
         }
-        c2 += (int)bsum[bi];
+        res_tb[pb] = tb;
+        res_cum[pb] = c2;
       }
-      res_tb = tb;
-      res_above = c2;
     }
-    cl.sync();
-    const int tb = *cl.map_shared_rank(&res_tb, own);
-    const int ab = *cl.map_shared_rank(&res_above, own);
-    above += ab;
+    __syncthreads();
+    const int tb = res_tb[pb];
+    above += res_cum[pb];  // keys in buckets above tb are above the threshold
     lo += (unsigned long long)tb << shift;
     bits = shift;
-    cl.sync();
+    pb ^= 1;
   }
   const unsigned long long T = lo;
   const int need = K - above;
 
-  // ordered emission: blocked ranges, packed (gt, eq) exclusive scan
-  const int chunk = (n + kCS - 1) / kCS;
-  const int c0 = rank * chunk, c1 = min(n, c0 + chunk);
-  const int len = max(0, c1 - c0);
+  // ordered emission: blocked sub-ranges, packed (gt, eq) exclusive scan
   const int E = (len + kT - 1) / kT;
-  const int e0 = c0 + threadIdx.x * E, e1 = min(c1, e0 + E);
+  const int e0 = threadIdx.x * E, e1 = min(len, e0 + E);
   unsigned long long cnt = 0;
   for (int i = e0; i < e1; ++i) {
-    const unsigned long long k = okey(z[i]);
+    const unsigned long long k = key_at(i);
     if (k > T) cnt += (1ull << 32);
     else if (k == T) cnt += 1ull;
   }
@@ -482,6 +645,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += y;
   }
+  __syncthreads();  // wbuf reuse
   if (lane == 31) wbuf[warp] = inc;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -498,12 +662,12 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
   for (int r = 0; r < rank; ++r) base += *cl.map_shared_rank(&cta_tot, r);
   int gt_b = (int)(base >> 32), eq_b = (int)(base & 0xffffffffu);
   for (int i = e0; i < e1; ++i) {
-    const unsigned long long k = okey(z[i]);
+    const unsigned long long k = key_at(i);
     if (k > T) {
-      out[gt_b + min(eq_b, need)] = src.pos(i);
+      out[gt_b + min(eq_b, need)] = src.pos(c0 + i);
       ++gt_b;
     } else if (k == T) {
-      if (eq_b < need) out[gt_b + eq_b] = src.pos(i);
+      if (eq_b < need) out[gt_b + eq_b] = src.pos(c0 + i);
       ++eq_b;
     }
   }
@@ -526,21 +690,44 @@ void fill_cfg(SelParams& p, const sfi_selector_params& prm) {
 }
 
 template <bool kExp>
-cudaError_t run3(const SelParams& p, int rows, int refine_blocks, int batches, cudaStream_t st,
+cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st) {
+  const int chunk = (n_max + kCS - 1) / kCS;
+  const dim3 gc(kCS, (unsigned)rows);
+  if (chunk <= kTopkSmemKeys) {
+    const size_t smem = (size_t)std::max(chunk, 1) * sizeof(unsigned long long);
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(sel_topk_kernel<kExp, true>),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kTopkSmemKeys * (int)sizeof(unsigned long long));
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    sel_topk_kernel<kExp, true><<<gc, kT, smem, st>>>(p);
+  } else {
+    sel_topk_kernel<kExp, false><<<gc, kT, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+template <bool kExp>
+cudaError_t run3(const SelParams& p, int rows, int n_max, int batches, cudaStream_t st,
                  int* launches) {
   const dim3 gc(kCS, (unsigned)rows);
-  if (p.W > 1)
+  if (p.W == 1 && p.alpha == 1.0)
+    sel_fuse_fast_kernel<kExp><<<gc, kT, 0, st>>>(p);
+  else if (p.W > 1)
     sel_fuse_kernel<kExp, kMaxW><<<gc, kT, 0, st>>>(p);
   else
     sel_fuse_kernel<kExp, 1><<<gc, kT, 0, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  sel_refine_kernel<kExp><<<dim3(refine_blocks, batches), 256, 0, st>>>(p);
+  sel_refine_kernel<kExp><<<dim3((n_max + kRefineT - 1) / kRefineT, batches), kRefineT, 0, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  sel_topk_kernel<kExp><<<gc, kT, 0, st>>>(p);
+  e = launch_topk<kExp>(p, rows, n_max, st);
   if (launches) *launches += 3;
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace
@@ -568,7 +755,7 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
   p.K = s.k_budget;
   fill_cfg(p, prm);
   if (s.n_kv_heads > 16) return cudaErrorInvalidValue;
-  return run3<false>(p, (int)slices, (s.max_positions + 255) / 256, s.batch, st, launches);
+  return run3<false>(p, (int)slices, s.max_positions, s.batch, st, launches);
 }
 
 cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* logits, const double* norms,
@@ -593,7 +780,7 @@ cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* l
   p.K = K;
   fill_cfg(p, prm);
   if (H > 16 || W > kMaxW || W < 1) return cudaErrorInvalidValue;
-  return run3<true>(p, H, (n + 255) / 256, 1, st, launches);
+  return run3<true>(p, H, n, 1, st, launches);
 }
 
 cudaError_t launch_topk_explicit(int rows, int n, int K, const double* scores, const int32_t* allowed,
@@ -610,9 +797,8 @@ cudaError_t launch_topk_explicit(int rows, int n, int K, const double* scores, c
   p.H = 1;
   p.Lmax = n;
   p.K = K;
-  sel_topk_kernel<true><<<dim3(kCS, rows), kT, 0, st>>>(p);
   if (launches) *launches += 1;
-  return cudaGetLastError();
+  return launch_topk<true>(p, rows, n, st);
 }
 
 }  // namespace sfi_impl

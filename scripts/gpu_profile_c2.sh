@@ -1,0 +1,8 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
+timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; tail -5 gpurun_out/bench_c2.err; cat gpurun_out/bench_c2.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1; echo ncu1 $?
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 72 -c 1 -o gpurun_out/prof_sparse python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-graph > gpurun_out/ncu2.log 2>&1; echo ncu2 $?
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 0 -c 1 -o gpurun_out/prof_dense python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-graph > gpurun_out/ncu3.log 2>&1; echo ncu3 $?
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:sel_ -s 0 -c 3 -o gpurun_out/prof_selector python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-graph > gpurun_out/ncu4.log 2>&1; echo ncu4 $?
+ls -la gpurun_out

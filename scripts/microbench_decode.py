@@ -1,0 +1,100 @@
+"""Per-kernel microbenchmark on the C2 shapes (tuning aid, not the bench).
+
+    SFI_DECODE_TRACE=1 [SFI_DECODE_CTAS=n] python scripts/microbench_decode.py [--layers 4]
+
+Times sparse decode, dense decode, the three Selector kernels and compact build
+with CUDA events, and (with SFI_DECODE_TRACE) prints the per-CTA timeline of
+the last sparse / dense launch: prologue, first-tile latency, busy time.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2603_12038_b200 as sfi  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--layers", type=int, default=4)
+ap.add_argument("--batch", type=int, default=8)
+ap.add_argument("--ctx", type=int, default=32768)
+ap.add_argument("--hq", type=int, default=32)
+ap.add_argument("--iters", type=int, default=20)
+args = ap.parse_args()
+
+L, B, H, Hq, d = args.layers, args.batch, 8, args.hq, 128
+ctx = args.ctx
+c = sfi.SfiCache(L, B, H, Hq, d, ctx + 64, 4, 2048, 256)
+c.fill_synthetic(7, ctx)
+c.set_lengths([ctx] * B, [4] * B)
+c.step_advance()
+q = torch.randn(L, B, Hq, d, device="cuda")
+out = torch.zeros_like(q)
+logits = c.pooled_logits
+prm = sfi.SelectorParams()
+for l in range(L):
+    c.dense_decode(l, q[l], out[l], logits, 0)
+    c.selector(l, logits, prm)
+    c.compact_build(l, True)
+torch.cuda.synchronize()
+c.check_errors()
+lib = C.CDLL(sfi.LIBRARY_PATH)
+
+
+def timeit(fn, iters):
+    s = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for i in range(iters):
+        ev[i][0].record(s)
+        fn(i)
+        ev[i][1].record(s)
+    torch.cuda.synchronize()
+    ts = [a.elapsed_time(b) * 1e3 for a, b in ev][2:]
+    return float(np.median(ts)), float(np.min(ts))
+
+
+def trace(tag):
+    if not os.environ.get("SFI_DECODE_TRACE"):
+        return
+    buf = (C.c_int64 * (16 * 1024))()
+    n = lib.sfi_debug_decode_trace(buf, 1024)
+    a = np.frombuffer(buf, dtype=np.int64)[: 16 * n].reshape(n, 16).astype(np.float64)
+    live = a[a[:, 0] > 0]
+    t0 = live[:, 0].min()
+    start, pro, first, end = (live[:, i] - t0 for i in range(4))
+    busy = end - start
+    print(f"[{tag}] ctas={n} live={len(live)} launch spread={start.max()/1e3:.2f}us "
+          f"prologue med={np.median(pro-start)/1e3:.2f}us first-tile med={np.median(first-pro)/1e3:.2f}us "
+          f"busy med={np.median(busy)/1e3:.2f} max={busy.max()/1e3:.2f} min={busy.min()/1e3:.2f}us "
+          f"kernel span={end.max()/1e3:.2f}us emissions mean={live[:,4].mean():.2f} tiles mean={live[:,5].mean():.1f}")
+    print(f"   emission ns per CTA: total mean={live[:,7].mean():.0f} max={live[:,7].max():.0f}; "
+          f"combine mean={live[:,8].mean():.0f}; partial+fence mean={live[:,9].mean():.0f} max={live[:,9].max():.0f}; "
+          f"bar+atomic mean={live[:,10].mean():.0f} max={live[:,10].max():.0f}")
+    slow = np.argsort(-end)[:5]
+    for i in slow:
+        print(f"   slow cta: start={start[i]/1e3:.2f} pro={pro[i]/1e3:.2f} first={first[i]/1e3:.2f} "
+              f"end={end[i]/1e3:.2f} emis={live[i,4]:.0f} tiles={live[i,5]:.0f} sm={live[i,6]:.0f} "
+              f"emit={live[i,7]/1e3:.2f} comb={live[i,8]/1e3:.2f} fence={live[i,9]/1e3:.2f} bar={live[i,10]/1e3:.2f}us")
+
+
+res = {}
+res["sparse_us"] = timeit(lambda i: c.sparse_decode(i % L, q[i % L], out[i % L]), args.iters)
+trace("sparse")
+res["dense_us"] = timeit(lambda i: c.dense_decode(i % L, q[i % L], out[i % L], logits, 0), max(6, args.iters // 3))
+trace("dense")
+res["selector_us"] = timeit(lambda i: c.selector(i % L, logits, prm), 10)
+res["compact_us"] = timeit(lambda i: c.compact_build(i % L, False), 10)
+k = torch.randn(B, H, d, device="cuda").bfloat16()
+res["ring_append_us"] = timeit(lambda i: c.ring_append(i % L, k, k), 10)
+S = 256 + 4 + 2048
+sp_bytes = B * H * S * 4 * d
+de_bytes = B * H * (ctx + 1) * 4 * d
+res["sparse_GBs"] = sp_bytes / res["sparse_us"][0] / 1e3
+res["dense_GBs"] = de_bytes / res["dense_us"][0] / 1e3
+print(json.dumps(res))
+c.check_errors()
