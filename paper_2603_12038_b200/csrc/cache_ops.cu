@@ -20,6 +20,8 @@ namespace {
 // prefix_len += advance; recent_len = clamp(L - n_sink_b, 0, R) (slide_recent)
 __global__ void advance_kernel(int32_t* prefix_len, const int32_t* n_sink_b, int32_t* recent_len,
                                int B, int Lmax, int R, int advance, uint32_t* err) {
+  griddep_wait();
+  griddep_launch();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int L = prefix_len[b];
@@ -52,6 +54,8 @@ struct AppendParams {
 // bit-identical to the reference's sequential fp64 loop.
 __global__ void append_kernel(const AppendParams p) {
   __shared__ float xs[128];
+  griddep_wait();
+  griddep_launch();
   const int i = blockIdx.x;
   const int bh = blockIdx.y;
   const int b = bh / p.H;
@@ -104,6 +108,8 @@ struct CompactParams {
 
 // One warp per compact row: lanes 0-15 move the K row, lanes 16-31 the V row.
 __global__ void compact_kernel(const CompactParams p) {
+  griddep_wait();
+  griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.y;
   const int b = bh / p.H;
@@ -206,10 +212,9 @@ __global__ void fill_norms_kernel(const FillParams p) {
 }  // namespace
 
 cudaError_t launch_step_advance(const sfi_shape& s, const sfi_cache& c, cudaStream_t st) {
-  advance_kernel<<<(s.batch + 127) / 128, 128, 0, st>>>(c.prefix_len, c.n_sink_b, c.recent_len,
-                                                         s.batch, s.max_positions, s.n_recent, 1,
-                                                         c.error_flags);
-  return cudaGetLastError();
+  return launch_k(advance_kernel, dim3((s.batch + 127) / 128), dim3(128), 0, st, c.prefix_len,
+                  (const int32_t*)c.n_sink_b, c.recent_len, s.batch, s.max_positions, s.n_recent, 1,
+                  c.error_flags);
 }
 
 cudaError_t launch_set_recent_rule(const sfi_shape& s, const sfi_cache& c, cudaStream_t st) {
@@ -240,9 +245,7 @@ cudaError_t launch_append(const sfi_shape& s, const sfi_cache& c, int layer, int
   p.R = s.n_recent;
   p.count = count;
   p.block_mode = block_mode;
-  dim3 grid(count, s.batch * s.n_kv_heads);
-  append_kernel<<<grid, s.head_dim, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_k(append_kernel, dim3(count, s.batch * s.n_kv_heads), dim3(s.head_dim), 0, st, p);
 }
 
 cudaError_t launch_compact_build(const sfi_shape& s, const sfi_cache& c, int layer, int rebuild_ring,
@@ -271,8 +274,7 @@ cudaError_t launch_compact_build(const sfi_shape& s, const sfi_cache& c, int lay
   constexpr int kWarps = 8;
   dim3 grid((rows + kWarps - 1) / kWarps, s.batch * s.n_kv_heads);
   if (rows == 0) return cudaSuccess;
-  compact_kernel<<<grid, kWarps * 32, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_k(compact_kernel, grid, dim3(kWarps * 32), 0, st, p);
 }
 
 cudaError_t launch_fill_synthetic(const sfi_shape& s, const sfi_cache& c, uint64_t seed, int len,

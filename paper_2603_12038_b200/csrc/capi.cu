@@ -189,6 +189,14 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
 
 namespace sfi_impl {
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SFI_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 long long* decode_trace_buffer() {
   static long long* buf = nullptr;
   if (!buf && cudaMalloc(&buf, sizeof(long long) * 16 * kMaxCtas) != cudaSuccess) buf = nullptr;

@@ -97,6 +97,20 @@ __device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Every kernel of the step is launched with programmatic stream serialization.
+// Rule that keeps stream order transitive: a kernel first waits for its
+// predecessor grid (griddep_wait) before touching any data produced upstream,
+// and only then lets its own dependents launch (griddep_launch). The dependent
+// therefore starts (prologue, barrier init, descriptor prefetch) while this
+// kernel runs, but can never observe an upstream result early.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

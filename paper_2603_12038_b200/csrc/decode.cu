@@ -171,6 +171,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     trace[6] = smid();
   }
 
+  // PDL: lengths, selections and the freshly appended ring row are all
+  // produced upstream in the same stream
+  griddep_wait();
+  griddep_launch();
+
   // ---- per-slice tile counts -> exclusive prefix (every CTA, S <= kMaxSlices) ----
   for (int s = threadIdx.x; s < S; s += kThreads) {
     const Slice sl = make_slice(p, s, blockIdx.x == 0);
@@ -641,8 +646,7 @@ cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const C
     if (e != cudaSuccess) return e;
     cap = smem;
   }
-  fn<<<ctas, kThreads, smem, stream>>>(tmk, tmv, p);
-  return cudaGetLastError();
+  return launch_k(fn, dim3(ctas), dim3(kThreads), (size_t)smem, stream, tmk, tmv, p);
 }
 
 }  // namespace sfi_impl

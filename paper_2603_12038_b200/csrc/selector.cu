@@ -62,7 +62,8 @@ constexpr int kBinsPerCta = kBins / kCS;
 constexpr int kMaxW = 16;   // observation window rows (prefill window_prefill = 16)
 constexpr int kRefineT = 256;
 constexpr int kMaxNmsR = 16;  // smem halo of the refine kernel
-constexpr int kTopkSmemKeys = 24 * 1024;  // keys per CTA kept in shared memory
+constexpr int kTopkSmemKeys = 22 * 1024;  // keys per CTA kept in shared memory
+constexpr int kCandCap = 512;             // threshold-bucket size resolved by direct ranking
 constexpr double kMaskedLogit = -1e30;  // selector.hpp:42
 
 struct SelParams {
@@ -201,8 +202,10 @@ __device__ __forceinline__ void cluster_reduce(T (&v)[NV], int nv, T* wbuf, T (*
 // ---------------------------------------------------------------------------
 // Stage A, decode fast path: W = 1, alpha = 1.
 template <bool kExp>
-__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
     sel_fuse_fast_kernel(const SelParams p) {
+  griddep_wait();  // PDL: logits come from the preceding dense decode
+  griddep_launch();
   __shared__ double wbuf[kWarps * 5];
   __shared__ double red[2][5];
   cg::cluster_group cl = cg::this_cluster();
@@ -234,20 +237,33 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
   const double denom_u = src.u_denom();
   double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   bool badn = false;
-  for (int j = lo + threadIdx.x; j < hi; j += kT) {
-    const double v = src.logit(row, 0, j);
-    const double pj = (v <= kMaskedLogit) ? 0.0 : exp(v - mx);
-    const double norm = src.norm(row, j);
-    if (!isfinite(norm) || norm < 0.0) badn = true;
-    const double wr = prior_w(p, norm, src.u(j, denom_u));
-    if (!isfinite(wr) || wr < 0.0) badn = true;
-    A[j] = pj;
-    Bw[j] = wr;
-    s[0] += pj;
-    s[1] += wr;
-    s[2] += pj * pj;
-    s[3] += pj * wr;
-    s[4] += wr * wr;
+  constexpr int kU = 2;  // loads of kU iterations are issued before any use
+  for (int j0 = lo + threadIdx.x; j0 < hi; j0 += kU * kT) {
+    double vv[kU], nn[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * kT;
+      vv[u] = j < hi ? src.logit(row, 0, j) : 0.0;
+      nn[u] = j < hi ? src.norm(row, j) : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * kT;
+      if (j >= hi) break;
+      const double v = vv[u];
+      const double pj = (v <= kMaskedLogit) ? 0.0 : exp(v - mx);
+      const double norm = nn[u];
+      if (!isfinite(norm) || norm < 0.0) badn = true;
+      const double wr = prior_w(p, norm, src.u(j, denom_u));
+      if (!isfinite(wr) || wr < 0.0) badn = true;
+      A[j] = pj;
+      Bw[j] = wr;
+      s[0] += pj;
+      s[1] += wr;
+      s[2] += pj * pj;
+      s[3] += pj * wr;
+      s[4] += wr * wr;
+    }
   }
   if (badn) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
   cluster_reduce<5>(s, 5, wbuf, red, par, cl, OpSum());
@@ -267,7 +283,20 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
   const double a = (1.0 - lambda) * c1, bb = lambda * c2;
 
   // pass 3: z = log((1 - lambda) f + lambda r + eps)
-  for (int j = lo + threadIdx.x; j < hi; j += kT) A[j] = log(a * A[j] + bb * Bw[j] + p.eps);
+  for (int j0 = lo + threadIdx.x; j0 < hi; j0 += kU * kT) {
+    double pa[kU], wb[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * kT;
+      pa[u] = j < hi ? A[j] : 0.0;
+      wb[u] = j < hi ? Bw[j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * kT;
+      if (j < hi) A[j] = log(a * pa[u] + bb * wb[u] + p.eps);
+    }
+  }
   cl.sync();  // remote reads of `red` done before any CTA exits
 }
 
@@ -275,6 +304,8 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
 template <bool kExp, int WM>
 __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     sel_fuse_kernel(const SelParams p) {
+  griddep_wait();
+  griddep_launch();
   constexpr int kNV = (WM + 1) > 3 ? (WM + 1) : 3;
   __shared__ double wbuf[kWarps * kNV];
   __shared__ double red[2][kNV];
@@ -398,9 +429,11 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
 // ---------------------------------------------------------------------------
 // Stage B: soft-NMS per head, then cross-head exclusivity; one thread per
 // (b, j), the CTA's 256 positions x H heads (+ halo) staged in shared memory.
-template <bool kExp>
+template <bool kExp, int kH>
 __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p) {
-  __shared__ double tile[16][kRefineT + 2 * kMaxNmsR];
+  griddep_wait();
+  griddep_launch();
+  __shared__ double tile[kH][kRefineT + 2 * kMaxNmsR];
   const int b = blockIdx.y;
   const int j0 = blockIdx.x * kRefineT;
   const Src<kExp> src(p, b);
@@ -408,14 +441,26 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   if (j0 >= n) return;
   const int R = p.nms_radius;
   const bool staged = R <= kMaxNmsR;
+  // kH = 16 also serves head counts that are not a power of two (runtime guard)
+  const int Hr = kH == 16 ? p.H : kH;
   if (staged) {
+    // every thread stages column t and t + 256 (halo) of all heads; all loads
+    // are issued before the first shared store
     const int span = kRefineT + 2 * R;
-    for (int h = 0; h < p.H; ++h) {
-      const double* z = p.sa + (size_t)(b * p.H + h) * p.ld;
-      for (int t = threadIdx.x; t < span; t += kRefineT) {
-        const int j = j0 - R + t;
-        tile[h][t] = (j >= 0 && j < n) ? z[j] : 0.0;
-      }
+    const int t0 = threadIdx.x, t1 = threadIdx.x + kRefineT;
+    const int ja = j0 - R + t0, jb = j0 - R + t1;
+    const bool oka = ja >= 0 && ja < n, okb = t1 < span && jb < n;
+    double va[kH], vb[kH];
+#pragma unroll
+    for (int h = 0; h < kH; ++h) {
+      const double* z = p.sa + (size_t)(b * p.H + (h < Hr ? h : 0)) * p.ld;
+      va[h] = (h < Hr && oka) ? z[ja] : 0.0;
+      vb[h] = (h < Hr && okb) ? z[jb] : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < kH; ++h) {
+      tile[h][t0] = va[h];
+      if (t1 < span) tile[h][t1] = vb[h];
     }
     __syncthreads();
   }
@@ -423,10 +468,11 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   if (idx >= n) return;
   const int lo = max(0, idx - R);
   const int hi = min(n - 1, idx + R);
-  double zn[16];
+  double zn[kH];
 #pragma unroll
-  for (int h = 0; h < 16; ++h) {
-    if (h < p.H) {
+  for (int h = 0; h < kH; ++h) {
+    zn[h] = 0.0;
+    if (h < Hr) {
       double zj, m;
       if (staged) {
         const double* t = &tile[h][R + threadIdx.x - idx];  // t[j] = z[j] for j in [j0-R, j0+256+R)
@@ -445,14 +491,14 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   }
   double mxs = zn[0];
 #pragma unroll
-  for (int h = 1; h < 16; ++h)
-    if (h < p.H) mxs = smax(mxs, zn[h]);
+  for (int h = 1; h < kH; ++h)
+    if (h < Hr) mxs = smax(mxs, zn[h]);
   const bool t_one = (p.temperature == 1.0);
-  double e[16], x[16];
+  double e[kH], x[kH];
   double sum = 0.0;
 #pragma unroll
-  for (int h = 0; h < 16; ++h)
-    if (h < p.H) {
+  for (int h = 0; h < kH; ++h)
+    if (h < Hr) {
       x[h] = t_one ? (zn[h] - mxs) : (zn[h] - mxs) / p.temperature;
       e[h] = exp(x[h]);
       sum += e[h];
@@ -462,8 +508,8 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   const double le = log(p.eps);
   const double floor_e = p.eps * sum;
 #pragma unroll
-  for (int h = 0; h < 16; ++h)
-    if (h < p.H) {
+  for (int h = 0; h < kH; ++h)
+    if (h < Hr) {
       const double lr = (e[h] >= floor_e) ? (x[h] - ls) : le;
       p.sb[(size_t)(b * p.H + h) * p.ld + idx] = zn[h] + p.alpha_cross * lr;
     }
@@ -485,11 +531,17 @@ __device__ __forceinline__ unsigned long long okey(double x) {
 template <bool kExp, bool kSmem>
 __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     sel_topk_kernel(const SelParams p) {
+  griddep_wait();
+  griddep_launch();
   extern __shared__ unsigned long long skeys[];
   __shared__ uint32_t hist[2][kBins];
   __shared__ uint32_t bsum[2][kBinsPerCta];
   __shared__ uint32_t slice_tot[2];
-  __shared__ int res_tb[2], res_cum[2];
+  __shared__ int res_tb[2], res_cum[2], res_cnt[2];
+  __shared__ unsigned long long cand[kCandCap];       // this CTA's threshold-bucket keys
+  __shared__ int ncand;
+  __shared__ unsigned long long res_T;
+  __shared__ int res_gt;
   __shared__ unsigned long long wbuf[kWarps * 2];
   __shared__ unsigned long long red[2][2];
   __shared__ unsigned long long cta_tot;
@@ -608,15 +660,18 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
         int c2 = cum + inc2 - lsum;
         int tb = own * kBinsPerCta + (kBinsPerCta - 1 - lane * 8 - 7);
 #pragma unroll
+        int cnt = 0;
         for (int k = 0; k < 8; ++k) {
           if (c2 + (int)bv[k] >= need_rem) {
             tb = own * kBinsPerCta + (kBinsPerCta - 1 - (lane * 8 + k));
+            cnt = (int)bv[k];
             break;
           }
           c2 += (int)bv[k];
         }
         res_tb[pb] = tb;
         res_cum[pb] = c2;
+        res_cnt[pb] = cnt;
       }
     }
     __syncthreads();
@@ -625,6 +680,48 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     lo += (unsigned long long)tb << shift;
     bits = shift;
     pb ^= 1;
+    if (bits > 0 && res_cnt[pb ^ 1] <= kCandCap) {
+      // Candidate shortcut: the threshold bucket [lo, lo + 2^bits) holds few
+      // keys; gather them and rank them directly instead of more radix passes.
+      if (threadIdx.x == 0) ncand = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < len; i += kT) {
+        const unsigned long long k = key_at(i);
+        if (k >= lo && ((k - lo) >> bits) == 0ull) cand[atomicAdd(&ncand, 1)] = k;
+      }
+      cl.sync();  // every CTA's candidates complete
+      if (rank == 0) {
+        // gather all candidates (total <= kCandCap) into call[], CTA order; call
+        // aliases the histogram buffer of the pass just finished (no reader left)
+        unsigned long long* call = reinterpret_cast<unsigned long long*>(hist[pb ^ 1]);
+        int off = 0;
+        for (int r = 0; r < kCS; ++r) {
+          const int nr = *cl.map_shared_rank(&ncand, r);
+          const unsigned long long* src = cl.map_shared_rank(cand, r);
+          for (int i = threadIdx.x; i < nr; i += kT) call[off + i] = src[i];
+          off += nr;
+        }
+        __syncthreads();
+        // T = the need-th largest: #(> T) < need <= #(>= T)
+        const int need_rem2 = K - above;
+        for (int i = threadIdx.x; i < off; i += kT) {
+          const unsigned long long v = call[i];
+          int gt = 0, ge = 0;
+          for (int j = 0; j < off; ++j) {
+            gt += call[j] > v;
+            ge += call[j] >= v;
+          }
+          if (gt < need_rem2 && ge >= need_rem2) {  // same (T, gt) for all ties
+            res_T = v;
+            res_gt = gt;
+          }
+        }
+      }
+      cl.sync();  // rank 0's answer published
+      lo = *cl.map_shared_rank(&res_T, 0);
+      above += *cl.map_shared_rank(&res_gt, 0);
+      bits = 0;
+    }
   }
   const unsigned long long T = lo;
   const int need = K - above;
@@ -675,6 +772,280 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
   cl.sync();
 }
 
+// Single-CTA top-k for rows of up to kTopkCtaMax positions: no cluster
+// barriers. The high 32 bits of every order-preserving key live in shared
+// memory; radix passes (11-bit digits) and the candidate ranking run on them,
+// and the full 64-bit key is read back only for elements that tie with the
+// threshold on the high word. Same output contract as sel_topk_kernel.
+constexpr int kTopkCtaT = 1024;
+constexpr int kTopkCtaMax = 48 * 1024;
+
+template <bool kExp>
+__global__ void __launch_bounds__(kTopkCtaT) sel_topk_cta_kernel(const SelParams p) {
+  griddep_wait();
+  griddep_launch();
+  extern __shared__ uint32_t shi[];              // [n] high words
+  __shared__ uint32_t hist[kBins];
+  __shared__ unsigned long long cand[kCandCap];  // full keys of threshold-bucket elements
+  __shared__ uint32_t wred[32][2];
+  __shared__ int s_ncand, s_tb, s_cum, s_cnt, s_gt;
+  __shared__ unsigned long long s_T;
+  __shared__ unsigned long long wtot[32];
+  constexpr int kW = kTopkCtaT / 32;
+  const int row = blockIdx.x;
+  const Src<kExp> src(p, row / p.H);
+  const int n = src.n;
+  const int K = p.K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* out = p.sel + (size_t)row * K;
+  if (n <= 0 || K == 0) {
+    if (threadIdx.x == 0) p.n_sel[row] = 0;
+    return;
+  }
+  if (n <= K) {
+    for (int i = threadIdx.x; i < n; i += kTopkCtaT) out[i] = src.pos(i);
+    if (threadIdx.x == 0) p.n_sel[row] = n;
+    return;
+  }
+  const double* z = p.sb + (size_t)row * p.ld;
+  // pass 0: high words into smem + their range
+  uint32_t hmin = 0xffffffffu, hmax = 0u;
+  constexpr int kLU = 8;  // loads in flight per thread
+  for (int i0 = threadIdx.x; i0 < n; i0 += kLU * kTopkCtaT) {
+    double zv[kLU];
+#pragma unroll
+    for (int u = 0; u < kLU; ++u) {
+      const int i = i0 + u * kTopkCtaT;
+      zv[u] = i < n ? z[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kLU; ++u) {
+      const int i = i0 + u * kTopkCtaT;
+      if (i < n) {
+        const uint32_t h = (uint32_t)(okey(zv[u]) >> 32);
+        shi[i] = h;
+        hmin = min(hmin, h);
+        hmax = max(hmax, h);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hmin = min(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
+    hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+  }
+  if (lane == 0) {
+    wred[warp][0] = hmin;
+    wred[warp][1] = hmax;
+  }
+  __syncthreads();
+  hmin = wred[0][0];
+  hmax = wred[0][1];
+  for (int w = 1; w < kW; ++w) {
+    hmin = min(hmin, wred[w][0]);
+    hmax = max(hmax, wred[w][1]);
+  }
+  // radix over the high word: invariant threshold high word in [lo, lo + 2^bits)
+  uint32_t lo = hmin;
+  int bits = (hmax == hmin) ? 0 : 32 - __clz((int)(hmax - hmin));
+  int above = 0;
+  bool resolved = false;
+  unsigned long long T = 0;
+  while (true) {
+    // candidate shortcut (also the exit once the high word is pinned)
+    int cnt_range;
+    {
+      // count of keys with high word in the current range (cheap smem pass)
+      int c = 0;
+      for (int i = threadIdx.x; i < n; i += kTopkCtaT) {
+        const uint32_t h = shi[i];
+        c += (h >= lo && (bits >= 32 || ((h - lo) >> bits) == 0u));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      __syncthreads();
+      if (lane == 0) wred[warp][0] = (uint32_t)c;
+      __syncthreads();
+      cnt_range = 0;
+      for (int w = 0; w < kW; ++w) cnt_range += (int)wred[w][0];
+    }
+    if (cnt_range <= kCandCap) {
+      if (threadIdx.x == 0) s_ncand = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += kTopkCtaT) {
+        const uint32_t h = shi[i];
+        if (h >= lo && (bits >= 32 || ((h - lo) >> bits) == 0u)) cand[atomicAdd(&s_ncand, 1)] = okey(z[i]);
+      }
+      __syncthreads();
+      const int nc = s_ncand;
+      const int need_rem = K - above;
+      for (int i = threadIdx.x; i < nc; i += kTopkCtaT) {
+        const unsigned long long v = cand[i];
+        int gt = 0, ge = 0;
+        for (int j = 0; j < nc; ++j) {
+          gt += cand[j] > v;
+          ge += cand[j] >= v;
+        }
+        if (gt < need_rem && ge >= need_rem) {
+          s_T = v;
+          s_gt = gt;
+        }
+      }
+      __syncthreads();
+      T = s_T;
+      above += s_gt;
+      resolved = true;
+      break;
+    }
+    if (bits == 0) break;  // > kCandCap keys share one high word: exact pass below
+    const int shift = bits > 11 ? bits - 11 : 0;
+    const int nb = 1 << (bits - shift);
+    for (int i = threadIdx.x; i < kBins; i += kTopkCtaT) hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kTopkCtaT) {
+      const uint32_t h = shi[i];
+      if (h >= lo) {
+        const uint32_t d = (h - lo) >> shift;
+        if (d < (uint32_t)nb) atomicAdd(&hist[d], 1u);
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // threshold bucket, scanning from the top bin down (64 bins per lane)
+      const int need_rem = K - above;
+      int lsum = 0;
+      for (int k = 0; k < kBins / 32; ++k) lsum += (int)hist[kBins - 1 - (lane * (kBins / 32) + k)];
+      int inc = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, inc >= need_rem);
+      const int fl = m ? __ffs(m) - 1 : 31;
+      if (lane == fl) {
+        int c2 = inc - lsum, tb = 0, cnt = 0;
+        for (int k = 0; k < kBins / 32; ++k) {
+          const int bi = kBins - 1 - (lane * (kBins / 32) + k);
+          const int c = (int)hist[bi];
+          if (c2 + c >= need_rem) {
+            tb = bi;
+            cnt = c;
+            break;
+          }
+          c2 += c;
+        }
+        s_tb = tb;
+        s_cum = c2;
+        s_cnt = cnt;
+      }
+    }
+    __syncthreads();
+    above += s_cum;
+    lo += (uint32_t)s_tb << shift;
+    bits = shift;
+    __syncthreads();
+  }
+  if (!resolved) {
+    // Rare: more than kCandCap keys share the threshold high word `lo`.
+    // Resolve the low word by radix passes over those elements (global reads).
+    uint32_t llo = 0;
+    int lbits = 32;
+    while (lbits > 0) {
+      const int shift = lbits > 11 ? lbits - 11 : 0;
+      const int nb = 1 << (lbits - shift);
+      for (int i = threadIdx.x; i < kBins; i += kTopkCtaT) hist[i] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += kTopkCtaT) {
+        if (shi[i] != lo) continue;
+        const uint32_t l = (uint32_t)okey(z[i]);
+        if (l >= llo) {
+          const uint32_t d = (l - llo) >> shift;
+          if (d < (uint32_t)nb) atomicAdd(&hist[d], 1u);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int need_rem = K - above;
+        int c2 = 0, tb = 0;
+        for (int bi = nb - 1; bi >= 0; --bi) {
+          if (c2 + (int)hist[bi] >= need_rem) {
+            tb = bi;
+            break;
+          }
+          c2 += (int)hist[bi];
+        }
+        s_tb = tb;
+        s_cum = c2;
+      }
+      __syncthreads();
+      above += s_cum;
+      llo += (uint32_t)s_tb << shift;
+      lbits = shift;
+      __syncthreads();
+    }
+    T = ((unsigned long long)lo << 32) | llo;
+  }
+  const int need = K - above;
+  const uint32_t Th = (uint32_t)(T >> 32);
+
+  // ordered emission: blocked ranges, packed (gt, eq) exclusive scan
+  const int E = (n + kTopkCtaT - 1) / kTopkCtaT;
+  const int e0 = threadIdx.x * E, e1 = min(n, e0 + E);
+  auto cls = [&](int i) -> int {  // 2: > T, 1: == T, 0: < T
+    const uint32_t h = shi[i];
+    if (h != Th) return h > Th ? 2 : 0;
+    const unsigned long long k = okey(z[i]);
+    return k > T ? 2 : (k == T ? 1 : 0);
+  };
+  // classify this thread's E (<= 48) elements once; reads are rotated by the
+  // thread index so a warp's 32 threads hit 32 different banks
+  const int len = max(0, e1 - e0);
+  unsigned long long gtm = 0, eqm = 0;  // bit k: element e0 + k
+  {
+    const int rot = len ? (int)(threadIdx.x % (unsigned)len) : 0;
+    for (int kk = 0; kk < len; ++kk) {
+      int k = kk + rot;
+      if (k >= len) k -= len;
+      const int c = cls(e0 + k);
+      if (c == 2) gtm |= 1ull << k;
+      else if (c == 1) eqm |= 1ull << k;
+    }
+  }
+  const unsigned long long cnt = ((unsigned long long)__popcll(gtm) << 32) | (unsigned long long)__popcll(eqm);
+  unsigned long long inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wtot[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (int w = 0; w < kW; ++w) {
+      const unsigned long long t = wtot[w];
+      wtot[w] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  const unsigned long long base = wtot[warp] + (inc - cnt);
+  int gt_b = (int)(base >> 32), eq_b = (int)(base & 0xffffffffu);
+  unsigned long long sel = gtm | eqm;
+  while (sel) {  // position order within the block
+    const int k = __ffsll((long long)sel) - 1;
+    sel &= sel - 1;
+    if ((gtm >> k) & 1ull) {
+      out[gt_b + min(eq_b, need)] = src.pos(e0 + k);
+      ++gt_b;
+    } else {
+      if (eq_b < need) out[gt_b + eq_b] = src.pos(e0 + k);
+      ++eq_b;
+    }
+  }
+  if (threadIdx.x == 0) p.n_sel[row] = K;
+}
+
 void fill_cfg(SelParams& p, const sfi_selector_params& prm) {
   p.alpha = prm.alpha;
   p.gamma = prm.gamma;
@@ -691,6 +1062,18 @@ void fill_cfg(SelParams& p, const sfi_selector_params& prm) {
 
 template <bool kExp>
 cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st) {
+  if (n_max <= kTopkCtaMax) {
+    const size_t smem = (size_t)std::max(n_max, 1) * sizeof(uint32_t);
+    static bool cta_configured = false;
+    if (!cta_configured) {
+      cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(sel_topk_cta_kernel<kExp>),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kTopkCtaMax * (int)sizeof(uint32_t));
+      if (e != cudaSuccess) return e;
+      cta_configured = true;
+    }
+    return launch_k(sel_topk_cta_kernel<kExp>, dim3(rows), dim3(kTopkCtaT), smem, st, p);
+  }
   const int chunk = (n_max + kCS - 1) / kCS;
   const dim3 gc(kCS, (unsigned)rows);
   if (chunk <= kTopkSmemKeys) {
@@ -703,27 +1086,32 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
       if (e != cudaSuccess) return e;
       configured = true;
     }
-    sel_topk_kernel<kExp, true><<<gc, kT, smem, st>>>(p);
-  } else {
-    sel_topk_kernel<kExp, false><<<gc, kT, 0, st>>>(p);
+    return launch_k(sel_topk_kernel<kExp, true>, gc, dim3(kT), smem, st, p);
   }
-  return cudaGetLastError();
+  return launch_k(sel_topk_kernel<kExp, false>, gc, dim3(kT), 0, st, p);
 }
 
 template <bool kExp>
 cudaError_t run3(const SelParams& p, int rows, int n_max, int batches, cudaStream_t st,
                  int* launches) {
   const dim3 gc(kCS, (unsigned)rows);
+  cudaError_t e;
   if (p.W == 1 && p.alpha == 1.0)
-    sel_fuse_fast_kernel<kExp><<<gc, kT, 0, st>>>(p);
+    e = launch_k(sel_fuse_fast_kernel<kExp>, gc, dim3(kT), 0, st, p);
   else if (p.W > 1)
-    sel_fuse_kernel<kExp, kMaxW><<<gc, kT, 0, st>>>(p);
+    e = launch_k(sel_fuse_kernel<kExp, kMaxW>, gc, dim3(kT), 0, st, p);
   else
-    sel_fuse_kernel<kExp, 1><<<gc, kT, 0, st>>>(p);
-  cudaError_t e = cudaGetLastError();
+    e = launch_k(sel_fuse_kernel<kExp, 1>, gc, dim3(kT), 0, st, p);
   if (e != cudaSuccess) return e;
-  sel_refine_kernel<kExp><<<dim3((n_max + kRefineT - 1) / kRefineT, batches), kRefineT, 0, st>>>(p);
-  e = cudaGetLastError();
+  const dim3 gr((n_max + kRefineT - 1) / kRefineT, batches);
+  const dim3 br(kRefineT);
+  switch (p.H) {
+    case 1: e = launch_k(sel_refine_kernel<kExp, 1>, gr, br, 0, st, p); break;
+    case 2: e = launch_k(sel_refine_kernel<kExp, 2>, gr, br, 0, st, p); break;
+    case 4: e = launch_k(sel_refine_kernel<kExp, 4>, gr, br, 0, st, p); break;
+    case 8: e = launch_k(sel_refine_kernel<kExp, 8>, gr, br, 0, st, p); break;
+    default: e = launch_k(sel_refine_kernel<kExp, 16>, gr, br, 0, st, p); break;
+  }
   if (e != cudaSuccess) return e;
   e = launch_topk<kExp>(p, rows, n_max, st);
   if (launches) *launches += 3;
