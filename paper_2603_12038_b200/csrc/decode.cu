@@ -45,7 +45,8 @@ namespace {
 
 constexpr int kTile = 64;   // keys per pipeline stage
 constexpr int kNcw = 4;     // consumer warps (16 keys of each tile each)
-constexpr int kThreads = (kNcw + 1) * 32;
+constexpr int kThreads = (kNcw + 2) * 32;   // + TMA producer warp + epilogue warp
+constexpr int kBarThreads = (kNcw + 1) * 32; // consumers + epilogue on the hand-off barriers
 constexpr int kStages = 3;
 constexpr int kMaxSlices = 4096;
 
@@ -56,9 +57,19 @@ struct Geo {
   static constexpr int kTileBytes = kBoxes * kBoxBytes;   // one tensor, one tile
   static constexpr int kStageBytes = 2 * kTileBytes;      // K + V
   static constexpr int kRing = kStages * kStageBytes;
-  static constexpr int kComb = 3 * 8 * D * 4 + 3 * 2 * 8 * 4;  // warps 1..3 hand-off slots (O, m, l)
-  static constexpr int kSmemFixed = kRing + kComb + 256 /*barriers*/ + 1024 /*align*/;
 };
+
+// consumer -> epilogue hand-off: per consumer warp G rows of O plus (m, l)
+// for 8 rows. The 8-float column chunks of row g are XOR-swizzled by g so the
+// float2 stores from the mma layout (8 rows x 4 lanes) are conflict-free
+// without padding (padding would cost G = 8 its second CTA per SM).
+template <int D, int G>
+struct Comb {
+  static constexpr int kOFloats = kNcw * G * D;
+  static constexpr int kBytes = kOFloats * 4 + kNcw * 2 * 8 * 4;
+  static constexpr int kSmemFixed = Geo<D>::kRing + kBytes + 64 /*barriers*/;
+};
+__device__ __forceinline__ int comb_col(int col, int g) { return col ^ (g << 3); }
 
 struct Slice {
   int off[3];
@@ -149,17 +160,118 @@ __device__ __forceinline__ int slice_of(const int* pref, int S, int t) {
   return lo;
 }
 
+// Last-arriving contributor of slice s: merge the partials of the non-empty
+// CTAs in [c_first, c_last] in CTA order (deterministic) and write the G
+// output rows. One pass per chunk of 4 rows: lanes load (m, l) of one
+// contributor each (32 at a time, running max with rescaling across batches),
+// then every lane streams its D/32 columns of the rows for four contributors
+// per iteration so loads stay in flight instead of serialising on L2 latency.
+template <int D, int G>
+__device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, int P0, int c_first,
+                                         int c_last, int T, int Gc, int lane) {
+  constexpr int kCols = D / 32;
+  constexpr int kGB = G < 4 ? G : 4;
+  constexpr int kCB = 4;  // contributors per load batch
+  using Vec = typename std::conditional<kCols == 4, float4, float2>::type;
+#pragma unroll
+  for (int g0 = 0; g0 < G; g0 += kGB) {
+    float acc[kGB][kCols];
+    float L[kGB], M[kGB];
+#pragma unroll
+    for (int gg = 0; gg < kGB; ++gg) {
+      L[gg] = 0.f;
+      M[gg] = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kCols; ++k) acc[gg][k] = 0.f;
+    }
+    for (int cb = c_first; cb <= c_last; cb += 32) {
+      const int c = cb + lane;
+      const int c0s = c <= c_last ? cta_start(c, T, Gc) : 0;
+      const bool ok = c <= c_last && c0s < cta_start(c + 1, T, Gc);
+      const int pc = c * 2 + (c0s >= P0 ? 0 : 1);
+      float mi[kGB], li[kGB], sc[kGB];
+#pragma unroll
+      for (int gg = 0; gg < kGB; ++gg) {
+        mi[gg] = ok ? __ldcg(&p.part_ml[((size_t)pc * 2 + 0) * 8 + g0 + gg]) : -INFINITY;
+        li[gg] = ok ? __ldcg(&p.part_ml[((size_t)pc * 2 + 1) * 8 + g0 + gg]) : 0.f;
+      }
+#pragma unroll
+      for (int gg = 0; gg < kGB; ++gg) {
+        float mb = mi[gg];
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o2));
+        const float Mn = fmaxf(M[gg], mb);
+        const float Mu = (Mn == -INFINITY) ? 0.f : Mn;
+        const float r = fast_exp2(M[gg] - Mu);  // rescale of earlier batches (0 when none)
+#pragma unroll
+        for (int k = 0; k < kCols; ++k) acc[gg][k] *= r;
+        sc[gg] = ok ? fast_exp2(mi[gg] - Mu) : 0.f;
+        float lw = li[gg] * sc[gg];
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o2);
+        L[gg] = L[gg] * r + lw;
+        M[gg] = Mn;
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, ok);
+      while (mask) {  // contributors of this batch, kCB at a time, ascending
+        int src[kCB];
+        bool has[kCB];
+#pragma unroll
+        for (int j = 0; j < kCB; ++j) {
+          has[j] = mask != 0;
+          src[j] = has[j] ? __ffs(mask) - 1 : src[0];
+          if (has[j]) mask &= mask - 1;
+        }
+        Vec x[kCB][kGB];
+#pragma unroll
+        for (int j = 0; j < kCB; ++j) {
+          const int pj = __shfl_sync(0xffffffffu, pc, src[j]);
+#pragma unroll
+          for (int gg = 0; gg < kGB; ++gg)
+            x[j][gg] = __ldcg(reinterpret_cast<const Vec*>(p.part_o + ((size_t)pj * 8 + g0 + gg) * D) + lane);
+        }
+#pragma unroll
+        for (int j = 0; j < kCB; ++j)
+#pragma unroll
+          for (int gg = 0; gg < kGB; ++gg) {
+            const float sv = __shfl_sync(0xffffffffu, sc[gg], src[j]);
+            const float sj = has[j] ? sv : 0.f;
+            acc[gg][0] += x[j][gg].x * sj;
+            acc[gg][1] += x[j][gg].y * sj;
+            if constexpr (kCols == 4) {
+              acc[gg][2 % kCols] += x[j][gg].z * sj;
+              acc[gg][3 % kCols] += x[j][gg].w * sj;
+            }
+          }
+      }
+    }
+#pragma unroll
+    for (int gg = 0; gg < kGB; ++gg) {
+      const float inv = L[gg] > 0.f ? 1.f / L[gg] : 0.f;
+      Vec r;
+      r.x = acc[gg][0] * inv;
+      r.y = acc[gg][1] * inv;
+      if constexpr (kCols == 4) {
+        r.z = acc[gg][2 % kCols] * inv;
+        r.w = acc[gg][3 % kCols] * inv;
+      }
+      reinterpret_cast<Vec*>(outp + (g0 + gg) * D)[lane] = r;
+    }
+  }
+}
+
 template <int D, int G>
 __global__ void __launch_bounds__(kThreads, 2)
     decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                   const DecodeParams p) {
   static_assert(G >= 1 && G <= 8, "GQA group of at most 8 query heads per KV head");
   static_assert(D == 64 || D == 128, "head_dim 64 or 128");
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* comb_o = reinterpret_cast<float*>(smem + Geo<D>::kRing);           // [3][8][D]
-  float* comb_ml = comb_o + 3 * 8 * D;                                      // [3][2][8]
-  uint64_t* full = reinterpret_cast<uint64_t*>(comb_ml + 3 * 2 * 8);
+  // 1024-byte alignment (128B-swizzled TMA boxes) without padding slack: the
+  // kernel has no static shared memory, so the dynamic window starts at 0
+  extern __shared__ __align__(1024) uint8_t smem[];
+  float* comb_o = reinterpret_cast<float*>(smem + Geo<D>::kRing);           // [kNcw][G][kRow]
+  float* comb_ml = comb_o + Comb<D, G>::kOFloats;                           // [kNcw][2][8]
+  uint64_t* full = reinterpret_cast<uint64_t*>(comb_ml + kNcw * 2 * 8);
   uint64_t* empty = full + kStages;
   int* pref = reinterpret_cast<int*>(empty + kStages + 2);                  // [S + 1]
 
@@ -171,6 +283,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     trace[6] = smid();
   }
 
+  if (threadIdx.x == kNcw * 32) {  // descriptors are launch constants: fetch before the wait
+    tma_prefetch_desc(&tmk);
+    tma_prefetch_desc(&tmv);
+  }
   // PDL: lengths, selections and the freshly appended ring row are all
   // produced upstream in the same stream
   griddep_wait();
@@ -221,8 +337,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kNcw) {
     // ---------------- producer: TMA K/V tiles into the stage ring ----------------
     if (lane == 0) {
-      tma_prefetch_desc(&tmk);
-      tma_prefetch_desc(&tmv);
       const uint64_t pol = l2_policy_evict_first();
       int s = s_first;
       Slice sl = make_slice(p, s, false);
@@ -247,6 +361,128 @@ __global__ void __launch_bounds__(kThreads, 2)
     return;
   }
 
+  if (warp == kNcw + 1) {
+    // ---------------- epilogue: combine the 4 consumer partials, emit ----------------
+    // Lane l owns columns [l * D/32, (l + 1) * D/32) of every query row. The
+    // emission sequence is the CTA's non-empty slices in order, the same
+    // sequence the consumers walk.
+    constexpr int kCols = D / 32;
+    using Vec = typename std::conditional<kCols == 4, float4, float2>::type;
+    asm volatile("bar.arrive 2, %0;" ::"n"(kBarThreads));  // slots start free
+    int pend[2], n_pend = 0;  // partial slices awaiting publication
+    for (int s = s_first; s < S && pref[s] < te; ++s) {
+      const int P0 = pref[s], P1 = pref[s + 1];
+      if (P1 == P0) continue;
+      asm volatile("bar.sync 1, %0;" ::"n"(kBarThreads));
+      const long long e0 = trace ? (long long)globaltimer() : 0;
+      if (trace && lane == 0) {
+        if (trace[13] == 0) trace[13] = e0;
+        trace[14] = e0;
+      }
+      Vec acc[G];
+      float mr[G], lr[G];
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        float mw[kNcw], M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kNcw; ++w) {
+          mw[w] = comb_ml[(w * 2 + 0) * 8 + gg];
+          M = fmaxf(M, mw[w]);
+        }
+        const float Mu = (M == -INFINITY) ? 0.f : M;
+        float L = 0.f;
+        Vec a;
+        a.x = a.y = 0.f;
+        if constexpr (kCols == 4) a.z = a.w = 0.f;
+#pragma unroll
+        for (int w = 0; w < kNcw; ++w) {
+          const float sc = fast_exp2(mw[w] - Mu);
+          L += comb_ml[(w * 2 + 1) * 8 + gg] * sc;
+          const Vec x = *reinterpret_cast<const Vec*>(comb_o + (w * G + gg) * D +
+                                                      comb_col(lane * kCols, gg));
+          a.x += x.x * sc;
+          a.y += x.y * sc;
+          if constexpr (kCols == 4) {
+            a.z += x.z * sc;
+            a.w += x.w * sc;
+          }
+        }
+        acc[gg] = a;
+        mr[gg] = M;
+        lr[gg] = L;
+      }
+      __syncwarp();
+      asm volatile("bar.arrive 2, %0;" ::"n"(kBarThreads));  // slots free again
+      const int c_first = cta_of(P0, T, Gc), c_last = cta_of(P1 - 1, T, Gc);
+      const int b = s / p.H, h = s % p.H;
+      float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
+      if (c_first == c_last) {
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          const float inv = lr[gg] > 0.f ? 1.f / lr[gg] : 0.f;
+          Vec r = acc[gg];
+          r.x *= inv;
+          r.y *= inv;
+          if constexpr (kCols == 4) {
+            r.z *= inv;
+            r.w *= inv;
+          }
+          reinterpret_cast<Vec*>(outp + gg * D)[lane] = r;
+        }
+      } else {
+        // partial: written now, published (fence + counter) once this CTA's
+        // stream has ended — a fence issued while the producer's TMA loads are
+        // in flight stalls until they drain
+        const int slot = (s == s_first) ? 0 : 1;
+        const size_t part = (size_t)blockIdx.x * 2 + slot;
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          reinterpret_cast<Vec*>(p.part_o + (part * 8 + gg) * D)[lane] = acc[gg];
+          if (lane == gg) {
+            p.part_ml[(part * 2 + 0) * 8 + gg] = mr[gg];
+            p.part_ml[(part * 2 + 1) * 8 + gg] = lr[gg];
+          }
+        }
+        pend[n_pend++] = s;
+      }
+      if (trace && lane == 0) {
+        trace[4] += 1;  // emissions
+        trace[7] += (long long)globaltimer() - e0;
+      }
+    }
+    if (n_pend > 0) {
+      const long long e1 = trace ? (long long)globaltimer() : 0;
+      __threadfence();  // release this CTA's partials
+      __syncwarp();
+      if (trace && lane == 0) trace[9] = (long long)globaltimer() - e1;
+      for (int k = 0; k < n_pend; ++k) {
+        const int sp = pend[k];
+        const int P0 = pref[sp], P1 = pref[sp + 1];
+        const int c_first = cta_of(P0, T, Gc), c_last = cta_of(P1 - 1, T, Gc);
+        // contributors = CTAs in [c_first, c_last] with a non-empty range
+        int n_contrib = 0;
+        for (int cb = c_first; cb <= c_last; cb += 32) {
+          const int c = cb + lane;
+          const bool ok = c <= c_last && cta_start(c, T, Gc) < cta_start(c + 1, T, Gc);
+          n_contrib += __popc(__ballot_sync(0xffffffffu, ok));
+        }
+        int last = 0;
+        if (lane == 0) last = (atomicAdd(&p.counters[sp], 1) == n_contrib - 1);
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence();  // acquire the other contributors' partials
+          const int b = sp / p.H, h = sp % p.H;
+          merge_slice<D, G>(p, p.out + ((size_t)b * p.Hq + (size_t)h * G) * D, P0, c_first, c_last,
+                            T, Gc, lane);
+          if (lane == 0) p.counters[sp] = 0;
+        }
+      }
+      if (trace && lane == 0) trace[10] += (long long)globaltimer() - e1;
+    }
+    if (trace && lane == 0) trace[3] = (long long)globaltimer();
+    return;
+  }
+
   // ---------------- consumers ----------------
   const int g = lane >> 2, t4 = lane & 3;
   const float sl2 = p.scale_log2;
@@ -256,8 +492,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   int s = s_first;
   Slice sl = make_slice(p, s, false);
   bool fresh = true;
-  // hand-off slots start free: warp 0 pre-arrives on EMPTY (barrier 2)
-  if (warp == 0) asm volatile("bar.arrive 2, %0;" ::"n"(kNcw * 32));
 
   for (int t = tb, i = 0; t < te; ++t, ++i) {
     while (pref[s + 1] <= t) sl = make_slice(p, ++s, false);
@@ -405,208 +639,34 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
 
-    // ---- end of this CTA's part of slice s: combine 4 warps, emit ----
+    // ---- end of this CTA's part of slice s: hand the warp partial to the
+    // epilogue warp and keep consuming: EMPTY (barrier 2) -> slot -> FULL (barrier 1)
     if (t + 1 == pref[s + 1] || t + 1 == te) {
       float lr = l_run;
       lr += __shfl_xor_sync(0xffffffffu, lr, 1);
       lr += __shfl_xor_sync(0xffffffffu, lr, 2);
-      // row g's O (hi + lo halves) in place: o[n][0..1] = d 8n + 2t4 + {0,1}
+      const long long tw0 = trace ? (long long)globaltimer() : 0;
+      asm volatile("bar.sync 2, %0;" ::"n"(kBarThreads));
+      if (trace && threadIdx.x == 0) trace[8] += (long long)globaltimer() - tw0;
+      if (g < G) {
+        // row g's O (hi + lo halves): o[n][0..1] + o[n][2..3] = d 8n + 2t4 + {0,1}
+        float* dst = comb_o + (warp * G + g) * D;
 #pragma unroll
-      for (int n = 0; n < D / 8; ++n) {
-        o[n][0] += o[n][2];
-        o[n][1] += o[n][3];
-      }
-      const long long te0 = trace ? (long long)globaltimer() : 0;
-      if (warp != 0) {
-        // hand the warp partial to warp 0 and keep consuming tiles:
-        // EMPTY (barrier 2) -> write slot -> FULL (barrier 1, arrive only)
-        asm volatile("bar.sync 2, %0;" ::"n"(kNcw * 32));
-        if (g < G) {
-          float* dst = comb_o + ((warp - 1) * 8 + g) * D;
-#pragma unroll
-          for (int n = 0; n < D / 8; ++n)
-            *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(o[n][0], o[n][1]);
-          if (t4 == 0) {
-            comb_ml[((warp - 1) * 2 + 0) * 8 + g] = m_run;
-            comb_ml[((warp - 1) * 2 + 1) * 8 + g] = lr;
-          }
-        }
-        asm volatile("bar.arrive 1, %0;" ::"n"(kNcw * 32));
-      } else {
-        // warp 0: combine warps 0..3 in fixed order, then emit
-        asm volatile("bar.sync 1, %0;" ::"n"(kNcw * 32));
-        float mr = m_run;
-        if (g < G) {
-#pragma unroll 1
-          for (int w = 0; w < kNcw - 1; ++w) {
-            const float* src = comb_o + (w * 8 + g) * D;
-            const float m2 = comb_ml[(w * 2 + 0) * 8 + g];
-            const float l2 = comb_ml[(w * 2 + 1) * 8 + g];
-            const float M = fmaxf(mr, m2);
-            const float Mu = (M == -INFINITY) ? 0.f : M;
-            const float a1 = fast_exp2(mr - Mu), a2 = fast_exp2(m2 - Mu);
-#pragma unroll
-            for (int n = 0; n < D / 8; ++n) {
-              const float2 x = *reinterpret_cast<const float2*>(src + n * 8 + 2 * t4);
-              o[n][0] = o[n][0] * a1 + x.x * a2;
-              o[n][1] = o[n][1] * a1 + x.y * a2;
-            }
-            lr = lr * a1 + l2 * a2;
-            mr = M;
-          }
-        }
-        __syncwarp();
-        asm volatile("bar.arrive 2, %0;" ::"n"(kNcw * 32));  // slots free again
-        const long long te1 = trace ? (long long)globaltimer() : 0;
-        const int P0 = pref[s], P1 = pref[s + 1];
-        const int c_first = cta_of(P0, T, Gc), c_last = cta_of(P1 - 1, T, Gc);
-        const int b = s / p.H, h = s % p.H;
-        float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
-        if (c_first == c_last) {
-          if (g < G) {
-            const float inv = lr > 0.f ? 1.f / lr : 0.f;
-#pragma unroll
-            for (int n = 0; n < D / 8; ++n)
-              *reinterpret_cast<float2*>(outp + g * D + n * 8 + 2 * t4) =
-                  make_float2(o[n][0] * inv, o[n][1] * inv);
-          }
-        } else {
-          const size_t part = (size_t)blockIdx.x * 2 + ((s == s_first) ? 0 : 1);
-          if (g < G) {
-#pragma unroll
-            for (int n = 0; n < D / 8; ++n)
-              *reinterpret_cast<float2*>(p.part_o + (part * 8 + g) * D + n * 8 + 2 * t4) =
-                  make_float2(o[n][0], o[n][1]);
-            if (t4 == 0) {
-              p.part_ml[(part * 2 + 0) * 8 + g] = mr;
-              p.part_ml[(part * 2 + 1) * 8 + g] = lr;
-            }
-          }
-          __syncwarp();
-          // contributors = CTAs in [c_first, c_last] with a non-empty range; lanes
-          // enumerate them 32 at a time
-          int n_contrib = 0;
-          for (int cb = c_first; cb <= c_last; cb += 32) {
-            const int c = cb + lane;
-            const bool ok = c <= c_last && cta_start(c, T, Gc) < cta_start(c + 1, T, Gc);
-            n_contrib += __popc(__ballot_sync(0xffffffffu, ok));
-          }
-          int last = 0;
-          if (lane == 0) {
-            __threadfence();  // release this warp's partial
-            last = (atomicAdd(&p.counters[s], 1) == n_contrib - 1);
-          }
-          last = __shfl_sync(0xffffffffu, last, 0);
-          const long long te2 = trace ? (long long)globaltimer() : 0;
-          if (trace && lane == 0) trace[9] += te2 - te1;
-          if (last) {
-            __threadfence();  // acquire the other contributors' partials
-            // Merge in CTA order (deterministic). Pass A: row maxima with one
-            // contributor per lane. Pass B, for chunks of 4 rows: lanes load the
-            // scale factors of their contributor, then every lane streams its
-            // D/32 columns of the 4 rows for two contributors per iteration so
-            // loads stay in flight instead of serialising on L2 latency.
-            constexpr int kCols = D / 32;
-            constexpr int kGB = G < 4 ? G : 4;
-            using Vec = typename std::conditional<kCols == 4, float4, float2>::type;
-            float M[G];
-#pragma unroll
-            for (int gg = 0; gg < G; ++gg) M[gg] = -INFINITY;
-            for (int cb = c_first; cb <= c_last; cb += 32) {
-              const int c = cb + lane;
-              const int c0s = c <= c_last ? cta_start(c, T, Gc) : 0;
-              const bool ok = c <= c_last && c0s < cta_start(c + 1, T, Gc);
-              const size_t pc = (size_t)c * 2 + (c0s >= P0 ? 0 : 1);
-#pragma unroll
-              for (int gg = 0; gg < G; ++gg) {
-                float m = ok ? __ldcg(&p.part_ml[(pc * 2 + 0) * 8 + gg]) : -INFINITY;
-#pragma unroll
-                for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o2));
-                M[gg] = fmaxf(M[gg], m);
-              }
-            }
-#pragma unroll
-            for (int g0 = 0; g0 < G; g0 += kGB) {
-              float acc[kGB][kCols];
-              float L[kGB];
-#pragma unroll
-              for (int gg = 0; gg < kGB; ++gg) {
-                L[gg] = 0.f;
-#pragma unroll
-                for (int k = 0; k < kCols; ++k) acc[gg][k] = 0.f;
-              }
-              for (int cb = c_first; cb <= c_last; cb += 32) {
-                const int c = cb + lane;
-                const int c0s = c <= c_last ? cta_start(c, T, Gc) : 0;
-                const bool ok = c <= c_last && c0s < cta_start(c + 1, T, Gc);
-                const int pc = c * 2 + (c0s >= P0 ? 0 : 1);
-                float sc[kGB];
-#pragma unroll
-                for (int gg = 0; gg < kGB; ++gg) {
-                  const float Mu = (M[g0 + gg] == -INFINITY) ? 0.f : M[g0 + gg];
-                  sc[gg] = ok ? fast_exp2(__ldcg(&p.part_ml[((size_t)pc * 2 + 0) * 8 + g0 + gg]) - Mu) : 0.f;
-                  float lw = ok ? __ldcg(&p.part_ml[((size_t)pc * 2 + 1) * 8 + g0 + gg]) * sc[gg] : 0.f;
-#pragma unroll
-                  for (int o2 = 16; o2 > 0; o2 >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o2);
-                  L[gg] += lw;
-                }
-                unsigned mask = __ballot_sync(0xffffffffu, ok);
-                while (mask) {  // contributors of this chunk, two at a time, ascending
-                  const int a = __ffs(mask) - 1;
-                  mask &= mask - 1;
-                  const int bl = mask ? __ffs(mask) - 1 : a;
-                  const bool has_b = mask != 0;
-                  if (has_b) mask &= mask - 1;
-                  const int pa = __shfl_sync(0xffffffffu, pc, a);
-                  const int pb = __shfl_sync(0xffffffffu, pc, bl);
-                  Vec xa[kGB], xb[kGB];
-#pragma unroll
-                  for (int gg = 0; gg < kGB; ++gg) {
-                    xa[gg] = __ldcg(reinterpret_cast<const Vec*>(p.part_o + ((size_t)pa * 8 + g0 + gg) * D) + lane);
-                    xb[gg] = __ldcg(reinterpret_cast<const Vec*>(p.part_o + ((size_t)pb * 8 + g0 + gg) * D) + lane);
-                  }
-#pragma unroll
-                  for (int gg = 0; gg < kGB; ++gg) {
-                    const float sa = __shfl_sync(0xffffffffu, sc[gg], a);
-                    const float sbv = __shfl_sync(0xffffffffu, sc[gg], bl);
-                    const float sb = has_b ? sbv : 0.f;
-                    acc[gg][0] += xa[gg].x * sa + xb[gg].x * sb;
-                    acc[gg][1] += xa[gg].y * sa + xb[gg].y * sb;
-                    if constexpr (kCols == 4) {
-                      acc[gg][2 % kCols] += xa[gg].z * sa + xb[gg].z * sb;
-                      acc[gg][3 % kCols] += xa[gg].w * sa + xb[gg].w * sb;
-                    }
-                  }
-                }
-              }
-#pragma unroll
-              for (int gg = 0; gg < kGB; ++gg) {
-                const float inv = L[gg] > 0.f ? 1.f / L[gg] : 0.f;
-                Vec r;
-                r.x = acc[gg][0] * inv;
-                r.y = acc[gg][1] * inv;
-                if constexpr (kCols == 4) {
-                  r.z = acc[gg][2 % kCols] * inv;
-                  r.w = acc[gg][3 % kCols] * inv;
-                }
-                reinterpret_cast<Vec*>(outp + (g0 + gg) * D)[lane] = r;
-              }
-            }
-            if (lane == 0) p.counters[s] = 0;
-          }
-        }
-        if (trace && lane == 0) {
-          trace[4] += 1;  // emissions
-          trace[7] += (long long)globaltimer() - te0;
-          trace[8] += te1 - te0;
+        for (int n = 0; n < D / 8; ++n)
+          *reinterpret_cast<float2*>(dst + comb_col(n * 8 + 2 * t4, g)) =
+              make_float2(o[n][0] + o[n][2], o[n][1] + o[n][3]);
+        if (t4 == 0) {
+          comb_ml[(warp * 2 + 0) * 8 + g] = m_run;
+          comb_ml[(warp * 2 + 1) * 8 + g] = lr;
         }
       }
+      asm volatile("bar.arrive 1, %0;" ::"n"(kBarThreads));
       fresh = true;
     }
   }
-  // consume warp 0's final EMPTY arrival (balances barrier 2 before exit)
-  if (warp != 0) asm volatile("bar.sync 2, %0;" ::"n"(kNcw * 32));
-  if (trace && threadIdx.x == 0) trace[3] = (long long)globaltimer();
+  // consume the epilogue's final EMPTY arrival (balances barrier 2 before exit)
+  asm volatile("bar.sync 2, %0;" ::"n"(kBarThreads));
+  if (trace && threadIdx.x == 0) trace[12] = (long long)globaltimer();
 }
 
 using DecodeFn = void (*)(CUtensorMap, CUtensorMap, DecodeParams);
@@ -624,8 +684,18 @@ DecodeFn pick_g(int G) {
 
 }  // namespace
 
-int decode_smem_bytes(int D, int slices) {
-  const int fixed = D == 64 ? Geo<64>::kSmemFixed : Geo<128>::kSmemFixed;
+template <int D>
+int smem_fixed(int G) {
+  switch (G) {
+    case 1: return Comb<D, 1>::kSmemFixed;
+    case 2: return Comb<D, 2>::kSmemFixed;
+    case 4: return Comb<D, 4>::kSmemFixed;
+    default: return Comb<D, 8>::kSmemFixed;
+  }
+}
+
+int decode_smem_bytes(int D, int G, int slices) {
+  const int fixed = D == 64 ? smem_fixed<64>(G) : smem_fixed<128>(G);
   return fixed + (slices + 1) * (int)sizeof(int);
 }
 
@@ -636,7 +706,7 @@ cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const C
   DecodeFn fn = (D == 64) ? pick_g<64>(G) : pick_g<128>(G);
   const int S = p.B * p.H;
   if (!fn || S > kMaxSlices || ctas > kMaxCtas) return cudaErrorInvalidValue;
-  const int smem = decode_smem_bytes(D, S);
+  const int smem = decode_smem_bytes(D, G, S);
   // raise the dynamic-smem cap once per instantiation to the largest size used
   static int configured[2][9] = {};
   int& cap = configured[D == 64 ? 0 : 1][G];

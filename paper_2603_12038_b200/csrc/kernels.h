@@ -49,14 +49,14 @@ struct DecodeParams {
   uint32_t* err;
   float scale_log2;      // log2(e) / sqrt(d)
   float inv_sqrt_d;
-  long long* trace;      // debug: per-CTA globaltimer stamps [grid][8] (null = off)
+  long long* trace;      // debug: per-CTA globaltimer stamps [grid][16] (null = off)
 };
 
 // debug / tuning hooks (capi.cu): SFI_DECODE_CTAS overrides the decode grid,
 // SFI_DECODE_TRACE=1 records per-CTA timelines readable with sfi_debug_decode_trace.
 long long* decode_trace_buffer();
 
-int decode_smem_bytes(int D, int slices);
+int decode_smem_bytes(int D, int G, int slices);
 int decode_grid(int tiles_upper, int num_sms);
 cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv,
                           int D, int G, int ctas, cudaStream_t stream);

@@ -72,14 +72,20 @@ def trace(tag):
           f"prologue med={np.median(pro-start)/1e3:.2f}us first-tile med={np.median(first-pro)/1e3:.2f}us "
           f"busy med={np.median(busy)/1e3:.2f} max={busy.max()/1e3:.2f} min={busy.min()/1e3:.2f}us "
           f"kernel span={end.max()/1e3:.2f}us emissions mean={live[:,4].mean():.2f} tiles mean={live[:,5].mean():.1f}")
-    print(f"   emission ns per CTA: total mean={live[:,7].mean():.0f} max={live[:,7].max():.0f}; "
-          f"combine mean={live[:,8].mean():.0f}; partial+fence mean={live[:,9].mean():.0f} max={live[:,9].max():.0f}; "
-          f"bar+atomic mean={live[:,10].mean():.0f} max={live[:,10].max():.0f}")
+    cons_end = live[:, 12] - t0
+    print(f"   consumers done med={np.median(cons_end - start)/1e3:.2f}us max={cons_end.max()/1e3:.2f}us; "
+          f"epilogue busy mean={live[:,7].mean():.0f}ns max={live[:,7].max():.0f}; "
+          f"consumer EMPTY stall mean={live[:,8].mean():.0f}; partial+fence+atomic mean={live[:,9].mean():.0f} "
+          f"max={live[:,9].max():.0f}; merge mean={live[:,10].mean():.0f} max={live[:,10].max():.0f}")
+    e_first, e_last = live[:, 13] - t0, live[:, 14] - t0
+    print(f"   first emission at med={np.median(e_first - start)/1e3:.2f}us, last at med={np.median(e_last - start)/1e3:.2f}us; "
+          f"fence mean={live[:,9].mean():.0f} max={live[:,9].max():.0f}ns")
     slow = np.argsort(-end)[:5]
     for i in slow:
         print(f"   slow cta: start={start[i]/1e3:.2f} pro={pro[i]/1e3:.2f} first={first[i]/1e3:.2f} "
               f"end={end[i]/1e3:.2f} emis={live[i,4]:.0f} tiles={live[i,5]:.0f} sm={live[i,6]:.0f} "
-              f"emit={live[i,7]/1e3:.2f} comb={live[i,8]/1e3:.2f} fence={live[i,9]/1e3:.2f} bar={live[i,10]/1e3:.2f}us")
+              f"cons_end={cons_end[i]/1e3:.2f} epi={live[i,7]/1e3:.2f} stall={live[i,8]/1e3:.2f} "
+              f"fence={live[i,9]/1e3:.2f} merge={live[i,10]/1e3:.2f}us")
 
 
 res = {}
