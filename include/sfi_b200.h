@@ -14,6 +14,8 @@
  *                                                         scheduler.cpp:150-180
  *   sfi_compact_build   KvStore::reorganize               attention.cpp:186-217
  *   sfi_sparse_decode   attention_kernel_sparse           attention.cpp:525-550
+ *   sfi_fast_decode     append_layer + sparse attention of one fast step
+ *                       attention.cpp:354-360, 136-152, 270-291, 80-113
  *
  * Data layout (all device memory, caller-owned):
  *   k_cache, v_cache : bf16 [n_layers][batch][n_kv_heads][max_positions][head_dim]
@@ -171,6 +173,20 @@ SFI_API int sfi_dense_decode(const sfi_shape* shape, const sfi_cache* cache, int
  * selected rows; S = recent_len + n_sink_b + n_sel per (b, head)). */
 SFI_API int sfi_sparse_decode(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
                               const float* q, float* out, void* stream);
+
+/* Fast step, one layer, ONE launch: sfi_ring_append of the current token
+ * (k_new, v_new bf16 [batch][n_kv_heads][head_dim]; bit-identical paged row,
+ * ring slot and key norm) fused with sfi_sparse_decode (the token attends to
+ * itself, attention.cpp:354-360). flags: SFI_FAST_PREFETCH lets the kernel
+ * stream this layer's compact rows before its programmatic-dependent-launch
+ * wait — only valid when the kernel enqueued immediately before it on the
+ * stream does not write this layer's compact rows, n_sel or n_sink_b (true for
+ * every kernel of a fast step; false right after sfi_compact_build /
+ * sfi_set_selection of the same layer). */
+#define SFI_FAST_PREFETCH 1
+SFI_API int sfi_fast_decode(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                            const float* q, const void* k_new, const void* v_new, float* out,
+                            int32_t flags, void* stream);
 
 /* Selector, one layer: pooled logits over J_b (+ cached key norms) ->
  * sel/n_sel of `layer`, indices bit-exact with run_selector given identical

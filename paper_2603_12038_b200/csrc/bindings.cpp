@@ -302,6 +302,13 @@ PYBIND11_MODULE(_sfi_b200, m) {
     check(sfi_sparse_decode(&s, &c, layer, static_cast<const float*>(vp(q)), static_cast<float*>(vp(out)),
                             vp(stream)));
   });
+  m.def("fast_decode", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
+                          std::uintptr_t k, std::uintptr_t v, std::uintptr_t out, int flags,
+                          std::uintptr_t stream) {
+    check(sfi_fast_decode(&s, &c, layer, static_cast<const float*>(vp(q)), vp(k), vp(v),
+                          static_cast<float*>(vp(out)), flags, vp(stream)));
+  });
+  m.attr("FAST_PREFETCH") = SFI_FAST_PREFETCH;
   m.def("selector", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
                        const sfi_selector_params& prm, std::uintptr_t stream) {
     check(sfi_selector(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm, vp(stream)));

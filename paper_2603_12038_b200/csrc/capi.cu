@@ -49,8 +49,8 @@ int validate(const sfi_shape* s) {
   if (s->n_q_heads % s->n_kv_heads != 0)
     return fail(SFI_ERR_CONFIG, "shape: n_q_heads must be a multiple of n_kv_heads");
   const int G = group_of(*s);
-  if (G != 1 && G != 2 && G != 4 && G != 8)
-    return fail(SFI_ERR_UNSUPPORTED, "shape: GQA group size must be 1, 2, 4 or 8");
+  if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16)
+    return fail(SFI_ERR_UNSUPPORTED, "shape: GQA group size must be 1, 2, 4, 8 or 16");
   if (s->head_dim != 64 && s->head_dim != 128)
     return fail(SFI_ERR_UNSUPPORTED, "shape: head_dim must be 64 or 128");
   if (s->n_kv_heads > 16) return fail(SFI_ERR_UNSUPPORTED, "shape: at most 16 KV heads");
@@ -132,6 +132,7 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   if ((rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
   if (!q || !out) return fail(SFI_ERR_INVALID_ARGUMENT, "decode: q/out null");
   if (pool != SFI_POOL_MEAN && pool != SFI_POOL_MAX) return fail(SFI_ERR_CONFIG, "decode: bad pool mode");
+  if (group_of(*s) > 8) return fail(SFI_ERR_UNSUPPORTED, "dense decode: GQA group 16 not built yet");
   const int D = s->head_dim;
   const uint64_t slices = (uint64_t)s->n_layers * s->batch * s->n_kv_heads;
   const uint64_t rows_per = sparse ? (uint64_t)compact_rows(*s) : (uint64_t)s->max_positions;
@@ -181,6 +182,68 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   }
   SFI_CUDA(sfi_impl::launch_decode(p, tk, tv, D, group_of(*s), ctas, (cudaStream_t)stream),
            sparse ? "sfi_sparse_decode" : "sfi_dense_decode");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+// Fast step, one layer: sparse decode over the compact cache, fused with the
+// current token's append when k_new / v_new are given (fast_decode.cu).
+int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* q, const void* k_new,
+                const void* v_new, float* out, int flags, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc) return rc;
+  if ((rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!q || !out) return fail(SFI_ERR_INVALID_ARGUMENT, "decode: q/out null");
+  if ((k_new == nullptr) != (v_new == nullptr)) return fail(SFI_ERR_INVALID_ARGUMENT, "fast_decode: k/v null");
+  if (flags & ~SFI_FAST_PREFETCH) return fail(SFI_ERR_INVALID_ARGUMENT, "fast_decode: unknown flags");
+  const int D = s->head_dim;
+  const uint64_t slices = (uint64_t)s->n_layers * s->batch * s->n_kv_heads;
+  CUtensorMap tk, tv;
+  if ((rc = make_tmap(&tk, c->ck, slices * compact_rows(*s), D))) return rc;
+  if ((rc = make_tmap(&tv, c->cv, slices * compact_rows(*s), D))) return rc;
+  sfi_impl::FastParams p;
+  p.q = q;
+  p.out = out;
+  p.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  p.kc = static_cast<__nv_bfloat16*>(c->k_cache);
+  p.vc = static_cast<__nv_bfloat16*>(c->v_cache);
+  p.ck = static_cast<__nv_bfloat16*>(c->ck);
+  p.cv = static_cast<__nv_bfloat16*>(c->cv);
+  p.norms = c->key_norms;
+  p.prefix_len = c->prefix_len;
+  p.n_sink_b = c->n_sink_b;
+  p.recent_len = c->recent_len;
+  p.n_sel = c->n_sel;
+  p.err = c->error_flags;
+  p.layer = layer;
+  p.B = s->batch;
+  p.H = s->n_kv_heads;
+  p.Hq = s->n_q_heads;
+  p.Lmax = s->max_positions;
+  p.crows = compact_rows(*s);
+  p.R = s->n_recent;
+  p.prefetch = (flags & SFI_FAST_PREFETCH) ? 1 : 0;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  static const int env_c = [] {
+    const char* e = std::getenv("SFI_FAST_CLUSTER");
+    return e ? std::atoi(e) : 0;
+  }();
+  int C = sfi_impl::fast_cluster_size(s->batch * s->n_kv_heads, num_sms());
+  if (env_c == 1 || env_c == 2 || env_c == 4 || env_c == 8) C = env_c;
+  p.trace = nullptr;
+  static const bool env_trace = std::getenv("SFI_DECODE_TRACE") != nullptr;
+  const int grid = s->batch * s->n_kv_heads * C;
+  if (env_trace && grid <= sfi_impl::kMaxCtas) {
+    p.trace = sfi_impl::decode_trace_buffer();
+    if (!p.trace) return fail(SFI_ERR_CUDA, "trace buffer");
+    SFI_CUDA(cudaMemsetAsync(p.trace, 0, sizeof(long long) * 16 * sfi_impl::kMaxCtas, (cudaStream_t)stream),
+             "trace");
+    g_trace_ctas = grid;
+  }
+  SFI_CUDA(sfi_impl::launch_fast_decode(p, tk, tv, D, group_of(*s), C, (cudaStream_t)stream),
+           k_new ? "sfi_fast_decode" : "sfi_sparse_decode");
   g_launches = 1;
   return SFI_OK;
 }
@@ -360,7 +423,13 @@ SFI_API int sfi_dense_decode(const sfi_shape* s, const sfi_cache* c, int32_t lay
 
 SFI_API int sfi_sparse_decode(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q,
                               float* out, void* stream) {
-  return decode_common(s, c, layer, q, out, nullptr, SFI_POOL_MEAN, true, stream);
+  return fast_common(s, c, layer, q, nullptr, nullptr, out, 0, stream);
+}
+
+SFI_API int sfi_fast_decode(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q,
+                            const void* k_new, const void* v_new, float* out, int32_t flags, void* stream) {
+  if (!k_new || !v_new) return fail(SFI_ERR_INVALID_ARGUMENT, "fast_decode: k/v null");
+  return fast_common(s, c, layer, q, k_new, v_new, out, flags, stream);
 }
 
 SFI_API int sfi_selector(const sfi_shape* s, const sfi_cache* c, int32_t layer,

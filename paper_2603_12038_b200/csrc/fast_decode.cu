@@ -1,0 +1,612 @@
+// fast_decode.cu — K4: the fast-step sparse decode over the compact cache,
+// optionally fused with the current token's append (K3a) so a fast step is
+// ONE launch per layer.
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   sparse_segments       attention.cpp:270-291  compact rows (sink + selected)
+//                                                then the recent tail
+//   attend                attention.cpp:80-113   softmax(q.k / sqrt(d)) v
+//   KvStore::append_layer attention.cpp:136-152  row L-1 <- k, v; fp64 key norm
+//                                                summed in c order
+//   run_step              attention.cpp:354-360  the token is appended before
+//                                                attention, so it attends to itself
+//
+// B200 design:
+//   * one thread-block cluster of C CTAs per (b, kv head) slice; the slice's
+//     compact rows [0, R) (recent ring) and [R, R + n_sink_b + n_sel) (sink +
+//     selected) are cut into 64-row tiles and split evenly over the C CTAs;
+//   * the tile split depends only on n_sink_b / n_sel, which no kernel of a fast
+//     step writes, so with SFI_FAST_PREFETCH the TMA producer issues its first
+//     stages BEFORE the programmatic-dependent-launch wait: the K/V stream of
+//     layer l starts while layer l-1's kernel drains;
+//   * producer warp: TMA (128B swizzle, L2 evict-first) into a 3-stage mbarrier
+//     ring; 4 consumer warps: QK^T and PV with mma.sync m16n8k16 bf16 -> fp32
+//     (query rows = the G heads of the GQA group, bf16 hi/lo split so the fp32
+//     query keeps ~16 mantissa bits), online softmax in the log2 domain;
+//   * aux warp (cluster rank 0): the current token. Its K/V come from the
+//     caller's k_new / v_new: it persists them (paged row L-1, ring slot
+//     (L-1) % R, fp64 norm — bit-identical to sfi_ring_append) and contributes
+//     the token's key as one more softmax partial; the ring slot's stale row is
+//     masked out of the tiles, so no CTA ever reads a row this kernel writes;
+//   * merge: every CTA leaves its 5 partials (m, l, O) in its own shared memory;
+//     after one cluster barrier each CTA merges a 1/C share of the G x D
+//     outputs reading all partials over DSMEM (fixed order: deterministic).
+#include <cooperative_groups.h>
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace sfi_impl {
+
+using namespace sfi_dev;
+
+namespace {
+
+constexpr int kTile = 64;
+constexpr int kNcw = 4;                        // consumer warps
+constexpr int kThreads = (kNcw + 2) * 32;      // + producer warp + aux warp
+constexpr int kStages = 3;
+constexpr int kParts = kNcw + 1;               // softmax partials per CTA
+
+template <int D>
+struct FGeo {
+  static constexpr int kBoxes = D / 64;
+  static constexpr int kBoxBytes = kTile * 128;
+  static constexpr int kTileBytes = kBoxes * kBoxBytes;
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kRing = kStages * kStageBytes;
+};
+
+template <int D, int G>
+struct FPart {  // partials, written over the (drained) stage ring
+  static constexpr int kO = kParts * G * D;       // floats
+  static constexpr int kBytes = (kO + 2 * kParts * G + 2 * G) * 4;
+  static_assert(kBytes <= FGeo<D>::kRing, "partials must fit in the stage ring");
+};
+template <int D>
+constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row
+  return FGeo<D>::kRing + 64 + D * 8;
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
+  return base + (chunk >> 3) * FGeo<D>::kBoxBytes + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// Tile t of a slice (ring tiles first) -> first compact row.
+__device__ __forceinline__ int tile_row(int t, int t_ring, int R) {
+  return t < t_ring ? t * kTile : R + (t - t_ring) * kTile;
+}
+
+// CTA-local combine of the kParts warp partials (160 threads: consumers + aux):
+// O into part 0 in place (each element touched by one thread), (m, l) into
+// comb_m / comb_l. Ends with the CTA-local barrier 1.
+template <int D, int G>
+__device__ __forceinline__ void combine_cta(float* part_o, const float* part_m, const float* part_l,
+                                            float* comb_m, float* comb_l, int tid) {
+  constexpr int kT = (kNcw + 1) * 32;
+  for (int e = tid; e < G * D; e += kT) {
+    const int g = e / D;
+    float m[kParts], M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kParts; ++w) {
+      m[w] = part_m[w * G + g];
+      M = fmaxf(M, m[w]);
+    }
+    const float Mu = (M == -INFINITY) ? 0.f : M;
+    float Ls = 0.f, Os = 0.f;
+#pragma unroll
+    for (int w = 0; w < kParts; ++w) {
+      const float l = part_l[w * G + g];
+      const float sc = l > 0.f ? fast_exp2(m[w] - Mu) : 0.f;
+      Ls += l * sc;
+      Os += (l > 0.f ? part_o[w * G * D + e] : 0.f) * sc;
+    }
+    part_o[e] = Os;
+    if (e % D == 0) {
+      comb_m[g] = M;
+      comb_l[g] = Ls;
+    }
+  }
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kThreads, 2)
+    fast_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                       const FastParams p) {
+  static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "GQA group 1..16");
+  static_assert(D == 64 || D == 128, "head_dim 64 or 128");
+  constexpr int NH = (G == 16) ? 2 : 1;   // query heads per mma row-thread
+  constexpr int NQ = (G == 16) ? 2 : 1;   // A-operand blocks (hi / lo) per k-step
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + FGeo<D>::kRing);
+  uint64_t* empty = full + kStages;
+  float* part_o = reinterpret_cast<float*>(smem);        // [kParts][G][D] (after the stream)
+  float* part_m = part_o + FPart<D, G>::kO;              // [kParts][G]
+  float* part_l = part_m + kParts * G;                   // [kParts][G]
+  float* comb_m = part_l + kParts * G;                   // [G] CTA-combined (m, l);
+  float* comb_l = comb_m + G;                            //     O combined in place in part 0
+  double* ksq = reinterpret_cast<double*>(smem + FGeo<D>::kRing + 64);  // [D] k_c^2 (aux)
+
+  long long* trace = p.trace ? p.trace + (size_t)blockIdx.x * 16 : nullptr;
+  if (trace && threadIdx.x == 0) {
+    trace[0] = (long long)globaltimer();
+    trace[6] = smid();
+  }
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int s = blockIdx.x / C;          // slice = b * H + h
+  const int b = s / p.H, h = s % p.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t slice_g = (size_t)(p.layer * p.B + b) * p.H + h;  // (layer, b, h)
+
+  if (threadIdx.x == kNcw * 32) {
+    tma_prefetch_desc(&tmk);
+    tma_prefetch_desc(&tmv);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kNcw);
+    }
+    fence_barrier_init();
+  }
+  // Static tile split over the compact layout [0, R) + [R, R + n_sink + K):
+  // no global load before the producer's first TMA. In steady-state decode
+  // n_sel = K, so it equals the live split; shorter selections only leave
+  // masked rows in the last tiles.
+  const int t_ring = (p.R + kTile - 1) / kTile;
+  const int T = t_ring + (p.crows - p.R + kTile - 1) / kTile;
+  const int tb = (int)(((long long)rank * T) / C), te = (int)(((long long)(rank + 1) * T) / C);
+  const int row_base = (int)(slice_g * p.crows);
+  __syncthreads();
+
+  if (warp == kNcw) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      if (!p.prefetch) griddep_wait();  // the compact rows may come from the predecessor
+      const uint64_t pol = l2_policy_evict_first();
+      for (int t = tb, i = 0; t < te; ++t, ++i) {
+        if (i == kStages) griddep_wait();  // the rest needs freed stages anyway
+        const int st = i % kStages;
+        const uint32_t ph = (i / kStages) & 1;
+        mbar_wait(&empty[st], ph ^ 1);
+        const int row = row_base + tile_row(t, t_ring, p.R);
+        uint8_t* kdst = smem + st * FGeo<D>::kStageBytes;
+        uint8_t* vdst = kdst + FGeo<D>::kTileBytes;
+        mbar_arrive_expect_tx(&full[st], FGeo<D>::kStageBytes);
+#pragma unroll
+        for (int bx = 0; bx < FGeo<D>::kBoxes; ++bx) {
+          tma_load_2d(kdst + bx * FGeo<D>::kBoxBytes, &tmk, bx * 64, row, &full[st], pol);
+          tma_load_2d(vdst + bx * FGeo<D>::kBoxBytes, &tmv, bx * 64, row, &full[st], pol);
+        }
+      }
+    }
+    __syncwarp();
+    if (trace && lane == 0) trace[10] = (long long)globaltimer();
+    griddep_wait();
+    griddep_launch();
+    cluster_sync_all();  // partials published
+    cluster_sync_all();  // merge done: shared memory may be released
+    return;
+  }
+
+  griddep_wait();
+  griddep_launch();
+  if (trace && threadIdx.x == 0) {
+    trace[1] = (long long)globaltimer();
+    trace[5] = te - tb;
+  }
+  // post-wait: lengths of this step
+  const int L = p.prefix_len[b];
+  const int rl = p.recent_len[b];
+  const int nsb = p.n_sink_b[b];
+  const int nsel = p.n_sel[slice_g];
+  const int n_cs = nsb + nsel;  // sink + selected rows
+  const bool geom_ok = nsb >= 0 && nsel >= 0 && n_cs <= p.crows - p.R;
+  const bool fused = p.k_new != nullptr;
+  // ring slots holding the recent window minus (fused) the current token
+  const int s0 = ((L - rl) % p.R + p.R) % p.R;   // slot of recent_start = L - rl + 1
+  const int ring_valid = fused ? rl - 1 : rl;
+  bool ok = geom_ok && rl <= p.R && rl >= (fused ? 1 : 0) && L >= 1 && L <= p.Lmax;
+
+  if (warp == kNcw + 1) {
+    // ---------------- aux: the current token ----------------
+    constexpr int kC = D / 32;
+    float mq[G], lq[G];
+    float vv[kC];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      mq[g] = -INFINITY;
+      lq[g] = 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < kC; ++c) vv[c] = 0.f;
+    const bool mine = rank == 0 && ok && fused;
+    if (rank == 0 && !ok && lane == 0)
+      raise_error(p.err, (rl < 1 && fused) || L < 1 || L > p.Lmax ? SFI_ERR_OUT_OF_RANGE : SFI_ERR_CONFIG);
+    if (mine) {
+      const size_t src = ((size_t)b * p.H + h) * D + lane * kC;
+      __nv_bfloat16 kx[kC], vx[kC];
+      float qv[G][kC];
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        kx[c] = p.k_new[src + c];
+        vx[c] = p.v_new[src + c];
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int c = 0; c < kC; ++c) qv[g][c] = p.q[((size_t)b * p.Hq + (size_t)h * G + g) * D + lane * kC + c];
+      // persist: paged row L-1, ring slot (L-1) % R (attention.cpp:141-142)
+      const size_t prow = (slice_g * p.Lmax + (L - 1)) * D + lane * kC;
+      const size_t rrow = (slice_g * p.crows + (L - 1) % p.R) * D + lane * kC;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        p.kc[prow + c] = kx[c];
+        p.vc[prow + c] = vx[c];
+        p.ck[rrow + c] = kx[c];
+        p.cv[rrow + c] = vx[c];
+        const double x = (double)__bfloat162float(kx[c]);
+        ksq[lane * kC + c] = __dmul_rn(x, x);  // exact: bf16^2 fits in fp64
+        vv[c] = __bfloat162float(vx[c]);
+      }
+      // the token's key as one more partial: m = q.k * log2(e)/sqrt(d), l = 1, O = v
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float d0 = 0.f;
+#pragma unroll
+        for (int c = 0; c < kC; ++c) d0 += qv[g][c] * __bfloat162float(kx[c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+        mq[g] = d0 * p.scale_log2;
+        lq[g] = 1.f;
+      }
+    }
+    if (trace && lane == 0) trace[8] = (long long)globaltimer();
+    asm volatile("bar.sync 1, %0;" ::"n"((kNcw + 1) * 32));  // stage ring drained
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int c = 0; c < kC; ++c) part_o[(kNcw * G + g) * D + lane * kC + c] = (lq[g] > 0.f) ? vv[c] : 0.f;
+      if (lane == 0) {
+        part_m[kNcw * G + g] = mq[g];
+        part_l[kNcw * G + g] = lq[g];
+      }
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"((kNcw + 1) * 32));  // all partials written
+    combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x - 32);
+    cluster_sync_all();
+    // fp64 key norm: sequential over c in round-to-nearest ops (attention.cpp:
+    // 143-150; bit-identical to append_kernel), off the critical path
+    if (mine && lane == 0) {
+      double acc = 0.0;
+#pragma unroll 16
+      for (int c = 0; c < D; ++c) acc = __dadd_rn(acc, ksq[c]);
+      p.norms[slice_g * p.Lmax + (L - 1)] = __dsqrt_rn(acc);
+    }
+    __syncwarp();
+    cluster_sync_all();
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int g = lane >> 2, t4 = lane & 3;
+  // Q fragments. G <= 8: rows 0..7 = bf16 hi of head g, rows 8..15 = lo.
+  // G == 16: block 0 = hi of heads 0..15, block 1 = lo.
+  uint32_t qa[NQ][D / 16][4];
+  {
+    const float* qb = p.q + ((size_t)b * p.Hq + (size_t)h * G) * D;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int c = ks * 16 + half * 8 + 2 * t4;
+        if constexpr (G == 16) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {  // r: row g (head g) / row g + 8 (head g + 8)
+            const float2 v = *reinterpret_cast<const float2*>(qb + (g + 8 * r) * D + c);
+            float h0, l0, h1, l1;
+            split_bf16(v.x, h0, l0);
+            split_bf16(v.y, h1, l1);
+            qa[0][ks][half * 2 + r] = pack_bf16(h0, h1);
+            qa[NQ - 1][ks][half * 2 + r] = pack_bf16(l0, l1);
+          }
+        } else {
+          float x0 = 0.f, x1 = 0.f;
+          if (g < G) {
+            const float2 v = *reinterpret_cast<const float2*>(qb + g * D + c);
+            x0 = v.x;
+            x1 = v.y;
+          }
+          float h0, l0, h1, l1;
+          split_bf16(x0, h0, l0);
+          split_bf16(x1, h1, l1);
+          qa[0][ks][half * 2 + 0] = pack_bf16(h0, h1);
+          qa[0][ks][half * 2 + 1] = pack_bf16(l0, l1);
+        }
+      }
+  }
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_run[NH], l_run[NH];
+#pragma unroll
+  for (int i = 0; i < NH; ++i) {
+    m_run[i] = -INFINITY;
+    l_run[i] = 0.f;
+  }
+  const float sl2 = p.scale_log2;
+  const int kw = warp * 16;
+
+  // every tile is waited for and released even when the step is invalid, so
+  // the producer never blocks and no TMA write is in flight at exit
+  for (int t = tb, i = 0; t < te; ++t, ++i) {
+    const int st = i % kStages;
+    const uint32_t ph = (i / kStages) & 1;
+    // validity of this warp's keys kw + j*8 + 2*t4 + e
+    bool valid[2][2];
+    const bool ring = t < t_ring;
+    const int r0 = tile_row(t, t_ring, p.R) + kw;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = r0 + j * 8 + 2 * t4 + e;
+        if (ring) {
+          int dlt = r - s0;
+          if (dlt < 0) dlt += p.R;
+          valid[j][e] = r < p.R && dlt < ring_valid;
+        } else {
+          valid[j][e] = (r - p.R) < n_cs;
+        }
+      }
+    const bool any =
+        __any_sync(0xffffffffu, ok && (valid[0][0] | valid[0][1] | valid[1][0] | valid[1][1]));
+    mbar_wait(&full[st], ph);
+    if (trace && i == 0 && threadIdx.x == 0) trace[2] = (long long)globaltimer();
+    if (any) {
+      const uint32_t kbase = smem_u32(smem + st * FGeo<D>::kStageBytes);
+      const uint32_t vbase = kbase + FGeo<D>::kTileBytes;
+      float acc[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < D / 16; kc += 2) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(swz<D>(kbase, kw + j * 8 + (lane & 7), kc * 2 + (lane >> 3)), b0, b1, b2, b3);
+#pragma unroll
+          for (int qb = 0; qb < NQ; ++qb) {
+            mma_bf16(acc[j], qa[qb][kc], b0, b1);
+            mma_bf16(acc[j], qa[qb][kc + 1], b2, b3);
+          }
+        }
+      }
+      // scores of head(s) of this thread, log2 domain
+      float sc[NH][2][2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if constexpr (NH == 2) {
+            sc[0][j][e] = acc[j][e];
+            sc[NH - 1][j][e] = acc[j][e + 2];
+          } else {
+            sc[0][j][e] = acc[j][e] + acc[j][e + 2];
+          }
+#pragma unroll
+          for (int hh = 0; hh < NH; ++hh) sc[hh][j][e] = valid[j][e] ? sc[hh][j][e] * sl2 : -INFINITY;
+        }
+      float pr[NH][2][2], alpha[NH];
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        float mx = fmaxf(fmaxf(sc[hh][0][0], sc[hh][0][1]), fmaxf(sc[hh][1][0], sc[hh][1][1]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run[hh], mx);
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        alpha[hh] = fast_exp2(m_run[hh] - m_use);
+        float psum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            pr[hh][j][e] = fast_exp2(sc[hh][j][e] - m_use);
+            psum += pr[hh][j][e];
+          }
+        l_run[hh] = l_run[hh] * alpha[hh] + psum;
+        m_run[hh] = m_new;
+      }
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= alpha[0];
+        o[n][1] *= alpha[0];
+        o[n][2] *= alpha[NH - 1];
+        o[n][3] *= alpha[NH - 1];
+      }
+      // P as the A operand (see header): G <= 8 rows g / g+8 = hi / lo of head g;
+      // G == 16 block 0 = hi of heads (g, g+8), block 1 = lo.
+      uint32_t pa[NQ][4];
+      {
+        float hi[NH][2][2], lo[NH][2][2];
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) split_bf16(pr[hh][j][e], hi[hh][j][e], lo[hh][j][e]);
+        if constexpr (NH == 2) {
+          pa[0][0] = pack_bf16(hi[0][0][0], hi[0][0][1]);
+          pa[0][1] = pack_bf16(hi[1][0][0], hi[1][0][1]);
+          pa[0][2] = pack_bf16(hi[0][1][0], hi[0][1][1]);
+          pa[0][3] = pack_bf16(hi[1][1][0], hi[1][1][1]);
+          pa[NQ - 1][0] = pack_bf16(lo[0][0][0], lo[0][0][1]);
+          pa[NQ - 1][1] = pack_bf16(lo[1][0][0], lo[1][0][1]);
+          pa[NQ - 1][2] = pack_bf16(lo[0][1][0], lo[0][1][1]);
+          pa[NQ - 1][3] = pack_bf16(lo[1][1][0], lo[1][1][1]);
+        } else {
+          pa[0][0] = pack_bf16(hi[0][0][0], hi[0][0][1]);
+          pa[0][1] = pack_bf16(lo[0][0][0], lo[0][0][1]);
+          pa[0][2] = pack_bf16(hi[0][1][0], hi[0][1][1]);
+          pa[0][3] = pack_bf16(lo[0][1][0], lo[0][1][1]);
+        }
+      }
+#pragma unroll
+      for (int nd = 0; nd < D / 8; nd += 2) {
+        const int mi = lane >> 3;
+        uint32_t v0, v1, v2, v3;
+        ldsm_x4_t(swz<D>(vbase, kw + (mi & 1) * 8 + (lane & 7), nd + (mi >> 1)), v0, v1, v2, v3);
+#pragma unroll
+        for (int qb = 0; qb < NQ; ++qb) {
+          mma_bf16(o[nd], pa[qb], v0, v1);
+          mma_bf16(o[nd + 1], pa[qb], v2, v3);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+  // ---- publish this warp's partial over the drained stage ring ----
+#pragma unroll
+  for (int hh = 0; hh < NH; ++hh) {
+    l_run[hh] += __shfl_xor_sync(0xffffffffu, l_run[hh], 1);
+    l_run[hh] += __shfl_xor_sync(0xffffffffu, l_run[hh], 2);
+  }
+  if (trace && threadIdx.x == 0) trace[9] = (long long)globaltimer();
+  asm volatile("bar.sync 1, %0;" ::"n"((kNcw + 1) * 32));
+  if (trace && threadIdx.x == 0) trace[12] = (long long)globaltimer();
+  if constexpr (NH == 2) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      float* dst = part_o + (warp * G + g + 8 * hh) * D;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n)
+        *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(o[n][2 * hh], o[n][2 * hh + 1]);
+      if (t4 == 0) {
+        part_m[warp * G + g + 8 * hh] = m_run[hh];
+        part_l[warp * G + g + 8 * hh] = l_run[hh];
+      }
+    }
+  } else if (g < G) {
+    float* dst = part_o + (warp * G + g) * D;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n)
+      *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(o[n][0] + o[n][2], o[n][1] + o[n][3]);
+    if (t4 == 0) {
+      part_m[warp * G + g] = m_run[0];
+      part_l[warp * G + g] = l_run[0];
+    }
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"((kNcw + 1) * 32));  // all partials written
+  combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x);
+  cluster_sync_all();
+  if (trace && threadIdx.x == 0) trace[13] = (long long)globaltimer();
+
+  // ---- merge: this CTA's share of the G x D outputs over the C CTA partials ----
+  const int total = G * D;
+  const int share = (total + C - 1) / C;
+  const int e0 = rank * share, e1 = min(total, e0 + share);
+  float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
+  for (int e = e0 + (int)threadIdx.x; e < e1; e += kNcw * 32) {
+    const int gg = e / D;
+    float mc[8], lc[8], oc[8];
+    float M = -INFINITY;
+    for (int c0 = 0; c0 < C; c0 += 8) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c0 + c < C) M = fmaxf(M, *cl.map_shared_rank(comb_m + gg, c0 + c));
+    }
+    const float Mu = (M == -INFINITY) ? 0.f : M;
+    float Ls = 0.f, Os = 0.f;
+    for (int c0 = 0; c0 < C; c0 += 8) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c0 + c < C) {
+          mc[c] = *cl.map_shared_rank(comb_m + gg, c0 + c);
+          lc[c] = *cl.map_shared_rank(comb_l + gg, c0 + c);
+          oc[c] = *cl.map_shared_rank(part_o + e, c0 + c);
+        }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c0 + c < C) {
+          const float sc = lc[c] > 0.f ? fast_exp2(mc[c] - Mu) : 0.f;
+          Ls += lc[c] * sc;
+          Os += (lc[c] > 0.f ? oc[c] : 0.f) * sc;
+        }
+    }
+    outp[e] = Ls > 0.f ? Os / Ls : 0.f;
+    if (rank == 0 && e == 0 && ok && !(Ls > 0.f)) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+  }
+  if (trace && threadIdx.x == 0) trace[14] = (long long)globaltimer();
+  cluster_sync_all();
+  if (trace && threadIdx.x == 0) trace[3] = (long long)globaltimer();
+}
+
+using FastFn = void (*)(CUtensorMap, CUtensorMap, FastParams);
+
+template <int D>
+FastFn pick(int G) {
+  switch (G) {
+    case 1: return fast_decode_kernel<D, 1>;
+    case 2: return fast_decode_kernel<D, 2>;
+    case 4: return fast_decode_kernel<D, 4>;
+    case 8: return fast_decode_kernel<D, 8>;
+    case 16: return fast_decode_kernel<D, 16>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
+int fast_cluster_size(int slices, int num_sms) {
+  int c = 1;
+  while (c < 8 && slices * c * 2 <= 2 * num_sms) c *= 2;
+  return c;
+}
+
+cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
+                               int G, int C, cudaStream_t stream) {
+  FastFn fn = (D == 64) ? pick<64>(G) : pick<128>(G);
+  if (!fn || C < 1 || C > 8) return cudaErrorInvalidValue;
+  const int smem = D == 64 ? fast_smem_bytes<64>() : fast_smem_bytes<128>();
+  static bool configured[2][17] = {};
+  bool& done = configured[D == 64 ? 0 : 1][G];
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.B * p.H * C);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, fn, tmk, tmv, p);
+}
+
+}  // namespace sfi_impl

@@ -8,6 +8,8 @@
 
 #include <utility>
 
+#include <cuda_bf16.h>
+
 #include "sfi_b200.h"
 
 namespace sfi_impl {
@@ -60,6 +62,31 @@ int decode_smem_bytes(int D, int G, int slices);
 int decode_grid(int tiles_upper, int num_sms);
 cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv,
                           int D, int G, int ctas, cudaStream_t stream);
+
+// fast_decode.cu: fast-step sparse decode, optionally fused with the append
+struct FastParams {
+  const float* q;                 // [B][Hq][D]
+  float* out;                     // [B][Hq][D]
+  const __nv_bfloat16* k_new;     // [B][H][D] current token (null: already appended)
+  const __nv_bfloat16* v_new;
+  __nv_bfloat16* kc;              // paged cache (persist the current token)
+  __nv_bfloat16* vc;
+  __nv_bfloat16* ck;              // compact cache (ring slot)
+  __nv_bfloat16* cv;
+  double* norms;
+  const int32_t* prefix_len;
+  const int32_t* n_sink_b;
+  const int32_t* recent_len;
+  const int32_t* n_sel;           // [layers][B][H]
+  uint32_t* err;
+  int layer, B, H, Hq, Lmax, crows, R;
+  int prefetch;                   // SFI_FAST_PREFETCH: stream before the PDL wait
+  float scale_log2;               // log2(e) / sqrt(d)
+  long long* trace;               // debug: per-CTA globaltimer stamps [grid][16] (null = off)
+};
+int fast_cluster_size(int slices, int num_sms);
+cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
+                               int G, int C, cudaStream_t stream);
 
 // cache_ops.cu
 cudaError_t launch_step_advance(const sfi_shape& s, const sfi_cache& c, cudaStream_t st);

@@ -105,6 +105,17 @@ class SfiCache:
         _C.sparse_decode(self.shape, self.cache, layer, self._ptr(q, torch.float32),
                          self._ptr(out, torch.float32), self._stream(stream))
 
+    def fast_decode(self, layer: int, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
+                    out: torch.Tensor, prefetch: bool = False, stream=None):
+        """One fast step of one layer in ONE launch: ring_append(k_new, v_new) fused
+        with sparse_decode. prefetch=True streams the layer's compact rows before
+        the PDL wait (valid unless the preceding kernel rebuilt this layer's
+        compact cache, include/sfi_b200.h)."""
+        _C.fast_decode(self.shape, self.cache, layer, self._ptr(q, torch.float32),
+                       self._ptr(k_new, torch.bfloat16), self._ptr(v_new, torch.bfloat16),
+                       self._ptr(out, torch.float32), _C.FAST_PREFETCH if prefetch else 0,
+                       self._stream(stream))
+
     def selector(self, layer: int, logits: torch.Tensor, params=None, stream=None):
         _C.selector(self.shape, self.cache, layer, self._ptr(logits, torch.float32),
                     params if params is not None else _C.SelectorParams(), self._stream(stream))

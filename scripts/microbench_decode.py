@@ -88,9 +88,54 @@ def trace(tag):
               f"fence={live[i,9]/1e3:.2f} merge={live[i,10]/1e3:.2f}us")
 
 
+def trace_fast(tag):
+    if not os.environ.get("SFI_DECODE_TRACE"):
+        return
+    buf = (C.c_int64 * (16 * 1024))()
+    n = lib.sfi_debug_decode_trace(buf, 1024)
+    a = np.frombuffer(buf, dtype=np.int64)[: 16 * n].reshape(n, 16).astype(np.float64)
+    live = a[a[:, 0] > 0]
+    t0 = live[:, 0].min()
+    rel = lambda i: (live[:, i] - t0) / 1e3
+    st, wt, ft, cd, c1, md, en = rel(0), rel(1), rel(2), rel(12), rel(13), rel(14), rel(3)
+    q = lambda x: f"{np.percentile(x, 10):.2f}/{np.median(x):.2f}/{x.max():.2f}"
+    print(f"[{tag}] ctas={n} (p10/med/max us from first CTA start) start={q(st)} post-wait={q(wt)} "
+          f"first-tile={q(ft)} consumers-done={q(cd)} cluster-sync1={q(c1)} merge-done={q(md)} end={q(en)} "
+          f"tiles mean={live[:,5].mean():.1f}")
+    aux = (live[:, 8] - t0) / 1e3
+    aux = aux[live[:, 8] > 0]
+    print(f"   consumer-loop-done={q(rel(9))} producer-issued={q(rel(10))} aux-ready(rank0)={q(aux) if len(aux) else '-'}")
+    sms = live[:, 6].astype(int)
+    cnt = np.bincount(sms, minlength=148)
+    print(f"   CTAs per SM: {np.bincount(cnt)} ; busy(end-start) med={np.median(en-st):.2f}")
+
+
 res = {}
 res["sparse_us"] = timeit(lambda i: c.sparse_decode(i % L, q[i % L], out[i % L]), args.iters)
 trace("sparse")
+kn = torch.randn(L, B, H, d, device="cuda").bfloat16()
+res["fast_us"] = timeit(lambda i: c.fast_decode(i % L, q[i % L], kn[i % L], kn[i % L], out[i % L], prefetch=True), args.iters)
+trace_fast("fast single")
+res["fast_noprefetch_us"] = timeit(lambda i: c.fast_decode(i % L, q[i % L], kn[i % L], kn[i % L], out[i % L]), args.iters)
+
+
+def back_to_back(fn, n):  # n launches between two events (PDL overlap between launches)
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(3):
+        fn(i)
+    a.record(s)
+    for i in range(n):
+        fn(i)
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e3 / n
+
+
+res["fast_b2b_us"] = back_to_back(lambda i: c.fast_decode(i % L, q[i % L], kn[i % L], kn[i % L], out[i % L], prefetch=True), 64)
+trace_fast("fast b2b prefetch")
+res["fast_b2b_noprefetch_us"] = back_to_back(lambda i: c.fast_decode(i % L, q[i % L], kn[i % L], kn[i % L], out[i % L]), 64)
+res["sparse_b2b_us"] = back_to_back(lambda i: c.sparse_decode(i % L, q[i % L], out[i % L]), 64)
 res["dense_us"] = timeit(lambda i: c.dense_decode(i % L, q[i % L], out[i % L], logits, 0), max(6, args.iters // 3))
 trace("dense")
 res["selector_us"] = timeit(lambda i: c.selector(i % L, logits, prm), 10)
@@ -101,6 +146,42 @@ S = 256 + 4 + 2048
 sp_bytes = B * H * S * 4 * d
 de_bytes = B * H * (ctx + 1) * 4 * d
 res["sparse_GBs"] = sp_bytes / res["sparse_us"][0] / 1e3
+res["fast_b2b_GBs"] = sp_bytes / res["fast_b2b_us"] / 1e3
 res["dense_GBs"] = de_bytes / res["dense_us"][0] / 1e3
 print(json.dumps(res))
 c.check_errors()
+
+
+def graph_per_launch(fn, n, reps=5):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(n):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(reps):
+        g.replay()
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e3 / (n * reps)
+
+
+if not os.environ.get("SFI_DECODE_TRACE"):
+    gr = {}
+    gr["graph_fast_prefetch_us"] = graph_per_launch(
+        lambda i: c.fast_decode(i % L, q[i % L], kn[i % L], kn[i % L], out[i % L], prefetch=True), L)
+    def with_adv(i):
+        if i == 0:
+            c.step_advance()
+        c.fast_decode(i % L, q[i % L], kn[i % L], kn[i % L], out[i % L], prefetch=True)
+
+    gr["graph_adv_fast_prefetch_us"] = graph_per_launch(with_adv, L)
+    gr["graph_fast_us"] = graph_per_launch(
+        lambda i: c.fast_decode(i % L, q[i % L], kn[i % L], kn[i % L], out[i % L]), 36)
+    gr["graph_sparse_us"] = graph_per_launch(lambda i: c.sparse_decode(i % L, q[i % L], out[i % L]), 36)
+    gr["graph_dense_us"] = graph_per_launch(lambda i: c.dense_decode(i % L, q[i % L], out[i % L], logits, 0), 8)
+    gr["graph_fast_GBs"] = sp_bytes / gr["graph_fast_prefetch_us"] / 1e3
+    print(json.dumps(gr))

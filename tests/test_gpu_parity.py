@@ -325,3 +325,85 @@ def test_selector_error_paths():
     assert e.value.code == "non_finite_input"
     with pytest.raises(sfi.SfiError):
         sfi.select_top_k([1.0], [1], -1)
+
+
+@pytest.mark.parametrize("H,Hq,R,lens,prefetch", [
+    (2, 4, 32, [700, 650], True),      # G = 4
+    (2, 2, 100, [700, 333], False),    # G = 1, ring not a multiple of the 64-row tile
+    (4, 8, 64, [1200], True),          # G = 2
+    (1, 8, 32, [900, 40], True),       # G = 8; request 1: recent window still filling, |J| = 0
+    (2, 32, 64, [800], False),         # G = 16 (Qwen3-235B group)
+])
+def test_fast_decode_fused_matches_append_plus_sparse(H, Hq, R, lens, prefetch):
+    """sfi_fast_decode (ONE launch) == sfi_ring_append + attention_kernel_sparse:
+    paged row, ring slot and fp64 key norm bit-exact; output within 2e-3."""
+    torch = _torch()
+    B, ns, K, d = len(lens), 4, 64, 128
+    c = _cache(L=2, B=B, H=H, Hq=Hq, d=d, Lmax=1536, ns=ns, K=K, R=R)
+    c.fill_synthetic(seed=21, length=max(lens))
+    c.set_lengths(lens, [ns] * B)
+    rng = np.random.default_rng(R + Hq)
+    sels = {}
+    for l in range(2):
+        for b in range(B):
+            L, nsb, rl, j0, j1 = _window(c, b)
+            for h in range(H):
+                n = int(rng.integers(0, min(K, max(0, j1 - j0 + 1)) + 1))
+                pos = np.sort(rng.choice(np.arange(j0, j1 + 1), size=n, replace=False)).astype(np.int32)
+                c.sel[l, b, h, :n] = torch.from_numpy(pos).cuda()
+                c.n_sel[l, b, h] = n
+                sels[(l, b, h)] = pos
+        c.compact_build(l, rebuild_ring=True)
+    c.step_advance()
+    g = torch.Generator().manual_seed(17)
+    orc = oracle()
+    for l in range(2):
+        k_new = torch.from_numpy(bf16_round(torch.randn(B, H, d, generator=g).numpy())).bfloat16().cuda()
+        v_new = torch.from_numpy(bf16_round(torch.randn(B, H, d, generator=g).numpy())).bfloat16().cuda()
+        q = torch.randn(B, Hq, d, generator=g)
+        out = torch.full((B, Hq, d), float("nan")).cuda()
+        c.fast_decode(l, q.cuda().contiguous(), k_new, v_new, out, prefetch=prefetch)
+        torch.cuda.synchronize()
+        c.check_errors()
+        for b in range(B):
+            L, nsb, rl, j0, j1 = _window(c, b)
+            assert np.array_equal(c.k_cache[l, b, :, L - 1].float().cpu().numpy(), k_new[b].float().cpu().numpy())
+            assert np.array_equal(c.v_cache[l, b, :, L - 1].float().cpu().numpy(), v_new[b].float().cpu().numpy())
+            slot = (L - 1) % R
+            assert np.array_equal(c.ck[l, b, :, slot].float().cpu().numpy(), k_new[b].float().cpu().numpy())
+            assert np.array_equal(c.cv[l, b, :, slot].float().cpu().numpy(), v_new[b].float().cpu().numpy())
+            k, v = _rows(c, l, b, L)
+            st = store_from_rows(orc, k, v, Hq)
+            for h in range(H):
+                assert c.key_norms[l, b, h, L - 1].item() == st.key_norm(0, h, L)
+            sink = list(range(1, nsb + 1))
+            sel = [sels[(l, b, h)] for h in range(H)]
+            st.reorganize(0, sink, sel)
+            want, _ = st.attention_sparse(0, q[b].double().numpy(), sink, sel, L - rl + 1, rl)
+            assert rel_err(out[b].cpu().numpy().reshape(-1), want) < TOL, (l, b)
+
+
+def test_sparse_decode_group16():
+    """G = 16 through the plain sparse entry (current token already appended)."""
+    torch = _torch()
+    H, Hq, B, R, d = 2, 32, 1, 64, 128
+    c = _cache(L=1, B=B, H=H, Hq=Hq, d=d, Lmax=1024, ns=4, K=64, R=R)
+    c.fill_synthetic(seed=5, length=600)
+    c.set_lengths([600], [4])
+    L, nsb, rl, j0, j1 = _window(c, 0)
+    rng = np.random.default_rng(2)
+    sel = [np.sort(rng.choice(np.arange(j0, j1 + 1), size=64, replace=False)).astype(np.int32) for _ in range(H)]
+    for h in range(H):
+        c.sel[0, 0, h, :64] = torch.from_numpy(sel[h]).cuda()
+        c.n_sel[0, 0, h] = 64
+    c.compact_build(0, rebuild_ring=True)
+    q = torch.randn(B, Hq, d, generator=torch.Generator().manual_seed(4))
+    out = torch.zeros_like(q).cuda()
+    c.sparse_decode(0, q.cuda().contiguous(), out)
+    torch.cuda.synchronize()
+    c.check_errors()
+    k, v = _rows(c, 0, 0, L)
+    st = store_from_rows(oracle(), k, v, Hq)
+    st.reorganize(0, list(range(1, nsb + 1)), sel)
+    want, _ = st.attention_sparse(0, q[0].double().numpy(), list(range(1, nsb + 1)), sel, L - rl + 1, rl)
+    assert rel_err(out[0].cpu().numpy().reshape(-1), want) < TOL
