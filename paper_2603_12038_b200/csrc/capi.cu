@@ -132,7 +132,6 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   if ((rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
   if (!q || !out) return fail(SFI_ERR_INVALID_ARGUMENT, "decode: q/out null");
   if (pool != SFI_POOL_MEAN && pool != SFI_POOL_MAX) return fail(SFI_ERR_CONFIG, "decode: bad pool mode");
-  if (group_of(*s) > 8) return fail(SFI_ERR_UNSUPPORTED, "dense decode: GQA group 16 not built yet");
   const int D = s->head_dim;
   const uint64_t slices = (uint64_t)s->n_layers * s->batch * s->n_kv_heads;
   const uint64_t rows_per = sparse ? (uint64_t)compact_rows(*s) : (uint64_t)s->max_positions;
@@ -266,11 +265,14 @@ long long* decode_trace_buffer() {
   return buf;
 }
 
+// rows of one stream-K partial: 8, or 16 for GQA group 16 (decode.cu part_rows)
+static size_t part_rows(const sfi_shape& s) { return group_of(s) > 8 ? 16 : 8; }
+
 size_t workspace_bytes(const sfi_shape& s) {
   const size_t slices = (size_t)s.batch * s.n_kv_heads;
   size_t b = 0;
-  b += align_up((size_t)kMaxCtas * 2 * 8 * s.head_dim * sizeof(float));
-  b += align_up((size_t)kMaxCtas * 2 * 2 * 8 * sizeof(float));
+  b += align_up((size_t)kMaxCtas * 2 * part_rows(s) * s.head_dim * sizeof(float));
+  b += align_up((size_t)kMaxCtas * 2 * 2 * part_rows(s) * sizeof(float));
   b += align_up(slices * sizeof(int32_t));
   b += 2 * align_up(slices * (size_t)s.max_positions * sizeof(double));
   return b;
@@ -281,9 +283,9 @@ Workspace carve_workspace(const sfi_shape& s, void* base) {
   uint8_t* p = static_cast<uint8_t*>(base);
   Workspace w;
   w.part_o = reinterpret_cast<float*>(p);
-  p += align_up((size_t)kMaxCtas * 2 * 8 * s.head_dim * sizeof(float));
+  p += align_up((size_t)kMaxCtas * 2 * part_rows(s) * s.head_dim * sizeof(float));
   w.part_ml = reinterpret_cast<float*>(p);
-  p += align_up((size_t)kMaxCtas * 2 * 2 * 8 * sizeof(float));
+  p += align_up((size_t)kMaxCtas * 2 * 2 * part_rows(s) * sizeof(float));
   w.counters = reinterpret_cast<int32_t*>(p);
   p += align_up(slices * sizeof(int32_t));
   w.sel.a = reinterpret_cast<double*>(p);

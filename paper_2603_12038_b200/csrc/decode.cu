@@ -47,17 +47,24 @@ constexpr int kTile = 64;   // keys per pipeline stage
 constexpr int kNcw = 4;     // consumer warps (16 keys of each tile each)
 constexpr int kThreads = (kNcw + 2) * 32;   // + TMA producer warp + epilogue warp
 constexpr int kBarThreads = (kNcw + 1) * 32; // consumers + epilogue on the hand-off barriers
-constexpr int kStages = 3;
 constexpr int kMaxSlices = 4096;
 
-template <int D>
+// G = 16 holds 2x the consumer partials: 2 stages keep 2 CTAs per SM
+template <int G>
+__host__ __device__ constexpr int stages_for() { return G == 16 ? 2 : 3; }
+
+template <int D, int G>
 struct Geo {
+  static constexpr int kStages = stages_for<G>();
   static constexpr int kBoxes = D / 64;                   // 128-byte TMA boxes per row
   static constexpr int kBoxBytes = kTile * 128;           // 8 KB
   static constexpr int kTileBytes = kBoxes * kBoxBytes;   // one tensor, one tile
   static constexpr int kStageBytes = 2 * kTileBytes;      // K + V
   static constexpr int kRing = kStages * kStageBytes;
 };
+// rows of one published partial (m, l, O): 8, or 16 for G = 16
+template <int G>
+__host__ __device__ constexpr int part_rows() { return G > 8 ? 16 : 8; }
 
 // consumer -> epilogue hand-off: per consumer warp G rows of O plus (m, l)
 // for 8 rows. The 8-float column chunks of row g are XOR-swizzled by g so the
@@ -66,10 +73,11 @@ struct Geo {
 template <int D, int G>
 struct Comb {
   static constexpr int kOFloats = kNcw * G * D;
-  static constexpr int kBytes = kOFloats * 4 + kNcw * 2 * 8 * 4;
-  static constexpr int kSmemFixed = Geo<D>::kRing + kBytes + 64 /*barriers*/;
+  static constexpr int kBytes = kOFloats * 4 + kNcw * 2 * G * 4;
+  static constexpr int kSmemFixed = Geo<D, G>::kRing + kBytes + 64 /*barriers*/;
 };
-__device__ __forceinline__ int comb_col(int col, int g) { return col ^ (g << 3); }
+template <int D>
+__device__ __forceinline__ int comb_col(int col, int g) { return col ^ ((g << 3) & (D - 1)); }
 
 struct Slice {
   int off[3];
@@ -83,7 +91,7 @@ __device__ __forceinline__ int seg_tiles(int c) { return (c + kTile - 1) / kTile
 // 128B-swizzled address of 16-byte chunk `chunk` (8 bf16) of tile row `row`.
 template <int D>
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
-  return base + (chunk >> 3) * Geo<D>::kBoxBytes + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
+  return base + (chunk >> 3) * (kTile * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
 }
 
 // Segments are fixed slots (0: ring part 1, 1: ring wrap, 2: sink+selected)
@@ -172,6 +180,7 @@ __device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, int
   constexpr int kCols = D / 32;
   constexpr int kGB = G < 4 ? G : 4;
   constexpr int kCB = 4;  // contributors per load batch
+  constexpr int PR = part_rows<G>();
   using Vec = typename std::conditional<kCols == 4, float4, float2>::type;
 #pragma unroll
   for (int g0 = 0; g0 < G; g0 += kGB) {
@@ -192,8 +201,8 @@ __device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, int
       float mi[kGB], li[kGB], sc[kGB];
 #pragma unroll
       for (int gg = 0; gg < kGB; ++gg) {
-        mi[gg] = ok ? __ldcg(&p.part_ml[((size_t)pc * 2 + 0) * 8 + g0 + gg]) : -INFINITY;
-        li[gg] = ok ? __ldcg(&p.part_ml[((size_t)pc * 2 + 1) * 8 + g0 + gg]) : 0.f;
+        mi[gg] = ok ? __ldcg(&p.part_ml[((size_t)pc * 2 + 0) * PR + g0 + gg]) : -INFINITY;
+        li[gg] = ok ? __ldcg(&p.part_ml[((size_t)pc * 2 + 1) * PR + g0 + gg]) : 0.f;
       }
 #pragma unroll
       for (int gg = 0; gg < kGB; ++gg) {
@@ -228,7 +237,7 @@ __device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, int
           const int pj = __shfl_sync(0xffffffffu, pc, src[j]);
 #pragma unroll
           for (int gg = 0; gg < kGB; ++gg)
-            x[j][gg] = __ldcg(reinterpret_cast<const Vec*>(p.part_o + ((size_t)pj * 8 + g0 + gg) * D) + lane);
+            x[j][gg] = __ldcg(reinterpret_cast<const Vec*>(p.part_o + ((size_t)pj * PR + g0 + gg) * D) + lane);
         }
 #pragma unroll
         for (int j = 0; j < kCB; ++j)
@@ -264,14 +273,18 @@ template <int D, int G>
 __global__ void __launch_bounds__(kThreads, 2)
     decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                   const DecodeParams p) {
-  static_assert(G >= 1 && G <= 8, "GQA group of at most 8 query heads per KV head");
+  static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "GQA group 1..16");
   static_assert(D == 64 || D == 128, "head_dim 64 or 128");
+  constexpr int NH = (G == 16) ? 2 : 1;   // query heads per mma row-thread
+  constexpr int NQ = (G == 16) ? 2 : 1;   // A-operand blocks (hi / lo) per k-step
+  constexpr int PR = part_rows<G>();
+  constexpr int kStages = Geo<D, G>::kStages;
   // 1024-byte alignment (128B-swizzled TMA boxes) without padding slack: the
   // kernel has no static shared memory, so the dynamic window starts at 0
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* comb_o = reinterpret_cast<float*>(smem + Geo<D>::kRing);           // [kNcw][G][kRow]
-  float* comb_ml = comb_o + Comb<D, G>::kOFloats;                           // [kNcw][2][8]
-  uint64_t* full = reinterpret_cast<uint64_t*>(comb_ml + kNcw * 2 * 8);
+  float* comb_o = reinterpret_cast<float*>(smem + Geo<D, G>::kRing);        // [kNcw][G][kRow]
+  float* comb_ml = comb_o + Comb<D, G>::kOFloats;                           // [kNcw][2][G]
+  uint64_t* full = reinterpret_cast<uint64_t*>(comb_ml + kNcw * 2 * G);
   uint64_t* empty = full + kStages;
   int* pref = reinterpret_cast<int*>(empty + kStages + 2);                  // [S + 1]
 
@@ -348,13 +361,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         int off, nv;
         tile_at(sl, t - pref[s], off, nv);
         const int row = sl.row_base + off;
-        uint8_t* kdst = smem + st * Geo<D>::kStageBytes;
-        uint8_t* vdst = kdst + Geo<D>::kTileBytes;
-        mbar_arrive_expect_tx(&full[st], Geo<D>::kStageBytes);
+        uint8_t* kdst = smem + st * Geo<D, G>::kStageBytes;
+        uint8_t* vdst = kdst + Geo<D, G>::kTileBytes;
+        mbar_arrive_expect_tx(&full[st], Geo<D, G>::kStageBytes);
 #pragma unroll
-        for (int bx = 0; bx < Geo<D>::kBoxes; ++bx) {
-          tma_load_2d(kdst + bx * Geo<D>::kBoxBytes, &tmk, bx * 64, row, &full[st], pol);
-          tma_load_2d(vdst + bx * Geo<D>::kBoxBytes, &tmv, bx * 64, row, &full[st], pol);
+        for (int bx = 0; bx < Geo<D, G>::kBoxes; ++bx) {
+          tma_load_2d(kdst + bx * Geo<D, G>::kBoxBytes, &tmk, bx * 64, row, &full[st], pol);
+          tma_load_2d(vdst + bx * Geo<D, G>::kBoxBytes, &tmv, bx * 64, row, &full[st], pol);
         }
       }
     }
@@ -386,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         float mw[kNcw], M = -INFINITY;
 #pragma unroll
         for (int w = 0; w < kNcw; ++w) {
-          mw[w] = comb_ml[(w * 2 + 0) * 8 + gg];
+          mw[w] = comb_ml[(w * 2 + 0) * G + gg];
           M = fmaxf(M, mw[w]);
         }
         const float Mu = (M == -INFINITY) ? 0.f : M;
@@ -397,9 +410,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int w = 0; w < kNcw; ++w) {
           const float sc = fast_exp2(mw[w] - Mu);
-          L += comb_ml[(w * 2 + 1) * 8 + gg] * sc;
+          L += comb_ml[(w * 2 + 1) * G + gg] * sc;
           const Vec x = *reinterpret_cast<const Vec*>(comb_o + (w * G + gg) * D +
-                                                      comb_col(lane * kCols, gg));
+                                                      comb_col<D>(lane * kCols, gg));
           a.x += x.x * sc;
           a.y += x.y * sc;
           if constexpr (kCols == 4) {
@@ -437,10 +450,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         const size_t part = (size_t)blockIdx.x * 2 + slot;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
-          reinterpret_cast<Vec*>(p.part_o + (part * 8 + gg) * D)[lane] = acc[gg];
+          reinterpret_cast<Vec*>(p.part_o + (part * PR + gg) * D)[lane] = acc[gg];
           if (lane == gg) {
-            p.part_ml[(part * 2 + 0) * 8 + gg] = mr[gg];
-            p.part_ml[(part * 2 + 1) * 8 + gg] = lr[gg];
+            p.part_ml[(part * 2 + 0) * PR + gg] = mr[gg];
+            p.part_ml[(part * 2 + 1) * PR + gg] = lr[gg];
           }
         }
         pend[n_pend++] = s;
@@ -486,9 +499,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   // ---------------- consumers ----------------
   const int g = lane >> 2, t4 = lane & 3;
   const float sl2 = p.scale_log2;
-  uint32_t qa[D / 16][4];
+  uint32_t qa[NQ][D / 16][4];
   float o[D / 8][4];
-  float m_run = -INFINITY, l_run = 0.f;
+  float m_run[NH], l_run[NH];
   int s = s_first;
   Slice sl = make_slice(p, s, false);
   bool fresh = true;
@@ -496,31 +509,47 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int t = tb, i = 0; t < te; ++t, ++i) {
     while (pref[s + 1] <= t) sl = make_slice(p, ++s, false);
     if (fresh) {
-      // Q fragments: rows 0..7 = bf16 hi of query head g (< G), rows 8..15 = lo
+      // Q fragments. G <= 8: rows 0..7 = bf16 hi of head g (< G), rows 8..15 = lo.
+      // G == 16: block 0 = hi of heads 0..15, block 1 = lo.
       const int b = s / p.H, h = s % p.H;
-      const float* qg = p.q + ((size_t)b * p.Hq + (size_t)h * G + g) * D;
+      const float* qb = p.q + ((size_t)b * p.Hq + (size_t)h * G) * D;
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           const int c = ks * 16 + half * 8 + 2 * t4;
-          float x0 = 0.f, x1 = 0.f;
-          if (g < G) {
-            const float2 v = *reinterpret_cast<const float2*>(qg + c);
-            x0 = v.x;
-            x1 = v.y;
+          if constexpr (G == 16) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const float2 v = *reinterpret_cast<const float2*>(qb + (g + 8 * r) * D + c);
+              float h0, l0, h1, l1;
+              split_bf16(v.x, h0, l0);
+              split_bf16(v.y, h1, l1);
+              qa[0][ks][half * 2 + r] = pack_bf16(h0, h1);
+              qa[NQ - 1][ks][half * 2 + r] = pack_bf16(l0, l1);
+            }
+          } else {
+            float x0 = 0.f, x1 = 0.f;
+            if (g < G) {
+              const float2 v = *reinterpret_cast<const float2*>(qb + g * D + c);
+              x0 = v.x;
+              x1 = v.y;
+            }
+            float h0, l0, h1, l1;
+            split_bf16(x0, h0, l0);
+            split_bf16(x1, h1, l1);
+            qa[0][ks][half * 2 + 0] = pack_bf16(h0, h1);
+            qa[0][ks][half * 2 + 1] = pack_bf16(l0, l1);
           }
-          float h0, l0, h1, l1;
-          split_bf16(x0, h0, l0);
-          split_bf16(x1, h1, l1);
-          qa[ks][half * 2 + 0] = pack_bf16(h0, h1);
-          qa[ks][half * 2 + 1] = pack_bf16(l0, l1);
         }
       }
 #pragma unroll
       for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-      m_run = -INFINITY;
-      l_run = 0.f;
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        m_run[hh] = -INFINITY;
+        l_run[hh] = 0.f;
+      }
       fresh = false;
     }
     const int st = i % kStages;
@@ -531,8 +560,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (trace && i == 0 && threadIdx.x == 0) trace[2] = (long long)globaltimer();
     const int kw = warp * 16;  // this warp's first key in the tile
     if (kw < nv) {
-      const uint32_t kbase = smem_u32(smem + st * Geo<D>::kStageBytes);
-      const uint32_t vbase = kbase + Geo<D>::kTileBytes;
+      const uint32_t kbase = smem_u32(smem + st * Geo<D, G>::kStageBytes);
+      const uint32_t vbase = kbase + Geo<D, G>::kTileBytes;
       // ---- S = Q K^T for 16 keys ----
       float acc[2][4];
 #pragma unroll
@@ -543,17 +572,25 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int j = 0; j < 2; ++j) {
           uint32_t b0, b1, b2, b3;
           ldsm_x4(swz<D>(kbase, kw + j * 8 + (lane & 7), kc * 2 + (lane >> 3)), b0, b1, b2, b3);
-          mma_bf16(acc[j], qa[kc], b0, b1);
-          mma_bf16(acc[j], qa[kc + 1], b2, b3);
+#pragma unroll
+          for (int qb = 0; qb < NQ; ++qb) {
+            mma_bf16(acc[j], qa[qb][kc], b0, b1);
+            mma_bf16(acc[j], qa[qb][kc + 1], b2, b3);
+          }
         }
       }
-      float sc[2][2];
+      float sc[NH][2][2];
       bool valid[2][2];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          sc[j][e] = acc[j][e] + acc[j][e + 2];
+          if constexpr (NH == 2) {
+            sc[0][j][e] = acc[j][e];
+            sc[NH - 1][j][e] = acc[j][e + 2];
+          } else {
+            sc[0][j][e] = acc[j][e] + acc[j][e + 2];
+          }
           valid[j][e] = (kw + j * 8 + 2 * t4 + e) < nv;
         }
       // ---- pooled logits over J (dense slow step) ----
@@ -564,13 +601,16 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              float v = sc[j][e] * p.inv_sqrt_d;
+              float v;
               if (p.pool == SFI_POOL_MAX) {
-                if (g >= G) v = -INFINITY;
+                v = (NH == 2 || g < G) ? sc[0][j][e] * p.inv_sqrt_d : -INFINITY;
+                if constexpr (NH == 2) v = fmaxf(v, sc[NH - 1][j][e] * p.inv_sqrt_d);
                 v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
                 v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
                 v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
               } else {
+                v = sc[0][j][e] * p.inv_sqrt_d;
+                if constexpr (NH == 2) v += sc[NH - 1][j][e] * p.inv_sqrt_d;
                 v += __shfl_xor_sync(0xffffffffu, v, 4);
                 v += __shfl_xor_sync(0xffffffffu, v, 8);
                 v += __shfl_xor_sync(0xffffffffu, v, 16);
@@ -583,48 +623,65 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       // ---- online softmax (log2 domain) ----
-      float mx = -INFINITY;
+      float pr[NH][2][2], alpha[NH];
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int hh = 0; hh < NH; ++hh) {
+        float mx = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          sc[j][e] = valid[j][e] ? sc[j][e] * sl2 : -INFINITY;
-          mx = fmaxf(mx, sc[j][e]);
-        }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float m_new = fmaxf(m_run, mx);
-      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-      const float alpha = fast_exp2(m_run - m_use);
-      float pr[2][2], psum = 0.f;
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+          for (int e = 0; e < 2; ++e) {
+            sc[hh][j][e] = valid[j][e] ? sc[hh][j][e] * sl2 : -INFINITY;
+            mx = fmaxf(mx, sc[hh][j][e]);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run[hh], mx);
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        alpha[hh] = fast_exp2(m_run[hh] - m_use);
+        float psum = 0.f;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          pr[j][e] = fast_exp2(sc[j][e] - m_use);
-          psum += pr[j][e];
-        }
-      l_run = l_run * alpha + psum;
-      m_run = m_new;
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            pr[hh][j][e] = fast_exp2(sc[hh][j][e] - m_use);
+            psum += pr[hh][j][e];
+          }
+        l_run[hh] = l_run[hh] * alpha[hh] + psum;
+        m_run[hh] = m_new;
+      }
 #pragma unroll
       for (int n = 0; n < D / 8; ++n) {
-        o[n][0] *= alpha;
-        o[n][1] *= alpha;
-        o[n][2] *= alpha;
-        o[n][3] *= alpha;
+        o[n][0] *= alpha[0];
+        o[n][1] *= alpha[0];
+        o[n][2] *= alpha[NH - 1];
+        o[n][3] *= alpha[NH - 1];
       }
-      // ---- P as the A operand: rows 0..7 hi, rows 8..15 lo ----
-      uint32_t pa[4];
+      // ---- P as the A operand (rows as the Q fragments) ----
+      uint32_t pa[NQ][4];
       {
-        float h00, l00, h01, l01, h10, l10, h11, l11;
-        split_bf16(pr[0][0], h00, l00);
-        split_bf16(pr[0][1], h01, l01);
-        split_bf16(pr[1][0], h10, l10);
-        split_bf16(pr[1][1], h11, l11);
-        pa[0] = pack_bf16(h00, h01);
-        pa[1] = pack_bf16(l00, l01);
-        pa[2] = pack_bf16(h10, h11);
-        pa[3] = pack_bf16(l10, l11);
+        float hi[NH][2][2], lo[NH][2][2];
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) split_bf16(pr[hh][j][e], hi[hh][j][e], lo[hh][j][e]);
+        if constexpr (NH == 2) {
+          pa[0][0] = pack_bf16(hi[0][0][0], hi[0][0][1]);
+          pa[0][1] = pack_bf16(hi[1][0][0], hi[1][0][1]);
+          pa[0][2] = pack_bf16(hi[0][1][0], hi[0][1][1]);
+          pa[0][3] = pack_bf16(hi[1][1][0], hi[1][1][1]);
+          pa[NQ - 1][0] = pack_bf16(lo[0][0][0], lo[0][0][1]);
+          pa[NQ - 1][1] = pack_bf16(lo[1][0][0], lo[1][0][1]);
+          pa[NQ - 1][2] = pack_bf16(lo[0][1][0], lo[0][1][1]);
+          pa[NQ - 1][3] = pack_bf16(lo[1][1][0], lo[1][1][1]);
+        } else {
+          pa[0][0] = pack_bf16(hi[0][0][0], hi[0][0][1]);
+          pa[0][1] = pack_bf16(lo[0][0][0], lo[0][0][1]);
+          pa[0][2] = pack_bf16(hi[0][1][0], hi[0][1][1]);
+          pa[0][3] = pack_bf16(lo[0][1][0], lo[0][1][1]);
+        }
       }
       // ---- O += P V ----
 #pragma unroll
@@ -632,8 +689,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int mi = lane >> 3;
         uint32_t v0, v1, v2, v3;
         ldsm_x4_t(swz<D>(vbase, kw + (mi & 1) * 8 + (lane & 7), nd + (mi >> 1)), v0, v1, v2, v3);
-        mma_bf16(o[nd], pa, v0, v1);
-        mma_bf16(o[nd + 1], pa, v2, v3);
+#pragma unroll
+        for (int qb = 0; qb < NQ; ++qb) {
+          mma_bf16(o[nd], pa[qb], v0, v1);
+          mma_bf16(o[nd + 1], pa[qb], v2, v3);
+        }
       }
     }
     __syncwarp();
@@ -642,22 +702,40 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ---- end of this CTA's part of slice s: hand the warp partial to the
     // epilogue warp and keep consuming: EMPTY (barrier 2) -> slot -> FULL (barrier 1)
     if (t + 1 == pref[s + 1] || t + 1 == te) {
-      float lr = l_run;
-      lr += __shfl_xor_sync(0xffffffffu, lr, 1);
-      lr += __shfl_xor_sync(0xffffffffu, lr, 2);
+      float lr[NH];
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        lr[hh] = l_run[hh];
+        lr[hh] += __shfl_xor_sync(0xffffffffu, lr[hh], 1);
+        lr[hh] += __shfl_xor_sync(0xffffffffu, lr[hh], 2);
+      }
       const long long tw0 = trace ? (long long)globaltimer() : 0;
       asm volatile("bar.sync 2, %0;" ::"n"(kBarThreads));
       if (trace && threadIdx.x == 0) trace[8] += (long long)globaltimer() - tw0;
-      if (g < G) {
+      if constexpr (NH == 2) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int row = g + 8 * hh;
+          float* dst = comb_o + (warp * G + row) * D;
+#pragma unroll
+          for (int n = 0; n < D / 8; ++n)
+            *reinterpret_cast<float2*>(dst + comb_col<D>(n * 8 + 2 * t4, row)) =
+                make_float2(o[n][2 * hh], o[n][2 * hh + 1]);
+          if (t4 == 0) {
+            comb_ml[(warp * 2 + 0) * G + row] = m_run[hh];
+            comb_ml[(warp * 2 + 1) * G + row] = lr[hh];
+          }
+        }
+      } else if (g < G) {
         // row g's O (hi + lo halves): o[n][0..1] + o[n][2..3] = d 8n + 2t4 + {0,1}
         float* dst = comb_o + (warp * G + g) * D;
 #pragma unroll
         for (int n = 0; n < D / 8; ++n)
-          *reinterpret_cast<float2*>(dst + comb_col(n * 8 + 2 * t4, g)) =
+          *reinterpret_cast<float2*>(dst + comb_col<D>(n * 8 + 2 * t4, g)) =
               make_float2(o[n][0] + o[n][2], o[n][1] + o[n][3]);
         if (t4 == 0) {
-          comb_ml[(warp * 2 + 0) * 8 + g] = m_run;
-          comb_ml[(warp * 2 + 1) * 8 + g] = lr;
+          comb_ml[(warp * 2 + 0) * G + g] = m_run[0];
+          comb_ml[(warp * 2 + 1) * G + g] = lr[0];
         }
       }
       asm volatile("bar.arrive 1, %0;" ::"n"(kBarThreads));
@@ -678,6 +756,7 @@ DecodeFn pick_g(int G) {
     case 2: return decode_kernel<D, 2>;
     case 4: return decode_kernel<D, 4>;
     case 8: return decode_kernel<D, 8>;
+    case 16: return decode_kernel<D, 16>;
     default: return nullptr;
   }
 }
@@ -690,7 +769,8 @@ int smem_fixed(int G) {
     case 1: return Comb<D, 1>::kSmemFixed;
     case 2: return Comb<D, 2>::kSmemFixed;
     case 4: return Comb<D, 4>::kSmemFixed;
-    default: return Comb<D, 8>::kSmemFixed;
+    case 8: return Comb<D, 8>::kSmemFixed;
+    default: return Comb<D, 16>::kSmemFixed;
   }
 }
 
@@ -708,7 +788,7 @@ cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const C
   if (!fn || S > kMaxSlices || ctas > kMaxCtas) return cudaErrorInvalidValue;
   const int smem = decode_smem_bytes(D, G, S);
   // raise the dynamic-smem cap once per instantiation to the largest size used
-  static int configured[2][9] = {};
+  static int configured[2][17] = {};
   int& cap = configured[D == 64 ? 0 : 1][G];
   if (smem > cap) {
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),

@@ -407,3 +407,32 @@ def test_sparse_decode_group16():
     st.reorganize(0, list(range(1, nsb + 1)), sel)
     want, _ = st.attention_sparse(0, q[0].double().numpy(), list(range(1, nsb + 1)), sel, L - rl + 1, rl)
     assert rel_err(out[0].cpu().numpy().reshape(-1), want) < TOL
+
+
+@pytest.mark.parametrize("H,Hq,lens,pool", [
+    (2, 32, [900, 300], 0),   # G = 16 (Qwen3-235B group), mean pooling
+    (2, 32, [900], 1),        # G = 16, max pooling
+    (4, 32, [1500, 64], 0),   # G = 8
+    (8, 8, [700], 1),         # G = 1
+])
+def test_dense_decode_groups(H, Hq, lens, pool):
+    torch = _torch()
+    B = len(lens)
+    c = _cache(L=1, B=B, H=H, Hq=Hq, d=128, Lmax=1600, ns=4, K=64, R=32)
+    c.fill_synthetic(seed=H + Hq, length=max(lens))
+    c.set_lengths(lens, [4] * B)
+    q = torch.randn(B, Hq, 128, generator=torch.Generator().manual_seed(Hq))
+    out = torch.zeros_like(q).cuda()
+    logits = torch.zeros_like(c.pooled_logits)
+    c.dense_decode(0, q.cuda().contiguous(), out, logits, pool)
+    torch.cuda.synchronize()
+    c.check_errors()
+    orc = oracle("port")
+    for b in range(B):
+        L, nsb, rl, j0, j1 = _window(c, b)
+        k, v = _rows(c, 0, b, L)
+        st = store_from_rows(orc, k, v, Hq)
+        want_o, want_lg = st.dense_capture(0, q[b].double().numpy(), np.arange(j0, j1 + 1), pool)
+        assert rel_err(out[b].cpu().numpy().reshape(-1), want_o) < TOL
+        if j1 >= j0:
+            assert rel_err(logits[b, :, : j1 - j0 + 1].cpu().numpy(), want_lg) < TOL
