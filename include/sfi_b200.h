@@ -195,6 +195,25 @@ SFI_API int sfi_selector(const sfi_shape* shape, const sfi_cache* cache, int32_t
                          const float* pooled_logits, const sfi_selector_params* params,
                          void* stream);
 
+/* KV-head-sharded Selector. Every Selector stage is
+ * per head except cross-head exclusivity (selector.cpp:204-230), a softmax over
+ * ALL kv heads of a request at each position. A rank whose cache holds heads
+ * [shard * H, (shard + 1) * H) of n_shards * H (H = shape->n_kv_heads):
+ *   1. sfi_selector_fuse: evidence, prior, fusion -> z_base of its heads in
+ *      *z_local (device, inside the workspace; *z_bytes bytes, layout
+ *      [batch][H][max_positions] fp64);
+ *   2. all-gathers the z_local blocks of the n_shards ranks in rank order into
+ *      z_all (n_shards * z_bytes; e.g. ncclAllGather on the same stream);
+ *   3. sfi_selector_finish: soft-NMS and cross-head over all heads in global head
+ *      order, top-k of its own heads -> sel / n_sel. Indices are bit-identical
+ *      to the unsharded sfi_selector. */
+SFI_API int sfi_selector_fuse(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                              const float* pooled_logits, const sfi_selector_params* params,
+                              const double** z_local, size_t* z_bytes, void* stream);
+SFI_API int sfi_selector_finish(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                const sfi_selector_params* params, const double* z_all,
+                                int32_t n_shards, int32_t shard, void* stream);
+
 /* run_selector on explicit device arrays (the reference-facing form,
  * selector.cpp:254-299): H heads, a W x n window per head over an arbitrary
  * ascending allowed list. logits fp64 [H][W][n], norms fp64 [H][n] (CacheStats

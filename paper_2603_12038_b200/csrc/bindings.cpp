@@ -309,6 +309,18 @@ PYBIND11_MODULE(_sfi_b200, m) {
                           static_cast<float*>(vp(out)), flags, vp(stream)));
   });
   m.attr("FAST_PREFETCH") = SFI_FAST_PREFETCH;
+  m.def("selector_fuse", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
+                            const sfi_selector_params& prm, std::uintptr_t stream) {
+    const double* z = nullptr;
+    size_t bytes = 0;
+    check(sfi_selector_fuse(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm, &z, &bytes, vp(stream)));
+    return py::make_tuple(reinterpret_cast<std::uintptr_t>(z), bytes);
+  });
+  m.def("selector_finish", [](const sfi_shape& s, const sfi_cache& c, int layer, const sfi_selector_params& prm,
+                              std::uintptr_t z_all, int n_shards, int shard, std::uintptr_t stream) {
+    check(sfi_selector_finish(&s, &c, layer, &prm, static_cast<const double*>(vp(z_all)), n_shards, shard,
+                              vp(stream)));
+  });
   m.def("selector", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
                        const sfi_selector_params& prm, std::uintptr_t stream) {
     check(sfi_selector(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm, vp(stream)));

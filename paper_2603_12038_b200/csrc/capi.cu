@@ -434,12 +434,7 @@ SFI_API int sfi_fast_decode(const sfi_shape* s, const sfi_cache* c, int32_t laye
   return fast_common(s, c, layer, q, k_new, v_new, out, flags, stream);
 }
 
-SFI_API int sfi_selector(const sfi_shape* s, const sfi_cache* c, int32_t layer,
-                         const float* pooled_logits, const sfi_selector_params* prm, void* stream) {
-  g_launches = 0;
-  int rc = validate(s);
-  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
-  if (!pooled_logits || !prm) return fail(SFI_ERR_INVALID_ARGUMENT, "selector: null argument");
+static int check_selector_params(const sfi_selector_params* prm) {
   // SelectorConfig::validate (config.cpp:68-87)
   const bool ok = prm->alpha > 0.0 && prm->alpha <= 1.0 && prm->gamma >= 0.0 && prm->beta >= 0.0 &&
                   prm->p_curve >= 1.0 && prm->eta >= 0.0 && prm->lambda_clip >= 0.0 &&
@@ -449,13 +444,49 @@ SFI_API int sfi_selector(const sfi_shape* s, const sfi_cache* c, int32_t layer,
                   std::isfinite(prm->p_curve) && std::isfinite(prm->eta) &&
                   std::isfinite(prm->alpha_soft) && std::isfinite(prm->alpha_cross) &&
                   std::isfinite(prm->temperature) && std::isfinite(prm->epsilon);
-  if (!ok) return fail(SFI_ERR_CONFIG, "selector: invalid SelectorConfig");
+  return ok ? SFI_OK : fail(SFI_ERR_CONFIG, "selector: invalid SelectorConfig");
+}
+
+static int selector_common(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* logits,
+                           const sfi_selector_params* prm, int phases, const double* z_all, int n_shards,
+                           int shard, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!prm || ((phases & 1) && !logits)) return fail(SFI_ERR_INVALID_ARGUMENT, "selector: null argument");
+  if ((rc = check_selector_params(prm))) return rc;
+  if (z_all && (n_shards < 1 || shard < 0 || shard >= n_shards || n_shards * s->n_kv_heads > 16))
+    return fail(SFI_ERR_INVALID_ARGUMENT, "selector: bad shard layout (at most 16 heads in total)");
   sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
   int n = 0;
-  SFI_CUDA(sfi_impl::launch_selector(*s, *c, layer, pooled_logits, *prm, ws.sel, (cudaStream_t)stream, &n),
+  SFI_CUDA(sfi_impl::launch_selector(*s, *c, layer, logits, *prm, ws.sel, (cudaStream_t)stream, &n, phases,
+                                     z_all, n_shards, shard),
            "sfi_selector");
   g_launches = n;
   return SFI_OK;
+}
+
+SFI_API int sfi_selector(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                         const float* pooled_logits, const sfi_selector_params* prm, void* stream) {
+  return selector_common(s, c, layer, pooled_logits, prm, 3, nullptr, 1, 0, stream);
+}
+
+SFI_API int sfi_selector_fuse(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                              const float* pooled_logits, const sfi_selector_params* prm,
+                              const double** z_local, size_t* z_bytes, void* stream) {
+  const int rc = selector_common(s, c, layer, pooled_logits, prm, 1, nullptr, 1, 0, stream);
+  if (rc) return rc;
+  sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
+  if (z_local) *z_local = ws.sel.a;
+  if (z_bytes) *z_bytes = (size_t)s->batch * s->n_kv_heads * s->max_positions * sizeof(double);
+  return SFI_OK;
+}
+
+SFI_API int sfi_selector_finish(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                                const sfi_selector_params* prm, const double* z_all, int32_t n_shards,
+                                int32_t shard, void* stream) {
+  if (!z_all) return fail(SFI_ERR_INVALID_ARGUMENT, "selector_finish: z_all is null");
+  return selector_common(s, c, layer, nullptr, prm, 2, z_all, n_shards, shard, stream);
 }
 
 SFI_API size_t sfi_selector_explicit_scratch_bytes(int32_t H, int32_t n) {

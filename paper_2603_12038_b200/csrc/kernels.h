@@ -104,9 +104,12 @@ struct SelectorScratch {
   double* a;  // [B*H][Lmax]  p -> weights -> f -> z_base
   double* b;  // [B*H][Lmax]  w -> r -> z_adj
 };
+// phases: 1 = fuse (z_base into scr.a), 2 = refine + top-k; z_all != null:
+// head-sharded finish over the all-gathered z_base of n_shards shards
 cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
                             const sfi_selector_params& prm, const SelectorScratch& scr,
-                            cudaStream_t st, int* launches);
+                            cudaStream_t st, int* launches, int phases = 3,
+                            const double* z_all = nullptr, int n_shards = 1, int shard = 0);
 
 cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* logits,
                                      const double* norms, const int32_t* allowed,

@@ -89,6 +89,10 @@ struct SelParams {
   int B, H, Lmax, K;
   double alpha, gamma, beta, p_curve, eta, lambda_clip, alpha_soft, alpha_cross, temperature, eps;
   int nms_radius;
+  // KV-head sharding: z_base of all H_all heads gathered
+  // [n_shards][B][H][ld] (H = this shard's heads [h_off, h_off + H)); null = local
+  const double* z_all;
+  int H_all, h_off;
 };
 
 // Row geometry: n = |J|, j_min, position of index j, u(j).
@@ -426,6 +430,13 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
   cl.sync();
 }
 
+// z_base row of (request b, global head h): local scratch, or the all-gathered
+// [n_shards][B][H][ld] block of the head-sharded Selector
+__device__ __forceinline__ const double* zrow(const SelParams& p, int b, int h) {
+  if (p.z_all) return p.z_all + ((size_t)((h / p.H) * p.B + b) * p.H + (h % p.H)) * p.ld;
+  return p.sa + (size_t)(b * p.H + h) * p.ld;
+}
+
 // ---------------------------------------------------------------------------
 // Stage B: soft-NMS per head, then cross-head exclusivity; one thread per
 // (b, j), the CTA's 256 positions x H heads (+ halo) staged in shared memory.
@@ -442,7 +453,7 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   const int R = p.nms_radius;
   const bool staged = R <= kMaxNmsR;
   // kH = 16 also serves head counts that are not a power of two (runtime guard)
-  const int Hr = kH == 16 ? p.H : kH;
+  const int Hr = p.z_all ? p.H_all : (kH == 16 ? p.H : kH);
   if (staged) {
     // every thread stages column t and t + 256 (halo) of all heads; all loads
     // are issued before the first shared store
@@ -453,7 +464,7 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
     double va[kH], vb[kH];
 #pragma unroll
     for (int h = 0; h < kH; ++h) {
-      const double* z = p.sa + (size_t)(b * p.H + (h < Hr ? h : 0)) * p.ld;
+      const double* z = zrow(p, b, h < Hr ? h : 0);
       va[h] = (h < Hr && oka) ? z[ja] : 0.0;
       vb[h] = (h < Hr && okb) ? z[jb] : 0.0;
     }
@@ -480,7 +491,7 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
         m = zj;
         for (int i = lo; i <= hi; ++i) m = smax(m, t[i]);
       } else {
-        const double* z = p.sa + (size_t)(b * p.H + h) * p.ld;
+        const double* z = zrow(p, b, h);
         zj = z[idx];
         m = zj;
         for (int i = lo; i <= hi; ++i) m = smax(m, z[i]);
@@ -509,9 +520,9 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   const double floor_e = p.eps * sum;
 #pragma unroll
   for (int h = 0; h < kH; ++h)
-    if (h < Hr) {
+    if (h < Hr && h >= p.h_off && h < p.h_off + p.H) {  // this shard's heads only
       const double lr = (e[h] >= floor_e) ? (x[h] - ls) : le;
-      p.sb[(size_t)(b * p.H + h) * p.ld + idx] = zn[h] + p.alpha_cross * lr;
+      p.sb[(size_t)(b * p.H + h - p.h_off) * p.ld + idx] = zn[h] + p.alpha_cross * lr;
     }
 }
 
@@ -1091,21 +1102,25 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
   return launch_k(sel_topk_kernel<kExp, false>, gc, dim3(kT), 0, st, p);
 }
 
+// phases: 1 = fuse (z_base), 2 = refine + top-k
 template <bool kExp>
 cudaError_t run3(const SelParams& p, int rows, int n_max, int batches, cudaStream_t st,
-                 int* launches) {
+                 int* launches, int phases = 3) {
   const dim3 gc(kCS, (unsigned)rows);
-  cudaError_t e;
-  if (p.W == 1 && p.alpha == 1.0)
-    e = launch_k(sel_fuse_fast_kernel<kExp>, gc, dim3(kT), 0, st, p);
-  else if (p.W > 1)
-    e = launch_k(sel_fuse_kernel<kExp, kMaxW>, gc, dim3(kT), 0, st, p);
-  else
-    e = launch_k(sel_fuse_kernel<kExp, 1>, gc, dim3(kT), 0, st, p);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (phases & 1) {
+    if (p.W == 1 && p.alpha == 1.0)
+      e = launch_k(sel_fuse_fast_kernel<kExp>, gc, dim3(kT), 0, st, p);
+    else if (p.W > 1)
+      e = launch_k(sel_fuse_kernel<kExp, kMaxW>, gc, dim3(kT), 0, st, p);
+    else
+      e = launch_k(sel_fuse_kernel<kExp, 1>, gc, dim3(kT), 0, st, p);
+    if (launches) *launches += 1;
+  }
+  if (e != cudaSuccess || !(phases & 2)) return e;
   const dim3 gr((n_max + kRefineT - 1) / kRefineT, batches);
   const dim3 br(kRefineT);
-  switch (p.H) {
+  switch (p.z_all ? p.H_all : p.H) {
     case 1: e = launch_k(sel_refine_kernel<kExp, 1>, gr, br, 0, st, p); break;
     case 2: e = launch_k(sel_refine_kernel<kExp, 2>, gr, br, 0, st, p); break;
     case 4: e = launch_k(sel_refine_kernel<kExp, 4>, gr, br, 0, st, p); break;
@@ -1114,7 +1129,7 @@ cudaError_t run3(const SelParams& p, int rows, int n_max, int batches, cudaStrea
   }
   if (e != cudaSuccess) return e;
   e = launch_topk<kExp>(p, rows, n_max, st);
-  if (launches) *launches += 3;
+  if (launches) *launches += 2;
   return e;
 }
 
@@ -1122,8 +1137,13 @@ cudaError_t run3(const SelParams& p, int rows, int n_max, int batches, cudaStrea
 
 cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
                             const sfi_selector_params& prm, const SelectorScratch& scr,
-                            cudaStream_t st, int* launches) {
+                            cudaStream_t st, int* launches, int phases, const double* z_all,
+                            int n_shards, int shard) {
   SelParams p{};
+  p.z_all = z_all;
+  p.H_all = z_all ? n_shards * s.n_kv_heads : s.n_kv_heads;
+  p.h_off = z_all ? shard * s.n_kv_heads : 0;
+  if (p.H_all > 16) return cudaErrorInvalidValue;
   const size_t slices = (size_t)s.batch * s.n_kv_heads;
   p.logits32 = logits;
   p.norms_c = c.key_norms + (size_t)layer * slices * s.max_positions;
@@ -1143,7 +1163,7 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
   p.K = s.k_budget;
   fill_cfg(p, prm);
   if (s.n_kv_heads > 16) return cudaErrorInvalidValue;
-  return run3<false>(p, (int)slices, s.max_positions, s.batch, st, launches);
+  return run3<false>(p, (int)slices, s.max_positions, s.batch, st, launches, phases);
 }
 
 cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* logits, const double* norms,

@@ -120,6 +120,25 @@ class SfiCache:
         _C.selector(self.shape, self.cache, layer, self._ptr(logits, torch.float32),
                     params if params is not None else _C.SelectorParams(), self._stream(stream))
 
+    def selector_fuse(self, layer: int, logits: torch.Tensor, params=None, stream=None) -> torch.Tensor:
+        """Head-sharded Selector, phase 1: z_base of this cache's heads, returned as a
+        view fp64 [B][H][max_positions] of the workspace (valid until the next
+        Selector call on this cache)."""
+        ptr, nbytes = _C.selector_fuse(self.shape, self.cache, layer, self._ptr(logits, torch.float32),
+                                       params if params is not None else _C.SelectorParams(),
+                                       self._stream(stream))
+        off = ptr - self.workspace.data_ptr()
+        return self.workspace[off:off + nbytes].view(torch.float64).view(
+            self.shape.batch, self.shape.n_kv_heads, self.shape.max_positions)
+
+    def selector_finish(self, layer: int, z_all: torch.Tensor, n_shards: int, shard: int, params=None,
+                        stream=None):
+        """Phase 2 over the all-gathered z_base [n_shards][B][H][max_positions]: soft-NMS,
+        cross-head over all heads, top-k of this shard's heads -> sel / n_sel."""
+        _C.selector_finish(self.shape, self.cache, layer,
+                           params if params is not None else _C.SelectorParams(),
+                           self._ptr(z_all, torch.float64), n_shards, shard, self._stream(stream))
+
     def compact_build(self, layer: int, rebuild_ring: bool = False, stream=None):
         _C.compact_build(self.shape, self.cache, layer, int(bool(rebuild_ring)), self._stream(stream))
 
