@@ -38,9 +38,18 @@ CONFIGS = {
     "c2": ("Qwen3-8B-shaped attention, batch 8, 32K", 36, 32, 8, 8, 32768, 4, 2048, 256),
     "c3": ("Qwen3-32B-shaped attention, batch 4, 128K", 64, 64, 8, 4, 131072, 4, 2048, 256),
 }
+# multi-GPU partitioning per config: "dp" = independent request
+# batches per GPU (weak scaling); "heads" = KV-head sharding of ONE batch
+# (strong scaling, z_base all-gather in the Selector)
+SHARDING = {"c1": "dp", "c2": "dp", "c3": "heads"}
 HEAD_DIM = 128
 T_MAX = 64
 P_TRIGGER = 1.0 / 24.0
+
+
+def metric_name(cfg_name: str) -> str:
+    name, _, _, _, _, ctx = CONFIGS[cfg_name][:6]
+    return f"SFI decode tokens/s ({ctx // 1024}K ctx, {name.split(',')[0]}, batch {CONFIGS[cfg_name][4]})"
 
 
 def schedule(n_steps: int, seed: int) -> list[bool]:
@@ -120,19 +129,33 @@ class ClockSampler:
 # GPU arm
 
 class Workload:
-    def __init__(self, cfg_name: str, steps_total: int, device):
+    def __init__(self, cfg_name: str, steps_total: int, device, world: int = 1, layers: int = 0):
         import torch
 
         import paper_2603_12038_b200 as sfi
 
         (self.name, self.L, self.Hq, self.H, self.B, self.ctx, self.ns, self.K,
          self.R) = CONFIGS[cfg_name]
+        if layers:
+            self.L = layers
         self.cfg_name = cfg_name
         self.G = self.Hq // self.H
         self.Lmax = self.ctx + steps_total + 64
         self.torch = torch
-        self.cache = sfi.SfiCache(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
-                                  self.K, self.R, device=device)
+        self.mode = SHARDING[cfg_name] if world > 1 else "single"
+        self.shard = None
+        if self.mode == "heads":
+            from paper_2603_12038_b200.sharded import HeadShardedSfi
+
+            self.shard = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
+                                        self.K, self.R, device=device)
+            self.cache = self.shard.cache
+            self.H, self.Hq = self.shard.local_heads, self.shard.local_heads * self.G  # this rank's heads
+        else:
+            self.cache = sfi.SfiCache(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
+                                      self.K, self.R, device=device)
+        # tokens produced per step by the whole job, per rank's share of it
+        self.job_tokens = self.B * (world if self.mode == "dp" else 1)
         self.params = sfi.SelectorParams()
         t = torch
         g = t.Generator(device="cpu").manual_seed(2027)
@@ -163,7 +186,10 @@ class Workload:
             if slow:
                 c.ring_append(l, self.k_new[l], self.v_new[l])
                 c.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
-                c.selector(l, self.logits, self.params)
+                if self.shard is not None:
+                    self.shard.selector(l, self.logits, self.params)  # z_base all-gather (NCCL)
+                else:
+                    c.selector(l, self.logits, self.params)
                 c.compact_build(l, rebuild_ring=rebuild_ring)
             else:
                 # ONE launch: ring append fused with the sparse decode; the
@@ -254,12 +280,22 @@ def gpu_arm(args) -> dict:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.backend)
+    if args.backend == "gloo":  # testing: several ranks may share one GPU
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = dev if args.backend == "nccl" else torch.device("cpu")
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     W, K = args.warmup, args.steps
     sched = schedule(W + K + 1, seed=2026 + 1)[1:]  # step 0 of the schedule is the setup slow step
-    wl = Workload(args.config, W + K + 8, dev)
+    wl = Workload(args.config, W + K + 8, dev, world, args.layers)
     c = wl.cache
     use_graph = not args.no_graph
     graphs = {}
@@ -296,15 +332,12 @@ def gpu_arm(args) -> dict:
             run(slow)
         e1.record(stream)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(e0.elapsed_time(e1))
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
     c.check_errors()
     n_slow = sum(timed)
-    tokens = wl.B * K * world
+    tokens = wl.job_tokens * K
     value = tokens / (ms / 1e3)
 
     # ---- end to end through the public API with host buffers ----
@@ -334,14 +367,10 @@ def gpu_arm(args) -> dict:
             oh.copy_(wl.out, non_blocking=True)
         b.record(stream)
         torch.cuda.synchronize()
-        ems = a.elapsed_time(b)
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(a.elapsed_time(b))
         h2d = (wl.q.numel() * 4 + wl.k_new.numel() * 2 + wl.v_new.numel() * 2)
         d2h = wl.out.numel() * 4
-        e2e = {"value": wl.B * Ke * world / (ems / 1e3), "unit": "tokens/s",
+        e2e = {"value": wl.job_tokens * Ke / (ems / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": Ke}
 
     # ---- per-kernel device time (CUDA events on the launching stream) ----
@@ -377,15 +406,18 @@ def gpu_arm(args) -> dict:
             "traffic": None, "share_of_step": (share_sp if dom == "fast_decode" else share_de) / ms}
     fast_us = wl.L * (t_sp * 1e3)
     res = {
-        "metric": "SFI decode tokens/s (32K ctx, Qwen3-8B-shaped attention, batch 8)",
+        "metric": metric_name(args.config),
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / K, "higher_is_better": True,
+        "scaling": "strong" if wl.mode == "heads" else "weak", "vs_baseline": None,
         "dtype": "bf16 KV, fp32 accumulate; fp64 Selector", "data": "synthetic",
         "config": {"workload": wl.name + f" ({args.config.upper()})", "layers": wl.L,
-                   "q_heads": wl.Hq, "kv_heads": wl.H, "head_dim": HEAD_DIM, "batch_per_gpu": wl.B,
+                   "q_heads": CONFIGS[args.config][2], "kv_heads": CONFIGS[args.config][3],
+                   "kv_heads_per_gpu": wl.H, "head_dim": HEAD_DIM, "batch_per_gpu": wl.B,
                    "context": wl.ctx, "n_sink": wl.ns, "k_budget": wl.K, "n_recent": wl.R,
                    "schedule": f"seeded triggers p=1/24 + t_max={T_MAX}; {n_slow} slow / {K} steps",
-                   "parallelism": f"dp{world} (independent request batches)",
+                   "parallelism": (f"kv-head sharded x{world} (one batch; z_base all-gather per slow-step layer)"
+                                   if wl.mode == "heads" else f"dp{world} (independent request batches)"),
                    "cuda_graphs": use_graph,
                    "l2": "inputs larger than L2 (KV cache %.1f GB)" % (2 * c.sizes['kv_cache'] / 1e9)},
         "slow_steps": n_slow, "fast_step_us_kernels": fast_us,
@@ -552,7 +584,7 @@ def reference_arm(args) -> dict | None:
         total += nl * time_cpu_layer(sample, slow, threads)
     value = data["B"] * K / total
     return {
-        "impl": "reference", "metric": "SFI decode tokens/s (32K ctx, Qwen3-8B-shaped attention, batch 8)",
+        "impl": "reference", "metric": metric_name(args.config),
         "value": value, "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": K, "warmup": W, "ms_per_step": total / K * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32 KV, fp64 accumulate (reference)",
@@ -578,6 +610,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count (testing only)")
+    ap.add_argument("--backend", default=os.environ.get("SFI_DIST_BACKEND", "nccl"),
+                    help="torch.distributed backend (gloo: several ranks on one GPU, testing only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     res = reference_arm(args) if args.impl == "reference" else gpu_arm(args)
