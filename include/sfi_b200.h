@@ -214,6 +214,59 @@ SFI_API int sfi_selector_finish(const sfi_shape* shape, const sfi_cache* cache, 
                                 const sfi_selector_params* params, const double* z_all,
                                 int32_t n_shards, int32_t shard, void* stream);
 
+/* ---- Sequence sharding ------------------------------
+ * Rank r of P holds positions (pos_base, pos_base + max_positions] of every
+ * request (the last rank: everything from pos_base on; decode appends there).
+ * The request's GLOBAL lengths live in caller-owned device arrays g_prefix_len,
+ * g_n_sink, g_recent_len [batch]; sfi_seq_lengths (optionally advancing them
+ * by `advance` first, like sfi_step_advance) rewrites the cache's own
+ * prefix_len / n_sink_b / recent_len as this shard's LOCAL view (rows held,
+ * sink rows at its start, recent rows at its end) and writes j_off[b] (global J
+ * index of the shard's first J position) and n_glob[b] (global |J|). Every
+ * single-GPU entry point then runs unchanged on the shard. */
+SFI_API int sfi_seq_lengths(const sfi_shape* shape, const sfi_cache* cache, int32_t* g_prefix_len,
+                            const int32_t* g_n_sink, int32_t* g_recent_len, int32_t advance,
+                            int32_t pos_base, int32_t is_last, int32_t* j_off, int32_t* n_glob,
+                            void* stream);
+/* Partial attention of a shard: normalised O plus its natural-log sum-exp
+ * lse fp32 [batch][n_q_heads]; a shard without rows gives O = 0, lse = -inf. */
+SFI_API int sfi_dense_decode_partial(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                     const float* q, float* out, float* lse, float* pooled_logits,
+                                     int32_t pool_mode, void* stream);
+/* k_new / v_new NULL on shards that do not own the current position. */
+SFI_API int sfi_fast_decode_partial(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                    const float* q, const void* k_new, const void* v_new, float* out,
+                                    float* lse, int32_t flags, void* stream);
+/* out[row] = sum_p exp(lse_p[row] - LSE[row]) o_p[row] in part order (the
+ * all-gathered partials: o_parts [n_parts][rows][head_dim], lse [n_parts][rows]). */
+SFI_API int sfi_merge_partials(int32_t n_parts, int32_t rows, int32_t head_dim, const float* o_parts,
+                               const float* lse_parts, float* out, void* stream);
+/* Sequence-sharded Selector, decode path (W = 1, alpha = 1), per layer:
+ *   stats phase 1 -> row_max [B*H]      ; all-reduce MAX over ranks
+ *   stats phase 2 -> row_sums [B*H][5]  ; all-reduce SUM   (sum p, w, p^2, pw, w^2)
+ *   stats phase 3 -> z_base + edges [B*H][2R+2] (sfi_seq_edges_doubles) ; all-gather
+ *   finish: soft-NMS with the neighbours' edges, cross-head (all heads local),
+ *           local top-k -> candidates (z_adj, global position) [B*H][k_budget] ; all-gather
+ *   pick: global top-k of the P candidate lists (shard order = position order,
+ *         the reference's (score desc, position asc) rule) -> this shard's
+ *         positions, local, into sel / n_sel.
+ * Indices match the 1-GPU Selector (sums differ only in fp64 rounding order). */
+SFI_API size_t sfi_seq_edges_doubles(const sfi_shape* shape, const sfi_selector_params* params);
+SFI_API int sfi_seq_selector_stats(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                   const float* pooled_logits, const sfi_selector_params* params,
+                                   const int32_t* j_off, const int32_t* n_glob, int32_t phase,
+                                   double* row_max, double* row_sums, double* edges, void* stream);
+SFI_API int sfi_seq_selector_finish(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                    const sfi_selector_params* params, const int32_t* j_off,
+                                    const int32_t* n_glob, const double* edges_all, int32_t n_shards,
+                                    int32_t pos_base, double* cand_score, int32_t* cand_pos,
+                                    void* stream);
+SFI_API size_t sfi_seq_pick_scratch_bytes(const sfi_shape* shape, int32_t n_shards);
+SFI_API int sfi_seq_selector_pick(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                  int32_t n_shards, const double* cand_score_all,
+                                  const int32_t* cand_pos_all, int32_t pos_base, int32_t pos_end,
+                                  void* scratch, void* stream);
+
 /* run_selector on explicit device arrays (the reference-facing form,
  * selector.cpp:254-299): H heads, a W x n window per head over an arbitrary
  * ascending allowed list. logits fp64 [H][W][n], norms fp64 [H][n] (CacheStats

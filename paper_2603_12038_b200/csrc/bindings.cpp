@@ -309,6 +309,58 @@ PYBIND11_MODULE(_sfi_b200, m) {
                           static_cast<float*>(vp(out)), flags, vp(stream)));
   });
   m.attr("FAST_PREFETCH") = SFI_FAST_PREFETCH;
+  // sequence sharding (C4)
+  m.def("seq_lengths", [](const sfi_shape& s, const sfi_cache& c, std::uintptr_t gp, std::uintptr_t gs,
+                          std::uintptr_t gr, int advance, int base, int is_last, std::uintptr_t j_off,
+                          std::uintptr_t n_glob, std::uintptr_t stream) {
+    check(sfi_seq_lengths(&s, &c, static_cast<int32_t*>(vp(gp)), static_cast<const int32_t*>(vp(gs)),
+                          static_cast<int32_t*>(vp(gr)), advance, base, is_last, static_cast<int32_t*>(vp(j_off)),
+                          static_cast<int32_t*>(vp(n_glob)), vp(stream)));
+  });
+  m.def("dense_decode_partial", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
+                                   std::uintptr_t out, std::uintptr_t lse, std::uintptr_t logits, int pool,
+                                   std::uintptr_t stream) {
+    check(sfi_dense_decode_partial(&s, &c, layer, static_cast<const float*>(vp(q)), static_cast<float*>(vp(out)),
+                                   static_cast<float*>(vp(lse)), static_cast<float*>(vp(logits)), pool, vp(stream)));
+  });
+  m.def("fast_decode_partial", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
+                                  std::uintptr_t k, std::uintptr_t v, std::uintptr_t out, std::uintptr_t lse,
+                                  int flags, std::uintptr_t stream) {
+    check(sfi_fast_decode_partial(&s, &c, layer, static_cast<const float*>(vp(q)), vp(k), vp(v),
+                                  static_cast<float*>(vp(out)), static_cast<float*>(vp(lse)), flags, vp(stream)));
+  });
+  m.def("merge_partials", [](int n_parts, int rows, int d, std::uintptr_t o, std::uintptr_t lse, std::uintptr_t out,
+                             std::uintptr_t stream) {
+    check(sfi_merge_partials(n_parts, rows, d, static_cast<const float*>(vp(o)), static_cast<const float*>(vp(lse)),
+                             static_cast<float*>(vp(out)), vp(stream)));
+  });
+  m.def("seq_edges_doubles", [](const sfi_shape& s, const sfi_selector_params& prm) {
+    return sfi_seq_edges_doubles(&s, &prm);
+  });
+  m.def("seq_pick_scratch_bytes", [](const sfi_shape& s, int n_shards) { return sfi_seq_pick_scratch_bytes(&s, n_shards); });
+  m.def("seq_selector_stats", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
+                                 const sfi_selector_params& prm, std::uintptr_t j_off, std::uintptr_t n_glob, int phase,
+                                 std::uintptr_t row_max, std::uintptr_t row_sums, std::uintptr_t edges,
+                                 std::uintptr_t stream) {
+    check(sfi_seq_selector_stats(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm,
+                                 static_cast<const int32_t*>(vp(j_off)), static_cast<const int32_t*>(vp(n_glob)), phase,
+                                 static_cast<double*>(vp(row_max)), static_cast<double*>(vp(row_sums)),
+                                 static_cast<double*>(vp(edges)), vp(stream)));
+  });
+  m.def("seq_selector_finish", [](const sfi_shape& s, const sfi_cache& c, int layer, const sfi_selector_params& prm,
+                                  std::uintptr_t j_off, std::uintptr_t n_glob, std::uintptr_t edges_all, int n_shards,
+                                  int pos_base, std::uintptr_t cs, std::uintptr_t cp, std::uintptr_t stream) {
+    check(sfi_seq_selector_finish(&s, &c, layer, &prm, static_cast<const int32_t*>(vp(j_off)),
+                                  static_cast<const int32_t*>(vp(n_glob)), static_cast<const double*>(vp(edges_all)),
+                                  n_shards, pos_base, static_cast<double*>(vp(cs)), static_cast<int32_t*>(vp(cp)),
+                                  vp(stream)));
+  });
+  m.def("seq_selector_pick", [](const sfi_shape& s, const sfi_cache& c, int layer, int n_shards, std::uintptr_t cs,
+                                std::uintptr_t cp, int pos_base, int pos_end, std::uintptr_t scratch,
+                                std::uintptr_t stream) {
+    check(sfi_seq_selector_pick(&s, &c, layer, n_shards, static_cast<const double*>(vp(cs)),
+                                static_cast<const int32_t*>(vp(cp)), pos_base, pos_end, vp(scratch), vp(stream)));
+  });
   m.def("selector_fuse", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
                             const sfi_selector_params& prm, std::uintptr_t stream) {
     const double* z = nullptr;

@@ -211,6 +211,87 @@ __global__ void fill_norms_kernel(const FillParams p) {
 
 }  // namespace
 
+namespace {
+
+// Sequence shard lengths. The request's GLOBAL lengths live in
+// g_prefix / g_nsink / g_recent (advanced here by `advance`, slide_recent rule
+// scheduler.cpp:45-51); this shard owns positions (base, base + cap] (the last
+// shard: (base, inf)). Its cache's own lengths become the local view — rows
+// held, sink rows at its start (shard 0), recent rows at its end — so every
+// single-GPU kernel runs unchanged on the shard; j_off / n_glob place its J
+// slice inside the global J (scheduler.cpp:81-91).
+__global__ void seq_lengths_kernel(int32_t* g_prefix, const int32_t* g_nsink, int32_t* g_recent,
+                                   int advance, int R, int B, int base, int cap, int is_last,
+                                   int32_t* prefix_len, int32_t* n_sink_b, int32_t* recent_len,
+                                   int32_t* j_off, int32_t* n_glob, uint32_t* err) {
+  griddep_wait();
+  griddep_launch();
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int L = g_prefix[b];
+  const int nsb = g_nsink[b];
+  int rl = g_recent[b];
+  if (advance) {
+    L += advance;
+    g_prefix[b] = L;
+    rl = min(max(L - nsb, 0), R);
+    g_recent[b] = rl;
+  }
+  int Ll = L - base;
+  Ll = Ll < 0 ? 0 : Ll;
+  if (Ll > cap) {
+    if (is_last) raise_error(err, SFI_ERR_CONTEXT_OVERFLOW);
+    Ll = cap;
+  }
+  const int hi = base + Ll;  // last position held
+  const int nsl = max(0, min(nsb, hi) - base);
+  const int rlo = max(L - rl + 1, base + 1);
+  const int rll = max(0, min(L, hi) - rlo + 1);
+  prefix_len[b] = Ll;
+  n_sink_b[b] = nsl;
+  recent_len[b] = rll;
+  j_off[b] = (base + nsl + 1) - (nsb + 1);
+  n_glob[b] = max(0, L - rl - nsb);
+}
+
+// LSE merge of n_parts partial attention outputs, fixed part order
+__global__ void merge_partials_kernel(int n_parts, int rows, int D, const float* o_parts, const float* lse_parts,
+                                      float* out) {
+  griddep_wait();
+  griddep_launch();
+  const int row = blockIdx.x;
+  float M = -INFINITY;
+  for (int i = 0; i < n_parts; ++i) M = fmaxf(M, lse_parts[(size_t)i * rows + row]);
+  const float Mu = M == -INFINITY ? 0.f : M;
+  float S = 0.f;
+  for (int i = 0; i < n_parts; ++i) S += __expf(lse_parts[(size_t)i * rows + row] - Mu);
+  const float inv = S > 0.f ? 1.f / S : 0.f;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+    for (int i = 0; i < n_parts; ++i) {
+      const float w = __expf(lse_parts[(size_t)i * rows + row] - Mu);
+      acc += w * o_parts[((size_t)i * rows + row) * D + d];
+    }
+    out[(size_t)row * D + d] = acc * inv;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_seq_lengths(const sfi_shape& s, const sfi_cache& c, int32_t* g_prefix, const int32_t* g_nsink,
+                               int32_t* g_recent, int advance, int base, int is_last, int32_t* j_off,
+                               int32_t* n_glob, cudaStream_t st) {
+  return launch_k(seq_lengths_kernel, dim3((s.batch + 127) / 128), dim3(128), 0, st, g_prefix, g_nsink, g_recent,
+                  advance, s.n_recent, s.batch, base, s.max_positions, is_last, c.prefix_len, c.n_sink_b,
+                  c.recent_len, j_off, n_glob, c.error_flags);
+}
+
+cudaError_t launch_merge_partials(int n_parts, int rows, int D, const float* o_parts, const float* lse_parts,
+                                  float* out, cudaStream_t st) {
+  return launch_k(merge_partials_kernel, dim3(rows), dim3(D < 128 ? D : 128), 0, st, n_parts, rows, D, o_parts,
+                  lse_parts, out);
+}
+
 cudaError_t launch_step_advance(const sfi_shape& s, const sfi_cache& c, cudaStream_t st) {
   return launch_k(advance_kernel, dim3((s.batch + 127) / 128), dim3(128), 0, st, c.prefix_len,
                   (const int32_t*)c.n_sink_b, c.recent_len, s.batch, s.max_positions, s.n_recent, 1,

@@ -125,7 +125,7 @@ int num_sms() {
 }
 
 int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* q, float* out,
-                  float* logits, int pool, bool sparse, void* stream) {
+                  float* logits, int pool, bool sparse, void* stream, float* lse = nullptr) {
   g_launches = 0;
   int rc = validate(s);
   if (rc) return rc;
@@ -142,6 +142,7 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   sfi_impl::DecodeParams p;
   p.q = q;
   p.out = out;
+  p.lse = lse;
   p.logits = sparse ? nullptr : logits;
   p.pool = pool;
   p.layer = layer;
@@ -188,7 +189,7 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
 // Fast step, one layer: sparse decode over the compact cache, fused with the
 // current token's append when k_new / v_new are given (fast_decode.cu).
 int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* q, const void* k_new,
-                const void* v_new, float* out, int flags, void* stream) {
+                const void* v_new, float* out, int flags, void* stream, float* lse = nullptr) {
   g_launches = 0;
   int rc = validate(s);
   if (rc) return rc;
@@ -224,6 +225,7 @@ int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* 
   p.crows = compact_rows(*s);
   p.R = s->n_recent;
   p.prefetch = (flags & SFI_FAST_PREFETCH) ? 1 : 0;
+  p.lse = lse;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
   static const int env_c = [] {
     const char* e = std::getenv("SFI_FAST_CLUSTER");
@@ -487,6 +489,125 @@ SFI_API int sfi_selector_finish(const sfi_shape* s, const sfi_cache* c, int32_t 
                                 int32_t shard, void* stream) {
   if (!z_all) return fail(SFI_ERR_INVALID_ARGUMENT, "selector_finish: z_all is null");
   return selector_common(s, c, layer, nullptr, prm, 2, z_all, n_shards, shard, stream);
+}
+
+// ---- sequence sharding ----------------------------------
+
+SFI_API int sfi_seq_lengths(const sfi_shape* s, const sfi_cache* c, int32_t* g_prefix_len,
+                            const int32_t* g_n_sink, int32_t* g_recent_len, int32_t advance, int32_t pos_base,
+                            int32_t is_last, int32_t* j_off, int32_t* n_glob, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c))) return rc;
+  if (!g_prefix_len || !g_n_sink || !g_recent_len || !j_off || !n_glob)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "seq_lengths: null argument");
+  if (pos_base < 0 || advance < 0) return fail(SFI_ERR_INVALID_ARGUMENT, "seq_lengths: negative base/advance");
+  SFI_CUDA(sfi_impl::launch_seq_lengths(*s, *c, g_prefix_len, g_n_sink, g_recent_len, advance, pos_base,
+                                        is_last ? 1 : 0, j_off, n_glob, (cudaStream_t)stream),
+           "sfi_seq_lengths");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_dense_decode_partial(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q,
+                                     float* out, float* lse, float* pooled_logits, int32_t pool_mode,
+                                     void* stream) {
+  if (!lse) return fail(SFI_ERR_INVALID_ARGUMENT, "dense_decode_partial: lse is null");
+  return decode_common(s, c, layer, q, out, pooled_logits, pool_mode, false, stream, lse);
+}
+
+SFI_API int sfi_fast_decode_partial(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q,
+                                    const void* k_new, const void* v_new, float* out, float* lse, int32_t flags,
+                                    void* stream) {
+  if (!lse) return fail(SFI_ERR_INVALID_ARGUMENT, "fast_decode_partial: lse is null");
+  return fast_common(s, c, layer, q, k_new, v_new, out, flags, stream, lse);
+}
+
+SFI_API int sfi_merge_partials(int32_t n_parts, int32_t rows, int32_t head_dim, const float* o_parts,
+                               const float* lse_parts, float* out, void* stream) {
+  g_launches = 0;
+  if (n_parts < 1 || rows < 0 || head_dim < 1 || !o_parts || !lse_parts || !out)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "merge_partials: bad argument");
+  if (rows == 0) return SFI_OK;
+  SFI_CUDA(sfi_impl::launch_merge_partials(n_parts, rows, head_dim, o_parts, lse_parts, out,
+                                           (cudaStream_t)stream),
+           "sfi_merge_partials");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+static int seq_selector_check(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                              const sfi_selector_params* prm) {
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!prm) return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector: null params");
+  if ((rc = check_selector_params(prm))) return rc;
+  if (prm->alpha != 1.0)
+    return fail(SFI_ERR_UNSUPPORTED, "seq_selector: sequence sharding runs the decode path (W = 1, alpha = 1)");
+  if (prm->nms_radius > 16) return fail(SFI_ERR_UNSUPPORTED, "seq_selector: nms_radius <= 16");
+  return SFI_OK;
+}
+
+SFI_API size_t sfi_seq_edges_doubles(const sfi_shape* s, const sfi_selector_params* prm) {
+  if (!s || !prm) return 0;
+  return (size_t)s->batch * s->n_kv_heads * (2 * prm->nms_radius + 2);
+}
+
+SFI_API int sfi_seq_selector_stats(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                                   const float* pooled_logits, const sfi_selector_params* prm,
+                                   const int32_t* j_off, const int32_t* n_glob, int32_t phase, double* row_max,
+                                   double* row_sums, double* edges, void* stream) {
+  g_launches = 0;
+  int rc = seq_selector_check(s, c, layer, prm);
+  if (rc) return rc;
+  if (phase < 1 || phase > 3) return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_stats: phase 1..3");
+  if (!j_off || !n_glob || !row_max || !row_sums || (phase == 3 && !edges) || (phase < 3 && !pooled_logits))
+    return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_stats: null argument");
+  sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
+  SFI_CUDA(sfi_impl::launch_seq_selector_stats(*s, *c, layer, pooled_logits, *prm, ws.sel, j_off, n_glob, phase,
+                                               row_max, row_sums, edges, (cudaStream_t)stream),
+           "sfi_seq_selector_stats");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_seq_selector_finish(const sfi_shape* s, const sfi_cache* c, int32_t layer,
+                                    const sfi_selector_params* prm, const int32_t* j_off, const int32_t* n_glob,
+                                    const double* edges_all, int32_t n_shards, int32_t pos_base,
+                                    double* cand_score, int32_t* cand_pos, void* stream) {
+  g_launches = 0;
+  int rc = seq_selector_check(s, c, layer, prm);
+  if (rc) return rc;
+  if (!j_off || !n_glob || !edges_all || !cand_score || !cand_pos || n_shards < 1)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_finish: bad argument");
+  sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
+  int n = 0;
+  SFI_CUDA(sfi_impl::launch_seq_selector_finish(*s, *c, layer, *prm, ws.sel, j_off, n_glob, edges_all, n_shards,
+                                                pos_base, cand_score, cand_pos, (cudaStream_t)stream, &n),
+           "sfi_seq_selector_finish");
+  g_launches = n;
+  return SFI_OK;
+}
+
+SFI_API size_t sfi_seq_pick_scratch_bytes(const sfi_shape* s, int32_t n_shards) {
+  if (!s || n_shards < 1) return 0;
+  return sfi_impl::seq_pick_scratch_bytes(*s, n_shards);
+}
+
+SFI_API int sfi_seq_selector_pick(const sfi_shape* s, const sfi_cache* c, int32_t layer, int32_t n_shards,
+                                  const double* cand_score_all, const int32_t* cand_pos_all, int32_t pos_base,
+                                  int32_t pos_end, void* scratch, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (n_shards < 1 || !cand_score_all || !cand_pos_all || !scratch)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_pick: bad argument");
+  int n = 0;
+  SFI_CUDA(sfi_impl::launch_seq_selector_pick(*s, *c, layer, n_shards, cand_score_all, cand_pos_all, pos_base,
+                                              pos_end, scratch, (cudaStream_t)stream, &n),
+           "sfi_seq_selector_pick");
+  g_launches = n;
+  return SFI_OK;
 }
 
 SFI_API size_t sfi_selector_explicit_scratch_bytes(int32_t H, int32_t n) {

@@ -88,6 +88,11 @@ struct Slice {
 
 __device__ __forceinline__ int seg_tiles(int c) { return (c + kTile - 1) / kTile; }
 
+// natural-log LSE of a (m, l) pair whose m is in the log2 domain
+__device__ __forceinline__ float lse_of(float m, float l) {
+  return l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+}
+
 // 128B-swizzled address of 16-byte chunk `chunk` (8 bf16) of tile row `row`.
 template <int D>
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
@@ -175,7 +180,7 @@ __device__ __forceinline__ int slice_of(const int* pref, int S, int t) {
 // then every lane streams its D/32 columns of the rows for four contributors
 // per iteration so loads stay in flight instead of serialising on L2 latency.
 template <int D, int G>
-__device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, int P0, int c_first,
+__device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, float* lse, int P0, int c_first,
                                          int c_last, int T, int Gc, int lane) {
   constexpr int kCols = D / 32;
   constexpr int kGB = G < 4 ? G : 4;
@@ -265,6 +270,7 @@ __device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, int
         r.w = acc[gg][3 % kCols] * inv;
       }
       reinterpret_cast<Vec*>(outp + (g0 + gg) * D)[lane] = r;
+      if (lse && lane == 0) lse[g0 + gg] = lse_of(M[gg], L[gg]);
     }
   }
 }
@@ -310,7 +316,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     const Slice sl = make_slice(p, s, blockIdx.x == 0);
     const int n = slice_tiles(sl);
     pref[s + 1] = n;
-    if (n == 0 && blockIdx.x == 0) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+    if (n == 0 && blockIdx.x == 0) {
+      if (p.lse) {  // partial mode (sequence shard without rows): O = 0, lse = -inf
+        const int b = s / p.H, h = s % p.H;
+        for (int i = 0; i < G * D; ++i) p.out[((size_t)b * p.Hq + (size_t)h * G) * D + i] = 0.f;
+        for (int gg = 0; gg < G; ++gg) p.lse[(size_t)b * p.Hq + (size_t)h * G + gg] = -INFINITY;
+      } else {
+        raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+      }
+    }
   }
   if (threadIdx.x == 0) {
     pref[0] = 0;
@@ -441,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             r.w *= inv;
           }
           reinterpret_cast<Vec*>(outp + gg * D)[lane] = r;
+          if (p.lse && lane == gg) p.lse[(size_t)b * p.Hq + (size_t)h * G + gg] = lse_of(mr[gg], lr[gg]);
         }
       } else {
         // partial: written now, published (fence + counter) once this CTA's
@@ -485,7 +500,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (last) {
           __threadfence();  // acquire the other contributors' partials
           const int b = sp / p.H, h = sp % p.H;
-          merge_slice<D, G>(p, p.out + ((size_t)b * p.Hq + (size_t)h * G) * D, P0, c_first, c_last,
+          merge_slice<D, G>(p, p.out + ((size_t)b * p.Hq + (size_t)h * G) * D,
+                            p.lse ? p.lse + (size_t)b * p.Hq + (size_t)h * G : nullptr, P0, c_first, c_last,
                             T, Gc, lane);
           if (lane == 0) p.counters[sp] = 0;
         }

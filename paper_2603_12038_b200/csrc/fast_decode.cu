@@ -550,7 +550,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
     }
     outp[e] = Ls > 0.f ? Os / Ls : 0.f;
-    if (rank == 0 && e == 0 && ok && !(Ls > 0.f)) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+    if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
+      if (e % D == 0)
+        p.lse[(size_t)b * p.Hq + (size_t)h * G + gg] = Ls > 0.f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
+    } else if (rank == 0 && e == 0 && ok && !(Ls > 0.f)) {
+      raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+    }
   }
   if (trace && threadIdx.x == 0) trace[14] = (long long)globaltimer();
   cluster_sync_all();

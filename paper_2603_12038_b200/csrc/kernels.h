@@ -37,6 +37,7 @@ constexpr int kMaxCtas = 1024;  // stream-K decode grid cap (2 partial slots per
 struct DecodeParams {
   const float* q;      // [B][Hq][D]
   float* out;          // [B][Hq][D]
+  float* lse;          // [B][Hq] natural-log sum-exp (partial mode for sequence shards) or null
   float* logits;       // [B][H][Lmax] pooled logits over J (dense only) or null
   int pool;
   int layer, B, H, Hq, Lmax, crows, R;
@@ -83,6 +84,7 @@ struct FastParams {
   int prefetch;                   // SFI_FAST_PREFETCH: stream before the PDL wait
   float scale_log2;               // log2(e) / sqrt(d)
   long long* trace;               // debug: per-CTA globaltimer stamps [grid][16] (null = off)
+  float* lse;                     // [B][Hq] partial mode (sequence shards): LSE out, empty allowed
 };
 int fast_cluster_size(int slices, int num_sms);
 cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
@@ -118,6 +120,26 @@ cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* l
                                      int* launches);
 cudaError_t launch_topk_explicit(int rows, int n, int K, const double* scores, const int32_t* allowed,
                                  int32_t* sel, int32_t* n_sel, cudaStream_t st, int* launches);
+
+// sequence sharding
+cudaError_t launch_seq_lengths(const sfi_shape& s, const sfi_cache& c, int32_t* g_prefix, const int32_t* g_nsink,
+                               int32_t* g_recent, int advance, int base, int is_last, int32_t* j_off,
+                               int32_t* n_glob, cudaStream_t st);
+cudaError_t launch_merge_partials(int n_parts, int rows, int D, const float* o_parts, const float* lse_parts,
+                                  float* out, cudaStream_t st);
+cudaError_t launch_seq_selector_stats(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
+                                      const sfi_selector_params& prm, const SelectorScratch& scr,
+                                      const int32_t* j_off, const int32_t* n_glob, int phase, double* row_max,
+                                      double* row_sums, double* edges, cudaStream_t st);
+cudaError_t launch_seq_selector_finish(const sfi_shape& s, const sfi_cache& c, int layer,
+                                       const sfi_selector_params& prm, const SelectorScratch& scr,
+                                       const int32_t* j_off, const int32_t* n_glob, const double* edges_all,
+                                       int n_shards, int pos_base, double* cand_score, int32_t* cand_pos,
+                                       cudaStream_t st, int* launches);
+size_t seq_pick_scratch_bytes(const sfi_shape& s, int n_shards);
+cudaError_t launch_seq_selector_pick(const sfi_shape& s, const sfi_cache& c, int layer, int n_shards,
+                                     const double* cand_score_all, const int32_t* cand_pos_all, int pos_base,
+                                     int pos_end, void* scratch, cudaStream_t st, int* launches);
 
 // workspace carve-up (capi.cu)
 struct Workspace {

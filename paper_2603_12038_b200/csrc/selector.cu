@@ -93,14 +93,24 @@ struct SelParams {
   // [n_shards][B][H][ld] (H = this shard's heads [h_off, h_off + H)); null = local
   const double* z_all;
   int H_all, h_off;
+  // sequence sharding: this shard's J is the slice
+  // [j_off[b], j_off[b] + n) of the global J of n_glob[b] positions
+  const int32_t* j_off;
+  const int32_t* n_glob;
+  int seq_phase;            // 1 = local row max, 2 = local sums, 3 = z_base + edges (0 = unsharded)
+  double* row_max;          // [rows]       (phase 1 out, phase 2 in: all-reduced MAX)
+  double* row_sums;         // [rows][5]    (phase 2 out, phase 3 in: all-reduced SUM)
+  double* edges;            // [rows][2R+2] (phase 3 out): first R, last R z_base values, j_off, n
+  const double* edges_all;  // [n_shards][rows][2R+2] all-gathered edges (refine halo)
+  int n_shards;
 };
 
 // Row geometry: n = |J|, j_min, position of index j, u(j).
 template <bool kExp>
 struct Src {
   const SelParams& p;
-  int n, j_min;
-  __device__ __forceinline__ Src(const SelParams& pp, int b) : p(pp) {
+  int n, j_min, b_;
+  __device__ __forceinline__ Src(const SelParams& pp, int b) : p(pp), b_(b) {
     if (kExp) {
       n = p.n_fixed;
       j_min = n > 0 ? p.allowed[0] : 0;
@@ -122,10 +132,12 @@ struct Src {
   // make_cache_stats: (double)(allowed[i] - j_min) / ((double)(j_max - j_min) + eps)
   __device__ __forceinline__ double u(int j, double denom) const {
     if (kExp) return (double)(p.allowed[j] - j_min) / denom;
+    if (p.j_off) return (double)(j + p.j_off[b_]) / denom;  // global J index (sequence shard)
     return (double)j / denom;
   }
   __device__ __forceinline__ double u_denom() const {
     if (kExp) return (double)(p.allowed[n - 1] - j_min) + p.eps;
+    if (p.n_glob) return (double)(p.n_glob[b_] - 1) + p.eps;
     return (double)(n - 1) + p.eps;
   }
   __device__ __forceinline__ int pos(int j) const { return kExp ? p.allowed[j] : j_min + j; }
@@ -203,6 +215,26 @@ __device__ __forceinline__ void cluster_reduce(T (&v)[NV], int nv, T* wbuf, T (*
     }
 }
 
+// Sequence shard: the soft-NMS halo its neighbours need — the first and last
+// R z_base values of its J slice, then (j_off, n) — NaN where absent.
+template <bool kExp>
+__device__ __forceinline__ void write_edges(const SelParams& p, int row, const double* A, int n,
+                                            const Src<kExp>& src) {
+  const int R = p.nms_radius;
+  const int w = 2 * R + 2;
+  double* e = p.edges + (size_t)row * w;
+  for (int t = threadIdx.x; t < w; t += blockDim.x) {
+    double v;
+    if (t < R) v = (t < n) ? A[t] : __longlong_as_double(0x7ff8000000000000ll);
+    else if (t < 2 * R) {
+      const int i = n - R + (t - R);
+      v = (i >= 0 && i < n) ? A[i] : __longlong_as_double(0x7ff8000000000000ll);
+    } else if (t == 2 * R) v = (double)(p.j_off ? p.j_off[src.b_] : 0);
+    else v = (double)n;
+    e[t] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Stage A, decode fast path: W = 1, alpha = 1.
 template <bool kExp>
@@ -217,7 +249,15 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
   const int row = blockIdx.y;
   const Src<kExp> src(p, row / p.H);
   const int n = src.n;
-  if (n <= 0) return;  // uniform over the cluster
+  const int ph = p.seq_phase;
+  if (n <= 0) {  // uniform over the cluster
+    if (ph != 0 && rank == 0) {  // sequence shard without J positions: neutral stats
+      if (ph == 1 && threadIdx.x == 0) p.row_max[row] = kMaskedLogit;
+      if (ph == 2 && threadIdx.x < 5) p.row_sums[row * 5 + threadIdx.x] = 0.0;
+      if (ph == 3) write_edges(p, row, nullptr, 0, src);
+    }
+    return;
+  }
   const int chunk = (n + kCS - 1) / kCS;
   const int lo = rank * chunk;
   const int hi = min(n, lo + chunk);
@@ -227,6 +267,8 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
 
   // pass 1: row max (starts at kMaskedLogit), finite check
   double m1[1] = {kMaskedLogit};
+  if (ph >= 2) goto after_max;  // sequence shard: the max was all-reduced
+  {
   bool bad = false;
   for (int j = lo + threadIdx.x; j < hi; j += kT) {
     const double v = src.logit(row, 0, j);
@@ -235,14 +277,22 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
   }
   if (bad) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
   cluster_reduce<1>(m1, 1, wbuf, red, par, cl, OpMax());
-  const double mx = m1[0];
+  }
+  if (ph == 1) {
+    if (rank == 0 && threadIdx.x == 0) p.row_max[row] = m1[0];
+    cl.sync();
+    return;
+  }
+after_max:
+  const double mx = ph >= 2 ? p.row_max[row] : m1[0];
 
   // pass 2: p, w and the five sums
   const double denom_u = src.u_denom();
   double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   bool badn = false;
   constexpr int kU = 2;  // loads of kU iterations are issued before any use
-  for (int j0 = lo + threadIdx.x; j0 < hi; j0 += kU * kT) {
+  // (a sequence shard's phase 3 reuses the p, w of its phase 2)
+  for (int j0 = (ph == 3 ? hi : lo + threadIdx.x); j0 < hi; j0 += kU * kT) {
     double vv[kU], nn[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -270,7 +320,17 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
     }
   }
   if (badn) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
-  cluster_reduce<5>(s, 5, wbuf, red, par, cl, OpSum());
+  if (ph == 3) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) s[k] = p.row_sums[row * 5 + k];  // all-reduced over the shards
+  } else {
+    cluster_reduce<5>(s, 5, wbuf, red, par, cl, OpSum());
+  }
+  if (ph == 2) {
+    if (rank == 0 && threadIdx.x < 5) p.row_sums[row * 5 + threadIdx.x] = s[threadIdx.x];
+    cl.sync();
+    return;
+  }
   if (threadIdx.x == 0 && rank == 0 && (s[0] <= 0.0 || s[1] <= 0.0))
     raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
   // f = p c1, r = w c2 (normalize); fuse (selector.cpp:166-174)
@@ -300,6 +360,10 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
       const int j = j0 + u * kT;
       if (j < hi) A[j] = log(a * pa[u] + bb * wb[u] + p.eps);
     }
+  }
+  if (ph == 3) {
+    cl.sync();  // every CTA's z_base written
+    if (rank == 0) write_edges(p, row, A, n, src);
   }
   cl.sync();  // remote reads of `red` done before any CTA exits
 }
@@ -437,6 +501,22 @@ __device__ __forceinline__ const double* zrow(const SelParams& p, int b, int h) 
   return p.sa + (size_t)(b * p.H + h) * p.ld;
 }
 
+// z_base at global J index g from the all-gathered shard edges (first / last R
+// values of every shard's slice, then its j_off and n)
+__device__ __forceinline__ double halo(const SelParams& p, int row, int g, int R) {
+  const int w = 2 * R + 2;
+  const int rows = p.B * p.H;
+  for (int s = 0; s < p.n_shards; ++s) {
+    const double* e = p.edges_all + ((size_t)s * rows + row) * w;
+    const int so = (int)e[2 * R], sn = (int)e[2 * R + 1];
+    if (g >= so && g < so + sn) {
+      const int li = g - so;
+      return li < R ? e[li] : e[R + li - (sn - R)];
+    }
+  }
+  return 0.0;  // unreachable for a consistent shard layout
+}
+
 // ---------------------------------------------------------------------------
 // Stage B: soft-NMS per head, then cross-head exclusivity; one thread per
 // (b, j), the CTA's 256 positions x H heads (+ halo) staged in shared memory.
@@ -454,19 +534,25 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   const bool staged = R <= kMaxNmsR;
   // kH = 16 also serves head counts that are not a power of two (runtime guard)
   const int Hr = p.z_all ? p.H_all : (kH == 16 ? p.H : kH);
+  // sequence shard: local j covers global J index j + off of ng; the soft-NMS
+  // window reaches into the neighbours' edges
+  const bool seq = p.edges_all != nullptr;
+  const int off = seq ? p.j_off[b] : 0;
+  const int ng = seq ? p.n_glob[b] : n;
   if (staged) {
     // every thread stages column t and t + 256 (halo) of all heads; all loads
     // are issued before the first shared store
     const int span = kRefineT + 2 * R;
     const int t0 = threadIdx.x, t1 = threadIdx.x + kRefineT;
     const int ja = j0 - R + t0, jb = j0 - R + t1;
-    const bool oka = ja >= 0 && ja < n, okb = t1 < span && jb < n;
+    const bool oka = ja + off >= 0 && ja + off < ng, okb = t1 < span && jb + off < ng;
+    const bool loca = ja >= 0 && ja < n, locb = jb < n;
     double va[kH], vb[kH];
 #pragma unroll
     for (int h = 0; h < kH; ++h) {
       const double* z = zrow(p, b, h < Hr ? h : 0);
-      va[h] = (h < Hr && oka) ? z[ja] : 0.0;
-      vb[h] = (h < Hr && okb) ? z[jb] : 0.0;
+      va[h] = (h < Hr && oka) ? (loca ? z[ja] : halo(p, b * p.H + h, ja + off, R)) : 0.0;
+      vb[h] = (h < Hr && okb) ? (locb ? z[jb] : halo(p, b * p.H + h, jb + off, R)) : 0.0;
     }
 #pragma unroll
     for (int h = 0; h < kH; ++h) {
@@ -477,8 +563,8 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
   }
   const int idx = j0 + threadIdx.x;
   if (idx >= n) return;
-  const int lo = max(0, idx - R);
-  const int hi = min(n - 1, idx + R);
+  const int lo = max(-off, idx - R);
+  const int hi = min(ng - 1 - off, idx + R);
   double zn[kH];
 #pragma unroll
   for (int h = 0; h < kH; ++h) {
@@ -1102,6 +1188,88 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
   return launch_k(sel_topk_kernel<kExp, false>, gc, dim3(kT), 0, st, p);
 }
 
+// ---------------------------------------------------------------------------
+// Sequence sharding (C4): candidates of the local top-k, then the global pick.
+
+// (z_adj score, global position) of this shard's local top-k; -inf / 0 pads
+__global__ void sel_seq_cand_kernel(const SelParams p, int pos_base, double* cand_score, int32_t* cand_pos) {
+  griddep_wait();
+  griddep_launch();
+  const int row = blockIdx.x;
+  const Src<false> src(p, row / p.H);
+  const int cnt = p.n_sel[row];
+  for (int i = threadIdx.x; i < p.K; i += blockDim.x) {
+    double sc = -INFINITY;
+    int32_t pos = 0;
+    if (i < cnt) {
+      const int pl = p.sel[(size_t)row * p.K + i];
+      sc = p.sb[(size_t)row * p.ld + (pl - src.j_min)];
+      pos = pl + pos_base;
+    }
+    cand_score[(size_t)row * p.K + i] = sc;
+    cand_pos[(size_t)row * p.K + i] = pos;
+  }
+}
+
+// all-gathered [P][rows][K] scores -> [rows][P*K] (shard order = position order),
+// plus the index list 0..P*K-1 the explicit top-k ranks them by
+__global__ void sel_seq_gather_kernel(int P, int rows, int K, const double* cand_all, double* scores_t,
+                                      int32_t* iota) {
+  griddep_wait();
+  griddep_launch();
+  const int row = blockIdx.y;
+  const int n = P * K;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int sh = i / K, k = i % K;
+    scores_t[(size_t)row * n + i] = cand_all[((size_t)sh * rows + row) * K + k];
+    if (row == 0) iota[i] = i;
+  }
+}
+
+// global top-k indices (ascending = position order) -> this shard's positions,
+// local, ascending, into sel / n_sel; pads (position 0) dropped
+constexpr int kPickT = 256;
+__global__ void __launch_bounds__(kPickT) sel_seq_pick_kernel(int P, int rows, int K, const int32_t* idx_sel,
+                                                               const int32_t* idx_n, const int32_t* cand_pos_all,
+                                                               int pos_base, int pos_end, int32_t* sel,
+                                                               int32_t* n_sel) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ int wsum[kPickT / 32];
+  const int row = blockIdx.x;
+  const int cnt = idx_n[row];
+  const int per = (K + kPickT - 1) / kPickT;
+  const int i0 = threadIdx.x * per;
+  int keep = 0;
+  for (int i = i0; i < min(cnt, i0 + per); ++i) {
+    const int id = idx_sel[(size_t)row * K + i];
+    const int pos = cand_pos_all[((size_t)(id / K) * rows + row) * K + (id % K)];
+    keep += (pos > pos_base && pos <= pos_end) ? 1 : 0;
+  }
+  // block exclusive scan of keep
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = keep;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int base = 0, total = 0;
+  for (int w = 0; w < kPickT / 32; ++w) {
+    if (w < warp) base += wsum[w];
+    total += wsum[w];
+  }
+  int o = base + x - keep;
+  for (int i = i0; i < min(cnt, i0 + per); ++i) {
+    const int id = idx_sel[(size_t)row * K + i];
+    const int pos = cand_pos_all[((size_t)(id / K) * rows + row) * K + (id % K)];
+    if (pos > pos_base && pos <= pos_end) sel[(size_t)row * K + o++] = pos - pos_base;
+  }
+  if (threadIdx.x == 0) n_sel[row] = total;
+}
+
 // phases: 1 = fuse (z_base), 2 = refine + top-k
 template <bool kExp>
 cudaError_t run3(const SelParams& p, int rows, int n_max, int batches, cudaStream_t st,
@@ -1164,6 +1332,105 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
   fill_cfg(p, prm);
   if (s.n_kv_heads > 16) return cudaErrorInvalidValue;
   return run3<false>(p, (int)slices, s.max_positions, s.batch, st, launches, phases);
+}
+
+namespace {
+SelParams seq_params(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
+                     const sfi_selector_params& prm, const SelectorScratch& scr, const int32_t* j_off,
+                     const int32_t* n_glob) {
+  SelParams p{};
+  const size_t slices = (size_t)s.batch * s.n_kv_heads;
+  p.logits32 = logits;
+  p.norms_c = c.key_norms + (size_t)layer * slices * s.max_positions;
+  p.prefix_len = c.prefix_len;
+  p.n_sink_b = c.n_sink_b;
+  p.recent_len = c.recent_len;
+  p.W = 1;
+  p.ld = s.max_positions;
+  p.sa = scr.a;
+  p.sb = scr.b;
+  p.sel = c.sel + (size_t)layer * slices * s.k_budget;
+  p.n_sel = c.n_sel + (size_t)layer * slices;
+  p.err = c.error_flags;
+  p.B = s.batch;
+  p.H = s.n_kv_heads;
+  p.Lmax = s.max_positions;
+  p.K = s.k_budget;
+  p.j_off = j_off;
+  p.n_glob = n_glob;
+  fill_cfg(p, prm);
+  return p;
+}
+}  // namespace
+
+cudaError_t launch_seq_selector_stats(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
+                                      const sfi_selector_params& prm, const SelectorScratch& scr,
+                                      const int32_t* j_off, const int32_t* n_glob, int phase, double* row_max,
+                                      double* row_sums, double* edges, cudaStream_t st) {
+  SelParams p = seq_params(s, c, layer, logits, prm, scr, j_off, n_glob);
+  p.seq_phase = phase;
+  p.row_max = row_max;
+  p.row_sums = row_sums;
+  p.edges = edges;
+  const dim3 gc(kCS, (unsigned)(s.batch * s.n_kv_heads));
+  return launch_k(sel_fuse_fast_kernel<false>, gc, dim3(kT), 0, st, p);
+}
+
+cudaError_t launch_seq_selector_finish(const sfi_shape& s, const sfi_cache& c, int layer,
+                                       const sfi_selector_params& prm, const SelectorScratch& scr,
+                                       const int32_t* j_off, const int32_t* n_glob, const double* edges_all,
+                                       int n_shards, int pos_base, double* cand_score, int32_t* cand_pos,
+                                       cudaStream_t st, int* launches) {
+  SelParams p = seq_params(s, c, layer, nullptr, prm, scr, j_off, n_glob);
+  p.edges_all = edges_all;
+  p.n_shards = n_shards;
+  const int rows = s.batch * s.n_kv_heads;
+  cudaError_t e = run3<false>(p, rows, s.max_positions, s.batch, st, launches, 2);
+  if (e != cudaSuccess) return e;
+  if (launches) *launches += 1;
+  return launch_k(sel_seq_cand_kernel, dim3(rows), dim3(256), 0, st, p, pos_base, cand_score, cand_pos);
+}
+
+size_t seq_pick_scratch_bytes(const sfi_shape& s, int n_shards) {
+  const size_t rows = (size_t)s.batch * s.n_kv_heads, n = (size_t)n_shards * s.k_budget;
+  return rows * n * sizeof(double) + ((n * 4 + 255) / 256) * 256 + rows * s.k_budget * 4 + rows * 4 + 1024;
+}
+
+cudaError_t launch_seq_selector_pick(const sfi_shape& s, const sfi_cache& c, int layer, int n_shards,
+                                     const double* cand_score_all, const int32_t* cand_pos_all, int pos_base,
+                                     int pos_end, void* scratch, cudaStream_t st, int* launches) {
+  const int rows = s.batch * s.n_kv_heads, K = s.k_budget, n = n_shards * K;
+  const size_t slices = (size_t)rows;
+  int32_t* sel = c.sel + (size_t)layer * slices * K;
+  int32_t* n_sel = c.n_sel + (size_t)layer * slices;
+  if (K == 0) return cudaMemsetAsync(n_sel, 0, rows * sizeof(int32_t), st);
+  uint8_t* w = static_cast<uint8_t*>(scratch);
+  double* scores_t = reinterpret_cast<double*>(w);
+  w += (size_t)rows * n * sizeof(double);
+  int32_t* iota = reinterpret_cast<int32_t*>(w);
+  w += (((size_t)n * 4 + 255) / 256) * 256;
+  int32_t* idx_sel = reinterpret_cast<int32_t*>(w);
+  w += (size_t)rows * K * 4;
+  int32_t* idx_n = reinterpret_cast<int32_t*>(w);
+  cudaError_t e = launch_k(sel_seq_gather_kernel, dim3((n + 255) / 256, rows), dim3(256), 0, st, n_shards, rows,
+                           K, cand_score_all, scores_t, iota);
+  if (e != cudaSuccess) return e;
+  SelParams p{};
+  p.allowed = iota;
+  p.n_fixed = n;
+  p.W = 1;
+  p.ld = n;
+  p.sb = scores_t;
+  p.sel = idx_sel;
+  p.n_sel = idx_n;
+  p.B = rows;
+  p.H = 1;
+  p.Lmax = n;
+  p.K = K;
+  if ((e = launch_topk<true>(p, rows, n, st)) != cudaSuccess) return e;
+  if (launches) *launches += 3;
+  return launch_k(sel_seq_pick_kernel, dim3(rows), dim3(kPickT), 0, st, n_shards, rows, K,
+                  (const int32_t*)idx_sel, (const int32_t*)idx_n, cand_pos_all, pos_base, pos_end, sel, n_sel);
 }
 
 cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* logits, const double* norms,

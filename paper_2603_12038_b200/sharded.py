@@ -76,4 +76,178 @@ class HeadShardedSfi:
             self.cache.selector_finish(layer, z.unsqueeze(0), 1, 0, params)
 
     def __getattr__(self, name):  # everything else is per head: the local cache
+        if name == "cache":
+            raise AttributeError(name)
+        return getattr(self.cache, name)
+
+
+# ---------------------------------------------------------------------------
+# Sequence sharding (config C4: 256K context, too few KV heads to split)
+
+def all_reduce_(t: torch.Tensor, op, group=None) -> torch.Tensor:
+    """In-place all-reduce; gloo (CPU tests) stages CUDA tensors through host memory."""
+    if dist.get_backend(group) == "nccl" or not t.is_cuda:
+        dist.all_reduce(t, op=op, group=group)
+        return t
+    h = t.cpu()
+    dist.all_reduce(h, op=op, group=group)
+    t.copy_(h)
+    return t
+
+
+def seq_block(prompt_len: int, world: int) -> int:
+    """Positions per non-last shard: the prompt split evenly; decode tokens
+    land on the last shard."""
+    return -(-prompt_len // world)
+
+
+class SeqShardedSfi:
+    """This rank's shard of a sequence-sharded SFI cache: positions
+    (base, base + block] (the last rank: (base, max_positions]) of every
+    request, all KV heads. Per layer, slow steps exchange the Selector's row
+    statistics (max, 5 sums), soft-NMS edges and top-k candidates; every step
+    exchanges the (O, LSE) attention partials, merged in rank order.
+
+    The collective steps are separate methods so a single process can drive
+    P shards in lockstep (tests); `selector`, `dense_decode` and `fast_decode`
+    run them with torch.distributed on the current stream."""
+
+    def __init__(self, n_layers: int, batch: int, n_kv_heads: int, n_q_heads: int, head_dim: int,
+                 max_positions: int, prompt_len: int, n_sink: int = 4, k_budget: int = 2048,
+                 n_recent: int = 256, group=None, device=None, world: int | None = None,
+                 rank: int | None = None):
+        from . import _sfi_b200 as _C
+
+        self._C = _C
+        self.group = group
+        self.world = world if world is not None else dist.get_world_size(group)
+        self.rank = rank if rank is not None else dist.get_rank(group)
+        self.block = seq_block(prompt_len, self.world)
+        self.base = self.rank * self.block
+        self.is_last = self.rank == self.world - 1
+        cap = (max_positions - self.base) if self.is_last else self.block
+        if cap < 1 or (self.is_last and self.base >= prompt_len):
+            raise ValueError("sequence shard layout: the prompt must reach the last shard")
+        self.cap = cap
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.cache = SfiCache(n_layers, batch, n_kv_heads, n_q_heads, head_dim, cap, n_sink, k_budget,
+                              n_recent, device=device)
+        dev = self.cache.k_cache.device
+        B, H, Hq, P, K = batch, n_kv_heads, n_q_heads, self.world, k_budget
+        z = lambda *s, dt=torch.int32: torch.zeros(s, dtype=dt, device=dev)  # noqa: E731
+        self.g_prefix, self.g_nsink, self.g_recent = z(B), z(B), z(B)
+        self.j_off, self.n_glob = z(B), z(B)
+        self.params = _C.SelectorParams()
+        ne = _C.seq_edges_doubles(self.cache.shape, self.params)
+        f64 = torch.float64
+        self.row_max = z(B * H, dt=f64)
+        self.row_sums = z(B * H * 5, dt=f64)
+        self.edges = z(ne, dt=f64)
+        self.edges_all = z(P, ne, dt=f64)
+        self.cand_score, self.cand_pos = z(B * H * K, dt=f64), z(B * H * K)
+        self.cand_score_all, self.cand_pos_all = z(P, B * H * K, dt=f64), z(P, B * H * K)
+        self.pick_scratch = z(_C.seq_pick_scratch_bytes(self.cache.shape, P), dt=torch.uint8)
+        self.o_part = z(B, Hq, head_dim, dt=torch.float32)
+        self.lse_part = z(B, Hq, dt=torch.float32)
+        self.o_all = z(P, B, Hq, head_dim, dt=torch.float32)
+        self.lse_all = z(P, B, Hq, dt=torch.float32)
+        self.n_recent = n_recent
+
+    # -- lengths -------------------------------------------------------------
+    def set_lengths(self, prefix_len, n_sink_b):
+        """Global lengths of every request (host values, like SfiCache.set_lengths)."""
+        L = torch.tensor(list(map(int, prefix_len)), dtype=torch.int32)
+        ns = torch.tensor(list(map(int, n_sink_b)), dtype=torch.int32)
+        if self.is_last and int(L.min()) <= self.base:
+            raise ValueError("decode appends on the last shard: every prefix must reach it")
+        self.g_prefix.copy_(L)
+        self.g_nsink.copy_(ns)
+        self.g_recent.copy_(torch.clamp(L - ns, 0, self.n_recent))
+        self._lengths(0)
+        torch.cuda.current_stream().synchronize()
+
+    def _lengths(self, advance: int):
+        c = self.cache
+        self._C.seq_lengths(c.shape, c.cache, self.g_prefix.data_ptr(), self.g_nsink.data_ptr(),
+                            self.g_recent.data_ptr(), advance, self.base, int(self.is_last),
+                            self.j_off.data_ptr(), self.n_glob.data_ptr(), c._stream())
+
+    def step_advance(self):
+        self._lengths(1)
+
+    # -- attention partials ----------------------------------------------------
+    def dense_partial(self, layer, q, logits, pool=0):
+        c = self.cache
+        self._C.dense_decode_partial(c.shape, c.cache, layer, c._ptr(q, torch.float32), self.o_part.data_ptr(),
+                                     self.lse_part.data_ptr(), c._ptr(logits, torch.float32), pool, c._stream())
+
+    def fast_partial(self, layer, q, k_new, v_new, prefetch=False):
+        c = self.cache
+        own = self.is_last  # the current position is on the last shard
+        self._C.fast_decode_partial(c.shape, c.cache, layer, c._ptr(q, torch.float32),
+                                    c._ptr(k_new, torch.bfloat16) if own else 0,
+                                    c._ptr(v_new, torch.bfloat16) if own else 0, self.o_part.data_ptr(),
+                                    self.lse_part.data_ptr(), self._C.FAST_PREFETCH if prefetch else 0,
+                                    c._stream())
+
+    def merge(self, out):
+        """out = LSE merge of the gathered partials (o_all, lse_all) in rank order."""
+        B, Hq, d = self.o_part.shape
+        self._C.merge_partials(self.world, B * Hq, d, self.o_all.data_ptr(), self.lse_all.data_ptr(),
+                               self.cache._ptr(out, torch.float32), self.cache._stream())
+
+    def _exchange_partials(self):
+        all_gather_blocks(self.o_part, self.o_all, self.group)
+        all_gather_blocks(self.lse_part, self.lse_all, self.group)
+
+    def dense_decode(self, layer, q, out, logits, pool=0):
+        self.dense_partial(layer, q, logits, pool)
+        self._exchange_partials()
+        self.merge(out)
+
+    def fast_decode(self, layer, q, k_new, v_new, out, prefetch=False):
+        self.fast_partial(layer, q, k_new, v_new, prefetch)
+        self._exchange_partials()
+        self.merge(out)
+
+    def ring_append(self, layer, k_new, v_new):
+        if self.is_last:
+            self.cache.ring_append(layer, k_new, v_new)
+
+    # -- Selector phases ---------------------------------------------------------
+    def sel_stats(self, layer, logits, phase, params=None):
+        c = self.cache
+        self._C.seq_selector_stats(c.shape, c.cache, layer, c._ptr(logits, torch.float32) if logits is not None else 0,
+                                   params or self.params, self.j_off.data_ptr(), self.n_glob.data_ptr(), phase,
+                                   self.row_max.data_ptr(), self.row_sums.data_ptr(), self.edges.data_ptr(),
+                                   c._stream())
+
+    def sel_finish(self, layer, params=None):
+        c = self.cache
+        self._C.seq_selector_finish(c.shape, c.cache, layer, params or self.params, self.j_off.data_ptr(),
+                                    self.n_glob.data_ptr(), self.edges_all.data_ptr(), self.world, self.base,
+                                    self.cand_score.data_ptr(), self.cand_pos.data_ptr(), c._stream())
+
+    def sel_pick(self, layer):
+        c = self.cache
+        self._C.seq_selector_pick(c.shape, c.cache, layer, self.world, self.cand_score_all.data_ptr(),
+                                  self.cand_pos_all.data_ptr(), self.base, self.base + self.cap,
+                                  self.pick_scratch.data_ptr(), c._stream())
+
+    def selector(self, layer, logits, params=None):
+        self.sel_stats(layer, logits, 1, params)
+        all_reduce_(self.row_max, dist.ReduceOp.MAX, self.group)
+        self.sel_stats(layer, logits, 2, params)
+        all_reduce_(self.row_sums, dist.ReduceOp.SUM, self.group)
+        self.sel_stats(layer, None, 3, params)
+        all_gather_blocks(self.edges, self.edges_all, self.group)
+        self.sel_finish(layer, params)
+        all_gather_blocks(self.cand_score, self.cand_score_all, self.group)
+        all_gather_blocks(self.cand_pos, self.cand_pos_all, self.group)
+        self.sel_pick(layer)
+
+    def __getattr__(self, name):  # compact_build, check_errors, buffers: the local cache
+        if name == "cache":
+            raise AttributeError(name)
         return getattr(self.cache, name)
