@@ -149,3 +149,203 @@ def test_sequence_sharded_step_matches_one_gpu(P, H, Hq, prompt, K, B):
     Lg = L + 1
     assert torch.equal(last.k_cache[0, :, :, Lg - 1 - last.base].cpu(), full.k_cache[0, :, :, Lg - 1].cpu())
     assert torch.equal(last.key_norms[0, :, :, Lg - 1 - last.base].cpu(), full.key_norms[0, :, :, Lg - 1].cpu())
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _seq_gpu_worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2603_12038_b200 import SelectorParams, SfiCache
+        from paper_2603_12038_b200.sharded import SeqShardedSfi
+
+        B, H, Hq, d, prompt, K, R, ns = 1, 4, 64, 128, 6000, 256, 256, 4
+        Lmax = prompt + 16
+        full = SfiCache(1, B, H, Hq, d, Lmax, ns, K, R)
+        full.fill_synthetic(seed=3, length=prompt)  # identical on every rank
+        sh = SeqShardedSfi(1, B, H, Hq, d, Lmax, prompt, ns, K, R)
+        n = min(sh.cap, Lmax - sh.base)
+        sh.k_cache[:, :, :, :n].copy_(full.k_cache[:, :, :, sh.base:sh.base + n])
+        sh.v_cache[:, :, :, :n].copy_(full.v_cache[:, :, :, sh.base:sh.base + n])
+        sh.key_norms[:, :, :, :n].copy_(full.key_norms[:, :, :, sh.base:sh.base + n])
+        sh.set_lengths([prompt], [ns])
+        full.set_lengths([prompt], [ns])
+        g = torch.Generator().manual_seed(8)
+        qv = torch.randn(B, Hq, d, generator=g).cuda()
+        kn = torch.randn(B, H, d, generator=g).bfloat16().cuda()
+        ok = True
+        for step, slow in enumerate((True, False, False)):
+            full.step_advance()
+            sh.step_advance()
+            o_full = torch.zeros(B, Hq, d, device="cuda")
+            o_sh = torch.zeros_like(o_full)
+            if slow:
+                full.ring_append(0, kn, kn)
+                sh.ring_append(0, kn, kn)
+                lg_f, lg_s = torch.zeros_like(full.pooled_logits), torch.zeros_like(sh.pooled_logits)
+                full.dense_decode(0, qv, o_full, lg_f, 0)
+                full.selector(0, lg_f, SelectorParams())
+                full.compact_build(0, rebuild_ring=True)
+                sh.dense_decode(0, qv, o_sh, lg_s, 0)
+                sh.selector(0, lg_s)
+                sh.compact_build(0, rebuild_ring=True)
+                torch.cuda.synchronize()
+                sel = [torch.zeros(B, H, K, dtype=torch.int32) for _ in range(world)]
+                cnt = [torch.zeros(B, H, dtype=torch.int32) for _ in range(world)]
+                dist.all_gather(sel, sh.sel[0].cpu())
+                dist.all_gather(cnt, sh.n_sel[0].cpu())
+                for h in range(H):
+                    got = torch.cat([sel[r][0, h, : int(cnt[r][0, h])] + r * sh.block for r in range(world)])
+                    ok &= torch.equal(got, full.sel[0, 0, h, : int(full.n_sel[0, 0, h])].cpu())
+            else:
+                full.fast_decode(0, qv, kn, kn, o_full)
+                sh.fast_decode(0, qv, kn, kn, o_sh)
+            torch.cuda.synchronize()
+            full.check_errors()
+            sh.check_errors()
+            ok &= rel_err(o_sh.cpu().numpy(), o_full.cpu().numpy()) < TOL
+        q.put((rank, bool(ok)))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+def test_sequence_sharded_two_processes_one_gpu():
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seq_gpu_worker, args=(r, 2, port, qu)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(qu.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
+
+
+# ------------------------------------------------------------- CPU, gloo ----
+
+def _np_case(seed=4, H=4, n=2500):
+    rng = np.random.default_rng(seed)
+    vals = rng.normal(0.0, 0.4, size=(H, n))
+    norms = np.abs(rng.normal(11.0, 2.0, size=(H, n))) + 0.1
+    return vals, norms, np.arange(5, 5 + n, dtype=np.int32)
+
+
+def _seq_protocol_worker(rank, world, port, cuts, q):
+    """The device protocol of sequence-sharded Selector (sharded.py
+    SeqShardedSfi.selector), with a numpy restatement of the per-shard stages
+    (selector.cu decode fast path) and the real gloo collectives."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle import oracle as O
+        from paper_2603_12038_b200.sharded import all_gather_blocks, all_reduce_
+
+        vals, norms, allowed = _np_case()
+        H, ng = vals.shape
+        K, R, eps = 300, 2, 1e-8
+        a, b = cuts[rank], cuts[rank + 1]
+        v, nm, n = vals[:, a:b], norms[:, a:b], b - a
+        # phase 1: row max (from kMaskedLogit), all-reduce MAX
+        mx = torch.from_numpy(np.maximum(v.max(1) if n else -1e30, -1e30).astype(np.float64))
+        all_reduce_(mx, dist.ReduceOp.MAX)
+        # phase 2: p, prior w, five sums, all-reduce SUM
+        u = (np.arange(a, b) / ((ng - 1) + eps))[None, :]
+        p = np.exp(v - mx.numpy()[:, None])
+        w = (1.0 / (nm + eps)) * np.exp(-(u * u)) * np.sqrt(1.0 - u + eps)
+        sums = torch.from_numpy(np.stack([p.sum(1), w.sum(1), (p * p).sum(1), (p * w).sum(1), (w * w).sum(1)], 1))
+        all_reduce_(sums, dist.ReduceOp.SUM)
+        S = sums.numpy()
+        c1, c2 = 1.0 / S[:, 0], 1.0 / S[:, 1]
+        ff, fr, rr = S[:, 2] * c1 * c1, S[:, 3] * c1 * c2, S[:, 4] * c2 * c2
+        den = ff - 2 * fr + rr
+        lam = np.where(np.abs(den) >= eps, np.clip((ff - fr) / np.where(den == 0, 1, den), 0, 0.02), 0.0)
+        z = np.log((1 - lam)[:, None] * c1[:, None] * p + lam[:, None] * c2[:, None] * w + eps)
+        # phase 3: edges (first R, last R, j_off, n), all-gather
+        nan = float("nan")
+        edge = np.full((H, 2 * R + 2), nan)
+        for h in range(H):
+            for t in range(R):
+                if t < n:
+                    edge[h, t] = z[h, t]
+                if 0 <= n - R + t < n:
+                    edge[h, R + t] = z[h, n - R + t]
+            edge[h, 2 * R], edge[h, 2 * R + 1] = a, n
+        edges = torch.zeros(world, H, 2 * R + 2, dtype=torch.float64)
+        all_gather_blocks(torch.from_numpy(edge), edges)
+        E = edges.numpy()
+
+        def zg(h, gidx):  # z_base at global J index: local, else a neighbour's edge
+            if a <= gidx < b:
+                return z[h, gidx - a]
+            for s in range(world):
+                so, sn = int(E[s, h, 2 * R]), int(E[s, h, 2 * R + 1])
+                if so <= gidx < so + sn:
+                    li = gidx - so
+                    return E[s, h, li] if li < R else E[s, h, R + li - (sn - R)]
+            raise AssertionError(gidx)
+
+        zn = np.empty_like(z)
+        for h in range(H):
+            for j in range(n):
+                gj = a + j
+                m = max(zg(h, i) for i in range(max(0, gj - R), min(ng - 1, gj + R) + 1))
+                zn[h, j] = z[h, j] - 0.5 * (m - z[h, j])
+        mxh = zn.max(0)
+        e = np.exp(zn - mxh)
+        zadj = zn + 0.35 * np.log(np.maximum(e / e.sum(0), eps))
+        # local top-k candidates (score desc, position asc), padded, all-gather
+        cs = np.full((H, K), -np.inf)
+        cp = np.zeros((H, K), np.int32)
+        for h in range(H):
+            order = sorted(range(n), key=lambda j: (-zadj[h, j], j))[:K]
+            order.sort()
+            cs[h, : len(order)] = zadj[h, order]
+            cp[h, : len(order)] = allowed[a + np.array(order, dtype=int)] if order else []
+        cs_all = torch.zeros(world, H, K, dtype=torch.float64)
+        cp_all = torch.zeros(world, H, K, dtype=torch.int32)
+        all_gather_blocks(torch.from_numpy(cs), cs_all)
+        all_gather_blocks(torch.from_numpy(cp), cp_all)
+        # pick: global top-K of the rank-ordered candidates, keep own positions
+        ref, _ = O.load("best").run_selector(vals, allowed, norms, O.make_cfg(k_budget=K))
+        ok = True
+        for h in range(H):
+            sc = cs_all[:, h].reshape(-1).numpy()
+            ps = cp_all[:, h].reshape(-1).numpy()
+            idx = sorted(range(len(sc)), key=lambda i: (-sc[i], i))[:K]
+            mine = sorted(ps[i] for i in idx if ps[i] != 0 and allowed[a] <= ps[i] <= (allowed[b - 1] if n else -1))
+            want = [p_ for p_ in ref[h] if (n and allowed[a] <= p_ <= allowed[b - 1])]
+            ok &= list(mine) == list(want)
+        q.put((rank, bool(ok)))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("cuts", [[0, 1300, 2500], [0, 900, 901, 2500]])
+def test_sequence_sharded_selector_protocol_gloo(cuts):
+    world = len(cuts) - 1
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seq_protocol_worker, args=(r, world, port, cuts, qu)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(qu.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}, res
