@@ -37,11 +37,12 @@ CONFIGS = {
     "c1": ("Qwen3-0.6B-shaped attention, batch 1, 8K", 28, 16, 8, 1, 8192, 4, 512, 64),
     "c2": ("Qwen3-8B-shaped attention, batch 8, 32K", 36, 32, 8, 8, 32768, 4, 2048, 256),
     "c3": ("Qwen3-32B-shaped attention, batch 4, 128K", 64, 64, 8, 4, 131072, 4, 2048, 256),
+    "c4": ("Qwen3-235B-shaped attention, batch 1, 256K", 94, 64, 4, 1, 262144, 4, 2048, 256),
 }
 # multi-GPU partitioning per config: "dp" = independent request
 # batches per GPU (weak scaling); "heads" = KV-head sharding of ONE batch
 # (strong scaling, z_base all-gather in the Selector)
-SHARDING = {"c1": "dp", "c2": "dp", "c3": "heads"}
+SHARDING = {"c1": "dp", "c2": "dp", "c3": "heads", "c4": "seq"}
 HEAD_DIM = 128
 T_MAX = 64
 P_TRIGGER = 1.0 / 24.0
@@ -143,17 +144,24 @@ class Workload:
         self.Lmax = self.ctx + steps_total + 64
         self.torch = torch
         self.mode = SHARDING[cfg_name] if world > 1 else "single"
-        self.shard = None
+        self.world = world
+        fill_len = self.ctx
         if self.mode == "heads":
             from paper_2603_12038_b200.sharded import HeadShardedSfi
 
-            self.shard = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
-                                        self.K, self.R, device=device)
-            self.cache = self.shard.cache
-            self.H, self.Hq = self.shard.local_heads, self.shard.local_heads * self.G  # this rank's heads
-        else:
-            self.cache = sfi.SfiCache(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
+            self.drv = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
                                       self.K, self.R, device=device)
+            self.H, self.Hq = self.drv.local_heads, self.drv.local_heads * self.G  # this rank's heads
+        elif self.mode == "seq":
+            from paper_2603_12038_b200.sharded import SeqShardedSfi
+
+            self.drv = SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx, self.ns,
+                                     self.K, self.R, device=device)
+            fill_len = min(self.drv.cap, self.ctx - self.drv.base)  # this rank's positions
+        else:
+            self.drv = sfi.SfiCache(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
+                                    self.K, self.R, device=device)
+        self.cache = self.drv if self.mode in ("single", "dp") else self.drv.cache
         # tokens produced per step by the whole job, per rank's share of it
         self.job_tokens = self.B * (world if self.mode == "dp" else 1)
         self.params = sfi.SelectorParams()
@@ -166,52 +174,73 @@ class Workload:
         self.v_new = t.randn(L, B, H, d, generator=g).to(device).bfloat16()
         self.out = t.zeros(L, B, Hq, d, device=device)
         self.logits = self.cache.pooled_logits
-        c = self.cache
-        c.fill_synthetic(seed=2026 + 1, length=self.ctx)
-        c.set_lengths([self.ctx] * B, [self.ns] * B)
+        drv = self.drv
+        self.cache.fill_synthetic(seed=2026 + 1, length=fill_len)
+        self.set_lengths(self.ctx)
         # initial slow step (untimed): dense + Selector + compact incl. the ring
         self.step(slow=True, rebuild_ring=True)
         t.cuda.synchronize()
-        c.check_errors()
+        drv.check_errors()
         # exercise the fast path once eagerly (same prefix: undo its advance)
         self.step(slow=False)
-        c.set_lengths([self.ctx + 1] * B, [self.ns] * B)
+        self.set_lengths(self.ctx + 1)
         t.cuda.synchronize()
-        c.check_errors()
+        drv.check_errors()
+
+    def set_lengths(self, L: int):
+        self.drv.set_lengths([L] * self.B, [self.ns] * self.B)
 
     def step(self, slow: bool, rebuild_ring: bool = False):
-        c = self.cache
-        c.step_advance()
+        """One decode step of all layers through the mode's driver: SfiCache (1 GPU /
+        dp), HeadShardedSfi (z_base all-gather in the Selector) or SeqShardedSfi
+        (LSE-merged attention partials, sharded Selector statistics)."""
+        d = self.drv
+        d.step_advance()
         for l in range(self.L):
             if slow:
-                c.ring_append(l, self.k_new[l], self.v_new[l])
-                c.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
-                if self.shard is not None:
-                    self.shard.selector(l, self.logits, self.params)  # z_base all-gather (NCCL)
-                else:
-                    c.selector(l, self.logits, self.params)
-                c.compact_build(l, rebuild_ring=rebuild_ring)
+                d.ring_append(l, self.k_new[l], self.v_new[l])
+                d.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
+                d.selector(l, self.logits, self.params)
+                d.compact_build(l, rebuild_ring=rebuild_ring)
             else:
                 # ONE launch: ring append fused with the sparse decode; the
                 # compact rows of layer l are not written by the preceding
                 # kernel, so they stream before the PDL wait
-                c.fast_decode(l, self.q[l], self.k_new[l], self.v_new[l], self.out[l], prefetch=True)
+                d.fast_decode(l, self.q[l], self.k_new[l], self.v_new[l], self.out[l], prefetch=True)
+
+    # the attention kernels alone (per-kernel timing), no exchange
+    def fast_kernel(self, l: int):
+        if self.mode == "seq":
+            self.drv.fast_partial(l, self.q[l], self.k_new[l], self.v_new[l], prefetch=True)
+        else:
+            self.cache.fast_decode(l, self.q[l], self.k_new[l], self.v_new[l], self.out[l], prefetch=True)
+
+    def dense_kernel(self, l: int):
+        if self.mode == "seq":
+            self.drv.dense_partial(l, self.q[l], self.logits)
+        else:
+            self.cache.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
 
     def launches(self, slow: bool) -> int:
+        if self.mode == "seq":  # + merge per attention call; Selector: 3 stats + 4 finish + 3 pick
+            return 1 + self.L * ((2 + 10 + 1 + 1) if slow else 2)
         return 1 + self.L * (6 if slow else 1)
+
+    def shard_frac(self) -> float:  # this rank's share of a layer's rows (sequence shards)
+        return 1.0 / self.world if self.mode == "seq" else 1.0
 
     # algorithmic bytes of one launch (SURVEY §8(d))
     def bytes_sparse(self) -> float:
         # S rows of K+V (the current token's from k_new/v_new), q in, o out, and
         # the append: paged + ring row of K and V plus the fp64 norm
         S = self.R + self.ns + self.K
-        return (self.B * self.H * (S * 4 * HEAD_DIM + 2 * 4 * HEAD_DIM + 8)
+        return (self.B * self.H * (S * 4 * HEAD_DIM * self.shard_frac() + 2 * 4 * HEAD_DIM + 8)
                 + 2 * self.B * self.Hq * HEAD_DIM * 4)
 
     def bytes_dense(self, Lcur: int) -> float:
         rl = min(self.R, Lcur - self.ns)
         nj = Lcur - rl - self.ns
-        return (self.B * self.H * Lcur * 4 * HEAD_DIM + self.B * self.H * nj * 4
+        return ((self.B * self.H * Lcur * 4 * HEAD_DIM + self.B * self.H * nj * 4) * self.shard_frac()
                 + 2 * self.B * self.Hq * HEAD_DIM * 4)
 
 
@@ -227,9 +256,9 @@ def time_kernel(wl: Workload, which: str, iters: int) -> float:
         a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
         a.record(s)
         if which == "sparse":
-            c.fast_decode(l, wl.q[l], wl.k_new[l], wl.v_new[l], wl.out[l], prefetch=True)
+            wl.fast_kernel(l)
         else:
-            c.dense_decode(l, wl.q[l], wl.out[l], wl.logits, 0)
+            wl.dense_kernel(l)
         b.record(s)
         evs.append((a, b))
     t.cuda.synchronize()
@@ -261,7 +290,7 @@ def time_selector(wl: Workload, iters: int) -> tuple[float, float]:
         l = i % wl.L
         a, b, e = (t.cuda.Event(enable_timing=True) for _ in range(3))
         a.record(s)
-        c.selector(l, wl.logits, wl.params)
+        wl.drv.selector(l, wl.logits, wl.params)
         b.record(s)
         c.compact_build(l)
         e.record(s)
@@ -318,7 +347,7 @@ def gpu_arm(args) -> dict:
     for i in range(W):
         run(sched[i])
     torch.cuda.synchronize()
-    c.check_errors()
+    wl.drv.check_errors()
 
     timed = sched[W:W + K]
     if world > 1:
@@ -335,7 +364,7 @@ def gpu_arm(args) -> dict:
     ms = max_over_ranks(e0.elapsed_time(e1))
     if world > 1:
         dist.barrier()
-    c.check_errors()
+    wl.drv.check_errors()
     n_slow = sum(timed)
     tokens = wl.job_tokens * K
     value = tokens / (ms / 1e3)
@@ -353,7 +382,7 @@ def gpu_arm(args) -> dict:
         torch.cuda.synchronize()
         Ke = min(K, 32)
         sched_e = sched[W:W + Ke]
-        c.set_lengths([wl.ctx + 1] * wl.B, [wl.ns] * wl.B)
+        wl.set_lengths(wl.ctx + 1)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -375,7 +404,7 @@ def gpu_arm(args) -> dict:
 
     # ---- per-kernel device time (CUDA events on the launching stream) ----
     pk = peaks()
-    Lcur = int(c.prefix_len[0].item())
+    Lcur = wl.ctx + 1
     t_sp_iso = time_kernel(wl, "sparse", max(20, 2 * wl.L))
     t_de = time_kernel(wl, "dense", max(8, wl.L // 2))
     # in situ: the fast step's graph (advance + L fused launches, PDL-chained)
@@ -383,7 +412,7 @@ def gpu_arm(args) -> dict:
     # (the advance kernel's share is charged to them: conservative)
     t_fast_step = None
     if use_graph:
-        c.set_lengths([wl.ctx + 1] * wl.B, [wl.ns] * wl.B)
+        wl.set_lengths(wl.ctx + 1)
         t_fast_step = time_graph(graphs[False], 16)
     t_sp = t_fast_step / wl.L if t_fast_step else t_sp_iso
     t_sel, t_cb = time_selector(wl, max(6, wl.L // 4))
@@ -409,15 +438,18 @@ def gpu_arm(args) -> dict:
         "metric": metric_name(args.config),
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True,
-        "scaling": "strong" if wl.mode == "heads" else "weak", "vs_baseline": None,
+        "scaling": "strong" if wl.mode in ("heads", "seq") else "weak", "vs_baseline": None,
         "dtype": "bf16 KV, fp32 accumulate; fp64 Selector", "data": "synthetic",
         "config": {"workload": wl.name + f" ({args.config.upper()})", "layers": wl.L,
                    "q_heads": CONFIGS[args.config][2], "kv_heads": CONFIGS[args.config][3],
                    "kv_heads_per_gpu": wl.H, "head_dim": HEAD_DIM, "batch_per_gpu": wl.B,
                    "context": wl.ctx, "n_sink": wl.ns, "k_budget": wl.K, "n_recent": wl.R,
                    "schedule": f"seeded triggers p=1/24 + t_max={T_MAX}; {n_slow} slow / {K} steps",
-                   "parallelism": (f"kv-head sharded x{world} (one batch; z_base all-gather per slow-step layer)"
-                                   if wl.mode == "heads" else f"dp{world} (independent request batches)"),
+                   "parallelism": {
+                       "heads": f"kv-head sharded x{world} (one batch; z_base all-gather per slow-step layer)",
+                       "seq": f"sequence sharded x{world} (LSE-merged partials; sharded Selector stats, "
+                              "soft-NMS edges, top-k candidate merge)",
+                   }.get(wl.mode, f"dp{world} (independent request batches)"),
                    "cuda_graphs": use_graph,
                    "l2": "inputs larger than L2 (KV cache %.1f GB)" % (2 * c.sizes['kv_cache'] / 1e9)},
         "slow_steps": n_slow, "fast_step_us_kernels": fast_us,
