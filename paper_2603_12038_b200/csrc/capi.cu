@@ -276,7 +276,9 @@ size_t workspace_bytes(const sfi_shape& s) {
   b += align_up((size_t)kMaxCtas * 2 * part_rows(s) * s.head_dim * sizeof(float));
   b += align_up((size_t)kMaxCtas * 2 * 2 * part_rows(s) * sizeof(float));
   b += align_up(slices * sizeof(int32_t));
-  b += 2 * align_up(slices * (size_t)s.max_positions * sizeof(double));
+  b += 3 * align_up(slices * (size_t)s.max_positions * sizeof(double));
+  // two-pass decode Selector: [rows][chunks][6] statistics + [rows][chunks + 2] coefficients
+  b += align_up(slices * (size_t)(7 * ((s.max_positions + 511) / 512) + 2) * sizeof(double));
   return b;
 }
 
@@ -293,6 +295,10 @@ Workspace carve_workspace(const sfi_shape& s, void* base) {
   w.sel.a = reinterpret_cast<double*>(p);
   p += align_up(slices * (size_t)s.max_positions * sizeof(double));
   w.sel.b = reinterpret_cast<double*>(p);
+  p += align_up(slices * (size_t)s.max_positions * sizeof(double));
+  w.sel.c = reinterpret_cast<double*>(p);
+  p += align_up(slices * (size_t)s.max_positions * sizeof(double));
+  w.sel.stats = reinterpret_cast<double*>(p);
   return w;
 }
 

@@ -103,8 +103,10 @@ cudaError_t launch_fill_synthetic(const sfi_shape& s, const sfi_cache& c, uint64
 
 // selector.cu
 struct SelectorScratch {
-  double* a;  // [B*H][Lmax]  p -> weights -> f -> z_base
-  double* b;  // [B*H][Lmax]  w -> r -> z_adj
+  double* a;      // [B*H][Lmax]  p -> weights -> f -> z_base
+  double* b;      // [B*H][Lmax]  w -> r -> z_adj
+  double* c;      // [B*H][Lmax]  prior weights w (two-pass decode Selector)
+  double* stats;  // [B*H][ceil(Lmax / 512)][6] chunk statistics, then [B*H][chunks + 2] coefficients
 };
 // phases: 1 = fuse (z_base into scr.a), 2 = refine + top-k; z_all != null:
 // head-sharded finish over the all-gathered z_base of n_shards shards

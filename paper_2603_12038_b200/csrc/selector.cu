@@ -43,6 +43,8 @@
 // relative and checked by tests/test_gpu_parity.py.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -517,6 +519,37 @@ __device__ __forceinline__ double halo(const SelParams& p, int row, int g, int R
   return 0.0;  // unreachable for a consistent shard layout
 }
 
+// refine_cross_head (selector.cpp:204-230) at one position over the Hr heads in
+// head order, then z_adj of this shard's heads -> sb
+template <int kH>
+__device__ __forceinline__ void cross_head_store(const SelParams& p, int b, int idx, const double (&zn)[kH],
+                                                 int Hr) {
+  double mxs = zn[0];
+#pragma unroll
+  for (int h = 1; h < kH; ++h)
+    if (h < Hr) mxs = smax(mxs, zn[h]);
+  const bool t_one = (p.temperature == 1.0);
+  double e[kH], x[kH];
+  double sum = 0.0;
+#pragma unroll
+  for (int h = 0; h < kH; ++h)
+    if (h < Hr) {
+      x[h] = t_one ? (zn[h] - mxs) : (zn[h] - mxs) / p.temperature;
+      e[h] = exp(x[h]);
+      sum += e[h];
+    }
+  // log(max(e_h / sum, eps)) = x_h - log(sum) unless the responsibility is clipped
+  const double ls = log(sum);
+  const double le = log(p.eps);
+  const double floor_e = p.eps * sum;
+#pragma unroll
+  for (int h = 0; h < kH; ++h)
+    if (h < Hr && h >= p.h_off && h < p.h_off + p.H) {  // this shard's heads only
+      const double lr = (e[h] >= floor_e) ? (x[h] - ls) : le;
+      p.sb[(size_t)(b * p.H + h - p.h_off) * p.ld + idx] = zn[h] + p.alpha_cross * lr;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Stage B: soft-NMS per head, then cross-head exclusivity; one thread per
 // (b, j), the CTA's 256 positions x H heads (+ halo) staged in shared memory.
@@ -586,30 +619,245 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
       zn[h] = zj - p.alpha_soft * gap;
     }
   }
-  double mxs = zn[0];
+  cross_head_store<kH>(p, b, idx, zn, Hr);
+}
+
+// ---------------------------------------------------------------------------
+// Decode Selector, two passes (cache mode, W = 1, alpha = 1, unsharded):
+//   sel_pw_kernel  per (request, 1024-position chunk), all heads: the prior's
+//                  position factor exp(-beta u^p) (1 - u + eps)^eta once per
+//                  position (it is the same for every head), then per head
+//                  p = exp(v - m_c) with the chunk max m_c, w = (|k| + eps)^-gamma
+//                  * factor -> P, W (fp64) and the chunk's five sums -> stats.
+//   sel_z_kernel   per (request, 256 positions), all heads: row max and sums
+//                  from the chunk statistics (rescaled to the row max in chunk
+//                  order), lambda* per head, z = log(a p + b w + eps) for the tile
+//                  and its soft-NMS halo into shared memory, soft-NMS +
+//                  cross-head -> z_adj.
+// One exp + one reciprocal per (head, position) less than the three-kernel
+// path, and no z_base round trip.
+constexpr int kPwT = 256;
+constexpr int kPwPer = 2;
+constexpr int kChunk = kPwT * kPwPer;  // positions per statistics chunk
+constexpr int kPwHeads = 4;            // heads per CTA (blockIdx.z splits larger groups)
+
+__host__ __device__ __forceinline__ int n_chunks(int n) { return (n + kChunk - 1) / kChunk; }
+
+template <int kHT>
+__global__ void __launch_bounds__(kPwT) sel_pw_kernel(const SelParams p, double* P, double* Wt, double* stats,
+                                                      int ld_chunks) {
+  griddep_wait();  // PDL: logits come from the preceding dense decode
+  griddep_launch();
+  constexpr int kH = kHT < kPwHeads ? kHT : kPwHeads;  // heads of this CTA
+  constexpr int kW = kPwT / 32;
+  __shared__ double red[kW][kH][5];
+  __shared__ double mc[kH];
+  const int b = blockIdx.y;
+  const int h0 = blockIdx.z * kH;
+  const Src<false> src(p, b);
+  const int n = src.n;
+  const int c0 = blockIdx.x * kChunk;
+  if (c0 >= n) return;
+  const int Hr = min(kH, (kHT == 16 ? p.H : kHT) - h0);
+  if (Hr <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double denom_u = src.u_denom();
+  double fpos[kPwPer];
+  bool bad = false;
 #pragma unroll
-  for (int h = 1; h < kH; ++h)
-    if (h < Hr) mxs = smax(mxs, zn[h]);
-  const bool t_one = (p.temperature == 1.0);
-  double e[kH], x[kH];
-  double sum = 0.0;
+  for (int i = 0; i < kPwPer; ++i) {
+    const int j = c0 + threadIdx.x + i * kPwT;
+    if (j < n) {
+      const double u = src.u(j, denom_u);
+      fpos[i] = exp(-p.beta * pow_ref(u, p.p_curve)) * pow_ref(1.0 - u + p.eps, p.eta);
+    } else {
+      fpos[i] = 0.0;
+    }
+  }
+  // chunk max per head (starts at kMaskedLogit), finite check
+  float v[kH][kPwPer];
 #pragma unroll
-  for (int h = 0; h < kH; ++h)
+  for (int h = 0; h < kH; ++h) {
+    double m = kMaskedLogit;
+#pragma unroll
+    for (int i = 0; i < kPwPer; ++i) {
+      const int j = c0 + threadIdx.x + i * kPwT;
+      const bool ok = h < Hr && j < n;
+      v[h][i] = ok ? p.logits32[(size_t)(b * p.H + h0 + h) * p.ld + j] : -INFINITY;
+      if (ok) {
+        if (!isfinite(v[h][i])) bad = true;
+        m = smax(m, (double)v[h][i]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = smax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[warp][h][0] = m;
+  }
+  if (bad) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
+  __syncthreads();
+  if (threadIdx.x < Hr) {
+    double m = red[0][threadIdx.x][0];
+    for (int w = 1; w < kW; ++w) m = smax(m, red[w][threadIdx.x][0]);
+    mc[threadIdx.x] = m;
+  }
+  __syncthreads();
+  // p, w, the five sums per head
+  bool badn = false;
+#pragma unroll
+  for (int h = 0; h < kH; ++h) {
+    if (h >= Hr) break;
+    const int row = b * p.H + h0 + h;
+    const double m = mc[h];
+    double sp = 0.0, sw = 0.0, spp = 0.0, spw = 0.0, sww = 0.0;
+#pragma unroll
+    for (int i = 0; i < kPwPer; ++i) {
+      const int j = c0 + threadIdx.x + i * kPwT;
+      if (j < n) {
+        const double vv = (double)v[h][i];
+        const double nm = src.norm(row, j);
+        if (!isfinite(nm) || nm < 0.0) badn = true;
+        const double pj = (vv <= kMaskedLogit) ? 0.0 : exp(vv - m);
+        const double wr = pow_ref(nm + p.eps, -p.gamma) * fpos[i];
+        if (!isfinite(wr) || wr < 0.0) badn = true;
+        P[(size_t)row * p.ld + j] = pj;
+        Wt[(size_t)row * p.ld + j] = wr;
+        sp += pj;
+        sw += wr;
+        spp += pj * pj;
+        spw += pj * wr;
+        sww += wr * wr;
+      }
+    }
+    double x[5] = {sp, sw, spp, spw, sww};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x[k] += __shfl_xor_sync(0xffffffffu, x[k], o);
+      if (lane == 0) red[warp][h][k] = x[k];
+    }
+  }
+  if (badn) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
+  __syncthreads();
+  if (threadIdx.x < Hr * 5) {  // warps in index order: deterministic
+    const int h = threadIdx.x / 5, k = threadIdx.x % 5;
+    double acc = red[0][h][k];
+    for (int w = 1; w < kW; ++w) acc += red[w][h][k];
+    double* st = stats + ((size_t)(b * p.H + h0 + h) * ld_chunks + blockIdx.x) * 6;
+    st[1 + k] = acc;
+    if (k == 0) st[0] = mc[h];
+  }
+}
+
+// Per row: the row max M and the fused coefficients from the chunk statistics
+// (rescaled to M in chunk order): coef[row] = {a = (1 - lambda) / sum p,
+// b = lambda / sum w, then a * exp(m_c - M) for every chunk c}.
+__global__ void sel_coef_kernel(const SelParams p, const double* __restrict__ stats, double* __restrict__ coef,
+                                int ld_chunks) {
+  griddep_wait();
+  griddep_launch();
+  // one warp per row; lanes own chunks c = lane + 32 k; warp-tree reductions (fixed order)
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= p.B * p.H) return;
+  const Src<false> src(p, row / p.H);
+  const int n = src.n;
+  if (n <= 0) return;
+  const double* st = stats + (size_t)row * ld_chunks * 6;
+  double* cf = coef + (size_t)row * (ld_chunks + 2);
+  const int nc = n_chunks(n);
+  double M = kMaskedLogit;
+  for (int c = lane; c < nc; c += 32) M = smax(M, st[c * 6]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = smax(M, __shfl_xor_sync(0xffffffffu, M, o));
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+  for (int c = lane; c < nc; c += 32) {
+    const double* x = st + c * 6;
+    const double e = exp(x[0] - M);
+    cf[2 + c] = e;
+    s0 += x[1] * e;
+    s1 += x[2];
+    s2 += x[3] * (e * e);
+    s3 += x[4] * e;
+    s4 += x[5];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+    s4 += __shfl_xor_sync(0xffffffffu, s4, o);
+  }
+  if (lane == 0 && (s0 <= 0.0 || s1 <= 0.0)) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+  // f = p / sum p, r = w / sum w (normalize); fuse (selector.cpp:166-174)
+  const double c1 = 1.0 / s0, c2 = 1.0 / s1;
+  const double ff = s2 * c1 * c1, fr = s3 * c1 * c2, rr = s4 * c2 * c2;
+  const double denom = ff - 2.0 * fr + rr;
+  double lambda = 0.0;
+  if (fabs(denom) >= p.eps) {
+    lambda = (ff - fr) / denom;
+    lambda = (lambda < 0.0) ? 0.0 : (p.lambda_clip < lambda) ? p.lambda_clip : lambda;
+  }
+  const double a = (1.0 - lambda) * c1;
+  if (lane == 0) {
+    cf[0] = a;
+    cf[1] = lambda * c2;
+  }
+  __syncwarp();
+  for (int c = lane; c < nc; c += 32) cf[2 + c] *= a;
+}
+
+template <int kH>
+__global__ void __launch_bounds__(kRefineT) sel_z_kernel(const SelParams p, const double* P, const double* Wt,
+                                                         const double* coef, int ld_chunks) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double tile[kH][kRefineT + 2 * kMaxNmsR];
+  __shared__ double ca[kH][2];  // (1 - lambda) / sum p * exp(m_c - M) for the <= 2 chunks the tile touches
+  __shared__ double cb[kH];     // lambda / sum w
+  const int b = blockIdx.y;
+  const int j0 = blockIdx.x * kRefineT;
+  const Src<false> src(p, b);
+  const int n = src.n;
+  if (j0 >= n) return;
+  const int R = p.nms_radius;
+  const int Hr = kH == 16 ? p.H : kH;
+  const int chunk0 = max(0, j0 - R) / kChunk;
+  if (threadIdx.x < 3 * Hr) {
+    const int h = threadIdx.x / 3, k = threadIdx.x % 3;
+    const double* cf = coef + (size_t)(b * p.H + h) * (ld_chunks + 2);
+    const int c = chunk0 + k;
+    if (k < 2) ca[h][k] = c < n_chunks(n) ? cf[2 + c] : 0.0;
+    else cb[h] = cf[1];
+  }
+  __syncthreads();
+  // ---- z_base of the tile and its halo, all heads, into shared memory ----
+  const int span = kRefineT + 2 * R;
+  for (int it = threadIdx.x; it < span * Hr; it += kRefineT) {
+    const int h = it / span, t = it - h * span;
+    const int j = j0 - R + t;
+    if (j < 0 || j >= n) continue;
+    const size_t o = (size_t)(b * p.H + h) * p.ld + j;
+    tile[h][t] = log(ca[h][j / kChunk - chunk0] * P[o] + cb[h] * Wt[o] + p.eps);
+  }
+  __syncthreads();
+  const int idx = j0 + threadIdx.x;
+  if (idx >= n) return;
+  const int lo = max(0, idx - R);
+  const int hi = min(n - 1, idx + R);
+  double zn[kH];
+#pragma unroll
+  for (int h = 0; h < kH; ++h) {
+    zn[h] = 0.0;
     if (h < Hr) {
-      x[h] = t_one ? (zn[h] - mxs) : (zn[h] - mxs) / p.temperature;
-      e[h] = exp(x[h]);
-      sum += e[h];
+      const double* t = &tile[h][R + threadIdx.x - idx];  // t[j] = z[j] for j in [j0-R, j0+256+R)
+      const double zj = t[idx];
+      double mm = zj;
+      for (int i = lo; i <= hi; ++i) mm = smax(mm, t[i]);
+      zn[h] = zj - p.alpha_soft * (mm - zj);
     }
-  // log(max(e_h / sum, eps)) = x_h - log(sum) unless the responsibility is clipped
-  const double ls = log(sum);
-  const double le = log(p.eps);
-  const double floor_e = p.eps * sum;
-#pragma unroll
-  for (int h = 0; h < kH; ++h)
-    if (h < Hr && h >= p.h_off && h < p.h_off + p.H) {  // this shard's heads only
-      const double lr = (e[h] >= floor_e) ? (x[h] - ls) : le;
-      p.sb[(size_t)(b * p.H + h - p.h_off) * p.ld + idx] = zn[h] + p.alpha_cross * lr;
-    }
+  }
+  cross_head_store<kH>(p, b, idx, zn, Hr);
 }
 
 // ---------------------------------------------------------------------------
@@ -756,8 +1004,8 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
       if (lane == fl2) {
         int c2 = cum + inc2 - lsum;
         int tb = own * kBinsPerCta + (kBinsPerCta - 1 - lane * 8 - 7);
-#pragma unroll
         int cnt = 0;
+#pragma unroll
         for (int k = 0; k < 8; ++k) {
           if (c2 + (int)bv[k] >= need_rem) {
             tb = own * kBinsPerCta + (kBinsPerCta - 1 - (lane * 8 + k));
@@ -1331,6 +1579,40 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
   p.K = s.k_budget;
   fill_cfg(p, prm);
   if (s.n_kv_heads > 16) return cudaErrorInvalidValue;
+  static const bool legacy = [] {
+    const char* e = std::getenv("SFI_SELECTOR_3K");
+    return e && e[0] == '1';
+  }();
+  if (phases == 3 && !z_all && p.alpha == 1.0 && p.nms_radius <= kMaxNmsR && !legacy && scr.c) {
+    // decode Selector: P/W + chunk statistics, fused z / soft-NMS / cross-head, top-k
+    const int ldc = n_chunks(s.max_positions);
+    const dim3 gz((s.max_positions + kRefineT - 1) / kRefineT, s.batch);
+    const dim3 ba(kPwT), bz(kRefineT);
+    double* P = scr.a;
+    double* Wt = scr.c;
+    double* stt = scr.stats;
+    double* cf = scr.stats + slices * ldc * 6;  // [rows][ldc + 2] fused coefficients
+    cudaError_t e;
+#define SFI_SEL2(KH)                                                                             \
+  e = launch_k(sel_pw_kernel<KH>, dim3(ldc, s.batch, (KH + kPwHeads - 1) / kPwHeads), ba, 0, st, p, P, Wt, \
+               stt, ldc);                                                                            \
+  if (e == cudaSuccess)                                                                              \
+    e = launch_k(sel_coef_kernel, dim3(((unsigned)slices + 7) / 8), dim3(256), 0, st, p,             \
+                 (const double*)stt, cf, ldc);                                                       \
+  if (e == cudaSuccess) e = launch_k(sel_z_kernel<KH>, gz, bz, 0, st, p, (const double*)P,             \
+                                     (const double*)Wt, (const double*)cf, ldc);
+    switch (s.n_kv_heads) {
+      case 1: SFI_SEL2(1) break;
+      case 2: SFI_SEL2(2) break;
+      case 4: SFI_SEL2(4) break;
+      case 8: SFI_SEL2(8) break;
+      default: SFI_SEL2(16) break;
+    }
+#undef SFI_SEL2
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 3;
+    return launch_topk<false>(p, (int)slices, s.max_positions, st);
+  }
   return run3<false>(p, (int)slices, s.max_positions, s.batch, st, launches, phases);
 }
 
