@@ -66,6 +66,17 @@ def schedule(n_steps: int, seed: int) -> list[bool]:
     return out
 
 
+def measured_traffic(kernel: str, cfg_name: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    --set full capture (profiles/r01/traffic.json, C2 only), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            t = json.load(f)[kernel]
+        return t["dram_read_bytes"] + t["dram_write_bytes"] if cfg_name == "c2" else None
+    except Exception:
+        return None
+
+
 def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -432,7 +443,7 @@ def gpu_arm(args) -> dict:
     dom = "fast_decode" if share_sp >= share_de else "dense_decode"
     roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["GB/s"], "peak": pk["hbm_gbs"],
             "peak_source": pk["source"], "unit": "GB/s", "frac": kernels[dom]["frac"],
-            "traffic": None, "share_of_step": (share_sp if dom == "fast_decode" else share_de) / ms}
+            "traffic": measured_traffic(dom, args.config), "algorithmic_bytes": kernels[dom]["bytes"], "share_of_step": (share_sp if dom == "fast_decode" else share_de) / ms}
     fast_us = wl.L * (t_sp * 1e3)
     res = {
         "metric": metric_name(args.config),
