@@ -106,52 +106,75 @@ struct CompactParams {
   int rebuild_ring;
 };
 
-// One warp per compact row: lanes 0-15 move the K row, lanes 16-31 the V row.
+// Each warp moves kRowsPerWarp compact rows: lanes 0-15 the K row, lanes 16-31
+// the V row, every lane's loads for all its rows issued before any store (more
+// bytes in flight per SM: the gather is latency-bound at one row per warp).
+constexpr int kRowsPerWarp = 4;
+
 __global__ void compact_kernel(const CompactParams p) {
   griddep_wait();
   griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.y;
   const int b = bh / p.H;
-  const int i = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int i0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kRowsPerWarp;
   const size_t slice = (size_t)(p.layer * p.B) * p.H + bh;
   const int L = p.prefix_len[b];
   const int nsb = p.n_sink_b[b];
   const int nsel = p.n_sel[slice];
   const int rl = p.recent_len[b];
   if (nsb > p.crows - p.R - p.K || nsel > p.K || rl > p.R) {
-    if (i == 0 && lane == 0) raise_error(p.err, SFI_ERR_CONFIG);
+    if (i0 == 0 && lane == 0) raise_error(p.err, SFI_ERR_CONFIG);
     return;
   }
   const int total = nsb + nsel + (p.rebuild_ring ? rl : 0);
-  if (i >= total) return;
-  int pos, dst;
-  if (i < nsb) {
-    pos = i + 1;
-    dst = p.R + i;
-  } else if (i < nsb + nsel) {
-    const int k = i - nsb;
-    const int32_t* s = p.sel + slice * p.K;
-    pos = s[k];
-    dst = p.R + i;
-    if (lane == 0) {
-      if (pos <= nsb || (k > 0 && s[k - 1] >= pos)) raise_error(p.err, SFI_ERR_OVERLAP_VIOLATION);
-      if (pos < 1 || pos > L) raise_error(p.err, SFI_ERR_OUT_OF_RANGE);
-    }
-    if (pos < 1 || pos > L) return;
-  } else {
-    pos = (L - rl + 1) + (i - nsb - nsel);
-    dst = (pos - 1) % p.R;
-  }
-  const size_t srow = (slice * p.Lmax + (pos - 1)) * p.D;
-  const size_t drow = (slice * p.crows + dst) * p.D;
+  if (i0 >= total) return;
   const int half = lane >> 4, l16 = lane & 15;
-  const __nv_bfloat16* s = (half ? p.vc : p.kc) + srow;
-  __nv_bfloat16* d = (half ? p.cv : p.ck) + drow;
+  const int32_t* sl = p.sel + slice * p.K;
+  int src_row[kRowsPerWarp], dst_row[kRowsPerWarp];
+#pragma unroll
+  for (int r = 0; r < kRowsPerWarp; ++r) {
+    const int i = i0 + r;
+    int pos = 0, dst = -1;
+    if (i < nsb) {
+      pos = i + 1;
+      dst = p.R + i;
+    } else if (i < nsb + nsel) {
+      const int k = i - nsb;
+      pos = sl[k];
+      dst = p.R + i;
+      if (lane == 0) {
+        if (pos <= nsb || (k > 0 && sl[k - 1] >= pos)) raise_error(p.err, SFI_ERR_OVERLAP_VIOLATION);
+        if (pos < 1 || pos > L) raise_error(p.err, SFI_ERR_OUT_OF_RANGE);
+      }
+      if (pos < 1 || pos > L) dst = -1;
+    } else if (i < total) {
+      pos = (L - rl + 1) + (i - nsb - nsel);
+      dst = (pos - 1) % p.R;
+    }
+    src_row[r] = dst >= 0 ? pos - 1 : -1;
+    dst_row[r] = dst;
+  }
+  const __nv_bfloat16* sbase = half ? p.vc : p.kc;
+  __nv_bfloat16* dbase = half ? p.cv : p.ck;
   if (p.D == 128) {
-    reinterpret_cast<uint4*>(d)[l16] = reinterpret_cast<const uint4*>(s)[l16];
+    uint4 x[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+      if (src_row[r] >= 0)
+        x[r] = reinterpret_cast<const uint4*>(sbase + (slice * p.Lmax + src_row[r]) * p.D)[l16];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+      if (src_row[r] >= 0) reinterpret_cast<uint4*>(dbase + (slice * p.crows + dst_row[r]) * p.D)[l16] = x[r];
   } else {
-    reinterpret_cast<uint2*>(d)[l16] = reinterpret_cast<const uint2*>(s)[l16];
+    uint2 x[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+      if (src_row[r] >= 0)
+        x[r] = reinterpret_cast<const uint2*>(sbase + (slice * p.Lmax + src_row[r]) * p.D)[l16];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+      if (src_row[r] >= 0) reinterpret_cast<uint2*>(dbase + (slice * p.crows + dst_row[r]) * p.D)[l16] = x[r];
   }
 }
 
@@ -353,7 +376,7 @@ cudaError_t launch_compact_build(const sfi_shape& s, const sfi_cache& c, int lay
   p.rebuild_ring = rebuild_ring;
   const int rows = s.n_sink + s.k_budget + (rebuild_ring ? s.n_recent : 0);
   constexpr int kWarps = 8;
-  dim3 grid((rows + kWarps - 1) / kWarps, s.batch * s.n_kv_heads);
+  dim3 grid((rows + kWarps * kRowsPerWarp - 1) / (kWarps * kRowsPerWarp), s.batch * s.n_kv_heads);
   if (rows == 0) return cudaSuccess;
   return launch_k(compact_kernel, grid, dim3(kWarps * 32), 0, st, p);
 }

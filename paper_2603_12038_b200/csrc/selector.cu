@@ -1407,7 +1407,11 @@ void fill_cfg(SelParams& p, const sfi_selector_params& prm) {
 
 template <bool kExp>
 cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st) {
-  if (n_max <= kTopkCtaMax) {
+  static const bool force_cluster = [] {
+    const char* e = std::getenv("SFI_TOPK_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  if (n_max <= kTopkCtaMax && !force_cluster) {
     const size_t smem = (size_t)std::max(n_max, 1) * sizeof(uint32_t);
     static bool cta_configured = false;
     if (!cta_configured) {
