@@ -201,13 +201,18 @@ class Workload:
     def set_lengths(self, L: int):
         self.drv.set_lengths([L] * self.B, [self.ns] * self.B)
 
-    def step(self, slow: bool, rebuild_ring: bool = False):
+    def step(self, slow: bool, rebuild_ring: bool = False, io=None):
         """One decode step of all layers through the mode's driver: SfiCache (1 GPU /
         dp), HeadShardedSfi (z_base all-gather in the Selector) or SeqShardedSfi
-        (LSE-merged attention partials, sharded Selector statistics)."""
+        (LSE-merged attention partials, sharded Selector statistics). `io`: the
+        end-to-end variant's per-layer host copies (HostIO)."""
         d = self.drv
+        if io is not None:
+            io.begin()
         d.step_advance()
         for l in range(self.L):
+            if io is not None:
+                io.before(l)
             if slow:
                 d.ring_append(l, self.k_new[l], self.v_new[l])
                 d.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
@@ -218,6 +223,10 @@ class Workload:
                 # compact rows of layer l are not written by the preceding
                 # kernel, so they stream before the PDL wait
                 d.fast_decode(l, self.q[l], self.k_new[l], self.v_new[l], self.out[l], prefetch=True)
+            if io is not None:
+                io.after(l)
+        if io is not None:
+            io.end()
 
     # the attention kernels alone (per-kernel timing), no exchange
     def fast_kernel(self, l: int):
@@ -253,6 +262,56 @@ class Workload:
         nj = Lcur - rl - self.ns
         return ((self.B * self.H * Lcur * 4 * HEAD_DIM + self.B * self.H * nj * 4) * self.shard_frac()
                 + 2 * self.B * self.Hq * HEAD_DIM * 4)
+
+
+class HostIO:
+    """End-to-end step I/O: every step copies its inputs (q fp32, new K/V bf16) from
+    pinned host memory and its output back to pinned host memory, in groups of
+    layers on a copy stream ordered with the compute stream by events — a group's
+    inputs land while the previous group computes and its output returns while the
+    next group computes (few, large copies: each copy node costs microseconds)."""
+
+    def __init__(self, wl: Workload, group: int = 6):
+        t = wl.torch
+        self.t, self.wl = t, wl
+        self.cs = t.cuda.Stream()
+        pin = lambda x: t.empty_like(x, device="cpu").pin_memory()  # noqa: E731
+        self.qh, self.kh, self.vh, self.oh = pin(wl.q), pin(wl.k_new), pin(wl.v_new), pin(wl.out)
+        self.qh.copy_(wl.q)
+        self.kh.copy_(wl.k_new)
+        self.vh.copy_(wl.v_new)
+        self.groups = [(l0, min(wl.L, l0 + group)) for l0 in range(0, wl.L, group)]
+        self.ev_in = [t.cuda.Event() for _ in self.groups]
+        self.ev_out = [t.cuda.Event() for _ in self.groups]
+        self.h2d = wl.q.numel() * 4 + wl.k_new.numel() * 2 + wl.v_new.numel() * 2
+        self.d2h = wl.out.numel() * 4
+
+    def begin(self):
+        t, wl, cs = self.t, self.wl, self.cs
+        self.main = t.cuda.current_stream()
+        cs.wait_stream(self.main)  # fork
+        with t.cuda.stream(cs):
+            for gi, (l0, l1) in enumerate(self.groups):
+                wl.q[l0:l1].copy_(self.qh[l0:l1], non_blocking=True)
+                wl.k_new[l0:l1].copy_(self.kh[l0:l1], non_blocking=True)
+                wl.v_new[l0:l1].copy_(self.vh[l0:l1], non_blocking=True)
+                self.ev_in[gi].record(cs)
+
+    def before(self, l: int):
+        for gi, (l0, _) in enumerate(self.groups):
+            if l == l0:
+                self.main.wait_event(self.ev_in[gi])
+
+    def after(self, l: int):
+        for gi, (l0, l1) in enumerate(self.groups):
+            if l == l1 - 1:
+                self.ev_out[gi].record(self.main)
+                with self.t.cuda.stream(self.cs):
+                    self.cs.wait_event(self.ev_out[gi])
+                    self.oh[l0:l1].copy_(self.wl.out[l0:l1], non_blocking=True)
+
+    def end(self):
+        self.main.wait_stream(self.cs)  # join: the step ends when its output is on the host
 
 
 def time_kernel(wl: Workload, which: str, iters: int) -> float:
@@ -383,15 +442,16 @@ def gpu_arm(args) -> dict:
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        qh = torch.empty_like(wl.q, device="cpu").pin_memory()
-        kh = torch.empty_like(wl.k_new, device="cpu").pin_memory()
-        vh = torch.empty_like(wl.v_new, device="cpu").pin_memory()
-        oh = torch.empty_like(wl.out, device="cpu").pin_memory()
-        qh.copy_(wl.q)
-        kh.copy_(wl.k_new)
-        vh.copy_(wl.v_new)
-        torch.cuda.synchronize()
-        Ke = min(K, 32)
+        io = HostIO(wl)
+        ge = {}
+        if use_graph:
+            for slow in (False, True):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    wl.step(slow, io=io)
+                ge[slow] = g
+            torch.cuda.synchronize()
+        Ke = K  # the same schedule as the device-resident timing
         sched_e = sched[W:W + Ke]
         wl.set_lengths(wl.ctx + 1)
         if world > 1:
@@ -400,18 +460,16 @@ def gpu_arm(args) -> dict:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for slow in sched_e:
-            wl.q.copy_(qh, non_blocking=True)
-            wl.k_new.copy_(kh, non_blocking=True)
-            wl.v_new.copy_(vh, non_blocking=True)
-            run(slow)
-            oh.copy_(wl.out, non_blocking=True)
+            if use_graph:
+                ge[slow].replay()
+            else:
+                wl.step(slow, io=io)
         b.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(a.elapsed_time(b))
-        h2d = (wl.q.numel() * 4 + wl.k_new.numel() * 2 + wl.v_new.numel() * 2)
-        d2h = wl.out.numel() * 4
         e2e = {"value": wl.job_tokens * Ke / (ems / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": Ke}
+               "h2d_bytes_per_step": io.h2d, "d2h_bytes_per_step": io.d2h, "steps": Ke,
+               "copies": "pinned host <-> HBM in 6-layer groups on a copy stream, event-ordered with compute"}
 
     # ---- per-kernel device time (CUDA events on the launching stream) ----
     pk = peaks()
