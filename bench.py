@@ -141,7 +141,8 @@ class ClockSampler:
 # GPU arm
 
 class Workload:
-    def __init__(self, cfg_name: str, steps_total: int, device, world: int = 1, layers: int = 0):
+    def __init__(self, cfg_name: str, steps_total: int, device, world: int = 1, layers: int = 0,
+                 sync_slow: bool = False):
         import torch
 
         import paper_2603_12038_b200 as sfi
@@ -186,6 +187,10 @@ class Workload:
         self.out = t.zeros(L, B, Hq, d, device=device)
         self.logits = self.cache.pooled_logits
         drv = self.drv
+        # asynchronous slow step (1 GPU / dp): Selector + compact overlap the next layers' dense decode
+        self.pipe = None
+        if self.mode in ("single", "dp") and not sync_slow:
+            self.pipe = sfi.SlowStepPipeline(self.cache)
         self.cache.fill_synthetic(seed=2026 + 1, length=fill_len)
         self.set_lengths(self.ctx)
         # initial slow step (untimed): dense + Selector + compact incl. the ring
@@ -210,10 +215,15 @@ class Workload:
         if io is not None:
             io.begin()
         d.step_advance()
+        pipe = self.pipe if (slow and self.pipe is not None) else None
+        if pipe is not None:
+            pipe.begin()
         for l in range(self.L):
             if io is not None:
                 io.before(l)
-            if slow:
+            if pipe is not None:  # dense on this stream, Selector + compact on the aux stream
+                pipe.layer(l, self.q[l], self.out[l], self.k_new[l], self.v_new[l], self.params, rebuild_ring)
+            elif slow:
                 d.ring_append(l, self.k_new[l], self.v_new[l])
                 d.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
                 d.selector(l, self.logits, self.params)
@@ -225,6 +235,8 @@ class Workload:
                 d.fast_decode(l, self.q[l], self.k_new[l], self.v_new[l], self.out[l], prefetch=True)
             if io is not None:
                 io.after(l)
+        if pipe is not None:
+            pipe.end()
         if io is not None:
             io.end()
 
@@ -394,7 +406,7 @@ def gpu_arm(args) -> dict:
         return float(t.item())
     W, K = args.warmup, args.steps
     sched = schedule(W + K + 1, seed=2026 + 1)[1:]  # step 0 of the schedule is the setup slow step
-    wl = Workload(args.config, W + K + 8, dev, world, args.layers)
+    wl = Workload(args.config, W + K + 8, dev, world, args.layers, args.sync_slow)
     c = wl.cache
     use_graph = not args.no_graph
     graphs = {}
@@ -520,6 +532,8 @@ def gpu_arm(args) -> dict:
                               "soft-NMS edges, top-k candidate merge)",
                    }.get(wl.mode, f"dp{world} (independent request batches)"),
                    "cuda_graphs": use_graph,
+                   "slow_step": "synchronous" if wl.pipe is None else
+                                "async pipeline: dense on the main stream (1 CTA/SM), Selector + compact on an aux stream",
                    "l2": "inputs larger than L2 (KV cache %.1f GB)" % (2 * c.sizes['kv_cache'] / 1e9)},
         "slow_steps": n_slow, "fast_step_us_kernels": fast_us,
         "fast_step_us_graph": t_fast_step * 1e3 if t_fast_step else None,
@@ -712,6 +726,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (testing only)")
+    ap.add_argument("--sync-slow", action="store_true",
+                    help="slow steps without the asynchronous Selector pipeline (one stream)")
     ap.add_argument("--backend", default=os.environ.get("SFI_DIST_BACKEND", "nccl"),
                     help="torch.distributed backend (gloo: several ranks on one GPU, testing only)")
     args = ap.parse_args()

@@ -169,6 +169,16 @@ SFI_API int sfi_dense_decode(const sfi_shape* shape, const sfi_cache* cache, int
                              const float* q, float* out, float* pooled_logits,
                              int32_t pool_mode, void* stream);
 
+/* sfi_dense_decode with options. lse (optional): natural-log sum-exp per q head
+ * (partial mode, see sequence sharding). flags: SFI_DENSE_SHARE_SM sizes the
+ * stream-K grid to 3/4 of the SM slots so kernels on another stream — the
+ * previous layer's Selector in the asynchronous slow-step pipeline — run at
+ * the same time on the rest. */
+#define SFI_DENSE_SHARE_SM 2
+SFI_API int sfi_dense_decode_ex(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                const float* q, float* out, float* lse, float* pooled_logits,
+                                int32_t pool_mode, int32_t flags, void* stream);
+
 /* Fast step, one layer: attention over the compact cache only (ring + sink +
  * selected rows; S = recent_len + n_sink_b + n_sel per (b, head)). */
 SFI_API int sfi_sparse_decode(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,

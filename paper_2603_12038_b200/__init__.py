@@ -66,10 +66,10 @@ LIBRARY_PATH = _os.path.join(_HERE, "libsfi_b200.so")
 
 
 def __getattr__(name):
-    if name == "SfiCache":
-        from .device import SfiCache
+    if name in ("SfiCache", "SlowStepPipeline"):
+        from . import device
 
-        return SfiCache
+        return getattr(device, name)
     raise AttributeError(name)
 
 
@@ -80,5 +80,5 @@ __all__ = [
     "attention_kernel_dense", "attention_kernel_sparse", "compute_allowed", "default_config",
     "dense_capture", "fast_step_update", "flop_model", "init_decode_state", "make_cache_stats",
     "next_step_type", "run_selector", "run_selector_stages", "select_top_k", "slow_step_update",
-    "SfiCache", "LIBRARY_PATH",
+    "SfiCache", "SlowStepPipeline", "LIBRARY_PATH",
 ]

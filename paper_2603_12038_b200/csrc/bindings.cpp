@@ -302,6 +302,13 @@ PYBIND11_MODULE(_sfi_b200, m) {
     check(sfi_sparse_decode(&s, &c, layer, static_cast<const float*>(vp(q)), static_cast<float*>(vp(out)),
                             vp(stream)));
   });
+  m.def("dense_decode_ex", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
+                              std::uintptr_t out, std::uintptr_t lse, std::uintptr_t logits, int pool, int flags,
+                              std::uintptr_t stream) {
+    check(sfi_dense_decode_ex(&s, &c, layer, static_cast<const float*>(vp(q)), static_cast<float*>(vp(out)),
+                              static_cast<float*>(vp(lse)), static_cast<float*>(vp(logits)), pool, flags, vp(stream)));
+  });
+  m.attr("DENSE_SHARE_SM") = SFI_DENSE_SHARE_SM;
   m.def("fast_decode", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
                           std::uintptr_t k, std::uintptr_t v, std::uintptr_t out, int flags,
                           std::uintptr_t stream) {

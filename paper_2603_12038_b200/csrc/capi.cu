@@ -125,7 +125,7 @@ int num_sms() {
 }
 
 int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* q, float* out,
-                  float* logits, int pool, bool sparse, void* stream, float* lse = nullptr) {
+                  float* logits, int pool, bool sparse, void* stream, float* lse = nullptr, int flags = 0) {
   g_launches = 0;
   int rc = validate(s);
   if (rc) return rc;
@@ -165,7 +165,11 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
   const int per_slice = sparse ? (s->n_recent + 63) / 64 + 1 + (s->n_sink + s->k_budget + 63) / 64
                               : (s->max_positions + 63) / 64;
-  int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms());
+  // 7/8 of the 2-CTAs-per-SM slots measures fastest alone (fewer in-flight
+  // streams per HBM channel); SFI_DENSE_SHARE_SM leaves a quarter of the slots to
+  // the Selector kernels of the asynchronous slow-step pipeline
+  int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms(),
+                                   (flags & SFI_DENSE_SHARE_SM) ? 6 : 7);
   static const int env_ctas = [] {
     const char* e = std::getenv("SFI_DECODE_CTAS");
     return e ? std::atoi(e) : 0;
@@ -513,6 +517,12 @@ SFI_API int sfi_seq_lengths(const sfi_shape* s, const sfi_cache* c, int32_t* g_p
            "sfi_seq_lengths");
   g_launches = 1;
   return SFI_OK;
+}
+
+SFI_API int sfi_dense_decode_ex(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q, float* out,
+                                float* lse, float* pooled_logits, int32_t pool_mode, int32_t flags, void* stream) {
+  if (flags & ~SFI_DENSE_SHARE_SM) return fail(SFI_ERR_INVALID_ARGUMENT, "dense_decode_ex: unknown flags");
+  return decode_common(s, c, layer, q, out, pooled_logits, pool_mode, false, stream, lse, flags);
 }
 
 SFI_API int sfi_dense_decode_partial(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q,

@@ -101,6 +101,15 @@ class SfiCache:
                         self._ptr(out, torch.float32), self._ptr(logits, torch.float32), pool,
                         self._stream(stream))
 
+    def dense_decode_ex(self, layer: int, q: torch.Tensor, out: torch.Tensor, logits: torch.Tensor | None = None,
+                        pool: int = 0, share_sm: bool = False, lse: torch.Tensor | None = None, stream=None):
+        """dense_decode with options: share_sm = one CTA per SM (room for concurrent
+        kernels on another stream); lse = natural-log sum-exp per q head."""
+        _C.dense_decode_ex(self.shape, self.cache, layer, self._ptr(q, torch.float32),
+                           self._ptr(out, torch.float32), self._ptr(lse, torch.float32),
+                           self._ptr(logits, torch.float32), pool, _C.DENSE_SHARE_SM if share_sm else 0,
+                           self._stream(stream))
+
     def sparse_decode(self, layer: int, q: torch.Tensor, out: torch.Tensor, stream=None):
         _C.sparse_decode(self.shape, self.cache, layer, self._ptr(q, torch.float32),
                          self._ptr(out, torch.float32), self._stream(stream))
@@ -157,3 +166,51 @@ class SfiCache:
     @staticmethod
     def last_launch_count() -> int:
         return _C.last_launch_count()
+
+
+class SlowStepPipeline:
+    """Asynchronous slow step (the paper's layer-wise pipeline, PAPER.md:478-495;
+    SURVEY §8f-1) over one SfiCache.
+
+    The dense decode of every layer runs on the caller's stream on 3/4 of the SM
+    slots (SFI_DENSE_SHARE_SM); the Selector and the compact build of layer l run
+    on an auxiliary stream as soon as layer l's pooled logits exist, on the slots
+    the dense kernels leave free, while layers l+1.. stream their KV. The refreshed selection is only read by the next fast step, after `end()`
+    joins the streams. Pooled logits go through a ring of `slots` buffers: dense(l)
+    waits until the Selector of layer l - slots released its slot."""
+
+    def __init__(self, cache: SfiCache, slots: int = 4, share_sm: bool = True):
+        self.c = cache
+        self.share_sm = share_sm
+        dev = cache.k_cache.device
+        s = cache.shape
+        self.slots = slots
+        self.aux = torch.cuda.Stream(device=dev)
+        self.logits = torch.zeros((slots, s.batch, s.n_kv_heads, s.max_positions), dtype=torch.float32,
+                                  device=dev)
+        self.ev_ready = [torch.cuda.Event() for _ in range(slots)]
+        self.ev_free = [torch.cuda.Event() for _ in range(slots)]
+        self.used = [False] * slots
+
+    def begin(self):
+        self.main = torch.cuda.current_stream()
+        self.aux.wait_stream(self.main)  # fork
+        self.used = [False] * self.slots
+
+    def layer(self, l: int, q: torch.Tensor, out: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
+              params=None, rebuild_ring: bool = False):
+        c, main, s = self.c, self.main, l % self.slots
+        if self.used[s]:
+            main.wait_event(self.ev_free[s])
+        c.ring_append(l, k_new, v_new)
+        c.dense_decode_ex(l, q, out, self.logits[s], 0, share_sm=self.share_sm)
+        self.ev_ready[s].record(main)
+        with torch.cuda.stream(self.aux):
+            self.aux.wait_event(self.ev_ready[s])
+            c.selector(l, self.logits[s], params)
+            c.compact_build(l, rebuild_ring=rebuild_ring)
+            self.ev_free[s].record(self.aux)
+        self.used[s] = True
+
+    def end(self):
+        self.main.wait_stream(self.aux)  # join: the next fast step reads the new compact rows
