@@ -578,22 +578,28 @@ FastFn pick(int G) {
 
 }  // namespace
 
+// CTAs per slice: the largest power of two that keeps the grid within the two
+// CTA slots of every SM, up to 8 (portable clusters); up to 16 (non-portable)
+// when the slices are so few that 8 per slice would leave most SMs idle.
 int fast_cluster_size(int slices, int num_sms) {
   int c = 1;
   while (c < 8 && slices * c * 2 <= 2 * num_sms) c *= 2;
+  if (c == 8 && slices * 32 <= num_sms) c = 16;
   return c;
 }
 
 cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
                                int G, int C, cudaStream_t stream) {
   FastFn fn = (D == 64) ? pick<64>(G) : pick<128>(G);
-  if (!fn || C < 1 || C > 8) return cudaErrorInvalidValue;
+  if (!fn || C < 1 || C > 16) return cudaErrorInvalidValue;
   const int smem = D == 64 ? fast_smem_bytes<64>() : fast_smem_bytes<128>();
   static bool configured[2][17] = {};
   bool& done = configured[D == 64 ? 0 : 1][G];
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     done = true;
   }
