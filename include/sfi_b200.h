@@ -205,6 +205,23 @@ SFI_API int sfi_selector(const sfi_shape* shape, const sfi_cache* cache, int32_t
                          const float* pooled_logits, const sfi_selector_params* params,
                          void* stream);
 
+/* Prefill tail-window capture (prefill_dense attention.cpp:460-500, capture
+ * :367-409): for the W <= 16 window rows of every request — queries q fp32
+ * [batch][W][n_q_heads][head_dim] at 1-based positions q_pos int32 [batch][W]
+ * (device) — the raw logits q.k/sqrt(d) over J_b pooled across each GQA group
+ * (mean or max), kMaskedLogit (-1e30) where the position is ahead of the row.
+ * logits_out fp32 [batch][n_kv_heads][W][max_positions], entry (b, h, w, p - J_b.front()).
+ * The cache holds the prompt (rows 1..L_b) and its lengths define J_b. */
+SFI_API int sfi_prefill_capture(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                const float* q, int32_t W, const int32_t* q_pos, float* logits_out,
+                                int32_t pool_mode, void* stream);
+/* sfi_selector over a W-row window (logits [batch][n_kv_heads][W][max_positions]
+ * as written by sfi_prefill_capture): evidence is the alpha power mean of the W
+ * row softmaxes (evidence_from_window selector.cpp:96-127). */
+SFI_API int sfi_selector_window(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                const float* logits, int32_t W, const sfi_selector_params* params,
+                                void* stream);
+
 /* KV-head-sharded Selector. Every Selector stage is
  * per head except cross-head exclusivity (selector.cpp:204-230), a softmax over
  * ALL kv heads of a request at each position. A rank whose cache holds heads

@@ -28,7 +28,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                  "-I" + INC, "-I" + CSRC]
-CU = ["decode.cu", "fast_decode.cu", "cache_ops.cu", "selector.cu", "capi.cu"]
+CU = ["decode.cu", "fast_decode.cu", "capture.cu", "cache_ops.cu", "selector.cu", "capi.cu"]
 CPP = ["host.cpp"]
 HEADERS = [os.path.join(INC, h) for h in ("sfi_b200.h", "sfi_b200.hpp")] + [
     os.path.join(CSRC, h) for h in ("common.cuh", "kernels.h")]

@@ -368,6 +368,15 @@ PYBIND11_MODULE(_sfi_b200, m) {
     check(sfi_seq_selector_pick(&s, &c, layer, n_shards, static_cast<const double*>(vp(cs)),
                                 static_cast<const int32_t*>(vp(cp)), pos_base, pos_end, vp(scratch), vp(stream)));
   });
+  m.def("prefill_capture", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q, int W,
+                              std::uintptr_t q_pos, std::uintptr_t out, int pool, std::uintptr_t stream) {
+    check(sfi_prefill_capture(&s, &c, layer, static_cast<const float*>(vp(q)), W,
+                              static_cast<const int32_t*>(vp(q_pos)), static_cast<float*>(vp(out)), pool, vp(stream)));
+  });
+  m.def("selector_window", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits, int W,
+                              const sfi_selector_params& prm, std::uintptr_t stream) {
+    check(sfi_selector_window(&s, &c, layer, static_cast<const float*>(vp(logits)), W, &prm, vp(stream)));
+  });
   m.def("selector_fuse", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
                             const sfi_selector_params& prm, std::uintptr_t stream) {
     const double* z = nullptr;

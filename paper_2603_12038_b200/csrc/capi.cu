@@ -461,7 +461,7 @@ static int check_selector_params(const sfi_selector_params* prm) {
 
 static int selector_common(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* logits,
                            const sfi_selector_params* prm, int phases, const double* z_all, int n_shards,
-                           int shard, void* stream) {
+                           int shard, void* stream, int W = 1) {
   g_launches = 0;
   int rc = validate(s);
   if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
@@ -472,7 +472,7 @@ static int selector_common(const sfi_shape* s, const sfi_cache* c, int32_t layer
   sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
   int n = 0;
   SFI_CUDA(sfi_impl::launch_selector(*s, *c, layer, logits, *prm, ws.sel, (cudaStream_t)stream, &n, phases,
-                                     z_all, n_shards, shard),
+                                     z_all, n_shards, shard, W),
            "sfi_selector");
   g_launches = n;
   return SFI_OK;
@@ -481,6 +481,42 @@ static int selector_common(const sfi_shape* s, const sfi_cache* c, int32_t layer
 SFI_API int sfi_selector(const sfi_shape* s, const sfi_cache* c, int32_t layer,
                          const float* pooled_logits, const sfi_selector_params* prm, void* stream) {
   return selector_common(s, c, layer, pooled_logits, prm, 3, nullptr, 1, 0, stream);
+}
+
+SFI_API int sfi_selector_window(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* logits,
+                                int32_t W, const sfi_selector_params* prm, void* stream) {
+  if (W < 1) return fail(SFI_ERR_OUT_OF_RANGE, "evidence_from_window: window width must be >= 1");
+  if (W > 16) return fail(SFI_ERR_UNSUPPORTED, "selector: window width <= 16");
+  return selector_common(s, c, layer, logits, prm, 3, nullptr, 1, 0, stream, W);
+}
+
+SFI_API int sfi_prefill_capture(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q, int32_t W,
+                                const int32_t* q_pos, float* logits_out, int32_t pool_mode, void* stream) {
+  g_launches = 0;
+  int rc = validate(s);
+  if (rc || (rc = check_cache(s, c)) || (rc = check_layer(s, layer))) return rc;
+  if (!q || !q_pos || !logits_out) return fail(SFI_ERR_INVALID_ARGUMENT, "prefill_capture: null argument");
+  if (W < 1 || W > 16) return fail(SFI_ERR_UNSUPPORTED, "prefill_capture: window rows 1..16");
+  if (pool_mode != SFI_POOL_MEAN && pool_mode != SFI_POOL_MAX) return fail(SFI_ERR_CONFIG, "prefill_capture: bad pool mode");
+  sfi_impl::CaptureParams p;
+  p.q = q;
+  p.q_pos = q_pos;
+  p.k_cache = static_cast<const __nv_bfloat16*>(c->k_cache);
+  p.out = logits_out;
+  p.prefix_len = c->prefix_len;
+  p.n_sink_b = c->n_sink_b;
+  p.recent_len = c->recent_len;
+  p.layer = layer;
+  p.B = s->batch;
+  p.H = s->n_kv_heads;
+  p.Hq = s->n_q_heads;
+  p.Lmax = s->max_positions;
+  p.W = W;
+  p.pool = pool_mode;
+  p.inv_sqrt_d = (float)(1.0 / std::sqrt((double)s->head_dim));
+  SFI_CUDA(sfi_impl::launch_capture(p, s->head_dim, (cudaStream_t)stream), "sfi_prefill_capture");
+  g_launches = 1;
+  return SFI_OK;
 }
 
 SFI_API int sfi_selector_fuse(const sfi_shape* s, const sfi_cache* c, int32_t layer,

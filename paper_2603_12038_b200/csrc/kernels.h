@@ -115,7 +115,7 @@ struct SelectorScratch {
 cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
                             const sfi_selector_params& prm, const SelectorScratch& scr,
                             cudaStream_t st, int* launches, int phases = 3,
-                            const double* z_all = nullptr, int n_shards = 1, int shard = 0);
+                            const double* z_all = nullptr, int n_shards = 1, int shard = 0, int W = 1);
 
 cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* logits,
                                      const double* norms, const int32_t* allowed,
@@ -144,6 +144,20 @@ size_t seq_pick_scratch_bytes(const sfi_shape& s, int n_shards);
 cudaError_t launch_seq_selector_pick(const sfi_shape& s, const sfi_cache& c, int layer, int n_shards,
                                      const double* cand_score_all, const int32_t* cand_pos_all, int pos_base,
                                      int pos_end, void* scratch, cudaStream_t st, int* launches);
+
+// capture.cu: prefill tail-window capture
+struct CaptureParams {
+  const float* q;              // [B][W][Hq][D]
+  const int32_t* q_pos;        // [B][W] 1-based positions of the window rows
+  const __nv_bfloat16* k_cache;
+  float* out;                  // [B][H][W][Lmax], entry (b, h, w, p - j_min)
+  const int32_t* prefix_len;
+  const int32_t* n_sink_b;
+  const int32_t* recent_len;
+  int layer, B, H, Hq, Lmax, W, pool;
+  float inv_sqrt_d;
+};
+cudaError_t launch_capture(const CaptureParams& p, int D, cudaStream_t st);
 
 // workspace carve-up (capi.cu)
 struct Workspace {

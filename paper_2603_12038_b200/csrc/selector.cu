@@ -70,7 +70,7 @@ constexpr double kMaskedLogit = -1e30;  // selector.hpp:42
 
 struct SelParams {
   // cache mode
-  const float* logits32;    // [rows][ld] fp32, W = 1
+  const float* logits32;    // [rows][W][ld] fp32
   const double* norms_c;    // this layer's cache norms: [rows][Lmax] by position
   const int32_t* prefix_len;
   const int32_t* n_sink_b;
@@ -125,7 +125,7 @@ struct Src {
   }
   __device__ __forceinline__ double logit(int row, int w, int j) const {
     if (kExp) return p.logits64[((size_t)row * p.W + w) * p.ld + j];
-    return (double)p.logits32[(size_t)row * p.ld + j];
+    return (double)p.logits32[((size_t)row * p.W + w) * p.ld + j];
   }
   __device__ __forceinline__ double norm(int row, int j) const {
     if (kExp) return p.norms_e[(size_t)row * p.ld + j];
@@ -1558,7 +1558,7 @@ cudaError_t run3(const SelParams& p, int rows, int n_max, int batches, cudaStrea
 cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
                             const sfi_selector_params& prm, const SelectorScratch& scr,
                             cudaStream_t st, int* launches, int phases, const double* z_all,
-                            int n_shards, int shard) {
+                            int n_shards, int shard, int W) {
   SelParams p{};
   p.z_all = z_all;
   p.H_all = z_all ? n_shards * s.n_kv_heads : s.n_kv_heads;
@@ -1587,7 +1587,8 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
     const char* e = std::getenv("SFI_SELECTOR_3K");
     return e && e[0] == '1';
   }();
-  if (phases == 3 && !z_all && p.alpha == 1.0 && p.nms_radius <= kMaxNmsR && !legacy && scr.c) {
+  p.W = W;
+  if (phases == 3 && !z_all && W == 1 && p.alpha == 1.0 && p.nms_radius <= kMaxNmsR && !legacy && scr.c) {
     // decode Selector: P/W + chunk statistics, fused z / soft-NMS / cross-head, top-k
     const int ldc = n_chunks(s.max_positions);
     const dim3 gz((s.max_positions + kRefineT - 1) / kRefineT, s.batch);

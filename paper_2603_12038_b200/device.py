@@ -129,6 +129,19 @@ class SfiCache:
         _C.selector(self.shape, self.cache, layer, self._ptr(logits, torch.float32),
                     params if params is not None else _C.SelectorParams(), self._stream(stream))
 
+    def prefill_capture(self, layer: int, q_win: torch.Tensor, q_pos: torch.Tensor, out: torch.Tensor,
+                        pool: int = 0, stream=None):
+        """Prefill tail-window capture: q_win fp32 [B][W][Hq][d] at 1-based positions
+        q_pos int32 [B][W] -> pooled logits over J, out fp32 [B][H][W][max_positions]."""
+        _C.prefill_capture(self.shape, self.cache, layer, self._ptr(q_win, torch.float32), q_win.shape[1],
+                           self._ptr(q_pos, torch.int32), self._ptr(out, torch.float32), pool,
+                           self._stream(stream))
+
+    def selector_window(self, layer: int, logits: torch.Tensor, W: int, params=None, stream=None):
+        """Selector over a W-row window (prefill): logits fp32 [B][H][W][max_positions]."""
+        _C.selector_window(self.shape, self.cache, layer, self._ptr(logits, torch.float32), W,
+                           params if params is not None else _C.SelectorParams(), self._stream(stream))
+
     def selector_fuse(self, layer: int, logits: torch.Tensor, params=None, stream=None) -> torch.Tensor:
         """Head-sharded Selector, phase 1: z_base of this cache's heads, returned as a
         view fp64 [B][H][max_positions] of the workspace (valid until the next

@@ -478,3 +478,47 @@ def test_async_slow_step_pipeline_matches_synchronous():
     assert rel_err(outs[1].cpu().numpy(), outs[0].cpu().numpy()) < 1e-5
     assert torch.equal(sync.n_sel, asyn.n_sel) and torch.equal(sync.sel, asyn.sel)
     assert torch.equal(sync.ck, asyn.ck) and torch.equal(sync.cv, asyn.cv)
+
+
+@pytest.mark.parametrize("pool", [0, 1])
+def test_prefill_capture_and_window_selector(pool):
+    """Prefill tail-window capture (attention.cpp:460-500, :367-409) and the W > 1
+    Selector on it (evidence power mean, selector.cpp:96-127) vs the reference."""
+    torch = _torch()
+    from oracle import oracle as O
+    from paper_2603_12038_b200 import SelectorParams
+
+    B, H, Hq, d, W, K = 2, 2, 8, 128, 16, 64
+    G = Hq // H
+    lens = [700, 500]
+    c = _cache(L=1, B=B, H=H, Hq=Hq, d=d, Lmax=800, ns=4, K=K, R=32)
+    c.fill_synthetic(seed=31 + pool, length=max(lens))
+    c.set_lengths(lens, [4] * B)
+    g = torch.Generator().manual_seed(12 + pool)
+    q = torch.randn(B, W, Hq, d, generator=g)
+    q_pos = torch.tensor([[L - W + 1 + w for w in range(W)] for L in lens], dtype=torch.int32)
+    out = torch.full((B, H, W, c.shape.max_positions), float("nan")).cuda()
+    c.prefill_capture(0, q.cuda().contiguous(), q_pos.cuda().contiguous(), out, pool)
+    c.selector_window(0, out, W, SelectorParams())
+    torch.cuda.synchronize()
+    c.check_errors()
+    orc = oracle()
+    for b in range(B):
+        L, nsb, rl, j0, j1 = _window(c, b)
+        n = j1 - j0 + 1
+        k, _ = _rows(c, 0, b, L)  # [H][L][d]
+        got = out[b, :, :, :n].double().cpu().numpy()  # [H][W][n]
+        pos = np.arange(j0, j1 + 1)
+        for h in range(H):
+            for w in range(W):
+                lg = (q[b, w, h * G:(h + 1) * G].double().numpy() @ k[h, j0 - 1:j1].T.astype(np.float64)) / np.sqrt(d)
+                want = lg.max(0) if pool == 1 else lg.mean(0)
+                live = pos <= int(q_pos[b, w])
+                assert np.all(got[h, w, ~live] <= -1e30)
+                assert rel_err(got[h, w, live], want[live]) < TOL, (b, h, w)
+        norms = c.key_norms[0, b, :, j0 - 1:j1].cpu().numpy()
+        want_sel, _ = orc.run_selector(got.reshape(H, W * n), pos, norms, O.make_cfg(k_budget=K),
+                                       width=W)
+        for h in range(H):
+            ns_ = int(c.n_sel[0, b, h])
+            assert np.array_equal(c.sel[0, b, h, :ns_].cpu().numpy(), want_sel[h]), (b, h)
