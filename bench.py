@@ -254,9 +254,14 @@ class Workload:
             self.cache.dense_decode(l, self.q[l], self.out[l], self.logits, 0)
 
     def launches(self, slow: bool) -> int:
-        if self.mode == "seq":  # + merge per attention call; Selector: 3 stats + 4 finish + 3 pick
-            return 1 + self.L * ((2 + 10 + 1 + 1) if slow else 2)
-        return 1 + self.L * (6 if slow else 1)
+        """Our kernels per step (collectives' own kernels not counted)."""
+        if not slow:  # advance + one fused launch per layer (+ the LSE merge when sequence-sharded)
+            return 1 + self.L * (2 if self.mode == "seq" else 1)
+        if self.mode == "seq":  # append (last rank), dense + merge, Selector 3 stats + finish 3 + pick 3, compact
+            return 1 + self.L * (1 + 2 + 9 + 1)
+        if self.mode == "heads":  # append, dense, Selector fuse + refine + top-k, compact
+            return 1 + self.L * 6
+        return 1 + self.L * 7  # append, dense, Selector pw + coef + z + top-k, compact
 
     def shard_frac(self) -> float:  # this rank's share of a layer's rows (sequence shards)
         return 1.0 / self.world if self.mode == "seq" else 1.0
