@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "kernels.h"
@@ -256,6 +257,19 @@ int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* 
 }  // namespace
 
 namespace sfi_impl {
+
+cudaError_t ensure_kernel_attrs(const void* fn, int smem, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> caps;  // configured smem cap per kernel
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = caps.find(fn);
+  if (it != caps.end() && it->second >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess && nonportable_cluster)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) caps[fn] = smem;
+  return e;
+}
 
 bool pdl_enabled() {
   static const bool on = [] {

@@ -805,15 +805,8 @@ cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const C
   const int S = p.B * p.H;
   if (!fn || S > kMaxSlices || ctas > kMaxCtas) return cudaErrorInvalidValue;
   const int smem = decode_smem_bytes(D, G, S);
-  // raise the dynamic-smem cap once per instantiation to the largest size used
-  static int configured[2][17] = {};
-  int& cap = configured[D == 64 ? 0 : 1][G];
-  if (smem > cap) {
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    cap = smem;
-  }
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(fn), smem);
+  if (e != cudaSuccess) return e;
   return launch_k(fn, dim3(ctas), dim3(kThreads), (size_t)smem, stream, tmk, tmv, p);
 }
 

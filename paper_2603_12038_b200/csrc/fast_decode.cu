@@ -689,16 +689,8 @@ cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, cons
   FastFn fn = (D == 64) ? pick<64>(G) : pick<128>(G);
   if (!fn || C < 1 || C > 16) return cudaErrorInvalidValue;
   const int smem = D == 64 ? fast_smem_bytes<64>() : fast_smem_bytes<128>();
-  static bool configured[2][17] = {};
-  bool& done = configured[D == 64 ? 0 : 1][G];
-  if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(fn), smem, /*nonportable_cluster=*/true);
+  if (e != cudaSuccess) return e;
   FastParams q = p;
   static const bool no_push = [] {
     const char* e = std::getenv("SFI_FAST_PUSH");

@@ -16,6 +16,9 @@ namespace sfi_impl {
 
 // Launch with programmatic stream serialization (PDL) unless SFI_PDL=0.
 bool pdl_enabled();
+// Thread-safe, once per (kernel, size): raise the kernel's dynamic shared
+// memory cap to at least `smem` bytes (and allow non-portable cluster sizes).
+cudaError_t ensure_kernel_attrs(const void* fn, int smem, bool nonportable_cluster = false);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args&&... args) {

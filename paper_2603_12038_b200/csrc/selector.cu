@@ -1413,28 +1413,18 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
   }();
   if (n_max <= kTopkCtaMax && !force_cluster) {
     const size_t smem = (size_t)std::max(n_max, 1) * sizeof(uint32_t);
-    static bool cta_configured = false;
-    if (!cta_configured) {
-      cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(sel_topk_cta_kernel<kExp>),
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kTopkCtaMax * (int)sizeof(uint32_t));
-      if (e != cudaSuccess) return e;
-      cta_configured = true;
-    }
+    cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(sel_topk_cta_kernel<kExp>),
+                                        kTopkCtaMax * (int)sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
     return launch_k(sel_topk_cta_kernel<kExp>, dim3(rows), dim3(kTopkCtaT), smem, st, p);
   }
   const int chunk = (n_max + kCS - 1) / kCS;
   const dim3 gc(kCS, (unsigned)rows);
   if (chunk <= kTopkSmemKeys) {
     const size_t smem = (size_t)std::max(chunk, 1) * sizeof(unsigned long long);
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(sel_topk_kernel<kExp, true>),
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kTopkSmemKeys * (int)sizeof(unsigned long long));
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+    cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(sel_topk_kernel<kExp, true>),
+                                        kTopkSmemKeys * (int)sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
     return launch_k(sel_topk_kernel<kExp, true>, gc, dim3(kT), smem, st, p);
   }
   return launch_k(sel_topk_kernel<kExp, false>, gc, dim3(kT), 0, st, p);
