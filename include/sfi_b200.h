@@ -348,6 +348,10 @@ SFI_API int32_t sfi_last_launch_count(void);
  * prologue done, first tile landed, end, emissions, tiles, smid) into `out`;
  * returns the CTA count. SFI_DECODE_CTAS=<n> overrides the decode grid. */
 SFI_API int32_t sfi_debug_decode_trace(int64_t* out, int32_t max_ctas);
+/* Debug: with SFI_LAYER_TRACE set, every fast-step launch keeps its per-CTA
+ * timeline in a slot of its layer (no reset); copies [layers][max_ctas][16]
+ * int64 into `out` and returns the CTA count of the last launch. */
+SFI_API int32_t sfi_debug_layer_trace(int64_t* out, int32_t layers, int32_t max_ctas);
 
 #ifdef __cplusplus
 }

@@ -191,6 +191,17 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   return SFI_OK;
 }
 
+constexpr int kLayerTraceMax = 128;
+long long* layer_trace_buffer() {
+  static long long* buf = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (cudaMalloc(&buf, sizeof(long long) * 16 * sfi_impl::kMaxCtas * kLayerTraceMax) != cudaSuccess) buf = nullptr;
+    else cudaMemset(buf, 0, sizeof(long long) * 16 * sfi_impl::kMaxCtas * kLayerTraceMax);
+  });
+  return buf;
+}
+
 // Fast step, one layer: sparse decode over the compact cache, fused with the
 // current token's append when k_new / v_new are given (fast_decode.cu).
 int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* q, const void* k_new,
@@ -240,8 +251,16 @@ int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* 
   if (env_c == 1 || env_c == 2 || env_c == 4 || env_c == 8 || env_c == 16) C = env_c;
   p.trace = nullptr;
   static const bool env_trace = std::getenv("SFI_DECODE_TRACE") != nullptr;
+  static const bool env_layer_trace = std::getenv("SFI_LAYER_TRACE") != nullptr;
   const int grid = s->batch * s->n_kv_heads * C;
-  if (env_trace && grid <= sfi_impl::kMaxCtas) {
+  if (env_layer_trace && grid <= sfi_impl::kMaxCtas && layer < kLayerTraceMax) {
+    // per-layer slots, no reset: a graph of one step's launches leaves every
+    // layer's CTA timeline behind (sfi_debug_layer_trace)
+    long long* buf = layer_trace_buffer();
+    if (!buf) return fail(SFI_ERR_CUDA, "layer trace buffer");
+    p.trace = buf + (size_t)layer * sfi_impl::kMaxCtas * 16;
+    g_trace_ctas = grid;
+  } else if (env_trace && grid <= sfi_impl::kMaxCtas) {
     p.trace = sfi_impl::decode_trace_buffer();
     if (!p.trace) return fail(SFI_ERR_CUDA, "trace buffer");
     SFI_CUDA(cudaMemsetAsync(p.trace, 0, sizeof(long long) * 16 * sfi_impl::kMaxCtas, (cudaStream_t)stream),
@@ -327,6 +346,17 @@ extern "C" {
 SFI_API const char* sfi_version(void) { return "sfi_b200 0.1 (sm_100a)"; }
 SFI_API const char* sfi_last_error(void) { return g_err.c_str(); }
 SFI_API int32_t sfi_last_launch_count(void) { return g_launches; }
+
+SFI_API int32_t sfi_debug_layer_trace(int64_t* out, int32_t layers, int32_t max_ctas) {
+  long long* buf = layer_trace_buffer();
+  if (!buf || !out || layers <= 0 || layers > kLayerTraceMax || max_ctas <= 0) return 0;
+  const int n = std::min(max_ctas, sfi_impl::kMaxCtas);
+  for (int l = 0; l < layers; ++l)
+    if (cudaMemcpy(out + (size_t)l * n * 16, buf + (size_t)l * sfi_impl::kMaxCtas * 16, sizeof(long long) * 16 * n,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return 0;
+  return g_trace_ctas;
+}
 
 SFI_API int32_t sfi_debug_decode_trace(int64_t* out, int32_t max_ctas) {
   long long* buf = sfi_impl::decode_trace_buffer();
