@@ -35,7 +35,6 @@
 #include <cuda.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cmath>
 
 #include "common.cuh"
@@ -70,11 +69,9 @@ struct FPart {  // partials, written over the (drained) stage ring
   static constexpr int kBytes = (kO + 2 * kParts * G + 2 * G) * 4;
   static_assert(kBytes <= FGeo<D>::kRing, "partials must fit in the stage ring");
 };
-// leader inbox of the push merge: (C - 1) partials of G x D + 2G floats
-constexpr int kInboxBytes = 8448;
 template <int D>
-constexpr int fast_smem_bytes() {  // stage ring | mbarriers | fp64 k^2 row | leader inbox
-  return FGeo<D>::kRing + 64 + D * 8 + kInboxBytes;
+constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row
+  return FGeo<D>::kRing + 64 + D * 8;
 }
 
 template <int D>
@@ -85,27 +82,6 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
-}
-__device__ __forceinline__ void cluster_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// arrive (release, cluster scope) on the mbarrier at the same offset in CTA `rank`
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, int rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "SFI_CWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra SFI_CWAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
 }
 
 // Tile t of a slice (ring tiles first) -> first compact row.
@@ -145,58 +121,6 @@ __device__ __forceinline__ void combine_cta(float* part_o, const float* part_m, 
   }
 }
 
-// Push merge (160 threads: consumers + aux). Every CTA but the cluster leader
-// writes its combined partial into the leader's inbox over DSMEM and arrives on
-// the leader's inbox mbarrier, then exits; the leader waits for the C - 1
-// arrivals and merges its own partial and the inbox in rank order. No
-// cluster-wide barrier at the end, so the peers' SM slots free up early for the
-// next layer's kernel.
-template <int D, int G>
-__device__ __forceinline__ void push_merge(const FastParams& p, cg::cluster_group& cl, int rank, int C,
-                                           const float* part_o, const float* comb_m, const float* comb_l,
-                                           float* inbox, uint64_t* inbox_bar, int b, int h, bool ok, int tid) {
-  constexpr int kT = (kNcw + 1) * 32;
-  constexpr int stride = G * D + 2 * G;
-  cluster_wait();                                      // peers' barrier inits
-  asm volatile("bar.sync 3, %0;" ::"n"(kT));          // this CTA's combine complete
-  if (rank != 0) {
-    float* dst = cl.map_shared_rank(inbox, 0) + (rank - 1) * stride;
-    for (int e = tid; e < G * D; e += kT) dst[e] = part_o[e];
-    if (tid < G) {
-      dst[G * D + tid] = comb_m[tid];
-      dst[G * D + G + tid] = comb_l[tid];
-    }
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-    asm volatile("bar.sync 3, %0;" ::"n"(kT));
-    if (tid == 0) mbar_arrive_remote(inbox_bar, 0);
-    return;
-  }
-  mbar_wait_cluster(inbox_bar, 0);
-  float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
-  for (int e = tid; e < G * D; e += kT) {
-    const int gg = e / D;
-    float M = comb_m[gg];
-    for (int c = 0; c < C - 1; ++c) M = fmaxf(M, inbox[c * stride + G * D + gg]);
-    const float Mu = (M == -INFINITY) ? 0.f : M;
-    float Ls = 0.f, Os = 0.f;
-    for (int c = 0; c < C; ++c) {
-      const float m = c == 0 ? comb_m[gg] : inbox[(c - 1) * stride + G * D + gg];
-      const float l = c == 0 ? comb_l[gg] : inbox[(c - 1) * stride + G * D + G + gg];
-      const float o = c == 0 ? part_o[e] : inbox[(c - 1) * stride + e];
-      const float sc = l > 0.f ? fast_exp2(m - Mu) : 0.f;
-      Ls += l * sc;
-      Os += (l > 0.f ? o : 0.f) * sc;
-    }
-    outp[e] = Ls > 0.f ? Os / Ls : 0.f;
-    if (p.lse) {
-      if (e % D == 0)
-        p.lse[(size_t)b * p.Hq + (size_t)h * G + gg] = Ls > 0.f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
-    } else if (e == 0 && ok && !(Ls > 0.f)) {
-      raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
-    }
-  }
-}
-
 template <int D, int G>
 __global__ void __launch_bounds__(kThreads, 2)
     fast_decode_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
@@ -214,8 +138,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   float* comb_m = part_l + kParts * G;                   // [G] CTA-combined (m, l);
   float* comb_l = comb_m + G;                            //     O combined in place in part 0
   double* ksq = reinterpret_cast<double*>(smem + FGeo<D>::kRing + 64);  // [D] k_c^2 (aux)
-  float* inbox = reinterpret_cast<float*>(smem + FGeo<D>::kRing + 64 + D * 8);  // leader: [C-1][G*D+2G]
-  uint64_t* inbox_bar = empty + kStages;
 
   long long* trace = p.trace ? p.trace + (size_t)blockIdx.x * 16 : nullptr;
   if (trace && threadIdx.x == 0) {
@@ -239,12 +161,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kNcw);
     }
-    if (p.push) mbar_init(inbox_bar, C - 1);
     fence_barrier_init();
   }
-  // push merge: peers' inbox barrier inits become visible through this split
-  // cluster barrier, waited on just before the first remote access
-  if (p.push) cluster_arrive_relaxed();
   // Static tile split over the compact layout [0, R) + [R, R + n_sink + K):
   // no global load before the producer's first TMA. In steady-state decode
   // n_sel = K, so it equals the live split; shorter selections only leave
@@ -280,10 +198,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (trace && lane == 0) trace[10] = (long long)globaltimer();
     griddep_wait();
     griddep_launch();
-    if (p.push) {
-      cluster_wait();
-      return;
-    }
     cluster_sync_all();  // partials published
     cluster_sync_all();  // merge done: shared memory may be released
     return;
@@ -374,12 +288,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     asm volatile("bar.sync 2, %0;" ::"n"((kNcw + 1) * 32));  // all partials written
     combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x - 32);
-    if (p.push) {
-      push_merge<D, G>(p, cl, rank, C, part_o, comb_m, comb_l, inbox, inbox_bar, b, h, ok,
-                       (int)threadIdx.x - 32);
-    } else {
-      cluster_sync_all();
-    }
+    cluster_sync_all();
     // fp64 key norm: sequential over c in round-to-nearest ops (attention.cpp:
     // 143-150; bit-identical to append_kernel), off the critical path
     if (mine && lane == 0) {
@@ -389,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       p.norms[slice_g * p.Lmax + (L - 1)] = __dsqrt_rn(acc);
     }
     __syncwarp();
-    if (!p.push) cluster_sync_all();
+    cluster_sync_all();
     return;
   }
 
@@ -605,11 +514,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   asm volatile("bar.sync 2, %0;" ::"n"((kNcw + 1) * 32));  // all partials written
   combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x);
-  if (p.push) {
-    push_merge<D, G>(p, cl, rank, C, part_o, comb_m, comb_l, inbox, inbox_bar, b, h, ok, (int)threadIdx.x);
-    if (trace && threadIdx.x == 0) trace[3] = trace[14] = trace[13] = (long long)globaltimer();
-    return;
-  }
   cluster_sync_all();
   if (trace && threadIdx.x == 0) trace[13] = (long long)globaltimer();
 
@@ -691,12 +595,6 @@ cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, cons
   const int smem = D == 64 ? fast_smem_bytes<64>() : fast_smem_bytes<128>();
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(fn), smem, /*nonportable_cluster=*/true);
   if (e != cudaSuccess) return e;
-  FastParams q = p;
-  static const bool no_push = [] {
-    const char* e = std::getenv("SFI_FAST_PUSH");
-    return e && e[0] == '0';
-  }();
-  q.push = (!no_push && C >= 2 && (C - 1) * (G * D + 2 * G) * 4 <= kInboxBytes) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.B * p.H * C);
   cfg.blockDim = dim3(kThreads);
@@ -711,7 +609,7 @@ cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, cons
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, fn, tmk, tmv, q);
+  return cudaLaunchKernelEx(&cfg, fn, tmk, tmv, p);
 }
 
 }  // namespace sfi_impl

@@ -89,7 +89,6 @@ struct FastParams {
   float scale_log2;               // log2(e) / sqrt(d)
   long long* trace;               // debug: per-CTA globaltimer stamps [grid][16] (null = off)
   float* lse;                     // [B][Hq] partial mode (sequence shards): LSE out, empty allowed
-  int push;                       // set by launch_fast_decode: push merge into the leader's inbox
 };
 int fast_cluster_size(int slices, int num_sms);
 cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
