@@ -111,6 +111,20 @@ __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Named CTA barriers between warp roles. The roles reach a barrier from
+// different code paths (different instructions), so the non-.aligned
+// barrier forms are the ones PTX allows here; the warp reconverges first.
+template <int kId, int kThreads>
+__device__ __forceinline__ void named_bar_sync() {
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"n"(kId), "n"(kThreads) : "memory");
+}
+template <int kId, int kThreads>
+__device__ __forceinline__ void named_bar_arrive() {
+  __syncwarp();
+  asm volatile("barrier.arrive %0, %1;" ::"n"(kId), "n"(kThreads) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -395,12 +395,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     // sequence the consumers walk.
     constexpr int kCols = D / 32;
     using Vec = typename std::conditional<kCols == 4, float4, float2>::type;
-    asm volatile("bar.arrive 2, %0;" ::"n"(kBarThreads));  // slots start free
+    named_bar_arrive<2, kBarThreads>();  // slots start free
     int pend[2], n_pend = 0;  // partial slices awaiting publication
     for (int s = s_first; s < S && pref[s] < te; ++s) {
       const int P0 = pref[s], P1 = pref[s + 1];
       if (P1 == P0) continue;
-      asm volatile("bar.sync 1, %0;" ::"n"(kBarThreads));
+      named_bar_sync<1, kBarThreads>();
       const long long e0 = trace ? (long long)globaltimer() : 0;
       if (trace && lane == 0) {
         if (trace[13] == 0) trace[13] = e0;
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         lr[gg] = L;
       }
       __syncwarp();
-      asm volatile("bar.arrive 2, %0;" ::"n"(kBarThreads));  // slots free again
+      named_bar_arrive<2, kBarThreads>();  // slots free again
       const int c_first = cta_of(P0, T, Gc), c_last = cta_of(P1 - 1, T, Gc);
       const int b = s / p.H, h = s % p.H;
       float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         lr[hh] += __shfl_xor_sync(0xffffffffu, lr[hh], 2);
       }
       const long long tw0 = trace ? (long long)globaltimer() : 0;
-      asm volatile("bar.sync 2, %0;" ::"n"(kBarThreads));
+      named_bar_sync<2, kBarThreads>();
       if (trace && threadIdx.x == 0) trace[8] += (long long)globaltimer() - tw0;
       if constexpr (NH == 2) {
 #pragma unroll
@@ -754,12 +754,12 @@ __global__ void __launch_bounds__(kThreads, 2)
           comb_ml[(warp * 2 + 1) * G + g] = lr[0];
         }
       }
-      asm volatile("bar.arrive 1, %0;" ::"n"(kBarThreads));
+      named_bar_arrive<1, kBarThreads>();
       fresh = true;
     }
   }
   // consume the epilogue's final EMPTY arrival (balances barrier 2 before exit)
-  asm volatile("bar.sync 2, %0;" ::"n"(kBarThreads));
+  named_bar_sync<2, kBarThreads>();
   if (trace && threadIdx.x == 0) trace[12] = (long long)globaltimer();
 }
 

@@ -80,6 +80,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
+  __syncwarp();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
     if (trace && lane == 0) trace[8] = (long long)globaltimer();
-    asm volatile("bar.sync 1, %0;" ::"n"((kNcw + 1) * 32));  // stage ring drained
+    named_bar_sync<1, (kNcw + 1) * 32>();  // stage ring drained
 #pragma unroll
     for (int g = 0; g < G; ++g) {
 #pragma unroll
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         part_l[kNcw * G + g] = lq[g];
       }
     }
-    asm volatile("bar.sync 2, %0;" ::"n"((kNcw + 1) * 32));  // all partials written
+    named_bar_sync<2, (kNcw + 1) * 32>();  // all partials written
     combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x - 32);
     cluster_sync_all();
     // fp64 key norm: sequential over c in round-to-nearest ops (attention.cpp:
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     l_run[hh] += __shfl_xor_sync(0xffffffffu, l_run[hh], 2);
   }
   if (trace && threadIdx.x == 0) trace[9] = (long long)globaltimer();
-  asm volatile("bar.sync 1, %0;" ::"n"((kNcw + 1) * 32));
+  named_bar_sync<1, (kNcw + 1) * 32>();
   if (trace && threadIdx.x == 0) trace[12] = (long long)globaltimer();
   if constexpr (NH == 2) {
 #pragma unroll
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       part_l[warp * G + g] = l_run[0];
     }
   }
-  asm volatile("bar.sync 2, %0;" ::"n"((kNcw + 1) * 32));  // all partials written
+  named_bar_sync<2, (kNcw + 1) * 32>();  // all partials written
   combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x);
   cluster_sync_all();
   if (trace && threadIdx.x == 0) trace[13] = (long long)globaltimer();

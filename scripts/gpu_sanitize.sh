@@ -1,5 +1,6 @@
+# compute-sanitizer memcheck + racecheck + synccheck over the GPU parity suite (small shapes)
 export PYTHONPATH=$GRAFT_REPO_ROOT
-for k in "fast_decode_fused" "group16" "sparse_decode_vs"; do
-  echo "== $k"
-  timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 4 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "$k" -p no:cacheprovider 2>&1 | grep -vE "Host Frame|^=========\s*$" | grep -E "hazard|Write|Read|at |RACECHECK|kernel|passed|failed" | head -24
+for tool in memcheck racecheck synccheck; do
+  echo "== $tool"
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 10 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "not C2 and not 32768" 2>&1 | grep -vE "Host Frame|^=========\s*$" | tail -6
 done
