@@ -171,7 +171,7 @@ SFI_API int sfi_dense_decode(const sfi_shape* shape, const sfi_cache* cache, int
 
 /* sfi_dense_decode with options. lse (optional): natural-log sum-exp per q head
  * (partial mode, see sequence sharding). flags: SFI_DENSE_SHARE_SM sizes the
- * stream-K grid to 3/4 of the SM slots so kernels on another stream — the
+ * stream-K grid to 65% of the SM slots so kernels on another stream — the
  * previous layer's Selector in the asynchronous slow-step pipeline — run at
  * the same time on the rest. */
 #define SFI_DENSE_SHARE_SM 2

@@ -167,10 +167,11 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   const int per_slice = sparse ? (s->n_recent + 63) / 64 + 1 + (s->n_sink + s->k_budget + 63) / 64
                               : (s->max_positions + 63) / 64;
   // 7/8 of the 2-CTAs-per-SM slots measures fastest alone (fewer in-flight
-  // streams per HBM channel); SFI_DENSE_SHARE_SM leaves a quarter of the slots to
-  // the Selector kernels of the asynchronous slow-step pipeline
+  // streams per HBM channel); SFI_DENSE_SHARE_SM keeps 65% (192 CTAs on 148
+  // SMs, the measured optimum of the asynchronous slow-step pipeline) and
+  // leaves the rest to the Selector kernels running beside it
   int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms(),
-                                   (flags & SFI_DENSE_SHARE_SM) ? 6 : 7);
+                                   (flags & SFI_DENSE_SHARE_SM) ? 650 : 875);
   static const int env_ctas = [] {
     const char* e = std::getenv("SFI_DECODE_CTAS");
     return e ? std::atoi(e) : 0;

@@ -795,8 +795,8 @@ int decode_smem_bytes(int D, int G, int slices) {
   return fixed + (slices + 1) * (int)sizeof(int);
 }
 
-int decode_grid(int tiles_upper, int num_sms, int eighths) {
-  return std::max(1, std::min(2 * num_sms * eighths / 8, tiles_upper));
+int decode_grid(int tiles_upper, int num_sms, int permille) {
+  return std::max(1, std::min(2 * num_sms * permille / 1000, tiles_upper));
 }
 
 cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv,

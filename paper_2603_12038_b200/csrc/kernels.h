@@ -63,8 +63,8 @@ struct DecodeParams {
 long long* decode_trace_buffer();
 
 int decode_smem_bytes(int D, int G, int slices);
-// stream-K grid: `eighths` / 8 of the 2-CTAs-per-SM capacity, at most one CTA per tile
-int decode_grid(int tiles_upper, int num_sms, int eighths);
+// stream-K grid: `permille` / 1000 of the 2-CTAs-per-SM capacity, at most one CTA per tile
+int decode_grid(int tiles_upper, int num_sms, int permille);
 cudaError_t launch_decode(const DecodeParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv,
                           int D, int G, int ctas, cudaStream_t stream);
 

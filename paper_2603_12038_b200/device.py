@@ -185,7 +185,7 @@ class SlowStepPipeline:
     """Asynchronous slow step (the paper's layer-wise pipeline, PAPER.md:478-495;
     SURVEY §8f-1) over one SfiCache.
 
-    The dense decode of every layer runs on the caller's stream on 3/4 of the SM
+    The dense decode of every layer runs on the caller's stream on 65% of the SM
     slots (SFI_DENSE_SHARE_SM); the Selector and the compact build of layer l run
     on an auxiliary stream as soon as layer l's pooled logits exist, on the slots
     the dense kernels leave free, while layers l+1.. stream their KV. The refreshed selection is only read by the next fast step, after `end()`
