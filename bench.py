@@ -501,10 +501,12 @@ def gpu_arm(args) -> dict:
     # in situ: the fast step's graph (advance + L fused launches, PDL-chained)
     # replayed back to back; its launches' average duration = step time / L
     # (the advance kernel's share is charged to them: conservative)
-    t_fast_step = None
+    t_fast_step = t_slow_step = None
     if use_graph:
         wl.set_lengths(wl.ctx + 1)
         t_fast_step = time_graph(graphs[False], 16)
+        wl.set_lengths(wl.ctx + 1)
+        t_slow_step = time_graph(graphs[True], 3)
     t_sp = t_fast_step / wl.L if t_fast_step else t_sp_iso
     t_sel, t_cb = time_selector(wl, max(6, wl.L // 4))
     bsp, bde = wl.bytes_sparse(), wl.bytes_dense(Lcur)
@@ -547,6 +549,7 @@ def gpu_arm(args) -> dict:
                    "l2": "inputs larger than L2 (KV cache %.1f GB)" % (2 * c.sizes['kv_cache'] / 1e9)},
         "slow_steps": n_slow, "fast_step_us_kernels": fast_us,
         "fast_step_us_graph": t_fast_step * 1e3 if t_fast_step else None,
+        "slow_step_us_graph": t_slow_step * 1e3 if t_slow_step else None,
         "slow_step_us_kernels": wl.L * (t_de + t_sel + t_cb) * 1e3,
         "kernels": kernels, "roofline": roof,
         "gpu_launches": sum(wl.launches(s_) for s_ in timed),
