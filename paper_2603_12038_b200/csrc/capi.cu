@@ -249,7 +249,7 @@ int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* 
     return e ? std::atoi(e) : 0;
   }();
   int C = sfi_impl::fast_cluster_size(s->batch * s->n_kv_heads, num_sms());
-  if (env_c == 1 || env_c == 2 || env_c == 4 || env_c == 8 || env_c == 16) C = env_c;
+  if (env_c >= 1 && env_c <= 16) C = env_c;
   p.trace = nullptr;
   static const bool env_trace = std::getenv("SFI_DECODE_TRACE") != nullptr;
   static const bool env_layer_trace = std::getenv("SFI_LAYER_TRACE") != nullptr;
