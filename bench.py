@@ -420,15 +420,22 @@ def gpu_arm(args) -> dict:
     c = wl.cache
     use_graph = not args.no_graph
     graphs = {}
+    graph_note = None
     if use_graph:
         # both paths already ran eagerly in setup (kernel attributes, driver entry
         # points); capture records without executing, so prefix_len is untouched
-        for slow in (False, True):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                wl.step(slow)
-            graphs[slow] = g
-        torch.cuda.synchronize()
+        try:
+            for slow in (False, True):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    wl.step(slow)
+                graphs[slow] = g
+            torch.cuda.synchronize()
+        except Exception as ex:  # e.g. a collective backend that cannot be captured
+            use_graph, graphs = False, {}
+            graph_note = f"graph capture failed ({type(ex).__name__}); eager launches"
+            torch.cuda.synchronize()
+            wl.set_lengths(wl.ctx + 1)
 
     def run(slow: bool):
         if use_graph:
@@ -543,7 +550,7 @@ def gpu_arm(args) -> dict:
                        "seq": f"sequence sharded x{world} (LSE-merged partials; sharded Selector stats, "
                               "soft-NMS edges, top-k candidate merge)",
                    }.get(wl.mode, f"dp{world} (independent request batches)"),
-                   "cuda_graphs": use_graph,
+                   "cuda_graphs": use_graph if graph_note is None else graph_note,
                    "slow_step": "synchronous" if wl.pipe is None else
                                 "async pipeline: dense on the main stream (1 CTA/SM), Selector + compact on an aux stream",
                    "l2": "inputs larger than L2 (KV cache %.1f GB)" % (2 * c.sizes['kv_cache'] / 1e9)},
