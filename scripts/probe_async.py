@@ -20,7 +20,8 @@ def slow(kind):
             s = l % pipe.slots
             if l >= pipe.slots:
                 main.wait_event(pipe.ev_free[s])
-            c.ring_append(l, wl.k_new[l], wl.v_new[l])
+            if kind != "noappend":
+                c.ring_append(l, wl.k_new[l], wl.v_new[l])
             c.dense_decode_ex(l, wl.q[l], wl.out[l], pipe.logits[s], 0, share_sm=True)
             pipe.ev_ready[s].record(main)
             with torch.cuda.stream(aux):
@@ -35,7 +36,7 @@ def slow(kind):
 
 res = {}
 graphs = {}
-for kind in ("none", "sel", "compact", "all"):
+for kind in ("noappend", "none", "sel", "compact", "all"):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         slow(kind)()
