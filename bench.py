@@ -515,10 +515,34 @@ def gpu_arm(args) -> dict:
         wl.set_lengths(wl.ctx + 1)
         t_slow_step = time_graph(graphs[True], 3)
     t_sp = t_fast_step / wl.L if t_fast_step else t_sp_iso
+    # diagnostic: the same fused fast step with every layer in ONE launch (layer-batched
+    # view of the cache), i.e. the kernel without the per-layer launch boundary
+    t_lb = None
+    if wl.mode in ("single", "dp"):
+        try:
+            lbv = wl.cache.layer_batched_view()
+            qv, kv_, vv_, ov = (x.view(-1, *x.shape[2:]) for x in (wl.q, wl.k_new, wl.v_new, wl.out))
+            s_ = torch.cuda.current_stream()
+            lbv.fast_decode(0, qv, kv_, vv_, ov, prefetch=True)
+            torch.cuda.synchronize()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(s_)
+            for _ in range(5):
+                lbv.fast_decode(0, qv, kv_, vv_, ov, prefetch=True)
+            eb.record(s_)
+            torch.cuda.synchronize()
+            t_lb = ea.elapsed_time(eb) / 5 / wl.L
+            del lbv
+        except Exception:
+            t_lb = None
     t_sel, t_cb = time_selector(wl, max(6, wl.L // 4))
     bsp, bde = wl.bytes_sparse(), wl.bytes_dense(Lcur)
     kernels = {
         "fast_decode": {"ms": t_sp, "GB/s": bsp / t_sp / 1e6, "bytes": bsp, "isolated_ms": t_sp_iso,
+                        "layer_batched": (None if t_lb is None else
+                                          {"ms_per_layer": t_lb, "GB/s": bsp / t_lb / 1e6,
+                                           "frac": bsp / t_lb / 1e6 / pk["hbm_gbs"],
+                                           "note": "diagnostic: all layers in one launch (no per-layer boundary)"}),
                         "timing": ("fast-step graph replay / layers (in situ, PDL chain)" if t_fast_step
                                    else "isolated launches between events")},
         "dense_decode": {"ms": t_de, "GB/s": bde / t_de / 1e6, "bytes": bde},

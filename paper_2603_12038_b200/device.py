@@ -45,6 +45,9 @@ class SfiCache:
         self.error_flags = z((1,), dtype=torch.int32, device=dev)
         self.workspace = z((self.sizes["workspace"],), dtype=torch.uint8, device=dev)
         self.pooled_logits = z((B, H, max_positions), dtype=torch.float32, device=dev)
+        self._bind()
+
+    def _bind(self):
         c = _C.Cache()
         c.k_cache, c.v_cache = self.k_cache.data_ptr(), self.v_cache.data_ptr()
         c.key_norms = self.key_norms.data_ptr()
@@ -56,6 +59,33 @@ class SfiCache:
         c.workspace = self.workspace.data_ptr()
         c.workspace_bytes = self.sizes["workspace"]
         self.cache = c
+
+    def layer_batched_view(self) -> "SfiCache":
+        """Diagnostic view of all layers as ONE layer of n_layers x batch requests
+        (same K/V, compact and selection buffers; own lengths and workspace): one
+        launch then streams what a step's per-layer launches stream, which
+        measures the kernels without the per-layer launch boundary."""
+        s0 = self.shape
+        L, B = s0.n_layers, s0.batch
+        s = _C.Shape()
+        s.n_layers, s.batch, s.n_kv_heads, s.n_q_heads = 1, L * B, s0.n_kv_heads, s0.n_q_heads
+        s.head_dim, s.max_positions = s0.head_dim, s0.max_positions
+        s.n_sink, s.k_budget, s.n_recent = s0.n_sink, s0.k_budget, s0.n_recent
+        _C.shape_validate(s)
+        v = SfiCache.__new__(SfiCache)
+        v.shape, v.sizes, v.compact_rows = s, _C.buffer_sizes(s), self.compact_rows
+        flat = lambda t: t.view(1, L * B, *t.shape[2:])  # noqa: E731
+        v.k_cache, v.v_cache, v.key_norms = flat(self.k_cache), flat(self.v_cache), flat(self.key_norms)
+        v.ck, v.cv, v.sel, v.n_sel = flat(self.ck), flat(self.cv), flat(self.sel), flat(self.n_sel)
+        dev = self.k_cache.device
+        v.prefix_len = self.prefix_len.repeat(L)
+        v.n_sink_b = self.n_sink_b.repeat(L)
+        v.recent_len = self.recent_len.repeat(L)
+        v.error_flags = self.error_flags
+        v.workspace = torch.zeros((v.sizes["workspace"],), dtype=torch.uint8, device=dev)
+        v.pooled_logits = None
+        v._bind()
+        return v
 
     # -- plumbing -------------------------------------------------------------
     @staticmethod
