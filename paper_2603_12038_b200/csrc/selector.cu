@@ -212,7 +212,7 @@ __device__ __forceinline__ void cluster_reduce(T (&v)[NV], int nv, T* wbuf, T (*
   for (int k = 0; k < NV; ++k)
     if (k < nv) {
       T acc = *cl.map_shared_rank(&slot[k], 0);
-      for (int r = 1; r < kCS; ++r) acc = op(acc, *cl.map_shared_rank(&slot[k], r));
+      for (int r = 1; r < (int)cl.num_blocks(); ++r) acc = op(acc, *cl.map_shared_rank(&slot[k], r));
       v[k] = acc;
     }
 }
@@ -873,14 +873,16 @@ __device__ __forceinline__ unsigned long long okey(double x) {
 
 // kSmem: the CTA's block of keys lives in dynamic shared memory (one global
 // read); otherwise every pass re-reads z from global/L2.
-template <bool kExp, bool kSmem>
-__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
+template <bool kExp, bool kSmem, int CS>
+__global__ void __launch_bounds__(kT)
     sel_topk_kernel(const SelParams p) {
   griddep_wait();
   griddep_launch();
   extern __shared__ unsigned long long skeys[];
   __shared__ uint32_t hist[2][kBins];
-  __shared__ uint32_t bsum[2][kBinsPerCta];
+  constexpr int kBPC = kBins / CS;   // bins per CTA
+  constexpr int kBPL = kBPC / 32;    // bins per lane in the threshold scan
+  __shared__ uint32_t bsum[2][kBPC];
   __shared__ uint32_t slice_tot[2];
   __shared__ int res_tb[2], res_cum[2], res_cnt[2];
   __shared__ unsigned long long cand[kCandCap];       // this CTA's threshold-bucket keys
@@ -902,13 +904,13 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     return;
   }
   if (n <= K) {  // |J| <= k: all of J (selector.cpp:239)
-    for (int i = rank * kT + threadIdx.x; i < n; i += kCS * kT) out[i] = src.pos(i);
+    for (int i = rank * kT + threadIdx.x; i < n; i += CS * kT) out[i] = src.pos(i);
     if (rank == 0 && threadIdx.x == 0) p.n_sel[row] = n;
     return;
   }
   const double* z = p.sb + (size_t)row * p.ld;
   // this CTA's contiguous block of the row
-  const int chunk = (n + kCS - 1) / kCS;
+  const int chunk = (n + CS - 1) / CS;
   const int c0 = rank * chunk, c1 = min(n, c0 + chunk);
   const int len = max(0, c1 - c0);
   auto key_at = [&](int i) -> unsigned long long {  // i relative to c0
@@ -950,11 +952,11 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     // zero the other buffer for the next pass (its last readers passed barrier (1))
     for (int i = threadIdx.x; i < kBins; i += kT) hist[pb ^ 1][i] = 0;
     uint32_t mine = 0;
-    for (int bi = threadIdx.x; bi < kBinsPerCta; bi += kT) {
-      const int gb = rank * kBinsPerCta + bi;
+    for (int bi = threadIdx.x; bi < kBPC; bi += kT) {
+      const int gb = rank * kBPC + bi;
       uint32_t s = 0;
       if (gb < nb)
-        for (int r = 0; r < kCS; ++r) s += cl.map_shared_rank(hcur, r)[gb];
+        for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(hcur, r)[gb];
       bsum[pb][bi] = s;
       mine += s;
     }
@@ -974,23 +976,23 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
     const int need_rem = K - above;
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
-      const int tr = lane < kCS ? (int)*cl.map_shared_rank(&slice_tot[pb], kCS - 1 - lane) : 0;
+      const int tr = lane < CS ? (int)*cl.map_shared_rank(&slice_tot[pb], CS - 1 - lane) : 0;
       int inc = tr;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += y;
       }
-      const unsigned m1 = __ballot_sync(0xffffffffu, lane < kCS && inc >= need_rem);
-      const int fl = m1 ? __ffs(m1) - 1 : kCS - 1;
-      const int own = kCS - 1 - fl;
+      const unsigned m1 = __ballot_sync(0xffffffffu, lane < CS && inc >= need_rem);
+      const int fl = m1 ? __ffs(m1) - 1 : CS - 1;
+      const int own = CS - 1 - fl;
       const int cum = __shfl_sync(0xffffffffu, inc - tr, fl);  // keys in ranks above `own`
       const uint32_t* ob = cl.map_shared_rank(&bsum[pb][0], own);
-      uint32_t bv[8];
+      uint32_t bv[kBPL];
       int lsum = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        bv[k] = ob[kBinsPerCta - 1 - (lane * 8 + k)];  // descending bins
+      for (int k = 0; k < kBPL; ++k) {
+        bv[k] = ob[kBPC - 1 - (lane * kBPL + k)];  // descending bins
         lsum += (int)bv[k];
       }
       int inc2 = lsum;
@@ -1003,12 +1005,12 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
       const int fl2 = m2 ? __ffs(m2) - 1 : 31;
       if (lane == fl2) {
         int c2 = cum + inc2 - lsum;
-        int tb = own * kBinsPerCta + (kBinsPerCta - 1 - lane * 8 - 7);
+        int tb = own * kBPC + (kBPC - 1 - lane * kBPL - (kBPL - 1));
         int cnt = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < kBPL; ++k) {
           if (c2 + (int)bv[k] >= need_rem) {
-            tb = own * kBinsPerCta + (kBinsPerCta - 1 - (lane * 8 + k));
+            tb = own * kBPC + (kBPC - 1 - (lane * kBPL + k));
             cnt = (int)bv[k];
             break;
           }
@@ -1040,7 +1042,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT)
         // aliases the histogram buffer of the pass just finished (no reader left)
         unsigned long long* call = reinterpret_cast<unsigned long long*>(hist[pb ^ 1]);
         int off = 0;
-        for (int r = 0; r < kCS; ++r) {
+        for (int r = 0; r < CS; ++r) {
           const int nr = *cl.map_shared_rank(&ncand, r);
           const unsigned long long* src = cl.map_shared_rank(cand, r);
           for (int i = threadIdx.x; i < nr; i += kT) call[off + i] = src[i];
@@ -1405,11 +1407,34 @@ void fill_cfg(SelParams& p, const sfi_selector_params& prm) {
   p.nms_radius = prm.nms_radius;
 }
 
+template <void (*Fn)(SelParams)>
+cudaError_t launch_topk_cluster(dim3 grid, size_t smem, int cs, cudaStream_t st, const SelParams& p) {
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(Fn),
+                                      kTopkSmemKeys * (int)sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, Fn, p);
+}
+
 template <bool kExp>
 cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st) {
-  static const bool force_cluster = [] {
+  // SFI_TOPK_CLUSTER=1: 8-CTA cluster top-k for every row length; =4: 4-CTA clusters
+  static const int force_cluster = [] {
     const char* e = std::getenv("SFI_TOPK_CLUSTER");
-    return e && e[0] == '1';
+    return e ? std::atoi(e) : 0;
   }();
   if (n_max <= kTopkCtaMax && !force_cluster) {
     const size_t smem = (size_t)std::max(n_max, 1) * sizeof(uint32_t);
@@ -1418,16 +1443,16 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
     if (e != cudaSuccess) return e;
     return launch_k(sel_topk_cta_kernel<kExp>, dim3(rows), dim3(kTopkCtaT), smem, st, p);
   }
-  const int chunk = (n_max + kCS - 1) / kCS;
-  const dim3 gc(kCS, (unsigned)rows);
+  const int cs = (force_cluster == 4) ? 4 : kCS;
+  const int chunk = (n_max + cs - 1) / cs;
+  const dim3 gc(cs, (unsigned)rows);
   if (chunk <= kTopkSmemKeys) {
     const size_t smem = (size_t)std::max(chunk, 1) * sizeof(unsigned long long);
-    cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(sel_topk_kernel<kExp, true>),
-                                        kTopkSmemKeys * (int)sizeof(unsigned long long));
-    if (e != cudaSuccess) return e;
-    return launch_k(sel_topk_kernel<kExp, true>, gc, dim3(kT), smem, st, p);
+    return cs == 4 ? launch_topk_cluster<sel_topk_kernel<kExp, true, 4>>(gc, smem, 4, st, p)
+                   : launch_topk_cluster<sel_topk_kernel<kExp, true, kCS>>(gc, smem, kCS, st, p);
   }
-  return launch_k(sel_topk_kernel<kExp, false>, gc, dim3(kT), 0, st, p);
+  return cs == 4 ? launch_topk_cluster<sel_topk_kernel<kExp, false, 4>>(gc, 0, 4, st, p)
+                 : launch_topk_cluster<sel_topk_kernel<kExp, false, kCS>>(gc, 0, kCS, st, p);
 }
 
 // ---------------------------------------------------------------------------
