@@ -184,7 +184,8 @@ __device__ __noinline__ void merge_slice(const DecodeParams& p, float* outp, flo
                                          int c_last, int T, int Gc, int lane) {
   constexpr int kCols = D / 32;
   constexpr int kGB = G < 4 ? G : 4;
-  constexpr int kCB = 4;  // contributors per load batch
+  // contributors per load batch: as many loads in flight as the registers allow
+  constexpr int kCB = kGB <= 1 ? 16 : (kGB == 2 ? 8 : 4);
   constexpr int PR = part_rows<G>();
   using Vec = typename std::conditional<kCols == 4, float4, float2>::type;
 #pragma unroll
