@@ -257,8 +257,8 @@ class Workload:
         """Our kernels per step (collectives' own kernels not counted)."""
         if not slow:  # advance + one fused launch per layer (+ the LSE merge when sequence-sharded)
             return 1 + self.L * (2 if self.mode == "seq" else 1)
-        if self.mode == "seq":  # append (last rank), dense + merge, Selector 3 stats + finish 3 + pick 3, compact
-            return 1 + self.L * (1 + 2 + 9 + 1)
+        if self.mode == "seq":  # append (last rank), dense + merge, Selector 2 stats + finish 3 + pick 3, compact
+            return 1 + self.L * (1 + 2 + 8 + 1)
         if self.mode == "heads":  # append, dense, Selector fuse + refine + top-k, compact
             return 1 + self.L * 6
         return 1 + self.L * 7  # append, dense, Selector pw + coef + z + top-k, compact

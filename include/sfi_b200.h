@@ -268,10 +268,13 @@ SFI_API int sfi_fast_decode_partial(const sfi_shape* shape, const sfi_cache* cac
  * all-gathered partials: o_parts [n_parts][rows][head_dim], lse [n_parts][rows]). */
 SFI_API int sfi_merge_partials(int32_t n_parts, int32_t rows, int32_t head_dim, const float* o_parts,
                                const float* lse_parts, float* out, void* stream);
-/* Sequence-sharded Selector, decode path (W = 1, alpha = 1), per layer:
- *   stats phase 1 -> row_max [B*H]      ; all-reduce MAX over ranks
- *   stats phase 2 -> row_sums [B*H][5]  ; all-reduce SUM   (sum p, w, p^2, pw, w^2)
- *   stats phase 3 -> z_base + edges [B*H][2R+2] (sfi_seq_edges_doubles) ; all-gather
+/* Sequence-sharded Selector, decode path (W = 1, alpha = 1), per layer, three
+ * exchanges:
+ *   stats phase 1 -> row_stats [B*H][6]: local max and the five sums of
+ *                    p = exp(v - local max), w, p^2, pw, w^2 ; all-gather -> stats_all
+ *   stats phase 3 -> sums rescaled to the global max (shard order), p recomputed
+ *                    as exp(v - global max) from the same logits, z_base + edges
+ *                    [B*H][2R+2] (sfi_seq_edges_doubles) ; all-gather
  *   finish: soft-NMS with the neighbours' edges, cross-head (all heads local),
  *           local top-k -> candidates (z_adj, global position) [B*H][k_budget] ; all-gather
  *   pick: global top-k of the P candidate lists (shard order = position order,
@@ -282,7 +285,8 @@ SFI_API size_t sfi_seq_edges_doubles(const sfi_shape* shape, const sfi_selector_
 SFI_API int sfi_seq_selector_stats(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
                                    const float* pooled_logits, const sfi_selector_params* params,
                                    const int32_t* j_off, const int32_t* n_glob, int32_t phase,
-                                   double* row_max, double* row_sums, double* edges, void* stream);
+                                   double* row_stats, const double* stats_all, int32_t n_shards,
+                                   double* edges, void* stream);
 SFI_API int sfi_seq_selector_finish(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
                                     const sfi_selector_params* params, const int32_t* j_off,
                                     const int32_t* n_glob, const double* edges_all, int32_t n_shards,

@@ -347,12 +347,12 @@ PYBIND11_MODULE(_sfi_b200, m) {
   m.def("seq_pick_scratch_bytes", [](const sfi_shape& s, int n_shards) { return sfi_seq_pick_scratch_bytes(&s, n_shards); });
   m.def("seq_selector_stats", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
                                  const sfi_selector_params& prm, std::uintptr_t j_off, std::uintptr_t n_glob, int phase,
-                                 std::uintptr_t row_max, std::uintptr_t row_sums, std::uintptr_t edges,
+                                 std::uintptr_t row_stats, std::uintptr_t stats_all, int n_shards, std::uintptr_t edges,
                                  std::uintptr_t stream) {
     check(sfi_seq_selector_stats(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm,
                                  static_cast<const int32_t*>(vp(j_off)), static_cast<const int32_t*>(vp(n_glob)), phase,
-                                 static_cast<double*>(vp(row_max)), static_cast<double*>(vp(row_sums)),
-                                 static_cast<double*>(vp(edges)), vp(stream)));
+                                 static_cast<double*>(vp(row_stats)), static_cast<const double*>(vp(stats_all)),
+                                 n_shards, static_cast<double*>(vp(edges)), vp(stream)));
   });
   m.def("seq_selector_finish", [](const sfi_shape& s, const sfi_cache& c, int layer, const sfi_selector_params& prm,
                                   std::uintptr_t j_off, std::uintptr_t n_glob, std::uintptr_t edges_all, int n_shards,

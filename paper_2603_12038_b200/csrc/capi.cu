@@ -652,17 +652,18 @@ SFI_API size_t sfi_seq_edges_doubles(const sfi_shape* s, const sfi_selector_para
 
 SFI_API int sfi_seq_selector_stats(const sfi_shape* s, const sfi_cache* c, int32_t layer,
                                    const float* pooled_logits, const sfi_selector_params* prm,
-                                   const int32_t* j_off, const int32_t* n_glob, int32_t phase, double* row_max,
-                                   double* row_sums, double* edges, void* stream) {
+                                   const int32_t* j_off, const int32_t* n_glob, int32_t phase, double* row_stats,
+                                   const double* stats_all, int32_t n_shards, double* edges, void* stream) {
   g_launches = 0;
   int rc = seq_selector_check(s, c, layer, prm);
   if (rc) return rc;
-  if (phase < 1 || phase > 3) return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_stats: phase 1..3");
-  if (!j_off || !n_glob || !row_max || !row_sums || (phase == 3 && !edges) || (phase < 3 && !pooled_logits))
+  if (phase != 1 && phase != 3) return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_stats: phase 1 or 3");
+  if (!j_off || !n_glob || !row_stats || !pooled_logits ||
+      (phase == 3 && (!stats_all || !edges || n_shards < 1)))
     return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_stats: null argument");
   sfi_impl::Workspace ws = sfi_impl::carve_workspace(*s, c->workspace);
   SFI_CUDA(sfi_impl::launch_seq_selector_stats(*s, *c, layer, pooled_logits, *prm, ws.sel, j_off, n_glob, phase,
-                                               row_max, row_sums, edges, (cudaStream_t)stream),
+                                               row_stats, stats_all, n_shards, edges, (cudaStream_t)stream),
            "sfi_seq_selector_stats");
   g_launches = 1;
   return SFI_OK;

@@ -135,8 +135,8 @@ cudaError_t launch_merge_partials(int n_parts, int rows, int D, const float* o_p
                                   float* out, cudaStream_t st);
 cudaError_t launch_seq_selector_stats(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
                                       const sfi_selector_params& prm, const SelectorScratch& scr,
-                                      const int32_t* j_off, const int32_t* n_glob, int phase, double* row_max,
-                                      double* row_sums, double* edges, cudaStream_t st);
+                                      const int32_t* j_off, const int32_t* n_glob, int phase, double* row_stats,
+                                      const double* stats_all, int n_shards, double* edges, cudaStream_t st);
 cudaError_t launch_seq_selector_finish(const sfi_shape& s, const sfi_cache& c, int layer,
                                        const sfi_selector_params& prm, const SelectorScratch& scr,
                                        const int32_t* j_off, const int32_t* n_glob, const double* edges_all,

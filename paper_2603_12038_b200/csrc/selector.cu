@@ -99,9 +99,10 @@ struct SelParams {
   // [j_off[b], j_off[b] + n) of the global J of n_glob[b] positions
   const int32_t* j_off;
   const int32_t* n_glob;
-  int seq_phase;            // 1 = local row max, 2 = local sums, 3 = z_base + edges (0 = unsharded)
-  double* row_max;          // [rows]       (phase 1 out, phase 2 in: all-reduced MAX)
-  double* row_sums;         // [rows][5]    (phase 2 out, phase 3 in: all-reduced SUM)
+  int seq_phase;            // 1 = local statistics, 3 = z_base + edges (0 = unsharded)
+  double* row_stats;        // [rows][6] this shard's (max, sum p, sum w, sum p^2, sum pw, sum w^2),
+                            //   p relative to the local max (phase 1 out, phase 3 in)
+  const double* stats_all;  // [n_shards][rows][6] all-gathered row_stats (phase 3 in)
   double* edges;            // [rows][2R+2] (phase 3 out): first R, last R z_base values, j_off, n
   const double* edges_all;  // [n_shards][rows][2R+2] all-gathered edges (refine halo)
   int n_shards;
@@ -254,8 +255,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
   const int ph = p.seq_phase;
   if (n <= 0) {  // uniform over the cluster
     if (ph != 0 && rank == 0) {  // sequence shard without J positions: neutral stats
-      if (ph == 1 && threadIdx.x == 0) p.row_max[row] = kMaskedLogit;
-      if (ph == 2 && threadIdx.x < 5) p.row_sums[row * 5 + threadIdx.x] = 0.0;
+      if (ph == 1 && threadIdx.x < 6) p.row_stats[row * 6 + threadIdx.x] = threadIdx.x == 0 ? kMaskedLogit : 0.0;
       if (ph == 3) write_edges(p, row, nullptr, 0, src);
     }
     return;
@@ -269,7 +269,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
 
   // pass 1: row max (starts at kMaskedLogit), finite check
   double m1[1] = {kMaskedLogit};
-  if (ph >= 2) goto after_max;  // sequence shard: the max was all-reduced
+  if (ph == 3) goto after_max;  // sequence shard: w and the statistics come from phase 1
   {
   bool bad = false;
   for (int j = lo + threadIdx.x; j < hi; j += kT) {
@@ -280,20 +280,16 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kT, 2)
   if (bad) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
   cluster_reduce<1>(m1, 1, wbuf, red, par, cl, OpMax());
   }
-  if (ph == 1) {
-    if (rank == 0 && threadIdx.x == 0) p.row_max[row] = m1[0];
-    cl.sync();
-    return;
-  }
 after_max:
-  const double mx = ph >= 2 ? p.row_max[row] : m1[0];
+  // (phase 3 of a sequence shard: this shard's local max from its phase 1)
+  const double mx = ph == 3 ? p.row_stats[row * 6] : m1[0];
 
   // pass 2: p, w and the five sums
   const double denom_u = src.u_denom();
   double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   bool badn = false;
   constexpr int kU = 2;  // loads of kU iterations are issued before any use
-  // (a sequence shard's phase 3 reuses the p, w of its phase 2)
+  // (a sequence shard's phase 3 reuses the w of its phase 1)
   for (int j0 = (ph == 3 ? hi : lo + threadIdx.x); j0 < hi; j0 += kU * kT) {
     double vv[kU], nn[kU];
 #pragma unroll
@@ -322,14 +318,29 @@ after_max:
     }
   }
   if (badn) raise_error(p.err, SFI_ERR_NON_FINITE_INPUT);
+  double mg = mx;  // the global row max (sequence shard: the max over the gathered local maxima)
   if (ph == 3) {
+    // the shards' statistics, rescaled to the global row max in shard order
+    const int rows = p.B * p.H;
+    double M = kMaskedLogit;
+    for (int sh = 0; sh < p.n_shards; ++sh) M = smax(M, p.stats_all[((size_t)sh * rows + row) * 6]);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) s[k] = p.row_sums[row * 5 + k];  // all-reduced over the shards
+    for (int k = 0; k < 5; ++k) s[k] = 0.0;
+    for (int sh = 0; sh < p.n_shards; ++sh) {
+      const double* x = p.stats_all + ((size_t)sh * rows + row) * 6;
+      const double e = exp(x[0] - M);
+      s[0] += x[1] * e;
+      s[1] += x[2];
+      s[2] += x[3] * (e * e);
+      s[3] += x[4] * e;
+      s[4] += x[5];
+    }
+    mg = M;
   } else {
     cluster_reduce<5>(s, 5, wbuf, red, par, cl, OpSum());
   }
-  if (ph == 2) {
-    if (rank == 0 && threadIdx.x < 5) p.row_sums[row * 5 + threadIdx.x] = s[threadIdx.x];
+  if (ph == 1) {
+    if (rank == 0 && threadIdx.x < 6) p.row_stats[row * 6 + threadIdx.x] = threadIdx.x == 0 ? mx : s[threadIdx.x - 1];
     cl.sync();
     return;
   }
@@ -354,7 +365,12 @@ after_max:
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int j = j0 + u * kT;
-      pa[u] = j < hi ? A[j] : 0.0;
+      if (ph == 3) {  // p = exp(v - global max), the same bits as the unsharded pass 2
+        const double v = j < hi ? src.logit(row, 0, j) : kMaskedLogit;
+        pa[u] = (v <= kMaskedLogit) ? 0.0 : exp(v - mg);
+      } else {
+        pa[u] = j < hi ? A[j] : 0.0;
+      }
       wb[u] = j < hi ? Bw[j] : 0.0;
     }
 #pragma unroll
@@ -1667,12 +1683,13 @@ SelParams seq_params(const sfi_shape& s, const sfi_cache& c, int layer, const fl
 
 cudaError_t launch_seq_selector_stats(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,
                                       const sfi_selector_params& prm, const SelectorScratch& scr,
-                                      const int32_t* j_off, const int32_t* n_glob, int phase, double* row_max,
-                                      double* row_sums, double* edges, cudaStream_t st) {
+                                      const int32_t* j_off, const int32_t* n_glob, int phase, double* row_stats,
+                                      const double* stats_all, int n_shards, double* edges, cudaStream_t st) {
   SelParams p = seq_params(s, c, layer, logits, prm, scr, j_off, n_glob);
   p.seq_phase = phase;
-  p.row_max = row_max;
-  p.row_sums = row_sums;
+  p.row_stats = row_stats;
+  p.stats_all = stats_all;
+  p.n_shards = n_shards;
   p.edges = edges;
   const dim3 gc(kCS, (unsigned)(s.batch * s.n_kv_heads));
   return launch_k(sel_fuse_fast_kernel<false>, gc, dim3(kT), 0, st, p);

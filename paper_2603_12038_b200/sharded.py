@@ -84,17 +84,6 @@ class HeadShardedSfi:
 # ---------------------------------------------------------------------------
 # Sequence sharding (config C4: 256K context, too few KV heads to split)
 
-def all_reduce_(t: torch.Tensor, op, group=None) -> torch.Tensor:
-    """In-place all-reduce; gloo (CPU tests) stages CUDA tensors through host memory."""
-    if dist.get_backend(group) == "nccl" or not t.is_cuda:
-        dist.all_reduce(t, op=op, group=group)
-        return t
-    h = t.cpu()
-    dist.all_reduce(h, op=op, group=group)
-    t.copy_(h)
-    return t
-
-
 def seq_block(prompt_len: int, world: int) -> int:
     """Positions per non-last shard: the prompt split evenly; decode tokens
     land on the last shard."""
@@ -107,6 +96,9 @@ class SeqShardedSfi:
     request, all KV heads. Per layer, slow steps exchange the Selector's row
     statistics (max, 5 sums), soft-NMS edges and top-k candidates; every step
     exchanges the (O, LSE) attention partials, merged in rank order.
+    Slow steps add three exchanges per layer: the Selector's row statistics
+    (local max + five sums, rescaled to the global max on arrival), the
+    soft-NMS edges and the top-k candidates.
 
     The collective steps are separate methods so a single process can drive
     P shards in lockstep (tests); `selector`, `dense_decode` and `fast_decode`
@@ -141,8 +133,8 @@ class SeqShardedSfi:
         self.params = _C.SelectorParams()
         ne = _C.seq_edges_doubles(self.cache.shape, self.params)
         f64 = torch.float64
-        self.row_max = z(B * H, dt=f64)
-        self.row_sums = z(B * H * 5, dt=f64)
+        self.row_stats = z(B * H * 6, dt=f64)
+        self.stats_all = z(P, B * H * 6, dt=f64)
         self.edges = z(ne, dt=f64)
         self.edges_all = z(P, ne, dt=f64)
         self.cand_score, self.cand_pos = z(B * H * K, dt=f64), z(B * H * K)
@@ -217,11 +209,13 @@ class SeqShardedSfi:
 
     # -- Selector phases ---------------------------------------------------------
     def sel_stats(self, layer, logits, phase, params=None):
+        """phase 1: local row statistics (max, five sums relative to it) -> row_stats;
+        phase 3: z_base from the all-gathered statistics + soft-NMS edges."""
         c = self.cache
-        self._C.seq_selector_stats(c.shape, c.cache, layer, c._ptr(logits, torch.float32) if logits is not None else 0,
+        self._C.seq_selector_stats(c.shape, c.cache, layer, c._ptr(logits, torch.float32),
                                    params or self.params, self.j_off.data_ptr(), self.n_glob.data_ptr(), phase,
-                                   self.row_max.data_ptr(), self.row_sums.data_ptr(), self.edges.data_ptr(),
-                                   c._stream())
+                                   self.row_stats.data_ptr(), self.stats_all.data_ptr(), self.world,
+                                   self.edges.data_ptr(), c._stream())
 
     def sel_finish(self, layer, params=None):
         c = self.cache
@@ -236,11 +230,10 @@ class SeqShardedSfi:
                                   self.pick_scratch.data_ptr(), c._stream())
 
     def selector(self, layer, logits, params=None):
+        # three exchanges per layer: row statistics, soft-NMS edges, top-k candidates
         self.sel_stats(layer, logits, 1, params)
-        all_reduce_(self.row_max, dist.ReduceOp.MAX, self.group)
-        self.sel_stats(layer, logits, 2, params)
-        all_reduce_(self.row_sums, dist.ReduceOp.SUM, self.group)
-        self.sel_stats(layer, None, 3, params)
+        all_gather_blocks(self.row_stats, self.stats_all, self.group)
+        self.sel_stats(layer, logits, 3, params)
         all_gather_blocks(self.edges, self.edges_all, self.group)
         self.sel_finish(layer, params)
         all_gather_blocks(self.cand_score, self.cand_score_all, self.group)

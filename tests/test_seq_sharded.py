@@ -7,7 +7,8 @@ the unsharded cache on the same rows:
     merge) identical to the 1-GPU Selector on the same logits.
 The CPU test runs the same exchange protocol over gloo (world 2 and 3) with a
 numpy restatement of the decode Selector as the per-shard compute, against the
-reference Selector.
+reference Selector: local statistics -> all-gather -> global rescale, soft-NMS
+edges -> all-gather, top-k candidates -> all-gather -> pick.
 """
 from __future__ import annotations
 
@@ -25,16 +26,6 @@ from helpers import oracle, rel_err
 TOL = 2e-3
 
 
-def _emulate(shards, attr, op):
-    ts = [getattr(s, attr) for s in shards]
-    if op == "max":
-        r = torch.stack(ts).max(0).values
-    elif op == "sum":
-        r = torch.stack(ts).sum(0)
-    for t in ts:
-        t.copy_(r)
-
-
 def _gather(shards, src, dst):
     g = torch.stack([getattr(s, src) for s in shards])
     for s in shards:
@@ -44,12 +35,9 @@ def _gather(shards, src, dst):
 def _selector(shards, layer, logits_of):
     for s in shards:
         s.sel_stats(layer, logits_of(s), 1)
-    _emulate(shards, "row_max", "max")
+    _gather(shards, "row_stats", "stats_all")
     for s in shards:
-        s.sel_stats(layer, logits_of(s), 2)
-    _emulate(shards, "row_sums", "sum")
-    for s in shards:
-        s.sel_stats(layer, None, 3)
+        s.sel_stats(layer, logits_of(s), 3)
     _gather(shards, "edges", "edges_all")
     for s in shards:
         s.sel_finish(layer)
@@ -251,23 +239,28 @@ def _seq_protocol_worker(rank, world, port, cuts, q):
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         from oracle import oracle as O
-        from paper_2603_12038_b200.sharded import all_gather_blocks, all_reduce_
+        from paper_2603_12038_b200.sharded import all_gather_blocks
 
         vals, norms, allowed = _np_case()
         H, ng = vals.shape
         K, R, eps = 300, 2, 1e-8
         a, b = cuts[rank], cuts[rank + 1]
         v, nm, n = vals[:, a:b], norms[:, a:b], b - a
-        # phase 1: row max (from kMaskedLogit), all-reduce MAX
-        mx = torch.from_numpy(np.maximum(v.max(1) if n else -1e30, -1e30).astype(np.float64))
-        all_reduce_(mx, dist.ReduceOp.MAX)
-        # phase 2: p, prior w, five sums, all-reduce SUM
+        # phase 1: local max (from kMaskedLogit) and the five sums relative to it
+        ml = np.maximum(v.max(1) if n else -1e30, -1e30).astype(np.float64)
         u = (np.arange(a, b) / ((ng - 1) + eps))[None, :]
-        p = np.exp(v - mx.numpy()[:, None])
+        pl = np.exp(v - ml[:, None])
         w = (1.0 / (nm + eps)) * np.exp(-(u * u)) * np.sqrt(1.0 - u + eps)
-        sums = torch.from_numpy(np.stack([p.sum(1), w.sum(1), (p * p).sum(1), (p * w).sum(1), (w * w).sum(1)], 1))
-        all_reduce_(sums, dist.ReduceOp.SUM)
-        S = sums.numpy()
+        st = np.stack([ml, pl.sum(1), w.sum(1), (pl * pl).sum(1), (pl * w).sum(1), (w * w).sum(1)], 1)
+        stats_all = torch.zeros(world, H, 6, dtype=torch.float64)
+        all_gather_blocks(torch.from_numpy(st), stats_all)
+        # combine in shard order, rescaled to the global max
+        SA = stats_all.numpy()
+        M = SA[:, :, 0].max(0)
+        e = np.exp(SA[:, :, 0] - M[None, :])
+        S = np.stack([(SA[:, :, 1] * e).sum(0), SA[:, :, 2].sum(0), (SA[:, :, 3] * e * e).sum(0),
+                      (SA[:, :, 4] * e).sum(0), SA[:, :, 5].sum(0)], 1)
+        p = np.exp(v - M[:, None])  # phase 3 recomputes p against the global max
         c1, c2 = 1.0 / S[:, 0], 1.0 / S[:, 1]
         ff, fr, rr = S[:, 2] * c1 * c1, S[:, 3] * c1 * c2, S[:, 4] * c2 * c2
         den = ff - 2 * fr + rr
