@@ -130,6 +130,27 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Special registers read with volatile asm: never CSE'd into a spilled value.
+__device__ __forceinline__ unsigned sreg_cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned sreg_cluster_nctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned sreg_ctaid_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned sreg_tid_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ unsigned smid() {
   unsigned s;
   asm volatile("mov.u32 %0, %smid;" : "=r"(s));

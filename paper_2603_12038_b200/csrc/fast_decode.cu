@@ -28,9 +28,12 @@
 //     (L-1) % R, fp64 norm — bit-identical to sfi_ring_append) and contributes
 //     the token's key as one more softmax partial; the ring slot's stale row is
 //     masked out of the tiles, so no CTA ever reads a row this kernel writes;
-//   * merge: every CTA leaves its 5 partials (m, l, O) in its own shared memory;
-//     after one cluster barrier each CTA merges a 1/C share of the G x D
-//     outputs reading all partials over DSMEM (fixed order: deterministic).
+//   * merge: each CTA combines its 5 partials (m, l, O) locally, then PUSHES
+//     the combined partial to the owners (float4 remote shared-memory stores
+//     into a dedicated receive area; owner r merges a warp-aligned 1/C share
+//     of the G x D outputs); one release/acquire cluster barrier, then every
+//     owner merges from its own shared memory (fixed order: deterministic).
+//     No exit barrier: after the publish barrier no CTA touches a peer.
 #include <cooperative_groups.h>
 #include <cuda.h>
 
@@ -65,13 +68,23 @@ struct FGeo {
 
 template <int D, int G>
 struct FPart {  // partials, written over the (drained) stage ring
-  static constexpr int kO = kParts * G * D;       // floats
-  static constexpr int kBytes = (kO + 2 * kParts * G + 2 * G) * 4;
+  static constexpr int kPD = D + 8;               // row stride: the mma-layout stores hit 8 rows at once
+  static constexpr int kO = kParts * G * kPD;     // floats
+  static constexpr int kBytes = (kO + 3 * kParts * G + 2 * G) * 4;
   static_assert(kBytes <= FGeo<D>::kRing, "partials must fit in the stage ring");
 };
-template <int D>
-constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row
-  return FGeo<D>::kRing + 64 + D * 8;
+// Merge receive area (dedicated: CTAs push into it while the owner may still be
+// streaming): [C][share] combined O + [C][G] m + [C][G] l, share <= G*D/C + 32.
+template <int D, int G>
+struct FRecv {
+  static constexpr int kFloats = G * D + 32 * 16 + 2 * 16 * G;
+};
+template <int D, int G>
+constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row | receive area
+  return FGeo<D>::kRing + 64 + D * 8 + FRecv<D, G>::kFloats * 4;
+}
+__host__ __device__ constexpr int merge_share(int G, int D, int C) {  // whole warps of 32 elements
+  return ((G * D + C - 1) / C + 31) & ~31;
 }
 
 template <int D>
@@ -79,10 +92,23 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
   return base + (chunk >> 3) * FGeo<D>::kBoxBytes + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
 }
 
-__device__ __forceinline__ void cluster_sync_all() {
+// Phase 1: the pushed partials (remote shared-memory stores) are performed
+// before the arrival (release), read after the wait (acquire). After it no CTA
+// touches a peer's shared memory, so there is no exit barrier.
+__device__ __forceinline__ void cluster_publish() {
   __syncwarp();
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Phase 0 of the cluster barrier: every CTA arrives when it starts and waits
+// just before its first remote store, so no CTA writes into a peer that has not
+// started.
+__device__ __forceinline__ void cluster_arrive_started() {
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_started() {
+  __syncwarp();
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
 // Tile t of a slice (ring tiles first) -> first compact row.
@@ -91,34 +117,138 @@ __device__ __forceinline__ int tile_row(int t, int t_ring, int R) {
 }
 
 // CTA-local combine of the kParts warp partials (160 threads: consumers + aux):
-// O into part 0 in place (each element touched by one thread), (m, l) into
-// comb_m / comb_l. Ends with the CTA-local barrier 1.
+// first the per-head (M, scales, L) — G threads, written to comb_m / comb_l /
+// part_s — then O into part 0 in place, four elements per thread per pass.
 template <int D, int G>
 __device__ __forceinline__ void combine_cta(float* part_o, const float* part_m, const float* part_l,
-                                            float* comb_m, float* comb_l, int tid) {
+                                            float* comb_m, float* comb_l, float* part_s, int tid) {
   constexpr int kT = (kNcw + 1) * 32;
-  for (int e = tid; e < G * D; e += kT) {
-    const int g = e / D;
+  constexpr int kPD = FPart<D, G>::kPD;
+  if (tid < G) {
     float m[kParts], M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kParts; ++w) {
-      m[w] = part_m[w * G + g];
+      m[w] = part_m[w * G + tid];
       M = fmaxf(M, m[w]);
     }
     const float Mu = (M == -INFINITY) ? 0.f : M;
-    float Ls = 0.f, Os = 0.f;
+    float Ls = 0.f;
 #pragma unroll
     for (int w = 0; w < kParts; ++w) {
-      const float l = part_l[w * G + g];
-      const float sc = l > 0.f ? fast_exp2(m[w] - Mu) : 0.f;
+      const float l = part_l[w * G + tid];
+      const float sc = l > 0.f ? fast_exp2(m[w] - Mu) : 0.f;  // l == 0: partial O is zero
+      part_s[w * G + tid] = sc;
       Ls += l * sc;
-      Os += (l > 0.f ? part_o[w * G * D + e] : 0.f) * sc;
     }
-    part_o[e] = Os;
-    if (e % D == 0) {
-      comb_m[g] = M;
-      comb_l[g] = Ls;
+    comb_m[tid] = M;
+    comb_l[tid] = Ls;
+  }
+  named_bar_sync<3, kT>();
+#pragma unroll 2
+  for (int e = tid * 4; e < G * D; e += kT * 4) {
+    const int g = e / D;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < kParts; ++w) {
+      const float sc = part_s[w * G + g];
+      const float4 x = *reinterpret_cast<const float4*>(part_o + (w * G + g) * kPD + (e - g * D));
+      acc.x = fmaf(x.x, sc, acc.x);
+      acc.y = fmaf(x.y, sc, acc.y);
+      acc.z = fmaf(x.z, sc, acc.z);
+      acc.w = fmaf(x.w, sc, acc.w);
     }
+    *reinterpret_cast<float4*>(part_o + g * kPD + (e - g * D)) = acc;
+  }
+}
+
+// Push this CTA's combined partial to the owners (160 threads, after
+// combine_cta): owner r merges elements [r*share, (r+1)*share) and receives, in
+// slot `rank`, this CTA's O for them (float4 remote stores) and (m, l) of their
+// heads.
+template <int D, int G>
+__device__ __forceinline__ void push_partials(const cg::cluster_group& cl, const float* part_o, const float* comb_m,
+                                              const float* comb_l, float* recv_o, float* recv_m, float* recv_l,
+                                              int share, int rank, int tid) {
+  constexpr int kT = (kNcw + 1) * 32;
+  constexpr int kPD = FPart<D, G>::kPD;
+  named_bar_sync<3, kT>();  // combined O complete (phase 0 was waited for before griddep_wait)
+  for (int e = tid * 4; e < G * D; e += kT * 4) {
+    const int r = e / share;  // share is a multiple of 32: a float4 never straddles owners
+    const int g = e / D;
+    const float4 v = *reinterpret_cast<const float4*>(part_o + g * kPD + (e - g * D));
+    *cl.map_shared_rank(reinterpret_cast<float4*>(recv_o + rank * share + (e - r * share)), r) = v;
+  }
+  if (tid < G) {
+    const int r0 = (tid * D) / share, r1 = ((tid + 1) * D - 1) / share;
+    for (int r = r0; r <= r1; ++r) {
+      *cl.map_shared_rank(recv_m + rank * G + tid, r) = comb_m[tid];
+      *cl.map_shared_rank(recv_l + rank * G + tid, r) = comb_l[tid];
+    }
+  }
+}
+
+// After the publish barrier (whose acquire invalidates L1, where register
+// spills live) everything is re-derived from special registers, kernel
+// parameters and shared memory, so the merge issues no local-memory reloads.
+template <int D, int G>
+__device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem) {
+  const int C = (int)sreg_cluster_nctarank();
+  const int rank = (int)sreg_cluster_ctarank();
+  const int tid = (int)sreg_tid_x();
+  const int warp = tid >> 5, lane = tid & 31;
+  const int s = (int)sreg_ctaid_x() / C;
+  const int b = s / p.H, h = s % p.H;
+  const int share = merge_share(G, D, C);
+  const float* recv_o = reinterpret_cast<const float*>(smem + FGeo<D>::kRing + 64 + D * 8);
+  const float* recv_m = recv_o + G * D + 32 * 16;
+  const float* recv_l = recv_m + 16 * G;
+  const bool ok = *reinterpret_cast<const int*>(smem + FGeo<D>::kRing + 48) != 0;
+  long long* trace = p.trace ? p.trace + (size_t)sreg_ctaid_x() * 16 : nullptr;
+  if (trace && tid == 0) trace[13] = (long long)globaltimer();
+  const long long c_merge0 = clock64();
+
+  // ---- merge: this CTA's share of the G x D outputs over the C pushed partials ----
+  // Shares are whole warps of 32 elements of one head: lane c reads CTA c's
+  // (m, l) of that head (shuffled to the warp), each lane its element's C
+  // partial O values; fixed order over c: deterministic.
+  const int total = G * D;
+  const int e0 = rank * share, e1 = min(total, e0 + share);
+  float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
+  for (int eb = e0 + warp * 32; eb < e1; eb += kNcw * 32) {  // warp-uniform
+    const int gg = eb / D;
+    const int e = eb + lane;
+    float mc = -INFINITY, lc = 0.f, oc[16];
+    if (lane < C) {
+      mc = recv_m[lane * G + gg];
+      lc = recv_l[lane * G + gg];
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c < C) oc[c] = recv_o[c * share + (e - e0)];
+    float M = mc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float Mu = (M == -INFINITY) ? 0.f : M;
+    const float sc = lc > 0.f ? fast_exp2(mc - Mu) : 0.f;  // l == 0: that CTA's O is zero
+    float Ls = lc * sc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
+    float Os = 0.f;
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c < C) Os = fmaf(oc[c], __shfl_sync(0xffffffffu, sc, c), Os);
+    outp[e] = Ls > 0.f ? Os / Ls : 0.f;
+    if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
+      if (lane == 0 && e % D == 0)
+        p.lse[(size_t)b * p.Hq + (size_t)h * G + gg] = Ls > 0.f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
+    } else if (rank == 0 && e == 0 && ok && !(Ls > 0.f)) {
+      raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+    }
+  }
+  if (trace && tid == 0) {
+    trace[7] = clock64() - c_merge0;  // merge cycles
+    trace[14] = (long long)globaltimer();
+    trace[3] = (long long)globaltimer();
   }
 }
 
@@ -133,12 +263,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + FGeo<D>::kRing);
   uint64_t* empty = full + kStages;
-  float* part_o = reinterpret_cast<float*>(smem);        // [kParts][G][D] (after the stream)
+  constexpr int kPD = FPart<D, G>::kPD;
+  float* part_o = reinterpret_cast<float*>(smem);        // [kParts][G][kPD] (after the stream)
   float* part_m = part_o + FPart<D, G>::kO;              // [kParts][G]
   float* part_l = part_m + kParts * G;                   // [kParts][G]
   float* comb_m = part_l + kParts * G;                   // [G] CTA-combined (m, l);
   float* comb_l = comb_m + G;                            //     O combined in place in part 0
+  float* part_s = comb_l + G;                            // [kParts][G] combine scales
   double* ksq = reinterpret_cast<double*>(smem + FGeo<D>::kRing + 64);  // [D] k_c^2 (aux)
+  float* recv_o = reinterpret_cast<float*>(smem + FGeo<D>::kRing + 64 + D * 8);  // [C][share]
+  float* recv_m = recv_o + G * D + 32 * 16;                                      // [C][G]
+  float* recv_l = recv_m + 16 * G;                                               // [C][G]
 
   long long* trace = p.trace ? p.trace + (size_t)blockIdx.x * 16 : nullptr;
   if (trace && threadIdx.x == 0) {
@@ -172,7 +307,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int T = t_ring + (p.crows - p.R + kTile - 1) / kTile;
   const int tb = (int)(((long long)rank * T) / C), te = (int)(((long long)(rank + 1) * T) / C);
   const int row_base = (int)(slice_g * p.crows);
+  const int share = merge_share(G, D, C);
   __syncthreads();
+  cluster_arrive_started();  // phase 0: this CTA runs (its receive area may be written)
 
   if (warp == kNcw) {
     // ---------------- producer ----------------
@@ -199,11 +336,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (trace && lane == 0) trace[10] = (long long)globaltimer();
     griddep_wait();
     griddep_launch();
-    cluster_sync_all();  // partials published
-    cluster_sync_all();  // merge done: shared memory may be released
+    cluster_wait_started();
+    cluster_publish();  // partials pushed
     return;
   }
 
+  cluster_wait_started();  // off the critical path: under PDL this CTA waits for its predecessor anyway
   griddep_wait();
   griddep_launch();
   if (trace && threadIdx.x == 0) {
@@ -281,15 +419,16 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int g = 0; g < G; ++g) {
 #pragma unroll
-      for (int c = 0; c < kC; ++c) part_o[(kNcw * G + g) * D + lane * kC + c] = (lq[g] > 0.f) ? vv[c] : 0.f;
+      for (int c = 0; c < kC; ++c) part_o[(kNcw * G + g) * kPD + lane * kC + c] = (lq[g] > 0.f) ? vv[c] : 0.f;
       if (lane == 0) {
         part_m[kNcw * G + g] = mq[g];
         part_l[kNcw * G + g] = lq[g];
       }
     }
     named_bar_sync<2, (kNcw + 1) * 32>();  // all partials written
-    combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x - 32);
-    cluster_sync_all();
+    combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, part_s, (int)threadIdx.x - 32);
+    push_partials<D, G>(cl, part_o, comb_m, comb_l, recv_o, recv_m, recv_l, share, rank, (int)threadIdx.x - 32);
+    cluster_publish();
     // fp64 key norm: sequential over c in round-to-nearest ops (attention.cpp:
     // 143-150; bit-identical to append_kernel), off the critical path
     if (mine && lane == 0) {
@@ -298,8 +437,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int c = 0; c < D; ++c) acc = __dadd_rn(acc, ksq[c]);
       p.norms[slice_g * p.Lmax + (L - 1)] = __dsqrt_rn(acc);
     }
-    __syncwarp();
-    cluster_sync_all();
     return;
   }
 
@@ -494,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if constexpr (NH == 2) {
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
-      float* dst = part_o + (warp * G + g + 8 * hh) * D;
+      float* dst = part_o + (warp * G + g + 8 * hh) * kPD;
 #pragma unroll
       for (int n = 0; n < D / 8; ++n)
         *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(o[n][2 * hh], o[n][2 * hh + 1]);
@@ -504,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   } else if (g < G) {
-    float* dst = part_o + (warp * G + g) * D;
+    float* dst = part_o + (warp * G + g) * kPD;
 #pragma unroll
     for (int n = 0; n < D / 8; ++n)
       *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(o[n][0] + o[n][2], o[n][1] + o[n][3]);
@@ -514,53 +651,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   }
   named_bar_sync<2, (kNcw + 1) * 32>();  // all partials written
-  combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, (int)threadIdx.x);
-  cluster_sync_all();
-  if (trace && threadIdx.x == 0) trace[13] = (long long)globaltimer();
-
-  // ---- merge: this CTA's share of the G x D outputs over the C CTA partials ----
-  const int total = G * D;
-  const int share = (total + C - 1) / C;
-  const int e0 = rank * share, e1 = min(total, e0 + share);
-  float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
-  for (int e = e0 + (int)threadIdx.x; e < e1; e += kNcw * 32) {
-    const int gg = e / D;
-    float mc[8], lc[8], oc[8];
-    float M = -INFINITY;
-    for (int c0 = 0; c0 < C; c0 += 8) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c0 + c < C) M = fmaxf(M, *cl.map_shared_rank(comb_m + gg, c0 + c));
-    }
-    const float Mu = (M == -INFINITY) ? 0.f : M;
-    float Ls = 0.f, Os = 0.f;
-    for (int c0 = 0; c0 < C; c0 += 8) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c0 + c < C) {
-          mc[c] = *cl.map_shared_rank(comb_m + gg, c0 + c);
-          lc[c] = *cl.map_shared_rank(comb_l + gg, c0 + c);
-          oc[c] = *cl.map_shared_rank(part_o + e, c0 + c);
-        }
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c0 + c < C) {
-          const float sc = lc[c] > 0.f ? fast_exp2(mc[c] - Mu) : 0.f;
-          Ls += lc[c] * sc;
-          Os += (lc[c] > 0.f ? oc[c] : 0.f) * sc;
-        }
-    }
-    outp[e] = Ls > 0.f ? Os / Ls : 0.f;
-    if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
-      if (e % D == 0)
-        p.lse[(size_t)b * p.Hq + (size_t)h * G + gg] = Ls > 0.f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
-    } else if (rank == 0 && e == 0 && ok && !(Ls > 0.f)) {
-      raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
-    }
-  }
-  if (trace && threadIdx.x == 0) trace[14] = (long long)globaltimer();
-  cluster_sync_all();
-  if (trace && threadIdx.x == 0) trace[3] = (long long)globaltimer();
+  if (trace && threadIdx.x == 0) trace[11] = (long long)globaltimer();
+  combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, part_s, (int)threadIdx.x);
+  push_partials<D, G>(cl, part_o, comb_m, comb_l, recv_o, recv_m, recv_l, share, rank, (int)threadIdx.x);
+  if (trace && threadIdx.x == 0) trace[15] = (long long)globaltimer();
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(smem + FGeo<D>::kRing + 48) = ok;
+  const long long c_pub0 = clock64();
+  cluster_publish();
+  if (trace && threadIdx.x == 0) trace[4] = clock64() - c_pub0;  // publish barrier cycles
+  merge_pushed<D, G>(p, smem);
 }
 
 using FastFn = void (*)(CUtensorMap, CUtensorMap, FastParams);
@@ -589,11 +688,22 @@ int fast_cluster_size(int slices, int num_sms) {
   return c;
 }
 
+template <int D>
+int fast_smem(int G) {
+  switch (G) {
+    case 1: return fast_smem_bytes<D, 1>();
+    case 2: return fast_smem_bytes<D, 2>();
+    case 4: return fast_smem_bytes<D, 4>();
+    case 8: return fast_smem_bytes<D, 8>();
+    default: return fast_smem_bytes<D, 16>();
+  }
+}
+
 cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
                                int G, int C, cudaStream_t stream) {
   FastFn fn = (D == 64) ? pick<64>(G) : pick<128>(G);
   if (!fn || C < 1 || C > 16) return cudaErrorInvalidValue;
-  const int smem = D == 64 ? fast_smem_bytes<64>() : fast_smem_bytes<128>();
+  const int smem = D == 64 ? fast_smem<64>(G) : fast_smem<128>(G);
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(fn), smem, /*nonportable_cluster=*/true);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
