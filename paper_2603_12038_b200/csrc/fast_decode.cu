@@ -86,19 +86,19 @@ constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 
 __host__ __device__ constexpr int merge_share(int G, int D, int C) {  // whole warps of 32 elements
   return ((G * D + C - 1) / C + 31) & ~31;
 }
+// Bytes owner r receives: from each of the C CTAs its O over [e0, e1) and
+// (m, l) of every head that range touches.
+__host__ __device__ constexpr uint32_t merge_rx_bytes(int G, int D, int C, int r) {
+  const int share = merge_share(G, D, C);
+  const int e0 = r * share, e1 = (e0 + share < G * D) ? e0 + share : G * D;
+  return e1 > e0 ? (uint32_t)C * (uint32_t)((e1 - e0) * 4 + ((e1 - 1) / D - e0 / D + 1) * 8) : 0u;
+}
 
 template <int D>
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
   return base + (chunk >> 3) * FGeo<D>::kBoxBytes + row * 128 + (((chunk & 7) ^ (row & 7)) << 4);
 }
 
-// Phase 1: the pushed partials (remote shared-memory stores) are performed
-// before the arrival (release), read after the wait (acquire). After it no CTA
-// touches a peer's shared memory, so there is no exit barrier.
-__device__ __forceinline__ void cluster_publish() {
-  __syncwarp();
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 // Phase 0 of the cluster barrier: every CTA arrives when it starts and waits
 // just before its first remote store, so no CTA writes into a peer that has not
 // started.
@@ -166,30 +166,32 @@ __device__ __forceinline__ void combine_cta(float* part_o, const float* part_m, 
 // slot `rank`, this CTA's O for them (float4 remote stores) and (m, l) of their
 // heads.
 template <int D, int G>
-__device__ __forceinline__ void push_partials(const cg::cluster_group& cl, const float* part_o, const float* comb_m,
-                                              const float* comb_l, float* recv_o, float* recv_m, float* recv_l,
+__device__ __forceinline__ void push_partials(const float* part_o, const float* comb_m, const float* comb_l,
+                                              float* recv_o, float* recv_m, float* recv_l, uint64_t* rx_bar,
                                               int share, int rank, int tid) {
   constexpr int kT = (kNcw + 1) * 32;
   constexpr int kPD = FPart<D, G>::kPD;
   named_bar_sync<3, kT>();  // combined O complete (phase 0 was waited for before griddep_wait)
+  const uint32_t bar = smem_u32(rx_bar);
   for (int e = tid * 4; e < G * D; e += kT * 4) {
     const int r = e / share;  // share is a multiple of 32: a float4 never straddles owners
     const int g = e / D;
     const float4 v = *reinterpret_cast<const float4*>(part_o + g * kPD + (e - g * D));
-    *cl.map_shared_rank(reinterpret_cast<float4*>(recv_o + rank * share + (e - r * share)), r) = v;
+    st_async_v4(mapa_shared(smem_u32(recv_o + rank * share + (e - r * share)), r), v, mapa_shared(bar, r));
   }
   if (tid < G) {
     const int r0 = (tid * D) / share, r1 = ((tid + 1) * D - 1) / share;
     for (int r = r0; r <= r1; ++r) {
-      *cl.map_shared_rank(recv_m + rank * G + tid, r) = comb_m[tid];
-      *cl.map_shared_rank(recv_l + rank * G + tid, r) = comb_l[tid];
+      const uint32_t rb = mapa_shared(bar, r);
+      st_async_f32(mapa_shared(smem_u32(recv_m + rank * G + tid), r), comb_m[tid], rb);
+      st_async_f32(mapa_shared(smem_u32(recv_l + rank * G + tid), r), comb_l[tid], rb);
     }
   }
 }
 
-// After the publish barrier (whose acquire invalidates L1, where register
-// spills live) everything is re-derived from special registers, kernel
-// parameters and shared memory, so the merge issues no local-memory reloads.
+// The owner's merge, once its receive mbarrier has seen every pushed byte.
+// Everything is re-derived from special registers, kernel parameters and
+// shared memory (no long-lived registers across the wait).
 template <int D, int G>
 __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem) {
   const int C = (int)sreg_cluster_nctarank();
@@ -204,7 +206,12 @@ __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem)
   const float* recv_l = recv_m + 16 * G;
   const bool ok = *reinterpret_cast<const int*>(smem + FGeo<D>::kRing + 48) != 0;
   long long* trace = p.trace ? p.trace + (size_t)sreg_ctaid_x() * 16 : nullptr;
-  if (trace && tid == 0) trace[13] = (long long)globaltimer();
+  const long long c_pub0 = clock64();
+  mbar_wait(reinterpret_cast<uint64_t*>(smem + FGeo<D>::kRing + 56), 0);  // every partial landed
+  if (trace && tid == 0) {
+    trace[4] = clock64() - c_pub0;  // receive-wait cycles
+    trace[13] = (long long)globaltimer();
+  }
   const long long c_merge0 = clock64();
 
   // ---- merge: this CTA's share of the G x D outputs over the C pushed partials ----
@@ -223,8 +230,7 @@ __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem)
       lc = recv_l[lane * G + gg];
     }
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
-      if (c < C) oc[c] = recv_o[c * share + (e - e0)];
+    for (int c = 0; c < 16; ++c) oc[c] = c < C ? recv_o[c * share + (e - e0)] : 0.f;  // predicated, no branch
     float M = mc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
@@ -233,10 +239,12 @@ __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem)
     float Ls = lc * sc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
+    float scs[16];  // lanes >= C hold sc = 0
+#pragma unroll
+    for (int c = 0; c < 16; ++c) scs[c] = __shfl_sync(0xffffffffu, sc, c);
     float Os = 0.f;
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
-      if (c < C) Os = fmaf(oc[c], __shfl_sync(0xffffffffu, sc, c), Os);
+    for (int c = 0; c < 16; ++c) Os = fmaf(oc[c], scs[c], Os);
     outp[e] = Ls > 0.f ? Os / Ls : 0.f;
     if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
       if (lane == 0 && e % D == 0)
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + FGeo<D>::kRing);
   uint64_t* empty = full + kStages;
+  uint64_t* rx_bar = reinterpret_cast<uint64_t*>(smem + FGeo<D>::kRing + 56);  // merge receive (flag at +48)
   constexpr int kPD = FPart<D, G>::kPD;
   float* part_o = reinterpret_cast<float*>(smem);        // [kParts][G][kPD] (after the stream)
   float* part_m = part_o + FPart<D, G>::kO;              // [kParts][G]
@@ -297,7 +306,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kNcw);
     }
+    mbar_init(rx_bar, 1);
     fence_barrier_init();
+    // the owner's one arrival: the bytes the C peers will push (complete_tx may
+    // land before or after it; the phase completes when both balance)
+    mbar_arrive_expect_tx(rx_bar, merge_rx_bytes(G, D, C, rank));
   }
   // Static tile split over the compact layout [0, R) + [R, R + n_sink + K):
   // no global load before the producer's first TMA. In steady-state decode
@@ -337,7 +350,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     griddep_wait();
     griddep_launch();
     cluster_wait_started();
-    cluster_publish();  // partials pushed
     return;
   }
 
@@ -348,20 +360,23 @@ __global__ void __launch_bounds__(kThreads, 2)
     trace[1] = (long long)globaltimer();
     trace[5] = te - tb;
   }
-  // post-wait: lengths of this step
+  // post-wait: lengths of this step (loads issued here; the consumers derive
+  // from them only after issuing their q loads, so both round trips overlap)
   const int L = p.prefix_len[b];
   const int rl = p.recent_len[b];
   const int nsb = p.n_sink_b[b];
   const int nsel = p.n_sel[slice_g];
-  const int n_cs = nsb + nsel;  // sink + selected rows
-  const bool geom_ok = nsb >= 0 && nsel >= 0 && n_cs <= p.crows - p.R;
   const bool fused = p.k_new != nullptr;
-  // ring slots holding the recent window minus (fused) the current token
-  const int s0 = ((L - rl) % p.R + p.R) % p.R;   // slot of recent_start = L - rl + 1
-  const int ring_valid = fused ? rl - 1 : rl;
-  bool ok = geom_ok && rl <= p.R && rl >= (fused ? 1 : 0) && L >= 1 && L <= p.Lmax;
+#define SFI_FAST_DERIVE_LENGTHS                                                                    \
+  const int n_cs = nsb + nsel; /* sink + selected rows */                                          \
+  const bool geom_ok = nsb >= 0 && nsel >= 0 && n_cs <= p.crows - p.R;                             \
+  /* ring slots holding the recent window minus (fused) the current token */                       \
+  const int s0 = ((L - rl) % p.R + p.R) % p.R; /* slot of recent_start = L - rl + 1 */             \
+  const int ring_valid = fused ? rl - 1 : rl;                                                      \
+  const bool ok = geom_ok && rl <= p.R && rl >= (fused ? 1 : 0) && L >= 1 && L <= p.Lmax;
 
   if (warp == kNcw + 1) {
+    SFI_FAST_DERIVE_LENGTHS
     // ---------------- aux: the current token ----------------
     constexpr int kC = D / 32;
     float mq[G], lq[G];
@@ -427,8 +442,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     named_bar_sync<2, (kNcw + 1) * 32>();  // all partials written
     combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, part_s, (int)threadIdx.x - 32);
-    push_partials<D, G>(cl, part_o, comb_m, comb_l, recv_o, recv_m, recv_l, share, rank, (int)threadIdx.x - 32);
-    cluster_publish();
+    push_partials<D, G>(part_o, comb_m, comb_l, recv_o, recv_m, recv_l, rx_bar, share, rank, (int)threadIdx.x - 32);
     // fp64 key norm: sequential over c in round-to-nearest ops (attention.cpp:
     // 143-150; bit-identical to append_kernel), off the critical path
     if (mine && lane == 0) {
@@ -477,6 +491,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
   }
+  SFI_FAST_DERIVE_LENGTHS
+#undef SFI_FAST_DERIVE_LENGTHS
   float o[D / 8][4];
 #pragma unroll
   for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -650,15 +666,12 @@ __global__ void __launch_bounds__(kThreads, 2)
       part_l[warp * G + g] = l_run[0];
     }
   }
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(smem + FGeo<D>::kRing + 48) = ok;  // for the merge
   named_bar_sync<2, (kNcw + 1) * 32>();  // all partials written
   if (trace && threadIdx.x == 0) trace[11] = (long long)globaltimer();
   combine_cta<D, G>(part_o, part_m, part_l, comb_m, comb_l, part_s, (int)threadIdx.x);
-  push_partials<D, G>(cl, part_o, comb_m, comb_l, recv_o, recv_m, recv_l, share, rank, (int)threadIdx.x);
+  push_partials<D, G>(part_o, comb_m, comb_l, recv_o, recv_m, recv_l, rx_bar, share, rank, (int)threadIdx.x);
   if (trace && threadIdx.x == 0) trace[15] = (long long)globaltimer();
-  if (threadIdx.x == 0) *reinterpret_cast<int*>(smem + FGeo<D>::kRing + 48) = ok;
-  const long long c_pub0 = clock64();
-  cluster_publish();
-  if (trace && threadIdx.x == 0) trace[4] = clock64() - c_pub0;  // publish barrier cycles
   merge_pushed<D, G>(p, smem);
 }
 
