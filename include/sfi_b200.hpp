@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <optional>
 #include <vector>
 
 #include "sfi_b200.h"
@@ -105,6 +106,7 @@ struct ModelSpec {
   int max_positions = 32768;
   double rope_base = 10000.0;
   int hidden() const { return n_query_heads * head_dim; }
+  int ff_dim() const { return 2 * hidden(); }
   int group_size() const { return n_query_heads / n_kv_heads; }
   void validate() const;
 };
@@ -217,8 +219,15 @@ class KvStore {
 
   const DeviceCache& device() const { return *dev_; }
   void* stream() const { return stream_; }
-  // Syncs the device view of (prefix_len, n_sink_b, recent_len).
-  void set_window(int n_sink_b, int recent_len) const;
+  const CacheLimits& limits() const { return limits_; }
+  // Syncs the device view of (prefix_len, n_sink_b, recent_len); `len` < 0
+  // means size(). A step attends to the token it is appending (attention.cpp:
+  // 354-360), so the request loop passes size() + 1 while a token is open.
+  void set_window(int n_sink_b, int recent_len, Pos len = -1) const;
+  // Cached fp64 key norms of positions [first, first + count) of one head.
+  std::vector<double> key_norms(int layer, int head, Pos first, int count) const;
+  // Layers of the open token appended so far (-1: no token open).
+  int pending_layers() const { return pending_layers_; }
 
  private:
   struct LayerState {
@@ -280,5 +289,104 @@ void slow_step_update(DecodeState& state,
                       const std::vector<std::vector<std::vector<Pos>>>& selected_per_layer,
                       const CacheLimits& limits);
 double flop_model(double prefix_len, double support, double slow_fraction);
+
+// ---------------------------------------------------------------------------
+// The request loop around the device hot path (engine.cpp).
+//
+// ToyModel is the reference's small decoder (attention.hpp:46-83,
+// model.cpp:36-167; same mt19937_64 / normal_distribution draws, so
+// ToyModel::random(spec, seed) holds the reference's weights bit for bit). It
+// is the activation source of the end-to-end checks: its
+// projections, RoPE, MLP and LM head run on the host in fp64 exactly as the
+// reference orders them, while every attention, logit capture, Selector and
+// compact rebuild of run_request / run_dense runs through the device path
+// (sm_100a kernels over the KvStore's HBM buffers, bf16 KV).
+class ToyModel {
+ public:
+  struct Matrix {  // row-major (out x in)
+    int rows = 0, cols = 0;
+    std::vector<double> v;
+    const double* row(int r) const { return v.data() + static_cast<std::size_t>(r) * cols; }
+  };
+  struct LayerWeights {
+    std::vector<double> ln1, ln2;
+    Matrix wq, wk, wv, wo;
+    Matrix w_gate, w_up, w_down;
+  };
+  static ToyModel random(const ModelSpec& spec, std::uint64_t seed);
+
+  const ModelSpec& spec() const { return spec_; }
+  const Matrix& embedding() const { return embed_; }
+  const LayerWeights& layer(int i) const { return layers_[i]; }
+  const std::vector<double>& final_norm() const { return ln_f_; }
+  const Matrix& lm_head() const { return lm_head_; }
+  const std::vector<double>& lm_bias() const { return lm_bias_; }
+
+ private:
+  ModelSpec spec_;
+  Matrix embed_;
+  std::vector<LayerWeights> layers_;
+  std::vector<double> ln_f_;
+  Matrix lm_head_;
+  std::vector<double> lm_bias_;
+};
+
+// attention.hpp:157-182
+struct StepOutput {
+  std::vector<double> vocab_logits;
+  std::optional<std::vector<LogitWindow>> attn_logits;  // slow steps: one window per layer
+  std::uint64_t flop_count = 0;
+  std::uint64_t kv_read_count = 0;
+};
+struct CaptureSpec {
+  bool window = false;
+  std::vector<Pos> allowed;  // J, ascending, one contiguous range (decode / prefill J)
+  PoolMode pool = PoolMode::kMean;
+};
+
+// attention.hpp:184-204, attention.cpp:249-254
+StepOutput dense_attention_step(const ToyModel& model, TokenId token, KvStore& store,
+                                const CaptureSpec& capture);
+StepOutput sparse_attention_step(const ToyModel& model, TokenId token, KvStore& store,
+                                 const std::vector<SupportSet>& support);
+std::vector<LogitWindow> prefill_dense(const ToyModel& model, const std::vector<TokenId>& tokens,
+                                       KvStore& store, int window_width, const std::vector<Pos>& allowed,
+                                       PoolMode pool);
+TokenId argmax_token(const std::vector<double>& logits);
+
+// scheduler.hpp:79-135
+enum class StepCause { kInitial, kTrigger, kForced, kNone };
+struct StepRecord {
+  int t = 0;
+  bool slow = false;
+  StepCause cause = StepCause::kNone;
+  int support_size = 0;
+  int allowed_size = 0;
+  Pos prefix_len = 0;
+};
+struct RunOptions {
+  bool collect_logits = true;
+  bool capture_selected = false;
+};
+struct RequestResult {
+  std::vector<TokenId> tokens;
+  std::vector<StepRecord> log;
+  std::vector<std::vector<double>> step_logits;
+  std::uint64_t total_flops = 0;
+  std::uint64_t total_kv_reads = 0;
+  std::uint64_t dense_equiv_reads = 0;
+  std::vector<double> fast_retention;
+  std::vector<std::vector<std::vector<std::vector<Pos>>>> selected_per_step;
+};
+struct DenseResult {
+  std::vector<TokenId> tokens;
+  std::vector<std::vector<double>> step_logits;
+  std::uint64_t total_kv_reads = 0;
+  std::uint64_t total_flops = 0;
+};
+RequestResult run_request(const ToyModel& model, const std::vector<TokenId>& prompt, const CacheLimits& limits,
+                          const TriggerConfig& trig, const SelectorConfig& cfg, int max_new,
+                          const RunOptions& opts = {});
+DenseResult run_dense(const ToyModel& model, const std::vector<TokenId>& prompt, int max_new);
 
 }  // namespace sfi_b200

@@ -78,6 +78,17 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
+class ToySpec(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("n_layers", "n_query_heads", "n_kv_heads", "head_dim",
+                                         "vocab_size", "max_positions")] + [("rope_base", C.c_double)]
+
+
+class ToyLimits(C.Structure):
+    _fields_ = [("n_sink", C.c_int32), ("n_recent", C.c_int32), ("k_budget", C.c_int32),
+                ("trigger_tokens", C.c_void_p), ("n_trigger", C.c_int32), ("t_max", C.c_int32),
+                ("window_prefill", C.c_int32)]
+
+
 class Oracle:
     """One oracle library (kind 'reference' or 'port')."""
 
@@ -102,6 +113,59 @@ class Oracle:
                      "orc_store_reorganize", "orc_store_compact", "orc_attention_dense",
                      "orc_attention_sparse", "orc_dense_capture"):
             getattr(L, name).restype = C.c_int
+        if self.kind == "reference":  # toy model + request loop: reference library only
+            L.orc_toy_checksum.restype = C.c_double
+            L.orc_toy_checksum.argtypes = [C.c_void_p, C.c_uint64]
+            L.orc_toy_run_request.restype = C.c_int
+            L.orc_toy_run_dense.restype = C.c_int
+
+    # ---- toy model + request loop (reference only, scheduler.cpp:213-365) ----
+    @staticmethod
+    def _toy_spec(spec: dict) -> ToySpec:
+        return ToySpec(**{k: spec[k] for k in ("n_layers", "n_query_heads", "n_kv_heads", "head_dim",
+                                               "vocab_size", "max_positions")},
+                       rope_base=float(spec.get("rope_base", 10000.0)))
+
+    def toy_checksum(self, spec: dict, seed: int) -> float:
+        ts = self._toy_spec(spec)
+        return self.lib.orc_toy_checksum(C.byref(ts), C.c_uint64(seed))
+
+    def toy_run_request(self, spec: dict, seed: int, prompt, limits: dict, cfg: SelectorCfg, max_new: int,
+                        logits: bool = True):
+        """Reference run_request; returns dict(tokens, slow, cause, logits [max_new][vocab])."""
+        ts = self._toy_spec(spec)
+        prompt = _i32(prompt)
+        trig = _i32(limits.get("trigger_tokens", [0, 1, 2, 3, 4]))
+        tl = ToyLimits(n_sink=limits.get("n_sink", 4), n_recent=limits.get("n_recent", 256),
+                       k_budget=limits.get("k_budget", 2048), trigger_tokens=trig.ctypes.data,
+                       n_trigger=len(trig), t_max=limits.get("t_max", 64),
+                       window_prefill=limits.get("window_prefill", 16))
+        tok = np.zeros(max_new, np.int32)
+        slow = np.zeros(max_new, np.int32)
+        cause = np.zeros(max_new, np.int32)
+        lg = np.zeros((max_new, spec["vocab_size"]), np.float64) if logits else None
+        L, H, K = spec["n_layers"], spec["n_kv_heads"], tl.k_budget
+        sel = np.zeros((max_new, L, H, max(K, 1)), np.int32)
+        nsel = np.zeros((max_new, L, H), np.int32)
+        err = C.create_string_buffer(512)
+        rc = self.lib.orc_toy_run_request(C.byref(ts), C.c_uint64(seed), _ptr(prompt), C.c_int(len(prompt)),
+                                          C.byref(tl), C.byref(cfg), C.c_int(max_new), _ptr(tok), _ptr(slow),
+                                          _ptr(cause), _ptr(lg), _ptr(sel), _ptr(nsel), err, C.c_int(512))
+        self._check(rc, err)
+        selected = [[[sel[i, l, h, : nsel[i, l, h]].tolist() for h in range(H)] for l in range(L)]
+                    for i in range(max_new)]
+        return dict(tokens=tok, slow=slow, cause=cause, logits=lg, selected=selected)
+
+    def toy_run_dense(self, spec: dict, seed: int, prompt, max_new: int, logits: bool = True):
+        ts = self._toy_spec(spec)
+        prompt = _i32(prompt)
+        tok = np.zeros(max_new, np.int32)
+        lg = np.zeros((max_new, spec["vocab_size"]), np.float64) if logits else None
+        err = C.create_string_buffer(512)
+        rc = self.lib.orc_toy_run_dense(C.byref(ts), C.c_uint64(seed), _ptr(prompt), C.c_int(len(prompt)),
+                                        C.c_int(max_new), _ptr(tok), _ptr(lg), err, C.c_int(512))
+        self._check(rc, err)
+        return dict(tokens=tok, logits=lg)
 
     def _check(self, rc: int, err) -> None:
         if rc:

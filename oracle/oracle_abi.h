@@ -106,6 +106,30 @@ int orc_dense_capture(void* store, int layer, const double* q, int nJ,
                       const int32_t* allowed, int pool, double* out,
                       double* logits, char* err, int errlen);
 
+/* ---- Toy model + request loop: REFERENCE LIBRARY ONLY (the port does not
+ * restate the toy decoder). ToyModel::random (model.cpp:141-167),
+ * run_request (scheduler.cpp:213-330), run_dense (:332-365). ---- */
+typedef struct {
+  int32_t n_layers, n_query_heads, n_kv_heads, head_dim, vocab_size, max_positions;
+  double rope_base;
+} orc_toy_spec;
+typedef struct {
+  int32_t n_sink, n_recent, k_budget; /* CacheLimits */
+  const int32_t* trigger_tokens;      /* TriggerConfig */
+  int32_t n_trigger, t_max, window_prefill;
+} orc_toy_limits;
+/* Order-fixed sum of every weight of ToyModel::random(spec, seed). */
+double orc_toy_checksum(const orc_toy_spec* spec, uint64_t seed);
+/* out_tokens / out_slow / out_cause (StepCause) [max_new]; out_logits
+ * [max_new][vocab] or NULL; out_sel [max_new][n_layers][H][k_budget] with
+ * out_nsel [max_new][n_layers][H] (the selected sets after each step) or NULL. */
+int orc_toy_run_request(const orc_toy_spec* spec, uint64_t seed, const int32_t* prompt, int plen,
+                        const orc_toy_limits* limits, const orc_selector_cfg* cfg, int max_new,
+                        int32_t* out_tokens, int32_t* out_slow, int32_t* out_cause,
+                        double* out_logits, int32_t* out_sel, int32_t* out_nsel, char* err, int errlen);
+int orc_toy_run_dense(const orc_toy_spec* spec, uint64_t seed, const int32_t* prompt, int plen,
+                      int max_new, int32_t* out_tokens, double* out_logits, char* err, int errlen);
+
 #pragma GCC visibility pop
 #ifdef __cplusplus
 }

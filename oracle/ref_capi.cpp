@@ -280,4 +280,100 @@ int orc_dense_capture(void*, int, const double*, int, const int32_t*, int, doubl
   return 102;
 }
 
+/* ---- toy model + request loop (reference only) ---- */
+
+namespace {
+sfi::ModelSpec toy_spec(const orc_toy_spec* t) {
+  sfi::ModelSpec spec;
+  spec.n_layers = t->n_layers;
+  spec.n_query_heads = t->n_query_heads;
+  spec.n_kv_heads = t->n_kv_heads;
+  spec.head_dim = t->head_dim;
+  spec.vocab_size = t->vocab_size;
+  spec.max_positions = t->max_positions;
+  spec.rope_base = t->rope_base;
+  return spec;
+}
+}  // namespace
+
+double orc_toy_checksum(const orc_toy_spec* t, uint64_t seed) {
+  try {
+    const sfi::ToyModel m = sfi::ToyModel::random(toy_spec(t), seed);
+    double acc = 0.0;
+    auto add = [&](const Eigen::MatrixXd& w) {
+      for (int r = 0; r < w.rows(); ++r)
+        for (int c = 0; c < w.cols(); ++c) acc += w(r, c);
+    };
+    add(m.embedding());
+    for (int l = 0; l < t->n_layers; ++l) {
+      const auto& lw = m.layer(l);
+      add(lw.wq);
+      add(lw.wk);
+      add(lw.wv);
+      add(lw.wo);
+      add(lw.w_gate);
+      add(lw.w_up);
+      add(lw.w_down);
+    }
+    add(m.lm_head());
+    return acc;
+  } catch (...) {
+    return 0.0;
+  }
+}
+
+int orc_toy_run_request(const orc_toy_spec* t, uint64_t seed, const int32_t* prompt, int plen,
+                        const orc_toy_limits* lim, const orc_selector_cfg* c, int max_new,
+                        int32_t* out_tokens, int32_t* out_slow, int32_t* out_cause,
+                        double* out_logits, int32_t* out_sel, int32_t* out_nsel, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const sfi::ToyModel m = sfi::ToyModel::random(toy_spec(t), seed);
+    sfi::CacheLimits limits;
+    limits.n_sink = lim->n_sink;
+    limits.n_recent = lim->n_recent;
+    limits.k_budget = lim->k_budget;
+    sfi::TriggerConfig trig;
+    trig.trigger_tokens.assign(lim->trigger_tokens, lim->trigger_tokens + lim->n_trigger);
+    trig.t_max = lim->t_max;
+    trig.window_prefill = lim->window_prefill;
+    sfi::RunOptions opts;
+    opts.collect_logits = out_logits != nullptr;
+    opts.capture_selected = out_sel != nullptr;
+    const sfi::RequestResult r = sfi::run_request(m, std::vector<sfi::TokenId>(prompt, prompt + plen), limits,
+                                                  trig, to_cfg(c), max_new, opts);
+    for (int i = 0; i < max_new; ++i) {
+      out_tokens[i] = r.tokens[i];
+      out_slow[i] = r.log[i].slow ? 1 : 0;
+      out_cause[i] = static_cast<int32_t>(r.log[i].cause);
+      if (out_logits)
+        std::copy(r.step_logits[i].begin(), r.step_logits[i].end(),
+                  out_logits + static_cast<std::size_t>(i) * t->vocab_size);
+      if (out_sel) {  // [max_new][n_layers][H][k_budget], counts [max_new][n_layers][H]
+        const int H = t->n_kv_heads, K = lim->k_budget;
+        for (int l = 0; l < t->n_layers; ++l)
+          for (int h = 0; h < H; ++h) {
+            const auto& v = r.selected_per_step[i][l][h];
+            const std::size_t o = (static_cast<std::size_t>(i) * t->n_layers + l) * H + h;
+            out_nsel[o] = static_cast<int32_t>(v.size());
+            std::copy(v.begin(), v.end(), out_sel + o * K);
+          }
+      }
+    }
+  });
+}
+
+int orc_toy_run_dense(const orc_toy_spec* t, uint64_t seed, const int32_t* prompt, int plen, int max_new,
+                      int32_t* out_tokens, double* out_logits, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const sfi::ToyModel m = sfi::ToyModel::random(toy_spec(t), seed);
+    const sfi::DenseResult r = sfi::run_dense(m, std::vector<sfi::TokenId>(prompt, prompt + plen), max_new);
+    for (int i = 0; i < max_new; ++i) {
+      out_tokens[i] = r.tokens[i];
+      if (out_logits)
+        std::copy(r.step_logits[i].begin(), r.step_logits[i].end(),
+                  out_logits + static_cast<std::size_t>(i) * t->vocab_size);
+    }
+  });
+}
+
 }  // extern "C"

@@ -11,6 +11,9 @@ Reference-named operators (hot path):
 Host-side scheduler bookkeeping (integer logic, scheduler.cpp):
     init_decode_state, compute_allowed, next_step_type,
     fast_step_update, slow_step_update, flop_model
+Request loop around the device path (scheduler.cpp:213-365), with the
+reference's toy decoder as the activation source:
+    ToyModel, run_request, run_dense, argmax_token
 Batched device API (production / bench): SfiCache (torch-allocated buffers).
 """
 from __future__ import annotations
@@ -39,13 +42,19 @@ from ._sfi_b200 import (  # noqa: F401,E402
     LogitWindow,
     ModelSpec,
     PoolMode,
+    RequestResult,
+    RunOptions,
     SelectorConfig,
     SelectorParams,
     SelectorStages,
     SfiError,
     SparseState,
+    StepCause,
+    StepRecord,
     SupportSet,
+    ToyModel,
     TriggerConfig,
+    argmax_token,
     attention_kernel_dense,
     attention_kernel_sparse,
     compute_allowed,
@@ -56,6 +65,8 @@ from ._sfi_b200 import (  # noqa: F401,E402
     init_decode_state,
     make_cache_stats,
     next_step_type,
+    run_dense,
+    run_request,
     run_selector,
     run_selector_stages,
     select_top_k,
@@ -81,4 +92,6 @@ __all__ = [
     "dense_capture", "fast_step_update", "flop_model", "init_decode_state", "make_cache_stats",
     "next_step_type", "run_selector", "run_selector_stages", "select_top_k", "slow_step_update",
     "SfiCache", "SlowStepPipeline", "LIBRARY_PATH",
+    "ToyModel", "StepCause", "StepRecord", "RunOptions", "RequestResult", "run_request", "run_dense",
+    "argmax_token",
 ]

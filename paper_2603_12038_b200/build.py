@@ -29,7 +29,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                  "-I" + INC, "-I" + CSRC]
 CU = ["decode.cu", "fast_decode.cu", "capture.cu", "cache_ops.cu", "selector.cu", "capi.cu"]
-CPP = ["host.cpp"]
+CPP = ["host.cpp", "engine.cpp"]
 HEADERS = [os.path.join(INC, h) for h in ("sfi_b200.h", "sfi_b200.hpp")] + [
     os.path.join(CSRC, h) for h in ("common.cuh", "kernels.h")]
 
@@ -53,6 +53,8 @@ def _compile(src: str) -> str:
     obj = os.path.join(OBJ, src + ".o")
     if _newer(obj, [path] + HEADERS):
         extra = ["-fmad=false"] if src == "selector.cu" else []
+        if src == "engine.cpp":  # the toy model's fp64 host math: no contraction, as in the reference build
+            extra = ["-Xcompiler", "-ffp-contract=off"]
         _run([NVCC] + COMMON + extra + ["-c", path, "-o", obj])
     return obj
 

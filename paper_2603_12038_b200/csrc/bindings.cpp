@@ -224,6 +224,59 @@ PYBIND11_MODULE(_sfi_b200, m) {
         py::arg("limits"));
   m.def("flop_model", &flop_model, py::arg("prefix_len"), py::arg("support"), py::arg("slow_fraction"));
 
+  // ---- request loop around the device path (engine.cpp; scheduler.hpp:79-135) ----
+  py::class_<ToyModel>(m, "ToyModel")
+      .def_static("random", &ToyModel::random, py::arg("spec"), py::arg("seed"))
+      .def("spec", &ToyModel::spec)
+      .def("weight_checksum", [](const ToyModel& t) {
+        // order-fixed sum over every weight (identity check against the reference's ToyModel::random)
+        double acc = 0.0;
+        auto add = [&](const std::vector<double>& v) { for (double x : v) acc += x; };
+        add(t.embedding().v);
+        for (int l = 0; l < t.spec().n_layers; ++l) {
+          const auto& lw = t.layer(l);
+          for (const auto* w : {&lw.wq, &lw.wk, &lw.wv, &lw.wo, &lw.w_gate, &lw.w_up, &lw.w_down}) add(w->v);
+        }
+        add(t.lm_head().v);
+        return acc;
+      });
+  py::enum_<StepCause>(m, "StepCause")
+      .value("initial", StepCause::kInitial)
+      .value("trigger", StepCause::kTrigger)
+      .value("forced", StepCause::kForced)
+      .value("none", StepCause::kNone);
+  py::class_<StepRecord>(m, "StepRecord")
+      .def_readonly("t", &StepRecord::t)
+      .def_readonly("slow", &StepRecord::slow)
+      .def_readonly("cause", &StepRecord::cause)
+      .def_readonly("support_size", &StepRecord::support_size)
+      .def_readonly("allowed_size", &StepRecord::allowed_size)
+      .def_readonly("prefix_len", &StepRecord::prefix_len);
+  py::class_<RunOptions>(m, "RunOptions")
+      .def(py::init<>())
+      .def_readwrite("collect_logits", &RunOptions::collect_logits)
+      .def_readwrite("capture_selected", &RunOptions::capture_selected);
+  py::class_<RequestResult>(m, "RequestResult")
+      .def_readonly("tokens", &RequestResult::tokens)
+      .def_readonly("log", &RequestResult::log)
+      .def_readonly("step_logits", &RequestResult::step_logits)
+      .def_readonly("total_flops", &RequestResult::total_flops)
+      .def_readonly("total_kv_reads", &RequestResult::total_kv_reads)
+      .def_readonly("dense_equiv_reads", &RequestResult::dense_equiv_reads)
+      .def_readonly("fast_retention", &RequestResult::fast_retention)
+      .def_readonly("selected_per_step", &RequestResult::selected_per_step);
+  py::class_<DenseResult>(m, "DenseResult")
+      .def_readonly("tokens", &DenseResult::tokens)
+      .def_readonly("step_logits", &DenseResult::step_logits)
+      .def_readonly("total_kv_reads", &DenseResult::total_kv_reads)
+      .def_readonly("total_flops", &DenseResult::total_flops);
+  m.def("argmax_token", &argmax_token, py::arg("logits"));
+  m.def("run_request", &run_request, py::arg("model"), py::arg("prompt"), py::arg("limits"), py::arg("trigger"),
+        py::arg("selector"), py::arg("max_new"), py::arg("opts") = RunOptions{},
+        py::call_guard<py::gil_scoped_release>());
+  m.def("run_dense", &run_dense, py::arg("model"), py::arg("prompt"), py::arg("max_new"),
+        py::call_guard<py::gil_scoped_release>());
+
   // ---- batched device API: the C ABI one-to-one --------------------------
   py::class_<sfi_shape>(m, "Shape")
       .def(py::init<>())

@@ -346,13 +346,27 @@ KvStore::KvStore(const ModelSpec& spec, const CacheLimits& limits, void* stream)
   dev_ = std::make_unique<DeviceCache>(s);
 }
 
-void KvStore::set_window(int n_sink_b, int recent_len) const {
-  if (n_sink_b == cur_nsb_ && recent_len == cur_rl_ && len_ == cur_len_) return;
-  const int32_t L = len_, nsb = n_sink_b, rl = recent_len;
+void KvStore::set_window(int n_sink_b, int recent_len, Pos len) const {
+  if (len < 0) len = len_;
+  if (n_sink_b == cur_nsb_ && recent_len == cur_rl_ && len == cur_len_) return;
+  const int32_t L = len, nsb = n_sink_b, rl = recent_len;
   check(sfi_set_lengths(&dev_->shape(), &dev_->cache(), &L, &nsb, &rl, stream_));
   cur_nsb_ = n_sink_b;
   cur_rl_ = recent_len;
-  cur_len_ = len_;
+  cur_len_ = len;
+}
+
+std::vector<double> KvStore::key_norms(int layer, int head, Pos first, int count) const {
+  std::vector<double> out(static_cast<size_t>(std::max(count, 0)));
+  if (count <= 0) return out;
+  const Pos visible = len_ + (pending_layers_ > layer ? 1 : 0);
+  if (first < 1 || first + count - 1 > visible)
+    fail(ErrorCode::kOutOfRange, "KvStore: key norm range not written");
+  const size_t off = (static_cast<size_t>(layer) * spec_.n_kv_heads + head) * spec_.max_positions + (first - 1);
+  cuda_check(cudaStreamSynchronize(st(stream_)), "key_norms");
+  cuda_check(cudaMemcpy(out.data(), dev_->cache().key_norms + off, out.size() * 8, cudaMemcpyDeviceToHost),
+             "key_norms");
+  return out;
 }
 
 void KvStore::begin_token() {
