@@ -77,14 +77,20 @@ struct FPart {  // partials, written over the (drained) stage ring
 // streaming): [C][share] combined O + [C][G] m + [C][G] l, share <= G*D/C + 32.
 template <int D, int G>
 struct FRecv {
-  static constexpr int kFloats = G * D + 32 * 16 + 2 * 16 * G;
+  // O area: C x share floats; a single owner (G <= 4, C <= 4) takes all C partials;
+  // then m, l [16][G] and the merge's scales [16][G] + 1 / L [G]
+  static constexpr int kO = (G <= 4 && 4 * G * D > G * D + 32 * 16) ? 4 * G * D : G * D + 32 * 16;
+  static constexpr int kFloats = kO + 3 * 16 * G + G;
 };
 template <int D, int G>
 constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row | receive area
   return FGeo<D>::kRing + 64 + D * 8 + FRecv<D, G>::kFloats * 4;
 }
-__host__ __device__ constexpr int merge_share(int G, int D, int C) {  // whole warps of 32 elements
-  return ((G * D + C - 1) / C + 31) & ~31;
+// Owner shares are whole warps of 32 elements. With few, small partials (G <= 4,
+// C <= 4) rank 0 merges everything and ranks 1.. exit right after their push,
+// freeing their SM slots for the next layer's CTAs (its prefetch starts early).
+__host__ __device__ constexpr int merge_share(int G, int D, int C) {
+  return (G <= 4 && C <= 4) ? ((G * D + 31) & ~31) : ((G * D + C - 1) / C + 31) & ~31;
 }
 // Bytes owner r receives: from each of the C CTAs its O over [e0, e1) and
 // (m, l) of every head that range touches.
@@ -202,7 +208,7 @@ __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem)
   const int b = s / p.H, h = s % p.H;
   const int share = merge_share(G, D, C);
   const float* recv_o = reinterpret_cast<const float*>(smem + FGeo<D>::kRing + 64 + D * 8);
-  const float* recv_m = recv_o + G * D + 32 * 16;
+  const float* recv_m = recv_o + FRecv<D, G>::kO;
   const float* recv_l = recv_m + 16 * G;
   const bool ok = *reinterpret_cast<const int*>(smem + FGeo<D>::kRing + 48) != 0;
   long long* trace = p.trace ? p.trace + (size_t)sreg_ctaid_x() * 16 : nullptr;
@@ -214,43 +220,53 @@ __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem)
   }
   const long long c_merge0 = clock64();
 
-  // ---- merge: this CTA's share of the G x D outputs over the C pushed partials ----
-  // Shares are whole warps of 32 elements of one head: lane c reads CTA c's
-  // (m, l) of that head (shuffled to the warp), each lane its element's C
-  // partial O values; fixed order over c: deterministic.
+  // ---- merge: this CTA's share [e0, e1) of the G x D outputs over the C pushed partials ----
+  // (1) a warp per head of the share (lane c = CTA c): M, the C scales and
+  // 1 / L by fixed butterfly trees (deterministic); (2) every consumer thread:
+  // float4 of outputs as sum_c O_c * scale_c (c order), times 1 / L.
   const int total = G * D;
   const int e0 = rank * share, e1 = min(total, e0 + share);
-  float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
-  for (int eb = e0 + warp * 32; eb < e1; eb += kNcw * 32) {  // warp-uniform
-    const int gg = eb / D;
-    const int e = eb + lane;
-    float mc = -INFINITY, lc = 0.f, oc[16];
-    if (lane < C) {
-      mc = recv_m[lane * G + gg];
-      lc = recv_l[lane * G + gg];
+  if (e1 > e0) {
+    float* scl = const_cast<float*>(recv_l) + 16 * G;  // [C][G] scales, then [G] 1 / L
+    const int g_lo = e0 / D, g_hi = (e1 - 1) / D;
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int g = g_lo + warp; g <= g_hi; g += kNcw) {  // a warp per head, lane c = CTA c
+      const float m = lane < C ? recv_m[lane * G + g] : -INFINITY;
+      const float l = lane < C ? recv_l[lane * G + g] : 0.f;
+      float M = m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      const float Mu = (M == -INFINITY) ? 0.f : M;
+      const float sc = l > 0.f ? fast_exp2(m - Mu) : 0.f;  // l == 0: that CTA's O is zero
+      if (lane < C) scl[lane * G + g] = sc;
+      float L = l * sc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+      if (lane == 0) {
+        scl[16 * G + g] = L > 0.f ? 1.f / L : 0.f;
+        if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
+          p.lse[(size_t)b * p.Hq + (size_t)h * G + g] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
+        } else if (rank == 0 && g == 0 && ok && !(L > 0.f)) {
+          raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+        }
+      }
     }
-#pragma unroll
-    for (int c = 0; c < 16; ++c) oc[c] = c < C ? recv_o[c * share + (e - e0)] : 0.f;  // predicated, no branch
-    float M = mc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const float Mu = (M == -INFINITY) ? 0.f : M;
-    const float sc = lc > 0.f ? fast_exp2(mc - Mu) : 0.f;  // l == 0: that CTA's O is zero
-    float Ls = lc * sc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
-    float scs[16];  // lanes >= C hold sc = 0
-#pragma unroll
-    for (int c = 0; c < 16; ++c) scs[c] = __shfl_sync(0xffffffffu, sc, c);
-    float Os = 0.f;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) Os = fmaf(oc[c], scs[c], Os);
-    outp[e] = Ls > 0.f ? Os / Ls : 0.f;
-    if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
-      if (lane == 0 && e % D == 0)
-        p.lse[(size_t)b * p.Hq + (size_t)h * G + gg] = Ls > 0.f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
-    } else if (rank == 0 && e == 0 && ok && !(Ls > 0.f)) {
-      raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+    named_bar_sync<4, kNcw * 32>();
+    float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
+    for (int e = e0 + tid * 4; e < e1; e += kNcw * 32 * 4) {
+      const int g = e / D;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+      for (int c = 0; c < C; ++c) {
+        const float sc = scl[c * G + g];
+        const float4 x = *reinterpret_cast<const float4*>(recv_o + c * share + (e - e0));
+        acc.x = fmaf(x.x, sc, acc.x);
+        acc.y = fmaf(x.y, sc, acc.y);
+        acc.z = fmaf(x.z, sc, acc.z);
+        acc.w = fmaf(x.w, sc, acc.w);
+      }
+      const float inv = scl[16 * G + g];
+      *reinterpret_cast<float4*>(outp + e) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     }
   }
   if (trace && tid == 0) {
@@ -281,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   float* part_s = comb_l + G;                            // [kParts][G] combine scales
   double* ksq = reinterpret_cast<double*>(smem + FGeo<D>::kRing + 64);  // [D] k_c^2 (aux)
   float* recv_o = reinterpret_cast<float*>(smem + FGeo<D>::kRing + 64 + D * 8);  // [C][share]
-  float* recv_m = recv_o + G * D + 32 * 16;                                      // [C][G]
+  float* recv_m = recv_o + FRecv<D, G>::kO;                                      // [C][G]
   float* recv_l = recv_m + 16 * G;                                               // [C][G]
 
   long long* trace = p.trace ? p.trace + (size_t)blockIdx.x * 16 : nullptr;
