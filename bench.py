@@ -288,8 +288,12 @@ class HostIO:
     inputs land while the previous group computes and its output returns while the
     next group computes (few, large copies: each copy node costs microseconds)."""
 
-    def __init__(self, wl: Workload, group: int = 6):
+    def __init__(self, wl: Workload, group: int | None = None):
         t = wl.torch
+        if group is None:  # >= 6 layers and >= ~512 KB of inputs per copy group
+            per_layer = (wl.q[0].numel() * 4 + wl.k_new[0].numel() * 4)
+            group = max(6, -(-(512 << 10) // per_layer))
+            group = int(os.environ.get("SFI_BENCH_IO_GROUP", group))
         self.t, self.wl = t, wl
         self.cs = t.cuda.Stream()
         pin = lambda x: t.empty_like(x, device="cpu").pin_memory()  # noqa: E731
@@ -498,7 +502,8 @@ def gpu_arm(args) -> dict:
         ems = max_over_ranks(a.elapsed_time(b))
         e2e = {"value": wl.job_tokens * Ke / (ems / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": io.h2d, "d2h_bytes_per_step": io.d2h, "steps": Ke,
-               "copies": "pinned host <-> HBM in layer groups (1 | 6 ... | 1) on a copy stream, event-ordered with compute"}
+               "copies": "pinned host <-> HBM in layer groups (" + " | ".join(str(l1 - l0) for l0, l1 in io.groups) +
+                         ") on a copy stream, event-ordered with compute"}
 
     # ---- per-kernel device time (CUDA events on the launching stream) ----
     pk = peaks()
