@@ -10,6 +10,10 @@
 
 namespace sfi_dev {
 
+// Online softmax (log2 domain): the running reference max is only raised when a
+// tile's max exceeds it by more than this (p <= 2^8 otherwise).
+constexpr float kLazyMax = 8.f;
+
 // Error word bits: 1 << status (sfi_status codes < 32).
 __device__ __forceinline__ void raise_error(uint32_t* flags, int code) {
   if (flags) atomicOr(flags, 1u << code);

@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       // ---- online softmax (log2 domain) ----
       float pr[NH][2][2], alpha[NH];
+      bool any_grow = false;
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh) {
         float mx = -INFINITY;
@@ -653,9 +654,14 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m_run[hh], mx);
+        // lazy rescaling: the reference max moves only when the tile's max
+        // exceeds it by more than 2^8 (p <= 256 otherwise; (m, l, O) stay a
+        // consistent triple), so O is rarely rescaled
+        const bool grow = mx > m_run[hh] + kLazyMax;
+        const float m_new = grow ? mx : m_run[hh];
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        alpha[hh] = fast_exp2(m_run[hh] - m_use);
+        alpha[hh] = grow ? fast_exp2(m_run[hh] - m_use) : 1.f;
+        any_grow |= grow;
         float psum = 0.f;
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -667,12 +673,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         l_run[hh] = l_run[hh] * alpha[hh] + psum;
         m_run[hh] = m_new;
       }
+      if (__any_sync(0xffffffffu, any_grow)) {
 #pragma unroll
-      for (int n = 0; n < D / 8; ++n) {
-        o[n][0] *= alpha[0];
-        o[n][1] *= alpha[0];
-        o[n][2] *= alpha[NH - 1];
-        o[n][3] *= alpha[NH - 1];
+        for (int n = 0; n < D / 8; ++n) {
+          o[n][0] *= alpha[0];
+          o[n][1] *= alpha[0];
+          o[n][2] *= alpha[NH - 1];
+          o[n][3] *= alpha[NH - 1];
+        }
       }
       // ---- P as the A operand (rows as the Q fragments) ----
       uint32_t pa[NQ][4];

@@ -582,14 +582,20 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int hh = 0; hh < NH; ++hh) sc[hh][j][e] = valid[j][e] ? sc[hh][j][e] * sl2 : -INFINITY;
         }
       float pr[NH][2][2], alpha[NH];
+      bool any_grow = false;
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh) {
         float mx = fmaxf(fmaxf(sc[hh][0][0], sc[hh][0][1]), fmaxf(sc[hh][1][0], sc[hh][1][1]));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m_run[hh], mx);
+        // lazy rescaling: the reference max moves only when the tile's max
+        // exceeds it by more than 2^8 (p <= 256 otherwise; (m, l, O) stay a
+        // consistent triple), so O is rarely rescaled
+        const bool grow = mx > m_run[hh] + kLazyMax;
+        const float m_new = grow ? mx : m_run[hh];
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        alpha[hh] = fast_exp2(m_run[hh] - m_use);
+        alpha[hh] = grow ? fast_exp2(m_run[hh] - m_use) : 1.f;
+        any_grow |= grow;
         float psum = 0.f;
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -601,12 +607,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         l_run[hh] = l_run[hh] * alpha[hh] + psum;
         m_run[hh] = m_new;
       }
+      if (__any_sync(0xffffffffu, any_grow)) {
 #pragma unroll
-      for (int n = 0; n < D / 8; ++n) {
-        o[n][0] *= alpha[0];
-        o[n][1] *= alpha[0];
-        o[n][2] *= alpha[NH - 1];
-        o[n][3] *= alpha[NH - 1];
+        for (int n = 0; n < D / 8; ++n) {
+          o[n][0] *= alpha[0];
+          o[n][1] *= alpha[0];
+          o[n][2] *= alpha[NH - 1];
+          o[n][3] *= alpha[NH - 1];
+        }
       }
       // P as the A operand (see header): G <= 8 rows g / g+8 = hi / lo of head g;
       // G == 16 block 0 = hi of heads (g, g+8), block 1 = lo.

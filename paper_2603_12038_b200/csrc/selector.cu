@@ -660,7 +660,7 @@ constexpr int kPwHeads = 4;            // heads per CTA (blockIdx.z splits large
 __host__ __device__ __forceinline__ int n_chunks(int n) { return (n + kChunk - 1) / kChunk; }
 
 template <int kHT>
-__global__ void __launch_bounds__(kPwT) sel_pw_kernel(const SelParams p, double* P, double* Wt, double* stats,
+__global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, double* P, double* Wt, double* stats,
                                                       int ld_chunks) {
   griddep_wait();  // PDL: logits come from the preceding dense decode
   griddep_launch();
@@ -824,7 +824,7 @@ __global__ void sel_coef_kernel(const SelParams p, const double* __restrict__ st
 }
 
 template <int kH>
-__global__ void __launch_bounds__(kRefineT) sel_z_kernel(const SelParams p, const double* P, const double* Wt,
+__global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const SelParams p, const double* P, const double* Wt,
                                                          const double* coef, int ld_chunks) {
   griddep_wait();
   griddep_launch();
