@@ -78,9 +78,9 @@ struct FPart {  // partials, written over the (drained) stage ring
 template <int D, int G>
 struct FRecv {
   // O area: C x share floats; a single owner (G <= 4, C <= 4) takes all C partials;
-  // then m, l [16][G] and the merge's scales [16][G] + 1 / L [G]
+  // then m, l [16][G]
   static constexpr int kO = (G <= 4 && 4 * G * D > G * D + 32 * 16) ? 4 * G * D : G * D + 32 * 16;
-  static constexpr int kFloats = kO + 3 * 16 * G + G;
+  static constexpr int kFloats = kO + 2 * 16 * G;
 };
 template <int D, int G>
 constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row | receive area
@@ -203,7 +203,6 @@ __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem)
   const int C = (int)sreg_cluster_nctarank();
   const int rank = (int)sreg_cluster_ctarank();
   const int tid = (int)sreg_tid_x();
-  const int warp = tid >> 5, lane = tid & 31;
   const int s = (int)sreg_ctaid_x() / C;
   const int b = s / p.H, h = s % p.H;
   const int share = merge_share(G, D, C);
@@ -221,52 +220,39 @@ __device__ __forceinline__ void merge_pushed(const FastParams& p, uint8_t* smem)
   const long long c_merge0 = clock64();
 
   // ---- merge: this CTA's share [e0, e1) of the G x D outputs over the C pushed partials ----
-  // (1) a warp per head of the share (lane c = CTA c): M, the C scales and
-  // 1 / L by fixed butterfly trees (deterministic); (2) every consumer thread:
-  // float4 of outputs as sum_c O_c * scale_c (c order), times 1 / L.
+  // One pass, no barrier: each thread owns float4s of outputs and forms its
+  // head's max, scales and L itself from the C (m, l) pairs (fixed c order:
+  // deterministic), accumulating sum_c O_c * scale_c alongside.
   const int total = G * D;
   const int e0 = rank * share, e1 = min(total, e0 + share);
-  if (e1 > e0) {
-    float* scl = const_cast<float*>(recv_l) + 16 * G;  // [C][G] scales, then [G] 1 / L
-    const int g_lo = e0 / D, g_hi = (e1 - 1) / D;
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int g = g_lo + warp; g <= g_hi; g += kNcw) {  // a warp per head, lane c = CTA c
-      const float m = lane < C ? recv_m[lane * G + g] : -INFINITY;
-      const float l = lane < C ? recv_l[lane * G + g] : 0.f;
-      float M = m;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-      const float Mu = (M == -INFINITY) ? 0.f : M;
-      const float sc = l > 0.f ? fast_exp2(m - Mu) : 0.f;  // l == 0: that CTA's O is zero
-      if (lane < C) scl[lane * G + g] = sc;
-      float L = l * sc;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-      if (lane == 0) {
-        scl[16 * G + g] = L > 0.f ? 1.f / L : 0.f;
-        if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
-          p.lse[(size_t)b * p.Hq + (size_t)h * G + g] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
-        } else if (rank == 0 && g == 0 && ok && !(L > 0.f)) {
-          raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
-        }
-      }
-    }
-    named_bar_sync<4, kNcw * 32>();
-    float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
-    for (int e = e0 + tid * 4; e < e1; e += kNcw * 32 * 4) {
-      const int g = e / D;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float* outp = p.out + ((size_t)b * p.Hq + (size_t)h * G) * D;
+  for (int e = e0 + tid * 4; e < e1; e += kNcw * 32 * 4) {
+    const int g = e / D;
+    float M = -INFINITY;
 #pragma unroll 4
-      for (int c = 0; c < C; ++c) {
-        const float sc = scl[c * G + g];
-        const float4 x = *reinterpret_cast<const float4*>(recv_o + c * share + (e - e0));
-        acc.x = fmaf(x.x, sc, acc.x);
-        acc.y = fmaf(x.y, sc, acc.y);
-        acc.z = fmaf(x.z, sc, acc.z);
-        acc.w = fmaf(x.w, sc, acc.w);
+    for (int c = 0; c < C; ++c) M = fmaxf(M, recv_m[c * G + g]);
+    const float Mu = (M == -INFINITY) ? 0.f : M;
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int c = 0; c < C; ++c) {
+      const float l = recv_l[c * G + g];
+      const float sc = l > 0.f ? fast_exp2(recv_m[c * G + g] - Mu) : 0.f;  // l == 0: that CTA's O is zero
+      L += l * sc;
+      const float4 x = *reinterpret_cast<const float4*>(recv_o + c * share + (e - e0));
+      acc.x = fmaf(x.x, sc, acc.x);
+      acc.y = fmaf(x.y, sc, acc.y);
+      acc.z = fmaf(x.z, sc, acc.z);
+      acc.w = fmaf(x.w, sc, acc.w);
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    *reinterpret_cast<float4*>(outp + e) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (e % D == 0) {
+      if (p.lse) {  // partial mode (sequence shard): natural-log LSE, empty allowed
+        p.lse[(size_t)b * p.Hq + (size_t)h * G + g] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
+      } else if (rank == 0 && e == 0 && ok && !(L > 0.f)) {
+        raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
       }
-      const float inv = scl[16 * G + g];
-      *reinterpret_cast<float4*>(outp + e) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     }
   }
   if (trace && tid == 0) {

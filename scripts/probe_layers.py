@@ -48,4 +48,4 @@ print("phase medians (us after CTA start), idx", idx, ":", np.round(ph, 2).tolis
 os.makedirs("gpurun_out", exist_ok=True)
 np.save(f"gpurun_out/layer_trace_{cfg}.npy", a)
 cyc = np.stack([np.median(a[l][:, [4, 7]], axis=0) for l in range(1, L)]).mean(0)
-print("median cycles: publish barrier, merge:", cyc.tolist())
+print("median cycles: receive wait, merge:", cyc.tolist())
