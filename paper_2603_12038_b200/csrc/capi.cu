@@ -170,8 +170,13 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   // streams per HBM channel); SFI_DENSE_SHARE_SM keeps 65% (192 CTAs on 148
   // SMs, the measured optimum of the asynchronous slow-step pipeline) and
   // leaves the rest to the Selector kernels running beside it
+  static const int env_share = [] {
+    const char* e = std::getenv("SFI_DENSE_SHARE_PERMILLE");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int share = (env_share > 0 && env_share <= 1000) ? env_share : 650;
   int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms(),
-                                   (flags & SFI_DENSE_SHARE_SM) ? 650 : 875);
+                                   (flags & SFI_DENSE_SHARE_SM) ? share : 875);
   static const int env_ctas = [] {
     const char* e = std::getenv("SFI_DECODE_CTAS");
     return e ? std::atoi(e) : 0;
