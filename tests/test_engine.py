@@ -124,6 +124,45 @@ def test_c8_trigger_replay_and_c9_segment_freezing():
     assert trig_slows > 0 and forced > 0
 
 
+def _compare(sfi, orc, sp, spec_d, seeds, rng, k, n_recent, t_max, steps, pool="mean"):
+    """Runs ours and the reference run_request; returns (identical streams, shared steps,
+    steps with identical selections, worst vocab-logit rel diff on those, slow-step Jaccards)."""
+    full = shared = same_sel_steps = 0
+    worst = 0.0
+    jacc = []
+    for seed in seeds:
+        model = sfi.ToyModel.random(sp, seed)
+        prompt = _prompt(rng, 48 + int(rng.integers(0, 48)))
+        lim = dict(n_sink=4, n_recent=n_recent, k_budget=k, t_max=t_max,
+                   trigger_tokens=[int(rng.integers(5, 256))], window_prefill=16)
+        opts = sfi.RunOptions()
+        opts.capture_selected = True
+        cfg = _selector(k)
+        cfg.pool = sfi.PoolMode.max if pool == "max" else sfi.PoolMode.mean
+        res = sfi.run_request(model, prompt, _limits(4, n_recent, k), _trigger(lim["trigger_tokens"], t_max),
+                              cfg, steps, opts)
+        ref = orc.toy_run_request(spec_d, seed, prompt, lim, orc_cfg(k, pool=1 if pool == "max" else 0), steps)
+        ours = np.array(res.tokens)
+        # steps whose inputs agree: every earlier token identical
+        n = steps if np.array_equal(ours, ref["tokens"]) else int(np.argmax(ours != ref["tokens"])) + 1
+        full += n == steps
+        shared += n
+        slow = np.array([r.slow for r in res.log], np.int32)
+        assert np.array_equal(slow[:n], ref["slow"][:n]), seed  # same schedule while the streams agree
+        lg = np.array(res.step_logits)
+        for t in range(n):
+            if t and slow[t]:
+                a = {(l, h, p) for l, x in enumerate(res.selected_per_step[t]) for h, y in enumerate(x) for p in y}
+                b = {(l, h, p) for l, x in enumerate(ref["selected"][t]) for h, y in enumerate(x) for p in y}
+                jacc.append(len(a & b) / max(1, len(a | b)))
+            # the step's support came from the previous step's selection
+            prev_same = t == 0 or res.selected_per_step[t - 1] == ref["selected"][t - 1]
+            if prev_same and res.selected_per_step[t] == ref["selected"][t]:
+                same_sel_steps += 1
+                worst = max(worst, np.abs(lg[t] - ref["logits"][t]).max() / np.abs(ref["logits"][t]).max())
+    return full, shared, same_sel_steps, worst, jacc
+
+
 @pytest.mark.gpu
 def test_run_request_vs_reference():
     import paper_2603_12038_b200 as sfi
@@ -131,52 +170,42 @@ def test_run_request_vs_reference():
     orc = oracle()
     if orc.kind != "reference":
         pytest.skip("reference library not built")
-    rng = np.random.default_rng(31337)
     runs, steps = 8, 32
-    full = same_sel_steps = shared = 0
-    worst_same_sel = 0.0
-    jacc = []
-    for run in range(runs):
-        seed = 4200 + run
-        model = sfi.ToyModel.random(_spec(), seed)
-        prompt = _prompt(rng, 48 + int(rng.integers(0, 48)))
-        lim = dict(n_sink=4, n_recent=12, k_budget=24, t_max=9, trigger_tokens=[int(rng.integers(5, 256))],
-                   window_prefill=16)
-        opts = sfi.RunOptions()
-        opts.capture_selected = True
-        res = sfi.run_request(model, prompt, _limits(4, 12, 24), _trigger(lim["trigger_tokens"], 9),
-                              _selector(24), steps, opts)
-        ref = orc.toy_run_request(SPEC, seed, prompt, lim, orc_cfg(24), steps)
-        ours = np.array(res.tokens)
-        # steps whose inputs agree: every earlier token identical
-        n = steps if np.array_equal(ours, ref["tokens"]) else int(np.argmax(ours != ref["tokens"])) + 1
-        full += n == steps
-        shared += n
-        slow = np.array([r.slow for r in res.log], np.int32)
-        assert np.array_equal(slow[:n], ref["slow"][:n]), run  # same schedule while the streams agree
-        lg = np.array(res.step_logits)
-        for t in range(n):
-            same = res.selected_per_step[t] == ref["selected"][t]
-            if t and slow[t]:
-                a = {(l, h, p) for l, x in enumerate(res.selected_per_step[t]) for h, y in enumerate(x) for p in y}
-                b = {(l, h, p) for l, x in enumerate(ref["selected"][t]) for h, y in enumerate(x) for p in y}
-                jacc.append(len(a & b) / max(1, len(a | b)))
-            # the step's support came from the previous step's selection
-            prev_same = t == 0 or res.selected_per_step[t - 1] == ref["selected"][t - 1]
-            if prev_same and same:
-                same_sel_steps += 1
-                rel = np.abs(lg[t] - ref["logits"][t]).max() / np.abs(ref["logits"][t]).max()
-                worst_same_sel = max(worst_same_sel, rel)
+    full, shared, same, worst, jacc = _compare(sfi, orc, _spec(), SPEC, [4200 + r for r in range(runs)],
+                                               np.random.default_rng(31337), 24, 12, 9, steps)
     print(f"\nrun_request vs reference: {full}/{runs} token streams identical over {steps} steps; "
-          f"{shared} shared steps, {same_sel_steps} with identical selections: worst vocab-logit rel diff "
-          f"{worst_same_sel:.2e}; slow-step selection Jaccard mean {np.mean(jacc):.3f} min {np.min(jacc):.3f}")
+          f"{shared} shared steps, {same} with identical selections: worst vocab-logit rel diff "
+          f"{worst:.2e}; slow-step selection Jaccard mean {np.mean(jacc):.3f} min {np.min(jacc):.3f}")
     # bf16 KV (device) vs fp32 KV (reference): logits agree to bf16 rounding where the supports agree
-    assert worst_same_sel < 1e-2
+    assert worst < 1e-2
     assert np.mean(jacc) > 0.8
     assert full >= runs // 2
 
 
-def orc_cfg(k):
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,pool", [((2, 16, 1, 128), "max"), ((3, 16, 4, 128), "mean")])
+def test_run_request_vs_reference_shapes(shape, pool):
+    """Other GQA groups / head dims / pooling: G = 16 with d = 128 and max pooling, G = 4 over 3 layers."""
+    import paper_2603_12038_b200 as sfi
+
+    orc = oracle()
+    if orc.kind != "reference":
+        pytest.skip("reference library not built")
+    L, Hq, H, d = shape
+    spec_d = dict(SPEC, n_layers=L, n_query_heads=Hq, n_kv_heads=H, head_dim=d)
+    sp = sfi.ModelSpec()
+    for k, v in spec_d.items():
+        setattr(sp, k, v)
+    full, shared, same, worst, jacc = _compare(sfi, orc, sp, spec_d, [5100, 5101, 5102],
+                                               np.random.default_rng(77 + L), 16, 16, 7, 24, pool)
+    print(f"\n{shape} {pool}: {full}/3 identical, {same}/{shared} steps with identical selections, "
+          f"worst rel {worst:.2e}, Jaccard {np.mean(jacc):.3f}")
+    assert worst < 1e-2
+    assert np.mean(jacc) > 0.8
+    assert full >= 2
+
+
+def orc_cfg(k, **kw):
     from oracle import oracle as O
 
-    return O.make_cfg(k_budget=k)
+    return O.make_cfg(k_budget=k, **kw)
