@@ -167,8 +167,17 @@ class Workload:
         elif self.mode == "seq":
             from paper_2603_12038_b200.sharded import SeqShardedSfi
 
-            self.drv = SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx, self.ns,
-                                     self.K, self.R, device=device)
+            # per-step (O, LSE) exchange through peer memory (CUDA IPC over NVLink,
+            # sfi_peer_merge) unless SFI_SEQ_EXCHANGE=allgather or the mapping fails
+            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "peer") == "peer"
+            try:
+                self.drv = SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx, self.ns,
+                                         self.K, self.R, device=device, peer=self.peer)
+            except Exception as e:  # pragma: no cover - depends on the box's P2P / IPC support
+                print(f"peer exchange unavailable ({e}); using all-gather", file=sys.stderr)
+                self.peer = False
+                self.drv = SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx, self.ns,
+                                         self.K, self.R, device=device)
             fill_len = min(self.drv.cap, self.ctx - self.drv.base)  # this rank's positions
         else:
             self.drv = sfi.SfiCache(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
@@ -255,10 +264,11 @@ class Workload:
 
     def launches(self, slow: bool) -> int:
         """Our kernels per step (collectives' own kernels not counted)."""
+        xch = 3 if getattr(self, "peer", False) else 2  # partial (+ publish) + merge
         if not slow:  # advance + one fused launch per layer (+ the LSE merge when sequence-sharded)
-            return 1 + self.L * (2 if self.mode == "seq" else 1)
+            return 1 + self.L * (xch if self.mode == "seq" else 1)
         if self.mode == "seq":  # append (last rank), dense + merge, Selector 2 stats + finish 3 + pick 3, compact
-            return 1 + self.L * (1 + 2 + 8 + 1)
+            return 1 + self.L * (1 + xch + 8 + 1)
         if self.mode == "heads":  # append, dense, Selector fuse + refine + top-k, compact
             return 1 + self.L * 6
         return 1 + self.L * 7  # append, dense, Selector pw + coef + z + top-k, compact
@@ -576,8 +586,9 @@ def gpu_arm(args) -> dict:
                    "schedule": f"seeded triggers p=1/24 + t_max={T_MAX}; {n_slow} slow / {K} steps",
                    "parallelism": {
                        "heads": f"kv-head sharded x{world} (one batch; z_base all-gather per slow-step layer)",
-                       "seq": f"sequence sharded x{world} (LSE-merged partials; sharded Selector stats, "
-                              "soft-NMS edges, top-k candidate merge)",
+                       "seq": f"sequence sharded x{world} (LSE-merged partials via "
+                              + ("peer memory, CUDA IPC over NVLink" if getattr(wl, "peer", False) else "all-gather")
+                              + "; sharded Selector stats, soft-NMS edges, top-k candidate merge)",
                    }.get(wl.mode, f"dp{world} (independent request batches)"),
                    "cuda_graphs": use_graph if graph_note is None else graph_note,
                    "slow_step": "synchronous" if wl.pipe is None else

@@ -268,6 +268,22 @@ SFI_API int sfi_fast_decode_partial(const sfi_shape* shape, const sfi_cache* cac
  * all-gathered partials: o_parts [n_parts][rows][head_dim], lse [n_parts][rows]). */
 SFI_API int sfi_merge_partials(int32_t n_parts, int32_t rows, int32_t head_dim, const float* o_parts,
                                const float* lse_parts, float* out, void* stream);
+
+/* Peer-memory partial exchange (sequence sharding over NVLink P2P, no
+ * collective launch): every rank maps every other rank's partial buffers and
+ * epoch flag (CUDA IPC handles exchanged once).
+ *   sfi_peer_publish: after the partial producer on `stream`, bumps this rank's
+ *     flag (system-scope release).
+ *   sfi_peer_merge: waits until every rank's flag reached this rank's own flag
+ *     (acquire), then merges the n_parts partials read in place, in rank order
+ *     (o_ptrs[i] fp32 [rows][head_dim], lse_ptrs[i] fp32 [rows]; device arrays of
+ *     device pointers) — bit-identical to sfi_merge_partials on gathered copies.
+ * A rank may rewrite a partial buffer once every rank has merged it: with one
+ * buffer per layer (>= 2 layers) the stream order guarantees it. */
+SFI_API int sfi_peer_publish(int32_t* flag, void* stream);
+SFI_API int sfi_peer_merge(int32_t n_parts, int32_t rows, int32_t head_dim, const float* const* o_ptrs,
+                           const float* const* lse_ptrs, const int32_t* const* flag_ptrs, const int32_t* my_flag,
+                           float* out, void* stream);
 /* Sequence-sharded Selector, decode path (W = 1, alpha = 1), per layer, three
  * exchanges:
  *   stats phase 1 -> row_stats [B*H][6]: local max and the five sums of

@@ -394,6 +394,16 @@ PYBIND11_MODULE(_sfi_b200, m) {
     check(sfi_merge_partials(n_parts, rows, d, static_cast<const float*>(vp(o)), static_cast<const float*>(vp(lse)),
                              static_cast<float*>(vp(out)), vp(stream)));
   });
+  m.def("peer_publish", [](std::uintptr_t flag, std::uintptr_t stream) {
+    check(sfi_peer_publish(static_cast<int32_t*>(vp(flag)), vp(stream)));
+  });
+  m.def("peer_merge", [](int n_parts, int rows, int d, std::uintptr_t o_ptrs, std::uintptr_t lse_ptrs,
+                         std::uintptr_t flag_ptrs, std::uintptr_t my_flag, std::uintptr_t out, std::uintptr_t stream) {
+    check(sfi_peer_merge(n_parts, rows, d, static_cast<const float* const*>(vp(o_ptrs)),
+                         static_cast<const float* const*>(vp(lse_ptrs)),
+                         static_cast<const int32_t* const*>(vp(flag_ptrs)), static_cast<const int32_t*>(vp(my_flag)),
+                         static_cast<float*>(vp(out)), vp(stream)));
+  });
   m.def("seq_edges_doubles", [](const sfi_shape& s, const sfi_selector_params& prm) {
     return sfi_seq_edges_doubles(&s, &prm);
   });

@@ -299,7 +299,69 @@ __global__ void merge_partials_kernel(int n_parts, int rows, int D, const float*
   }
 }
 
+// ---- peer-memory partial exchange (sequence sharding over NVLink P2P) ----
+// Every rank's partial slots and its epoch flag live in memory all ranks have
+// mapped (CUDA IPC handles; peer loads/stores over NVLink). A rank publishes a
+// partial by bumping its flag with a system-scope release after the kernel
+// that wrote it; a merging rank acquires every peer flag up to its own epoch
+// and reads the partials in place — no collective launch, no staging copy.
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void peer_publish_kernel(int32_t* flag) {
+  griddep_wait();  // the partial producer before us on the stream has completed
+  if (threadIdx.x == 0) asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(flag) : "memory");
+}
+
+// Same arithmetic and rank order as merge_partials_kernel: the merged output is
+// bit-identical to the all-gather path.
+__global__ void peer_merge_kernel(int n_parts, int rows, int D, const float* const* o_ptrs,
+                                  const float* const* lse_ptrs, const int32_t* const* flags,
+                                  const int32_t* my_flag, float* out) {
+  griddep_wait();
+  __shared__ const float* so[kMaxPeers];
+  __shared__ const float* sl[kMaxPeers];
+  if (threadIdx.x == 0) {
+    const int epoch = ld_acquire_sys(my_flag);  // this rank's own publish, earlier on the stream
+    for (int i = 0; i < n_parts; ++i) {
+      while (ld_acquire_sys(flags[i]) < epoch) __nanosleep(64);
+      so[i] = o_ptrs[i];
+      sl[i] = lse_ptrs[i];
+    }
+  }
+  __syncthreads();
+  griddep_launch();
+  const int row = blockIdx.x;
+  float M = -INFINITY;
+  for (int i = 0; i < n_parts; ++i) M = fmaxf(M, sl[i][row]);
+  const float Mu = M == -INFINITY ? 0.f : M;
+  float S = 0.f;
+  for (int i = 0; i < n_parts; ++i) S += __expf(sl[i][row] - Mu);
+  const float inv = S > 0.f ? 1.f / S : 0.f;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+    for (int i = 0; i < n_parts; ++i) {
+      const float w = __expf(sl[i][row] - Mu);
+      acc += w * so[i][(size_t)row * D + d];
+    }
+    out[(size_t)row * D + d] = acc * inv;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_peer_publish(int32_t* flag, cudaStream_t st) {
+  return launch_k(peer_publish_kernel, dim3(1), dim3(32), 0, st, flag);
+}
+
+cudaError_t launch_peer_merge(int n_parts, int rows, int D, const float* const* o_ptrs, const float* const* lse_ptrs,
+                              const int32_t* const* flags, const int32_t* my_flag, float* out, cudaStream_t st) {
+  return launch_k(peer_merge_kernel, dim3(rows), dim3(D < 128 ? D : 128), 0, st, n_parts, rows, D, o_ptrs, lse_ptrs,
+                  flags, my_flag, out);
+}
 
 cudaError_t launch_seq_lengths(const sfi_shape& s, const sfi_cache& c, int32_t* g_prefix, const int32_t* g_nsink,
                                int32_t* g_recent, int advance, int base, int is_last, int32_t* j_off,

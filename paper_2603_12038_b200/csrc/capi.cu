@@ -638,6 +638,29 @@ SFI_API int sfi_merge_partials(int32_t n_parts, int32_t rows, int32_t head_dim, 
   return SFI_OK;
 }
 
+SFI_API int sfi_peer_publish(int32_t* flag, void* stream) {
+  g_launches = 0;
+  if (!flag) return fail(SFI_ERR_INVALID_ARGUMENT, "peer_publish: null flag");
+  SFI_CUDA(sfi_impl::launch_peer_publish(flag, (cudaStream_t)stream), "sfi_peer_publish");
+  g_launches = 1;
+  return SFI_OK;
+}
+
+SFI_API int sfi_peer_merge(int32_t n_parts, int32_t rows, int32_t head_dim, const float* const* o_ptrs,
+                           const float* const* lse_ptrs, const int32_t* const* flag_ptrs, const int32_t* my_flag,
+                           float* out, void* stream) {
+  g_launches = 0;
+  if (n_parts < 1 || n_parts > sfi_impl::kMaxPeers || rows < 0 || head_dim < 1 || !o_ptrs || !lse_ptrs ||
+      !flag_ptrs || !my_flag || !out)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "peer_merge: bad argument");
+  if (rows == 0) return SFI_OK;
+  SFI_CUDA(sfi_impl::launch_peer_merge(n_parts, rows, head_dim, o_ptrs, lse_ptrs, flag_ptrs, my_flag, out,
+                                       (cudaStream_t)stream),
+           "sfi_peer_merge");
+  g_launches = 1;
+  return SFI_OK;
+}
+
 static int seq_selector_check(const sfi_shape* s, const sfi_cache* c, int32_t layer,
                               const sfi_selector_params* prm) {
   int rc = validate(s);

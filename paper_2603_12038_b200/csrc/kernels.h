@@ -131,6 +131,10 @@ cudaError_t launch_topk_explicit(int rows, int n, int K, const double* scores, c
 cudaError_t launch_seq_lengths(const sfi_shape& s, const sfi_cache& c, int32_t* g_prefix, const int32_t* g_nsink,
                                int32_t* g_recent, int advance, int base, int is_last, int32_t* j_off,
                                int32_t* n_glob, cudaStream_t st);
+constexpr int kMaxPeers = 64;
+cudaError_t launch_peer_publish(int32_t* flag, cudaStream_t st);
+cudaError_t launch_peer_merge(int n_parts, int rows, int D, const float* const* o_ptrs, const float* const* lse_ptrs,
+                              const int32_t* const* flags, const int32_t* my_flag, float* out, cudaStream_t st);
 cudaError_t launch_merge_partials(int n_parts, int rows, int D, const float* o_parts, const float* lse_parts,
                                   float* out, cudaStream_t st);
 cudaError_t launch_seq_selector_stats(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,

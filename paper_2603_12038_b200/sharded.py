@@ -40,6 +40,86 @@ def all_gather_blocks(local: torch.Tensor, out: torch.Tensor, group=None) -> tor
     return out
 
 
+def _enable_peer_access(world: int) -> None:
+    """Maps every visible GPU into this process's device (NVLink P2P), so IPC
+    buffers opened in another device's context are addressable from kernels on
+    ours. One process per GPU: a no-op on a single device."""
+    n = min(world, torch.cuda.device_count())
+    if n < 2:
+        return
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:  # pragma: no cover - cuda-python ships in the image
+        from cuda import cudart as rt
+    me = torch.cuda.current_device()
+    for other in range(n):
+        if other != me and torch.cuda.can_device_access_peer(me, other):
+            rt.cudaDeviceEnablePeerAccess(other, 0)  # "already enabled" is fine
+
+
+class PeerExchange:
+    """Sequence-shard partial exchange over peer memory (no collective launch).
+
+    Each rank owns `slots` partial buffers (o fp32 [rows][d], lse fp32 [rows])
+    and an epoch flag, allocated from the CUDA caching allocator and shared with
+    every rank once through CUDA IPC handles (torch.multiprocessing reductions,
+    exchanged with all_gather_object). Per exchange a rank writes its partial into
+    slot s, bumps its flag (sfi_peer_publish) and merges every rank's slot s in
+    place (sfi_peer_merge: acquire the peer flags, read over NVLink, rank order).
+    `peers` (lockstep tests in one process): the other shards' PeerExchange
+    objects, used directly instead of IPC."""
+
+    def __init__(self, world: int, rank: int, slots: int, rows: int, d: int, device, group=None,
+                 peers: list | None = None):
+        from . import _sfi_b200 as _C
+
+        if slots < 2:
+            raise ValueError("peer exchange needs >= 2 partial slots (one per layer)")
+        self._C, self.world, self.rank, self.slots, self.rows, self.d = _C, world, rank, slots, rows, d
+        self.o = torch.zeros(slots, rows, d, dtype=torch.float32, device=device)
+        self.lse = torch.zeros(slots, rows, dtype=torch.float32, device=device)
+        self.flag = torch.zeros(64, dtype=torch.int32, device=device)  # [0] used; own 256 B line
+        self._peer_views = None
+        if peers is None:
+            self.connect(self._exchange_handles(group))
+
+    def _exchange_handles(self, group):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        _enable_peer_access(self.world)
+        mine = [reduce_tensor(t) for t in (self.o, self.lse, self.flag)]
+        objs = [None] * self.world
+        dist.all_gather_object(objs, mine, group=group)
+        views = []
+        for r, rec in enumerate(objs):
+            views.append((self.o, self.lse, self.flag) if r == self.rank else tuple(fn(*args) for fn, args in rec))
+        return views
+
+    def connect(self, views):
+        """views[r] = (o, lse, flag) of rank r as addressable from this process."""
+        self._peer_views = views  # keeps the IPC mappings alive
+        dev = self.o.device
+        ptr = lambda xs: torch.tensor(xs, dtype=torch.int64, device=dev)  # noqa: E731
+        self.o_ptrs = ptr([[v[0][s].data_ptr() for v in views] for s in range(self.slots)])
+        self.lse_ptrs = ptr([[v[1][s].data_ptr() for v in views] for s in range(self.slots)])
+        self.flag_ptrs = ptr([v[2].data_ptr() for v in views])
+
+    def publish(self, stream: int):
+        self._C.peer_publish(self.flag.data_ptr(), stream)
+
+    def merge(self, slot: int, out_ptr: int, stream: int):
+        self._C.peer_merge(self.world, self.rows, self.d, self.o_ptrs[slot].data_ptr(),
+                           self.lse_ptrs[slot].data_ptr(), self.flag_ptrs.data_ptr(), self.flag.data_ptr(),
+                           out_ptr, stream)
+
+
+def connect_lockstep(shards) -> None:
+    """Wires the PeerExchange of P lockstep shards of one process to each other."""
+    views = [(s.px.o, s.px.lse, s.px.flag) for s in shards]
+    for s in shards:
+        s.px.connect(views)
+
+
 class HeadShardedSfi:
     """This rank's shard of a KV-head-sharded SFI cache (n_layers x batch x
     n_kv_heads/P heads). Same step API as SfiCache; only the Selector talks to
@@ -107,7 +187,10 @@ class SeqShardedSfi:
     def __init__(self, n_layers: int, batch: int, n_kv_heads: int, n_q_heads: int, head_dim: int,
                  max_positions: int, prompt_len: int, n_sink: int = 4, k_budget: int = 2048,
                  n_recent: int = 256, group=None, device=None, world: int | None = None,
-                 rank: int | None = None):
+                 rank: int | None = None, peer: bool = False, peers: list | None = None):
+        """peer=True: the per-step (O, LSE) exchange goes through PeerExchange
+        (peer memory, no collective launch); `peers` wires lockstep shards of
+        one process to each other instead of through IPC."""
         from . import _sfi_b200 as _C
 
         self._C = _C
@@ -145,6 +228,12 @@ class SeqShardedSfi:
         self.o_all = z(P, B, Hq, head_dim, dt=torch.float32)
         self.lse_all = z(P, B, Hq, dt=torch.float32)
         self.n_recent = n_recent
+        self.px = None
+        if peer or peers is not None:
+            if n_layers < 2:  # a slot may only be rewritten once every rank merged it
+                raise ValueError("peer exchange keeps one partial slot per layer: needs >= 2 layers")
+            self.px = PeerExchange(P, self.rank, max(2, n_layers), B * Hq, head_dim, dev, group,
+                                   peers=[] if peers is not None else None)
 
     # -- lengths -------------------------------------------------------------
     def set_lengths(self, prefix_len, n_sink_b):
@@ -169,19 +258,34 @@ class SeqShardedSfi:
         self._lengths(1)
 
     # -- attention partials ----------------------------------------------------
+    def _part_ptrs(self, layer):
+        if self.px is None:
+            return self.o_part.data_ptr(), self.lse_part.data_ptr()
+        slot = layer % self.px.slots
+        return self.px.o[slot].data_ptr(), self.px.lse[slot].data_ptr()
+
     def dense_partial(self, layer, q, logits, pool=0):
         c = self.cache
-        self._C.dense_decode_partial(c.shape, c.cache, layer, c._ptr(q, torch.float32), self.o_part.data_ptr(),
-                                     self.lse_part.data_ptr(), c._ptr(logits, torch.float32), pool, c._stream())
+        o, lse = self._part_ptrs(layer)
+        self._C.dense_decode_partial(c.shape, c.cache, layer, c._ptr(q, torch.float32), o, lse,
+                                     c._ptr(logits, torch.float32), pool, c._stream())
+        if self.px is not None:
+            self.px.publish(c._stream())
 
     def fast_partial(self, layer, q, k_new, v_new, prefetch=False):
         c = self.cache
         own = self.is_last  # the current position is on the last shard
+        o, lse = self._part_ptrs(layer)
         self._C.fast_decode_partial(c.shape, c.cache, layer, c._ptr(q, torch.float32),
                                     c._ptr(k_new, torch.bfloat16) if own else 0,
-                                    c._ptr(v_new, torch.bfloat16) if own else 0, self.o_part.data_ptr(),
-                                    self.lse_part.data_ptr(), self._C.FAST_PREFETCH if prefetch else 0,
-                                    c._stream())
+                                    c._ptr(v_new, torch.bfloat16) if own else 0, o, lse,
+                                    self._C.FAST_PREFETCH if prefetch else 0, c._stream())
+        if self.px is not None:
+            self.px.publish(c._stream())
+
+    def peer_merge(self, layer, out):
+        """out = LSE merge of every rank's partial of `layer`, read in place from peer memory."""
+        self.px.merge(layer % self.px.slots, self.cache._ptr(out, torch.float32), self.cache._stream())
 
     def merge(self, out):
         """out = LSE merge of the gathered partials (o_all, lse_all) in rank order."""
@@ -195,11 +299,17 @@ class SeqShardedSfi:
 
     def dense_decode(self, layer, q, out, logits, pool=0):
         self.dense_partial(layer, q, logits, pool)
+        if self.px is not None:
+            self.peer_merge(layer, out)
+            return
         self._exchange_partials()
         self.merge(out)
 
     def fast_decode(self, layer, q, k_new, v_new, out, prefetch=False):
         self.fast_partial(layer, q, k_new, v_new, prefetch)
+        if self.px is not None:
+            self.peer_merge(layer, out)
+            return
         self._exchange_partials()
         self.merge(out)
 

@@ -221,6 +221,140 @@ def test_sequence_sharded_two_processes_one_gpu():
     assert res == {0: True, 1: True}, res
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3])
+def test_sequence_sharded_peer_exchange_lockstep(P):
+    """Peer-memory (O, LSE) exchange (sfi_peer_publish / sfi_peer_merge) over 2 layers
+    and 3 steps: bit-identical to merging gathered copies, within 2e-3 of 1 GPU."""
+    from paper_2603_12038_b200 import SelectorParams, SfiCache
+    from paper_2603_12038_b200.sharded import SeqShardedSfi, connect_lockstep
+
+    B, H, Hq, d, prompt, K, R, ns, NL = 1, 4, 16, 128, 7000, 256, 256, 4, 2
+    Lmax = prompt + 16
+    full = SfiCache(NL, B, H, Hq, d, Lmax, ns, K, R)
+    full.fill_synthetic(seed=9, length=prompt)
+    shards = [SeqShardedSfi(NL, B, H, Hq, d, Lmax, prompt, ns, K, R, world=P, rank=r, peers=[]) for r in range(P)]
+    connect_lockstep(shards)
+    for s in shards:
+        n = min(s.cap, Lmax - s.base)
+        s.k_cache[:, :, :, :n].copy_(full.k_cache[:, :, :, s.base:s.base + n])
+        s.v_cache[:, :, :, :n].copy_(full.v_cache[:, :, :, s.base:s.base + n])
+        s.key_norms[:, :, :, :n].copy_(full.key_norms[:, :, :, s.base:s.base + n])
+        s.set_lengths([prompt] * B, [ns] * B)
+    full.set_lengths([prompt] * B, [ns] * B)
+    g = torch.Generator().manual_seed(P)
+    for step, slow in enumerate((True, False, False)):
+        full.step_advance()
+        for s in shards:
+            s.step_advance()
+        for layer in range(NL):
+            q = torch.randn(B, Hq, d, generator=g).cuda()
+            kn = torch.randn(B, H, d, generator=g).bfloat16().cuda()
+            o_full = torch.zeros(B, Hq, d, device="cuda")
+            outs = [torch.zeros_like(o_full) for _ in shards]
+            if slow:
+                full.ring_append(layer, kn, kn)
+                lg_full = torch.zeros_like(full.pooled_logits)
+                full.dense_decode(layer, q, o_full, lg_full, 0)
+                full.selector(layer, lg_full, SelectorParams())
+                full.compact_build(layer, rebuild_ring=True)
+                lgs = [torch.zeros_like(s.pooled_logits) for s in shards]
+                for s, lg in zip(shards, lgs):
+                    s.ring_append(layer, kn, kn)
+                    s.dense_partial(layer, q, lg)  # + publish
+            else:
+                full.fast_decode(layer, q, kn, kn, o_full)
+                for s in shards:
+                    s.fast_partial(layer, q, kn, kn)  # + publish
+            for s, o in zip(shards, outs):
+                s.peer_merge(layer, o)
+            # the same partials through the gather path
+            slot = layer % shards[0].px.slots
+            o_all = torch.stack([s.px.o[slot] for s in shards]).contiguous()
+            lse_all = torch.stack([s.px.lse[slot] for s in shards]).contiguous()
+            ref = torch.zeros_like(o_full)
+            shards[0]._C.merge_partials(P, B * Hq, d, o_all.data_ptr(), lse_all.data_ptr(), ref.data_ptr(),
+                                        torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            for o in outs:
+                assert torch.equal(o, ref), (step, layer)
+                assert rel_err(o.cpu().numpy(), o_full.cpu().numpy()) < TOL, (step, layer)
+            if slow:
+                _selector(shards, layer, lambda s: lgs[shards.index(s)])
+                for s in shards:
+                    s.compact_build(layer, rebuild_ring=True)
+    for s in shards:
+        s.check_errors()
+    assert all(int(s.px.flag[0]) == 3 * NL for s in shards)
+
+
+def _seq_peer_worker(rank, world, port, q):
+    """Two processes on one GPU: partials exchanged through CUDA IPC mappings
+    (PeerExchange), against the gather path in the same process and 1 GPU."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2603_12038_b200 import SfiCache
+        from paper_2603_12038_b200.sharded import SeqShardedSfi
+
+        B, H, Hq, d, prompt, K, R, ns, NL = 1, 4, 16, 128, 6000, 256, 256, 4, 2
+        Lmax = prompt + 16
+        full = SfiCache(NL, B, H, Hq, d, Lmax, ns, K, R)
+        full.fill_synthetic(seed=3, length=prompt)  # identical on every rank
+        shp = SeqShardedSfi(NL, B, H, Hq, d, Lmax, prompt, ns, K, R, peer=True)
+        shg = SeqShardedSfi(NL, B, H, Hq, d, Lmax, prompt, ns, K, R)
+        for sh in (shp, shg):
+            n = min(sh.cap, Lmax - sh.base)
+            sh.k_cache[:, :, :, :n].copy_(full.k_cache[:, :, :, sh.base:sh.base + n])
+            sh.v_cache[:, :, :, :n].copy_(full.v_cache[:, :, :, sh.base:sh.base + n])
+            sh.key_norms[:, :, :, :n].copy_(full.key_norms[:, :, :, sh.base:sh.base + n])
+            sh.set_lengths([prompt], [ns])
+        full.set_lengths([prompt], [ns])
+        g = torch.Generator().manual_seed(8)
+        ok = True
+        for step in range(3):
+            full.step_advance()
+            for sh in (shp, shg):
+                sh.step_advance()
+            for layer in range(NL):
+                qv = torch.randn(B, Hq, d, generator=g).cuda()
+                kn = torch.randn(B, H, d, generator=g).bfloat16().cuda()
+                o_full, o_p, o_g = (torch.zeros(B, Hq, d, device="cuda") for _ in range(3))
+                full.ring_append(layer, kn, kn)
+                full.dense_decode(layer, qv, o_full, None, 0)
+                for sh, o in ((shp, o_p), (shg, o_g)):
+                    sh.ring_append(layer, kn, kn)
+                    sh.dense_decode(layer, qv, o, None, 0)
+                torch.cuda.synchronize()
+                ok &= torch.equal(o_p, o_g)
+                ok &= rel_err(o_p.cpu().numpy(), o_full.cpu().numpy()) < TOL
+        full.check_errors()
+        shp.check_errors()
+        q.put((rank, bool(ok)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+def test_sequence_sharded_peer_exchange_two_processes_one_gpu():
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seq_peer_worker, args=(r, 2, port, qu)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(qu.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
+
+
 # ------------------------------------------------------------- CPU, gloo ----
 
 def _np_case(seed=4, H=4, n=2500):
