@@ -267,8 +267,9 @@ class Workload:
         xch = 3 if getattr(self, "peer", False) else 2  # partial (+ publish) + merge
         if not slow:  # advance + one fused launch per layer (+ the LSE merge when sequence-sharded)
             return 1 + self.L * (xch if self.mode == "seq" else 1)
-        if self.mode == "seq":  # append (last rank), dense + merge, Selector 2 stats + finish 3 + pick 3, compact
-            return 1 + self.L * (1 + xch + 8 + 1)
+        if self.mode == "seq":  # append (last rank), dense + merge, Selector 2 stats + finish 3 + pick 3
+            # (+ 3 publishes and 4 peer gathers over peer memory), compact
+            return 1 + self.L * (1 + xch + (15 if getattr(self, "peer", False) else 8) + 1)
         if self.mode == "heads":  # append, dense, Selector fuse + refine + top-k, compact
             return 1 + self.L * 6
         return 1 + self.L * 7  # append, dense, Selector pw + coef + z + top-k, compact
@@ -586,9 +587,10 @@ def gpu_arm(args) -> dict:
                    "schedule": f"seeded triggers p=1/24 + t_max={T_MAX}; {n_slow} slow / {K} steps",
                    "parallelism": {
                        "heads": f"kv-head sharded x{world} (one batch; z_base all-gather per slow-step layer)",
-                       "seq": f"sequence sharded x{world} (LSE-merged partials via "
-                              + ("peer memory, CUDA IPC over NVLink" if getattr(wl, "peer", False) else "all-gather")
-                              + "; sharded Selector stats, soft-NMS edges, top-k candidate merge)",
+                       "seq": f"sequence sharded x{world} (LSE-merged partials and sharded Selector stats, "
+                              "soft-NMS edges, top-k candidates exchanged via "
+                              + ("peer memory: CUDA IPC over NVLink, no collective launch" if getattr(wl, "peer", False)
+                                 else "all-gather") + ")",
                    }.get(wl.mode, f"dp{world} (independent request batches)"),
                    "cuda_graphs": use_graph if graph_note is None else graph_note,
                    "slow_step": "synchronous" if wl.pipe is None else

@@ -281,6 +281,12 @@ SFI_API int sfi_merge_partials(int32_t n_parts, int32_t rows, int32_t head_dim, 
  * A rank may rewrite a partial buffer once every rank has merged it: with one
  * buffer per layer (>= 2 layers) the stream order guarantees it. */
 SFI_API int sfi_peer_publish(int32_t* flag, void* stream);
+/* All-gather over the same protocol: dst[r] = rank r's `bytes`-byte block
+ * (src_ptrs[r], device array of device pointers), read in place once rank r's
+ * flag reached this rank's (bytes a multiple of 4). Used for the sequence-sharded
+ * Selector's statistics, soft-NMS edges and top-k candidates. */
+SFI_API int sfi_peer_gather(int32_t n_parts, int64_t bytes, const void* const* src_ptrs,
+                            const int32_t* const* flag_ptrs, const int32_t* my_flag, void* dst, void* stream);
 SFI_API int sfi_peer_merge(int32_t n_parts, int32_t rows, int32_t head_dim, const float* const* o_ptrs,
                            const float* const* lse_ptrs, const int32_t* const* flag_ptrs, const int32_t* my_flag,
                            float* out, void* stream);

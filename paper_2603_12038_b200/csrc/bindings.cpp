@@ -397,6 +397,12 @@ PYBIND11_MODULE(_sfi_b200, m) {
   m.def("peer_publish", [](std::uintptr_t flag, std::uintptr_t stream) {
     check(sfi_peer_publish(static_cast<int32_t*>(vp(flag)), vp(stream)));
   });
+  m.def("peer_gather", [](int n_parts, int64_t bytes, std::uintptr_t src_ptrs, std::uintptr_t flag_ptrs,
+                          std::uintptr_t my_flag, std::uintptr_t dst, std::uintptr_t stream) {
+    check(sfi_peer_gather(n_parts, bytes, static_cast<const void* const*>(vp(src_ptrs)),
+                          static_cast<const int32_t* const*>(vp(flag_ptrs)), static_cast<const int32_t*>(vp(my_flag)),
+                          vp(dst), vp(stream)));
+  });
   m.def("peer_merge", [](int n_parts, int rows, int d, std::uintptr_t o_ptrs, std::uintptr_t lse_ptrs,
                          std::uintptr_t flag_ptrs, std::uintptr_t my_flag, std::uintptr_t out, std::uintptr_t stream) {
     check(sfi_peer_merge(n_parts, rows, d, static_cast<const float* const*>(vp(o_ptrs)),

@@ -351,7 +351,34 @@ __global__ void peer_merge_kernel(int n_parts, int rows, int D, const float* con
   }
 }
 
+// All-gather over peer memory: block (r, c) waits for rank r's flag to reach
+// this rank's epoch, then copies its part of rank r's block (32-bit words).
+__global__ void peer_gather_kernel(long long words, const uint32_t* const* src, const int32_t* const* flags,
+                                   const int32_t* my_flag, uint32_t* dst) {
+  griddep_wait();
+  const int r = blockIdx.x;
+  __shared__ const uint32_t* s_src;
+  if (threadIdx.x == 0) {
+    const int epoch = ld_acquire_sys(my_flag);
+    while (ld_acquire_sys(flags[r]) < epoch) __nanosleep(64);
+    s_src = src[r];
+  }
+  __syncthreads();
+  griddep_launch();
+  const uint32_t* in = s_src;
+  uint32_t* out = dst + (size_t)r * words;
+  for (long long i = (long long)blockIdx.y * blockDim.x + threadIdx.x; i < words; i += (long long)gridDim.y * blockDim.x)
+    out[i] = in[i];
+}
+
 }  // namespace
+
+cudaError_t launch_peer_gather(int n_parts, long long words, const uint32_t* const* src, const int32_t* const* flags,
+                               const int32_t* my_flag, uint32_t* dst, cudaStream_t st) {
+  const long long per = (words + 255) / 256;
+  const int chunks = (int)std::min<long long>(std::max<long long>(per / 8, 1), 64);
+  return launch_k(peer_gather_kernel, dim3(n_parts, chunks), dim3(256), 0, st, words, src, flags, my_flag, dst);
+}
 
 cudaError_t launch_peer_publish(int32_t* flag, cudaStream_t st) {
   return launch_k(peer_publish_kernel, dim3(1), dim3(32), 0, st, flag);

@@ -646,6 +646,19 @@ SFI_API int sfi_peer_publish(int32_t* flag, void* stream) {
   return SFI_OK;
 }
 
+SFI_API int sfi_peer_gather(int32_t n_parts, int64_t bytes, const void* const* src_ptrs,
+                            const int32_t* const* flag_ptrs, const int32_t* my_flag, void* dst, void* stream) {
+  g_launches = 0;
+  if (n_parts < 1 || bytes < 0 || (bytes & 3) || !src_ptrs || !flag_ptrs || !my_flag || !dst)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "peer_gather: bad argument (bytes must be a multiple of 4)");
+  if (bytes == 0) return SFI_OK;
+  SFI_CUDA(sfi_impl::launch_peer_gather(n_parts, bytes / 4, reinterpret_cast<const uint32_t* const*>(src_ptrs),
+                                        flag_ptrs, my_flag, static_cast<uint32_t*>(dst), (cudaStream_t)stream),
+           "sfi_peer_gather");
+  g_launches = 1;
+  return SFI_OK;
+}
+
 SFI_API int sfi_peer_merge(int32_t n_parts, int32_t rows, int32_t head_dim, const float* const* o_ptrs,
                            const float* const* lse_ptrs, const int32_t* const* flag_ptrs, const int32_t* my_flag,
                            float* out, void* stream) {

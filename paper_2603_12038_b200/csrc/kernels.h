@@ -133,6 +133,8 @@ cudaError_t launch_seq_lengths(const sfi_shape& s, const sfi_cache& c, int32_t* 
                                int32_t* n_glob, cudaStream_t st);
 constexpr int kMaxPeers = 64;
 cudaError_t launch_peer_publish(int32_t* flag, cudaStream_t st);
+cudaError_t launch_peer_gather(int n_parts, long long words, const uint32_t* const* src, const int32_t* const* flags,
+                               const int32_t* my_flag, uint32_t* dst, cudaStream_t st);
 cudaError_t launch_peer_merge(int n_parts, int rows, int D, const float* const* o_ptrs, const float* const* lse_ptrs,
                               const int32_t* const* flags, const int32_t* my_flag, float* out, cudaStream_t st);
 cudaError_t launch_merge_partials(int n_parts, int rows, int D, const float* o_parts, const float* lse_parts,

@@ -70,7 +70,7 @@ class PeerExchange:
     objects, used directly instead of IPC."""
 
     def __init__(self, world: int, rank: int, slots: int, rows: int, d: int, device, group=None,
-                 peers: list | None = None):
+                 peers: list | None = None, shared: dict | None = None):
         from . import _sfi_b200 as _C
 
         if slots < 2:
@@ -79,6 +79,7 @@ class PeerExchange:
         self.o = torch.zeros(slots, rows, d, dtype=torch.float32, device=device)
         self.lse = torch.zeros(slots, rows, dtype=torch.float32, device=device)
         self.flag = torch.zeros(64, dtype=torch.int32, device=device)  # [0] used; own 256 B line
+        self.shared = dict(shared or {})  # further blocks all-gathered in place (gather())
         self._peer_views = None
         if peers is None:
             self.connect(self._exchange_handles(group))
@@ -87,13 +88,16 @@ class PeerExchange:
         from torch.multiprocessing.reductions import reduce_tensor
 
         _enable_peer_access(self.world)
-        mine = [reduce_tensor(t) for t in (self.o, self.lse, self.flag)]
+        mine = [reduce_tensor(t) for t in self.local_views()]
         objs = [None] * self.world
         dist.all_gather_object(objs, mine, group=group)
         views = []
         for r, rec in enumerate(objs):
-            views.append((self.o, self.lse, self.flag) if r == self.rank else tuple(fn(*args) for fn, args in rec))
+            views.append(self.local_views() if r == self.rank else tuple(fn(*args) for fn, args in rec))
         return views
+
+    def local_views(self):
+        return (self.o, self.lse, self.flag, *self.shared.values())
 
     def connect(self, views):
         """views[r] = (o, lse, flag) of rank r as addressable from this process."""
@@ -103,9 +107,16 @@ class PeerExchange:
         self.o_ptrs = ptr([[v[0][s].data_ptr() for v in views] for s in range(self.slots)])
         self.lse_ptrs = ptr([[v[1][s].data_ptr() for v in views] for s in range(self.slots)])
         self.flag_ptrs = ptr([v[2].data_ptr() for v in views])
+        self.src_ptrs = {name: ptr([v[3 + i].data_ptr() for v in views]) for i, name in enumerate(self.shared)}
 
     def publish(self, stream: int):
         self._C.peer_publish(self.flag.data_ptr(), stream)
+
+    def gather(self, name: str, dst: torch.Tensor, stream: int):
+        """dst[r] = rank r's block `name`, read in place once rank r published."""
+        t = self.shared[name]
+        self._C.peer_gather(self.world, t.numel() * t.element_size(), self.src_ptrs[name].data_ptr(),
+                            self.flag_ptrs.data_ptr(), self.flag.data_ptr(), dst.data_ptr(), stream)
 
     def merge(self, slot: int, out_ptr: int, stream: int):
         self._C.peer_merge(self.world, self.rows, self.d, self.o_ptrs[slot].data_ptr(),
@@ -115,7 +126,7 @@ class PeerExchange:
 
 def connect_lockstep(shards) -> None:
     """Wires the PeerExchange of P lockstep shards of one process to each other."""
-    views = [(s.px.o, s.px.lse, s.px.flag) for s in shards]
+    views = [s.px.local_views() for s in shards]
     for s in shards:
         s.px.connect(views)
 
@@ -233,7 +244,9 @@ class SeqShardedSfi:
             if n_layers < 2:  # a slot may only be rewritten once every rank merged it
                 raise ValueError("peer exchange keeps one partial slot per layer: needs >= 2 layers")
             self.px = PeerExchange(P, self.rank, max(2, n_layers), B * Hq, head_dim, dev, group,
-                                   peers=[] if peers is not None else None)
+                                   peers=[] if peers is not None else None,
+                                   shared=dict(row_stats=self.row_stats, edges=self.edges,
+                                               cand_score=self.cand_score, cand_pos=self.cand_pos))
 
     # -- lengths -------------------------------------------------------------
     def set_lengths(self, prefix_len, n_sink_b):
@@ -341,6 +354,20 @@ class SeqShardedSfi:
 
     def selector(self, layer, logits, params=None):
         # three exchanges per layer: row statistics, soft-NMS edges, top-k candidates
+        if self.px is not None:  # over peer memory: publish, then gather in place
+            st = self.cache._stream()
+            self.sel_stats(layer, logits, 1, params)
+            self.px.publish(st)
+            self.px.gather("row_stats", self.stats_all, st)
+            self.sel_stats(layer, logits, 3, params)
+            self.px.publish(st)
+            self.px.gather("edges", self.edges_all, st)
+            self.sel_finish(layer, params)
+            self.px.publish(st)
+            self.px.gather("cand_score", self.cand_score_all, st)
+            self.px.gather("cand_pos", self.cand_pos_all, st)
+            self.sel_pick(layer)
+            return
         self.sel_stats(layer, logits, 1, params)
         all_gather_blocks(self.row_stats, self.stats_all, self.group)
         self.sel_stats(layer, logits, 3, params)

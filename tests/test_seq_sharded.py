@@ -279,13 +279,37 @@ def test_sequence_sharded_peer_exchange_lockstep(P):
             for o in outs:
                 assert torch.equal(o, ref), (step, layer)
                 assert rel_err(o.cpu().numpy(), o_full.cpu().numpy()) < TOL, (step, layer)
-            if slow:
-                _selector(shards, layer, lambda s: lgs[shards.index(s)])
+            if slow:  # the Selector's three exchanges over peer memory, in lockstep
+                st = torch.cuda.current_stream().cuda_stream
+                for s, lg in zip(shards, lgs):
+                    s.sel_stats(layer, lg, 1)
+                    s.px.publish(st)
+                for s in shards:
+                    s.px.gather("row_stats", s.stats_all, st)
+                for s, lg in zip(shards, lgs):
+                    s.sel_stats(layer, lg, 3)
+                    s.px.publish(st)
+                for s in shards:
+                    s.px.gather("edges", s.edges_all, st)
+                for s in shards:
+                    s.sel_finish(layer)
+                    s.px.publish(st)
+                for s in shards:
+                    s.px.gather("cand_score", s.cand_score_all, st)
+                    s.px.gather("cand_pos", s.cand_pos_all, st)
+                    s.sel_pick(layer)
+                torch.cuda.synchronize()
+                for b in range(B):
+                    for h in range(H):
+                        want = full.sel[layer, b, h, : int(full.n_sel[layer, b, h])].cpu()
+                        got = torch.cat([s.sel[layer, b, h, : int(s.n_sel[layer, b, h])].cpu() + s.base
+                                         for s in shards])
+                        assert torch.equal(got, want), (layer, b, h)
                 for s in shards:
                     s.compact_build(layer, rebuild_ring=True)
     for s in shards:
         s.check_errors()
-    assert all(int(s.px.flag[0]) == 3 * NL for s in shards)
+    assert all(int(s.px.flag[0]) == 3 * NL + 3 * NL for s in shards)  # partials + Selector exchanges
 
 
 def _seq_peer_worker(rank, world, port, q):
@@ -296,7 +320,7 @@ def _seq_peer_worker(rank, world, port, q):
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
-        from paper_2603_12038_b200 import SfiCache
+        from paper_2603_12038_b200 import SelectorParams, SfiCache
         from paper_2603_12038_b200.sharded import SeqShardedSfi
 
         B, H, Hq, d, prompt, K, R, ns, NL = 1, 4, 16, 128, 6000, 256, 256, 4, 2
@@ -323,13 +347,20 @@ def _seq_peer_worker(rank, world, port, q):
                 kn = torch.randn(B, H, d, generator=g).bfloat16().cuda()
                 o_full, o_p, o_g = (torch.zeros(B, Hq, d, device="cuda") for _ in range(3))
                 full.ring_append(layer, kn, kn)
-                full.dense_decode(layer, qv, o_full, None, 0)
+                lg_f = torch.zeros_like(full.pooled_logits)
+                full.dense_decode(layer, qv, o_full, lg_f, 0)
+                full.selector(layer, lg_f, SelectorParams())
+                sels = []
                 for sh, o in ((shp, o_p), (shg, o_g)):
                     sh.ring_append(layer, kn, kn)
-                    sh.dense_decode(layer, qv, o, None, 0)
+                    lg = torch.zeros_like(sh.pooled_logits)
+                    sh.dense_decode(layer, qv, o, lg, 0)
+                    sh.selector(layer, lg)  # peer-memory exchanges for shp, all-gathers for shg
+                    sels.append((sh.sel[layer].clone(), sh.n_sel[layer].clone()))
                 torch.cuda.synchronize()
                 ok &= torch.equal(o_p, o_g)
                 ok &= rel_err(o_p.cpu().numpy(), o_full.cpu().numpy()) < TOL
+                ok &= torch.equal(sels[0][0], sels[1][0]) and torch.equal(sels[0][1], sels[1][1])
         full.check_errors()
         shp.check_errors()
         q.put((rank, bool(ok)))
