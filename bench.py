@@ -161,8 +161,15 @@ class Workload:
         if self.mode == "heads":
             from paper_2603_12038_b200.sharded import HeadShardedSfi
 
-            self.drv = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
-                                      self.K, self.R, device=device)
+            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "peer") == "peer"
+            try:  # z_base exchange in place over peer memory (CUDA IPC), else all-gather
+                self.drv = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
+                                          self.K, self.R, device=device, peer=self.peer)
+            except Exception as e:  # pragma: no cover - depends on the box's P2P / IPC support
+                print(f"peer exchange unavailable ({e}); using all-gather", file=sys.stderr)
+                self.peer = False
+                self.drv = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
+                                          self.K, self.R, device=device)
             self.H, self.Hq = self.drv.local_heads, self.drv.local_heads * self.G  # this rank's heads
         elif self.mode == "seq":
             from paper_2603_12038_b200.sharded import SeqShardedSfi
@@ -270,8 +277,8 @@ class Workload:
         if self.mode == "seq":  # append (last rank), dense + merge, Selector 2 stats + finish 3 + pick 3
             # (+ 3 publishes and 4 peer gathers over peer memory), compact
             return 1 + self.L * (1 + xch + (15 if getattr(self, "peer", False) else 8) + 1)
-        if self.mode == "heads":  # append, dense, Selector fuse + refine + top-k, compact
-            return 1 + self.L * 6
+        if self.mode == "heads":  # append, dense, Selector fuse + refine + top-k, compact (+ copy, publish, gather)
+            return 1 + self.L * (6 + (3 if getattr(self, "peer", False) else 0))
         return 1 + self.L * 7  # append, dense, Selector pw + coef + z + top-k, compact
 
     def shard_frac(self) -> float:  # this rank's share of a layer's rows (sequence shards)
@@ -586,7 +593,9 @@ def gpu_arm(args) -> dict:
                    "context": wl.ctx, "n_sink": wl.ns, "k_budget": wl.K, "n_recent": wl.R,
                    "schedule": f"seeded triggers p=1/24 + t_max={T_MAX}; {n_slow} slow / {K} steps",
                    "parallelism": {
-                       "heads": f"kv-head sharded x{world} (one batch; z_base all-gather per slow-step layer)",
+                       "heads": f"kv-head sharded x{world} (one batch; z_base per slow-step layer exchanged via "
+                                + ("peer memory: CUDA IPC over NVLink" if getattr(wl, "peer", False) else "all-gather")
+                                + ")",
                        "seq": f"sequence sharded x{world} (LSE-merged partials and sharded Selector stats, "
                               "soft-NMS edges, top-k candidates exchanged via "
                               + ("peer memory: CUDA IPC over NVLink, no collective launch" if getattr(wl, "peer", False)

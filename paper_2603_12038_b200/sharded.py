@@ -58,10 +58,11 @@ def _enable_peer_access(world: int) -> None:
 
 
 class PeerExchange:
-    """Sequence-shard partial exchange over peer memory (no collective launch).
+    """Shard exchanges over peer memory (no collective launch).
 
-    Each rank owns `slots` partial buffers (o fp32 [rows][d], lse fp32 [rows])
-    and an epoch flag, allocated from the CUDA caching allocator and shared with
+    Each rank owns `slots` attention-partial buffers (o fp32 [rows][d], lse fp32
+    [rows]; slots = 0 when only blocks are gathered), named `shared` blocks and an
+    epoch flag, allocated from the CUDA caching allocator and shared with
     every rank once through CUDA IPC handles (torch.multiprocessing reductions,
     exchanged with all_gather_object). Per exchange a rank writes its partial into
     slot s, bumps its flag (sfi_peer_publish) and merges every rank's slot s in
@@ -73,11 +74,11 @@ class PeerExchange:
                  peers: list | None = None, shared: dict | None = None):
         from . import _sfi_b200 as _C
 
-        if slots < 2:
+        if slots == 1:
             raise ValueError("peer exchange needs >= 2 partial slots (one per layer)")
         self._C, self.world, self.rank, self.slots, self.rows, self.d = _C, world, rank, slots, rows, d
-        self.o = torch.zeros(slots, rows, d, dtype=torch.float32, device=device)
-        self.lse = torch.zeros(slots, rows, dtype=torch.float32, device=device)
+        self.o = torch.zeros(max(slots, 1), max(rows, 1), max(d, 1), dtype=torch.float32, device=device)
+        self.lse = torch.zeros(max(slots, 1), max(rows, 1), dtype=torch.float32, device=device)
         self.flag = torch.zeros(64, dtype=torch.int32, device=device)  # [0] used; own 256 B line
         self.shared = dict(shared or {})  # further blocks all-gathered in place (gather())
         self._peer_views = None
@@ -138,7 +139,10 @@ class HeadShardedSfi:
 
     def __init__(self, n_layers: int, batch: int, n_kv_heads: int, n_q_heads: int, head_dim: int,
                  max_positions: int, n_sink: int = 4, k_budget: int = 2048, n_recent: int = 256,
-                 group=None, device=None):
+                 group=None, device=None, peer: bool = False):
+        """peer=True: the Selector's z_base all-gather reads every rank's block in
+        place over peer memory (PeerExchange: CUDA IPC, sfi_peer_gather), one
+        block slot per layer so a block is only rewritten after every rank read it."""
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -153,6 +157,14 @@ class HeadShardedSfi:
         dev = self.cache.k_cache.device
         self.z_all = torch.empty((self.world, batch, self.local_heads, max_positions), dtype=torch.float64,
                                  device=dev)
+        self.px = None
+        if peer and self.world > 1:
+            if n_layers < 2:
+                raise ValueError("peer exchange keeps one z_base slot per layer: needs >= 2 layers")
+            self.z_slots = torch.zeros((n_layers, batch, self.local_heads, max_positions), dtype=torch.float64,
+                                       device=dev)
+            self.px = PeerExchange(self.world, self.rank, 0, 0, 0, dev, group,
+                                   shared={f"z{l}": self.z_slots[l] for l in range(n_layers)})
 
     # q heads of this shard: [h0*G, h1*G) of the model's q heads
     def q_slice(self) -> slice:
@@ -160,7 +172,13 @@ class HeadShardedSfi:
 
     def selector(self, layer: int, logits: torch.Tensor, params=None):
         z = self.cache.selector_fuse(layer, logits, params)
-        if self.world > 1:
+        if self.px is not None:
+            st = self.cache._stream()
+            self.z_slots[layer].copy_(z)
+            self.px.publish(st)
+            self.px.gather(f"z{layer}", self.z_all, st)
+            self.cache.selector_finish(layer, self.z_all, self.world, self.rank, params)
+        elif self.world > 1:
             all_gather_blocks(z, self.z_all, self.group)
             self.cache.selector_finish(layer, self.z_all, self.world, self.rank, params)
         else:

@@ -137,7 +137,7 @@ def test_head_sharded_selector_bit_exact_simulated(P):
                 assert torch.equal(full.sel[0, b, h, :n_full].cpu(), c.sel[0, b, hl, :n_sh].cpu()), (s, b, hl)
 
 
-def _gpu_worker(rank, world, port, q):
+def _gpu_worker(rank, world, port, q, peer=False):
     try:
         _init(rank, world, port)
         torch.cuda.set_device(0)
@@ -145,22 +145,25 @@ def _gpu_worker(rank, world, port, q):
         from paper_2603_12038_b200.sharded import HeadShardedSfi
 
         B, H, Hq, L0, K, Lmax, d = 2, 4, 8, 3000, 128, 3200, 128
-        sh = HeadShardedSfi(1, B, H, Hq, d, Lmax, 4, K, 64)
+        sh = HeadShardedSfi(2, B, H, Hq, d, Lmax, 4, K, 64, peer=peer)
         g = torch.Generator().manual_seed(99)  # identical full data on every rank
         kf = torch.randn(B, H, L0, d, generator=g).bfloat16()
         vf = torch.randn(B, H, L0, d, generator=g).bfloat16()
         qf = torch.randn(B, Hq, d, generator=g)
-        sh.k_cache[0, :, :, :L0] = kf[:, sh.h0:sh.h1].cuda()
-        sh.v_cache[0, :, :, :L0] = vf[:, sh.h0:sh.h1].cuda()
         norms = kf.double().pow(2).sum(-1).sqrt()  # k^2 exact in fp64; order-free is fine for a Selector input
-        sh.key_norms[0, :, :, :L0] = norms[:, sh.h0:sh.h1].cuda()
+        for layer in range(2):  # the same data in both layers: peer mode uses one z_base slot per layer
+            sh.k_cache[layer, :, :, :L0] = kf[:, sh.h0:sh.h1].cuda()
+            sh.v_cache[layer, :, :, :L0] = vf[:, sh.h0:sh.h1].cuda()
+            sh.key_norms[layer, :, :, :L0] = norms[:, sh.h0:sh.h1].cuda()
         sh.set_lengths([L0] * B, [4] * B)
         out = torch.zeros(B, sh.local_heads * sh.G, d, device="cuda")
         logits = torch.zeros_like(sh.pooled_logits)
-        sh.dense_decode(0, qf[:, sh.q_slice()].contiguous().cuda(), out, logits, 0)
-        sh.selector(0, logits, SelectorParams())
+        for layer in (0, 1, 0, 1):
+            sh.dense_decode(layer, qf[:, sh.q_slice()].contiguous().cuda(), out, logits, 0)
+            sh.selector(layer, logits, SelectorParams())
         torch.cuda.synchronize()
         sh.check_errors()
+        same_layers = torch.equal(sh.sel[0], sh.sel[1]) and torch.equal(sh.n_sel[0], sh.n_sel[1])
         # rank 0 checks every shard's indices against the reference on the gathered logits
         nJ = L0 - 64 - 4
         lg = [torch.zeros(B, H // world, Lmax) for _ in range(world)]
@@ -181,7 +184,8 @@ def _gpu_worker(rank, world, port, q):
                                            norms[b, :, 4:4 + nJ].numpy(), O.make_cfg(k_budget=K))
                 for h in range(H):
                     ok &= np.array_equal(sel_all[b, h, : int(cnt_all[b, h])].numpy(), want[h])
-        q.put((rank, bool(ok)))
+        q.put((rank, bool(ok and same_layers)))
+        dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover
         import traceback
@@ -190,11 +194,13 @@ def _gpu_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_head_sharded_two_processes_one_gpu():
+@pytest.mark.parametrize("peer", [False, True])
+def test_head_sharded_two_processes_one_gpu(peer):
+    """z_base exchanged by all-gather, or in place over CUDA-IPC-mapped peer memory."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, peer)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
