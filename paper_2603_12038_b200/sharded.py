@@ -47,11 +47,13 @@ def _enable_peer_access(world: int) -> None:
     n = min(world, torch.cuda.device_count())
     if n < 2:
         return
+    me = torch.cuda.current_device()
+    if not all(torch.cuda.can_device_access_peer(me, o) for o in range(n) if o != me):
+        raise RuntimeError("peer access between the visible GPUs is not available")
     try:
         from cuda.bindings import runtime as rt
     except ImportError:  # pragma: no cover - cuda-python ships in the image
         from cuda import cudart as rt
-    me = torch.cuda.current_device()
     for other in range(n):
         if other != me and torch.cuda.can_device_access_peer(me, other):
             rt.cudaDeviceEnablePeerAccess(other, 0)  # "already enabled" is fine
@@ -81,9 +83,28 @@ class PeerExchange:
         self.lse = torch.zeros(max(slots, 1), max(rows, 1), dtype=torch.float32, device=device)
         self.flag = torch.zeros(64, dtype=torch.int32, device=device)  # [0] used; own 256 B line
         self.shared = dict(shared or {})  # further blocks all-gathered in place (gather())
+        self.shared["_probe"] = torch.zeros(64, dtype=torch.int32, device=device)
         self._peer_views = None
         if peers is None:
             self.connect(self._exchange_handles(group))
+            self._self_test(group)
+
+    def _self_test(self, group):
+        """One published round trip through every mapping; raises (callers fall
+        back to the all-gather path) unless every rank reads every block."""
+        probe = self.shared["_probe"]
+        probe.fill_(1000 + self.rank)
+        seen = torch.full((self.world, 64), -1, dtype=torch.int32, device=probe.device)
+        st = torch.cuda.current_stream().cuda_stream
+        self.publish(st)
+        self.gather("_probe", seen, st)
+        want = (1000 + torch.arange(self.world, device=probe.device, dtype=torch.int32))[:, None].expand(-1, 64)
+        ok = torch.tensor([int(torch.equal(seen, want))], dtype=torch.int32, device=probe.device)
+        if dist.get_backend(group) != "nccl":
+            ok = ok.cpu()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) != 1:
+            raise RuntimeError("peer-memory self-test failed: a rank could not read every mapped block")
 
     def _exchange_handles(self, group):
         from torch.multiprocessing.reductions import reduce_tensor
