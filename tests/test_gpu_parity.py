@@ -198,6 +198,7 @@ def _selector_case(B, H, Hq, Lmax, lens, K, ns=4, R=256, seed=1):
     (2, 2, 4, [700, 650], 64),
     (1, 8, 16, [8192], 512),        # C1 shape (Qwen3-0.6B heads), |J| = 8124
     (2, 8, 32, [32768, 20000], 2048),  # C2 shape (Qwen3-8B heads), |J| = 32508
+    (3, 4, 8, [200, 500, 5000], 256),  # ragged: empty J, |J| <= k (all of J), |J| > k
 ])
 def test_device_selector_indices_bit_exact(B, H, Hq, lens, K):
     c, logits = _selector_case(B, H, Hq, max(lens) + 8, lens, K)
@@ -208,6 +209,9 @@ def test_device_selector_indices_bit_exact(B, H, Hq, lens, K):
     for b in range(B):
         L, nsb, rl, j0, j1 = _window(c, b)
         n = j1 - j0 + 1
+        if n <= 0:  # empty J: nothing to select (scheduler.cpp:171-175)
+            assert int(c.n_sel[0, b].abs().sum()) == 0
+            continue
         vals = logits[b, :, :n].double().cpu().numpy()
         norms = c.key_norms[0, b, :, j0 - 1:j1].cpu().numpy()
         want, _ = orc.run_selector(vals, np.arange(j0, j1 + 1), norms, cfg)
