@@ -659,12 +659,14 @@ constexpr int kPwHeads = 4;            // heads per CTA (blockIdx.z splits large
 
 __host__ __device__ __forceinline__ int n_chunks(int n) { return (n + kChunk - 1) / kChunk; }
 
-template <int kHT>
+// kHC: heads per CTA (kPwHeads; 1 for small problems, where 4x the CTAs beat
+// sharing the position factor)
+template <int kHT, int kHC = kPwHeads>
 __global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, double* P, double* Wt, double* stats,
                                                       int ld_chunks) {
   griddep_wait();  // PDL: logits come from the preceding dense decode
   griddep_launch();
-  constexpr int kH = kHT < kPwHeads ? kHT : kPwHeads;  // heads of this CTA
+  constexpr int kH = kHT < kHC ? kHT : kHC;  // heads of this CTA
   constexpr int kW = kPwT / 32;
   __shared__ double red[kW][kH][5];
   __shared__ double mc[kH];
@@ -1629,9 +1631,12 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
     double* stt = scr.stats;
     double* cf = scr.stats + slices * ldc * 6;  // [rows][ldc + 2] fused coefficients
     cudaError_t e;
+    const bool small_pw = (size_t)ldc * s.batch * ((s.n_kv_heads + kPwHeads - 1) / kPwHeads) < 128;
 #define SFI_SEL2(KH)                                                                             \
-  e = launch_k(sel_pw_kernel<KH>, dim3(ldc, s.batch, (KH + kPwHeads - 1) / kPwHeads), ba, 0, st, p, P, Wt, \
-               stt, ldc);                                                                            \
+  e = small_pw ? launch_k(sel_pw_kernel<KH, 1>, dim3(ldc, s.batch, KH == 16 ? s.n_kv_heads : KH), ba, 0, st, p, \
+                          P, Wt, stt, ldc)                                                           \
+               : launch_k(sel_pw_kernel<KH>, dim3(ldc, s.batch, (KH + kPwHeads - 1) / kPwHeads), ba, 0, st, p, \
+                          P, Wt, stt, ldc);                                                          \
   if (e == cudaSuccess)                                                                              \
     e = launch_k(sel_coef_kernel, dim3(((unsigned)slices + 7) / 8), dim3(256), 0, st, p,             \
                  (const double*)stt, cf, ldc);                                                       \
