@@ -196,10 +196,16 @@ class Workload:
         t = torch
         g = t.Generator(device="cpu").manual_seed(2027)
         L, B, H, Hq, d = self.L, self.B, self.H, self.Hq, HEAD_DIM
-        # per-layer step inputs, resident in HBM (q fp32 from the projection; new K/V bf16)
-        self.q = t.randn(L, B, Hq, d, generator=g).to(device)
-        self.k_new = t.randn(L, B, H, d, generator=g).to(device).bfloat16()
-        self.v_new = t.randn(L, B, H, d, generator=g).to(device).bfloat16()
+        # per-layer step inputs, resident in HBM (q fp32 from the projection; new K/V bf16),
+        # packed per layer [q | k_new | v_new] so one copy moves a layer group's inputs
+        qb, kb = B * Hq * d * 4, B * H * d * 2
+        self.io = t.empty(L, qb + 2 * kb, dtype=t.uint8, device=device)
+        self.q = self.io[:, :qb].view(t.float32).view(L, B, Hq, d)
+        self.k_new = self.io[:, qb:qb + kb].view(t.bfloat16).view(L, B, H, d)
+        self.v_new = self.io[:, qb + kb:].view(t.bfloat16).view(L, B, H, d)
+        self.q.copy_(t.randn(L, B, Hq, d, generator=g))
+        self.k_new.copy_(t.randn(L, B, H, d, generator=g).bfloat16())
+        self.v_new.copy_(t.randn(L, B, H, d, generator=g).bfloat16())
         self.out = t.zeros(L, B, Hq, d, device=device)
         self.logits = self.cache.pooled_logits
         drv = self.drv
@@ -315,10 +321,8 @@ class HostIO:
         self.t, self.wl = t, wl
         self.cs = t.cuda.Stream()
         pin = lambda x: t.empty_like(x, device="cpu").pin_memory()  # noqa: E731
-        self.qh, self.kh, self.vh, self.oh = pin(wl.q), pin(wl.k_new), pin(wl.v_new), pin(wl.out)
-        self.qh.copy_(wl.q)
-        self.kh.copy_(wl.k_new)
-        self.vh.copy_(wl.v_new)
+        self.ioh, self.oh = pin(wl.io), pin(wl.out)  # [L][q | k_new | v_new] bytes, [L] outputs
+        self.ioh.copy_(wl.io)
         # one-layer groups at both ends: the first inputs and the last output are
         # the only copies the compute cannot hide
         cuts = [0] + ([1] if wl.L > 2 else []) + list(range(1 + group, wl.L - 1, group)) + \
@@ -336,9 +340,7 @@ class HostIO:
         cs.wait_stream(self.main)  # fork
         with t.cuda.stream(cs):
             for gi, (l0, l1) in enumerate(self.groups):
-                wl.q[l0:l1].copy_(self.qh[l0:l1], non_blocking=True)
-                wl.k_new[l0:l1].copy_(self.kh[l0:l1], non_blocking=True)
-                wl.v_new[l0:l1].copy_(self.vh[l0:l1], non_blocking=True)
+                wl.io[l0:l1].copy_(self.ioh[l0:l1], non_blocking=True)  # q, k_new, v_new of the group
                 self.ev_in[gi].record(cs)
 
     def before(self, l: int):
@@ -544,7 +546,7 @@ def gpu_arm(args) -> dict:
     if wl.mode in ("single", "dp"):
         try:
             lbv = wl.cache.layer_batched_view()
-            qv, kv_, vv_, ov = (x.view(-1, *x.shape[2:]) for x in (wl.q, wl.k_new, wl.v_new, wl.out))
+            qv, kv_, vv_, ov = (x.reshape(-1, *x.shape[2:]) for x in (wl.q, wl.k_new, wl.v_new, wl.out))
             s_ = torch.cuda.current_stream()
             lbv.fast_decode(0, qv, kv_, vv_, ov, prefetch=True)
             torch.cuda.synchronize()
