@@ -194,6 +194,46 @@ void test_selector_device() {  // test_selector.cpp:52-60, 295-301
 
 }  // namespace
 
+// The reference's run_request / run_dense call sites (scheduler.hpp:116-135)
+// against the device-path loop: C7 full retention (SFI tokens == dense tokens)
+// and the C8 schedule rule, through the C++ API.
+void test_request_loop_device() {
+  ModelSpec spec;
+  spec.n_layers = 2;
+  spec.n_query_heads = 8;
+  spec.n_kv_heads = 2;
+  spec.head_dim = 64;
+  spec.vocab_size = 256;
+  spec.max_positions = 1024;
+  const ToyModel model = ToyModel::random(spec, 9001);
+  std::vector<TokenId> prompt;
+  for (int i = 0; i < 70; ++i) prompt.push_back(5 + (i * 37) % 250);
+  CacheLimits full;
+  full.n_recent = 512;
+  full.k_budget = 64;
+  TriggerConfig trig;
+  trig.t_max = 8;
+  SelectorConfig cfg;
+  cfg.k_budget = 64;
+  const RequestResult r = run_request(model, prompt, full, trig, cfg, 24);
+  const DenseResult d = run_dense(model, prompt, 24);
+  CHECK(r.tokens.size() == 24 && r.log.size() == 24);
+  CHECK(r.tokens == d.tokens);  // C7 (acceptance.cpp:125-160)
+  int fast = 0, last_slow = 0;
+  for (int t = 0; t < 24; ++t) {  // C8 rule (acceptance.cpp:162-205)
+    const bool slow = t == 0 || trig.is_trigger(r.tokens[t - 1]) || t - last_slow >= trig.t_max;
+    if (slow) last_slow = t;
+    CHECK(slow == r.log[t].slow);
+    fast += !r.log[t].slow;
+  }
+  CHECK(fast > 0);
+  CHECK(r.total_kv_reads <= r.dense_equiv_reads);
+  CacheLimits small;
+  small.n_recent = 16;
+  small.k_budget = 64;
+  CHECK_THROWS_CODE(run_request(model, prompt, small, trig, SelectorConfig{}, 4), ErrorCode::kUnsupported);  // k mismatch
+}
+
 int main(int argc, char** argv) {
   const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
   std::vector<std::pair<const char*, std::function<void()>>> cases = {
@@ -205,6 +245,7 @@ int main(int argc, char** argv) {
   if (gpu) {
     cases.push_back({"reorganize_device", test_reorganize_device});
     cases.push_back({"selector_device", test_selector_device});
+    cases.push_back({"request_loop_device", test_request_loop_device});
   }
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

@@ -1,6 +1,7 @@
 """The reference's C++ call sites compile and run against include/sfi_b200.hpp
 and libsfi_b200.so (tests/cpp/test_api.cpp): host cases on CPU, device cases
-(KvStore::reorganize, run_selector, select_top_k KATs) on the B200."""
+(KvStore::reorganize, run_selector, select_top_k KATs, the run_request / run_dense
+request loop with C7 and C8) on the B200."""
 from __future__ import annotations
 
 import os
