@@ -249,6 +249,11 @@ int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* 
   p.prefetch = (flags & SFI_FAST_PREFETCH) ? 1 : 0;
   p.lse = lse;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  static const bool env_steal = [] {
+    const char* e = std::getenv("SFI_FAST_STEAL");
+    return e && e[0] == '1';
+  }();
+  p.steal = env_steal ? sfi_impl::carve_workspace(*s, c->workspace).steal : nullptr;
   static const int env_c = [] {
     const char* e = std::getenv("SFI_FAST_CLUSTER");
     return e ? std::atoi(e) : 0;
@@ -322,6 +327,7 @@ size_t workspace_bytes(const sfi_shape& s) {
   b += 3 * align_up(slices * (size_t)s.max_positions * sizeof(double));
   // two-pass decode Selector: [rows][chunks][6] statistics + [rows][chunks + 2] coefficients
   b += align_up(slices * (size_t)(7 * ((s.max_positions + 511) / 512) + 2) * sizeof(double));
+  b += align_up((size_t)s.n_layers * slices * 2 * sizeof(int32_t));  // fast-decode tile-claim counters
   return b;
 }
 
@@ -342,6 +348,8 @@ Workspace carve_workspace(const sfi_shape& s, void* base) {
   w.sel.c = reinterpret_cast<double*>(p);
   p += align_up(slices * (size_t)s.max_positions * sizeof(double));
   w.sel.stats = reinterpret_cast<double*>(p);
+  p += align_up(slices * (size_t)(7 * ((s.max_positions + 511) / 512) + 2) * sizeof(double));
+  w.steal = reinterpret_cast<int32_t*>(p);
   return w;
 }
 

@@ -15,6 +15,11 @@
 //   * one thread-block cluster of C CTAs per (b, kv head) slice; the slice's
 //     compact rows [0, R) (recent ring) and [R, R + n_sink_b + n_sel) (sink +
 //     selected) are cut into 64-row tiles and split evenly over the C CTAs;
+//   * SFI_FAST_STEAL=1 (opt-in): the producers claim tiles from a per-slice
+//     counter in L2 instead (intra-cluster balancing of HBM service variance;
+//     -2.4% per C2 layer, slower where a CTA has only 1-3 tiles). The
+//     summation order then varies run to run, so the static split stays the
+//     default (deterministic outputs);
 //   * the tile split depends only on n_sink_b / n_sel, which no kernel of a fast
 //     step writes, so with SFI_FAST_PREFETCH the TMA producer issues its first
 //     stages BEFORE the programmatic-dependent-launch wait: the K/V stream of
@@ -83,8 +88,12 @@ struct FRecv {
   static constexpr int kFloats = kO + 2 * 16 * G;
 };
 template <int D, int G>
-constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row | receive area
+__host__ __device__ constexpr int fast_smem_off_tiles() {  // [kStages] tile index of each stage (dynamic split)
   return FGeo<D>::kRing + 64 + D * 8 + FRecv<D, G>::kFloats * 4;
+}
+template <int D, int G>
+constexpr int fast_smem_bytes() {  // stage ring | 2 x kStages mbarriers | fp64 k^2 row | receive area | stage tiles
+  return fast_smem_off_tiles<D, G>() + 16;
 }
 // Owner shares are whole warps of 32 elements. With few, small partials (G <= 4,
 // C <= 4) rank 0 merges everything and ranks 1.. exit right after their push,
@@ -274,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + FGeo<D>::kRing);
   uint64_t* empty = full + kStages;
   uint64_t* rx_bar = reinterpret_cast<uint64_t*>(smem + FGeo<D>::kRing + 56);  // merge receive (flag at +48)
+  volatile int* stage_tile = reinterpret_cast<volatile int*>(smem + fast_smem_off_tiles<D, G>());
   constexpr int kPD = FPart<D, G>::kPD;
   float* part_o = reinterpret_cast<float*>(smem);        // [kParts][G][kPD] (after the stream)
   float* part_m = part_o + FPart<D, G>::kO;              // [kParts][G]
@@ -331,11 +341,32 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0) {
       if (!p.prefetch) griddep_wait();  // the compact rows may come from the predecessor
       const uint64_t pol = l2_policy_evict_first();
-      for (int t = tb, i = 0; t < te; ++t, ++i) {
-        if (i == kStages) griddep_wait();  // the rest needs freed stages anyway
+      // dynamic split (p.steal): tiles are claimed from the slice's counter in
+      // L2; a claim past T ends the stream with an empty stage (tile -1)
+      int32_t* claim = p.steal ? p.steal + slice_g * 2 : nullptr;
+      for (int t = tb, i = 0;; ++t, ++i) {
+        if (claim) {
+          if (i == kStages) griddep_wait();
+        } else if (t >= te) {
+          break;
+        } else if (i == kStages) {
+          griddep_wait();  // the rest needs freed stages anyway
+        }
         const int st = i % kStages;
         const uint32_t ph = (i / kStages) & 1;
         mbar_wait(&empty[st], ph ^ 1);
+        if (claim) {
+          t = atomicAdd(claim, 1);
+          stage_tile[st] = t < T ? t : -1;
+          if (t >= T) {  // end of stream: release the consumers without data
+            mbar_arrive(&full[st]);
+            if (atomicAdd(claim + 1, 1) == C - 1) {  // last producer of the cluster: reset
+              claim[0] = 0;
+              claim[1] = 0;
+            }
+            break;
+          }
+        }
         const int row = row_base + tile_row(t, t_ring, p.R);
         uint8_t* kdst = smem + st * FGeo<D>::kStageBytes;
         uint8_t* vdst = kdst + FGeo<D>::kTileBytes;
@@ -509,9 +540,16 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   // every tile is waited for and released even when the step is invalid, so
   // the producer never blocks and no TMA write is in flight at exit
-  for (int t = tb, i = 0; t < te; ++t, ++i) {
+  for (int t = tb, i = 0;; ++t, ++i) {
     const int st = i % kStages;
     const uint32_t ph = (i / kStages) & 1;
+    if (p.steal) {  // the producer's claim for this stage, published before its full arrival
+      mbar_wait(&full[st], ph);
+      t = stage_tile[st];
+      if (t < 0) break;
+    } else if (t >= te) {
+      break;
+    }
     // validity of this warp's keys kw + j*8 + 2*t4 + e
     bool valid[2][2];
     const bool ring = t < t_ring;
@@ -531,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     const bool any =
         __any_sync(0xffffffffu, ok && (valid[0][0] | valid[0][1] | valid[1][0] | valid[1][1]));
-    mbar_wait(&full[st], ph);
+    if (!p.steal) mbar_wait(&full[st], ph);
     if (trace && i == 0 && threadIdx.x == 0) trace[2] = (long long)globaltimer();
     if (any) {
       const uint32_t kbase = smem_u32(smem + st * FGeo<D>::kStageBytes);

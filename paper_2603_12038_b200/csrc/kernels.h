@@ -89,6 +89,7 @@ struct FastParams {
   float scale_log2;               // log2(e) / sqrt(d)
   long long* trace;               // debug: per-CTA globaltimer stamps [grid][16] (null = off)
   float* lse;                     // [B][Hq] partial mode (sequence shards): LSE out, empty allowed
+  int32_t* steal;                 // [layers][B][H][2] tile-claim / done counters (null: static split)
 };
 int fast_cluster_size(int slices, int num_sms);
 cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
@@ -173,6 +174,7 @@ struct Workspace {
   float* part_ml;
   int32_t* counters;
   SelectorScratch sel;
+  int32_t* steal;  // [layers][B][H][2] fast-decode tile-claim counters (zero at rest)
 };
 size_t workspace_bytes(const sfi_shape& s);
 Workspace carve_workspace(const sfi_shape& s, void* base);
