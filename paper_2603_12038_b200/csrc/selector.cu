@@ -661,7 +661,9 @@ __host__ __device__ __forceinline__ int n_chunks(int n) { return (n + kChunk - 1
 
 // kHC: heads per CTA (kPwHeads; 1 for small problems, where 4x the CTAs beat
 // sharing the position factor)
-template <int kHT, int kHC = kPwHeads>
+// kDef: the default exponents (gamma 1, p 2, eta 0.5) — the same operations
+// pow_ref selects at run time (1/x, x*x, sqrt), without the per-element dispatch.
+template <int kHT, int kHC = kPwHeads, bool kDef = false>
 __global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, double* P, double* Wt, double* stats,
                                                       int ld_chunks) {
   griddep_wait();  // PDL: logits come from the preceding dense decode
@@ -687,7 +689,8 @@ __global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, doub
     const int j = c0 + threadIdx.x + i * kPwT;
     if (j < n) {
       const double u = src.u(j, denom_u);
-      fpos[i] = exp(-p.beta * pow_ref(u, p.p_curve)) * pow_ref(1.0 - u + p.eps, p.eta);
+      fpos[i] = kDef ? exp(-p.beta * (u * u)) * sqrt(1.0 - u + p.eps)
+                     : exp(-p.beta * pow_ref(u, p.p_curve)) * pow_ref(1.0 - u + p.eps, p.eta);
     } else {
       fpos[i] = 0.0;
     }
@@ -735,7 +738,7 @@ __global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, doub
         const double nm = src.norm(row, j);
         if (!isfinite(nm) || nm < 0.0) badn = true;
         const double pj = (vv <= kMaskedLogit) ? 0.0 : exp(vv - m);
-        const double wr = pow_ref(nm + p.eps, -p.gamma) * fpos[i];
+        const double wr = (kDef ? 1.0 / (nm + p.eps) : pow_ref(nm + p.eps, -p.gamma)) * fpos[i];
         if (!isfinite(wr) || wr < 0.0) badn = true;
         P[(size_t)row * p.ld + j] = pj;
         Wt[(size_t)row * p.ld + j] = wr;
@@ -1632,11 +1635,16 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
     double* cf = scr.stats + slices * ldc * 6;  // [rows][ldc + 2] fused coefficients
     cudaError_t e;
     const bool small_pw = (size_t)ldc * s.batch * ((s.n_kv_heads + kPwHeads - 1) / kPwHeads) < 128;
+    const bool def_exp = p.gamma == 1.0 && p.p_curve == 2.0 && p.eta == 0.5;
 #define SFI_SEL2(KH)                                                                             \
-  e = small_pw ? launch_k(sel_pw_kernel<KH, 1>, dim3(ldc, s.batch, KH == 16 ? s.n_kv_heads : KH), ba, 0, st, p, \
-                          P, Wt, stt, ldc)                                                           \
-               : launch_k(sel_pw_kernel<KH>, dim3(ldc, s.batch, (KH + kPwHeads - 1) / kPwHeads), ba, 0, st, p, \
-                          P, Wt, stt, ldc);                                                          \
+  e = small_pw ? (def_exp ? launch_k(sel_pw_kernel<KH, 1, true>, dim3(ldc, s.batch, KH == 16 ? s.n_kv_heads : KH), \
+                                     ba, 0, st, p, P, Wt, stt, ldc)                                  \
+                         : launch_k(sel_pw_kernel<KH, 1>, dim3(ldc, s.batch, KH == 16 ? s.n_kv_heads : KH), ba, \
+                                    0, st, p, P, Wt, stt, ldc))                                      \
+               : (def_exp ? launch_k(sel_pw_kernel<KH, kPwHeads, true>,                              \
+                                     dim3(ldc, s.batch, (KH + kPwHeads - 1) / kPwHeads), ba, 0, st, p, P, Wt, stt, ldc) \
+                          : launch_k(sel_pw_kernel<KH>, dim3(ldc, s.batch, (KH + kPwHeads - 1) / kPwHeads), ba, 0, \
+                                     st, p, P, Wt, stt, ldc));                                       \
   if (e == cudaSuccess)                                                                              \
     e = launch_k(sel_coef_kernel, dim3(((unsigned)slices + 7) / 8), dim3(256), 0, st, p,             \
                  (const double*)stt, cf, ldc);                                                       \
