@@ -580,21 +580,33 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t kbase = smem_u32(smem + st * Geo<D, G>::kStageBytes);
       const uint32_t vbase = kbase + Geo<D, G>::kTileBytes;
       // ---- S = Q K^T for 16 keys ----
-      float acc[2][4];
+      // G = 16: the hi and lo query blocks accumulate in separate chains (2x the
+      // independent HMMA chains), summed once
+      float acc[2][4], acc_lo[2][4];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+      for (int j = 0; j < 2; ++j) {
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        acc_lo[j][0] = acc_lo[j][1] = acc_lo[j][2] = acc_lo[j][3] = 0.f;
+      }
 #pragma unroll
       for (int kc = 0; kc < D / 16; kc += 2) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint32_t b0, b1, b2, b3;
           ldsm_x4(swz<D>(kbase, kw + j * 8 + (lane & 7), kc * 2 + (lane >> 3)), b0, b1, b2, b3);
-#pragma unroll
-          for (int qb = 0; qb < NQ; ++qb) {
-            mma_bf16(acc[j], qa[qb][kc], b0, b1);
-            mma_bf16(acc[j], qa[qb][kc + 1], b2, b3);
+          mma_bf16(acc[j], qa[0][kc], b0, b1);
+          mma_bf16(acc[j], qa[0][kc + 1], b2, b3);
+          if constexpr (NQ == 2) {
+            mma_bf16(acc_lo[j], qa[NQ - 1][kc], b0, b1);
+            mma_bf16(acc_lo[j], qa[NQ - 1][kc + 1], b2, b3);
           }
         }
+      }
+      if constexpr (NQ == 2) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[j][e] += acc_lo[j][e];
       }
       float sc[NH][2][2];
       bool valid[2][2];
