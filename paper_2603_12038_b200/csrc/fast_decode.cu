@@ -27,17 +27,21 @@
 //   * producer warp: TMA (128B swizzle, L2 evict-first) into a 3-stage mbarrier
 //     ring; 4 consumer warps: QK^T and PV with mma.sync m16n8k16 bf16 -> fp32
 //     (query rows = the G heads of the GQA group, bf16 hi/lo split so the fp32
-//     query keeps ~16 mantissa bits), online softmax in the log2 domain;
+//     query keeps ~16 mantissa bits), online softmax in the log2 domain with
+//     lazy rescaling of the running max;
 //   * aux warp (cluster rank 0): the current token. Its K/V come from the
 //     caller's k_new / v_new: it persists them (paged row L-1, ring slot
 //     (L-1) % R, fp64 norm — bit-identical to sfi_ring_append) and contributes
 //     the token's key as one more softmax partial; the ring slot's stale row is
 //     masked out of the tiles, so no CTA ever reads a row this kernel writes;
 //   * merge: each CTA combines its 5 partials (m, l, O) locally, then PUSHES
-//     the combined partial to the owners (float4 remote shared-memory stores
-//     into a dedicated receive area; owner r merges a warp-aligned 1/C share
-//     of the G x D outputs); one release/acquire cluster barrier, then every
-//     owner merges from its own shared memory (fixed order: deterministic).
+//     the combined partial to the owners with st.async remote stores that
+//     complete_tx on the owner's receive mbarrier (owner r merges a warp-aligned
+//     1/C share of the G x D outputs; with G <= 4 and C <= 4 rank 0 merges all
+//     and the others exit right after pushing). No cluster barrier on the merge
+//     path: the owner waits on its own mbarrier, then merges from its shared
+//     memory in one pass (fixed order: deterministic). A phase-0 cluster
+//     arrive / wait at start guarantees every peer runs before it is written.
 //     No exit barrier: after the publish barrier no CTA touches a peer.
 #include <cooperative_groups.h>
 #include <cuda.h>
