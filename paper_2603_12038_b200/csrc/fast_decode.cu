@@ -41,8 +41,8 @@
 //     and the others exit right after pushing). No cluster barrier on the merge
 //     path: the owner waits on its own mbarrier, then merges from its shared
 //     memory in one pass (fixed order: deterministic). A phase-0 cluster
-//     arrive / wait at start guarantees every peer runs before it is written.
-//     No exit barrier: after the publish barrier no CTA touches a peer.
+//     arrive / wait at start guarantees every peer runs before it is written;
+//     no exit barrier: once pushed, no CTA touches a peer.
 #include <cooperative_groups.h>
 #include <cuda.h>
 
