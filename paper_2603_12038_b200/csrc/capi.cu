@@ -174,7 +174,10 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
     const char* e = std::getenv("SFI_DENSE_SHARE_PERMILLE");
     return e ? std::atoi(e) : 0;
   }();
-  const int share = (env_share > 0 && env_share <= 1000) ? env_share : 650;
+  // G = 16: the dense decode is consumer-latency-bound and wants every CTA slot
+  // (C4 async slow step 21.4 -> 20.2 ms); G <= 8 streams at HBM speed with 65%
+  const int share = (env_share > 0 && env_share <= 1000) ? env_share
+                    : (s->n_q_heads / s->n_kv_heads >= 16 ? 1000 : 650);
   int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms(),
                                    (flags & SFI_DENSE_SHARE_SM) ? share : 875);
   static const int env_ctas = [] {
