@@ -171,9 +171,10 @@ SFI_API int sfi_dense_decode(const sfi_shape* shape, const sfi_cache* cache, int
 
 /* sfi_dense_decode with options. lse (optional): natural-log sum-exp per q head
  * (partial mode, see sequence sharding). flags: SFI_DENSE_SHARE_SM sizes the
- * stream-K grid to 65% of the SM slots so kernels on another stream — the
- * previous layer's Selector in the asynchronous slow-step pipeline — run at
- * the same time on the rest. */
+ * stream-K grid to 65% of the SM slots (G <= 8; all of them at G = 16, where
+ * the kernel is latency-bound) so kernels on another stream — the previous
+ * layer's Selector in the asynchronous slow-step pipeline — run at the same
+ * time on the rest. */
 #define SFI_DENSE_SHARE_SM 2
 SFI_API int sfi_dense_decode_ex(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
                                 const float* q, float* out, float* lse, float* pooled_logits,

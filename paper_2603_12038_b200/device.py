@@ -216,7 +216,7 @@ class SlowStepPipeline:
     SURVEY §8f-1) over one SfiCache.
 
     The dense decode of every layer runs on the caller's stream on 65% of the SM
-    slots (SFI_DENSE_SHARE_SM); the Selector and the compact build of layer l run
+    slots (SFI_DENSE_SHARE_SM; all of them at G = 16); the Selector and the compact build of layer l run
     on an auxiliary stream as soon as layer l's pooled logits exist, on the slots
     the dense kernels leave free, while layers l+1.. stream their KV. The refreshed selection is only read by the next fast step, after `end()`
     joins the streams. Pooled logits go through a ring of `slots` buffers: dense(l)
