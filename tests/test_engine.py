@@ -73,6 +73,32 @@ def test_toy_weights_match_reference():
         assert ours == orc.toy_checksum(SPEC, seed), seed
 
 
+def test_request_loop_argument_errors():
+    """run_request / run_dense reject bad requests before any device work, with the
+    reference's codes and order (scheduler.cpp:218-231, :336-341)."""
+    import paper_2603_12038_b200 as sfi
+
+    model = sfi.ToyModel.random(_spec(), 1)
+    lim, trig, cfg = _limits(4, 16, 16), _trigger([0], 8), _selector(16)
+
+    def code(fn):
+        with pytest.raises(sfi.SfiError) as e:
+            fn()
+        return e.value.code
+
+    assert code(lambda: sfi.run_request(model, [], lim, trig, cfg, 4)) == "out_of_range"
+    assert code(lambda: sfi.run_request(model, [5, 6], lim, trig, cfg, 0)) == "out_of_range"
+    assert code(lambda: sfi.run_request(model, [5] * 2040, lim, trig, cfg, 16)) == "context_overflow"
+    assert code(lambda: sfi.run_request(model, [5, 6], _limits(4, 2048, 16), trig, cfg, 4)) == "config"
+    assert code(lambda: sfi.run_request(model, [5, 6], lim, trig, _selector(32), 4)) == "unsupported"
+    bad = _selector(16)
+    bad.alpha = 0.0
+    assert code(lambda: sfi.run_request(model, [5, 6], lim, trig, bad, 4)) == "config"
+    assert code(lambda: sfi.run_dense(model, [], 4)) == "out_of_range"
+    assert code(lambda: sfi.run_dense(model, [5, 6], 0)) == "out_of_range"
+    assert code(lambda: sfi.run_dense(model, [5] * 2040, 16)) == "context_overflow"
+
+
 # ---------------------------------------------------------------- GPU ----
 
 def _prompt(rng, n):
