@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2603_12038_b200 as sfi  # noqa: E402
 
-wl = bench.Workload("c2", 200, torch.device("cuda", 0))
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+wl = bench.Workload(cfg, 200, torch.device("cuda", 0))
 c = wl.cache
 pipe = sfi.SlowStepPipeline(c)
 ev_d = [torch.cuda.Event(enable_timing=True) for _ in range(wl.L)]
