@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, doub
         const double pj = (vv <= kMaskedLogit) ? 0.0 : exp(vv - m);
         const double wr = (kDef ? 1.0 / (nm + p.eps) : pow_ref(nm + p.eps, -p.gamma)) * fpos[i];
         if (!isfinite(wr) || wr < 0.0) badn = true;
-        P[(size_t)row * p.ld + j] = pj;
+        (void)P;  // p is recomputed by sel_z from the logits (saves its write + read)
         Wt[(size_t)row * p.ld + j] = wr;
         sp += pj;
         sw += wr;
@@ -829,12 +829,13 @@ __global__ void sel_coef_kernel(const SelParams p, const double* __restrict__ st
 }
 
 template <int kH>
-__global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const SelParams p, const double* P, const double* Wt,
+__global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const SelParams p, const double* stats, const double* Wt,
                                                          const double* coef, int ld_chunks) {
   griddep_wait();
   griddep_launch();
   __shared__ double tile[kH][kRefineT + 2 * kMaxNmsR];
   __shared__ double ca[kH][2];  // (1 - lambda) / sum p * exp(m_c - M) for the <= 2 chunks the tile touches
+  __shared__ double cm[kH][2];  // the chunk maxima m_c (p = exp(v - m_c) is recomputed, not stored)
   __shared__ double cb[kH];     // lambda / sum w
   const int b = blockIdx.y;
   const int j0 = blockIdx.x * kRefineT;
@@ -848,8 +849,12 @@ __global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const 
     const int h = threadIdx.x / 3, k = threadIdx.x % 3;
     const double* cf = coef + (size_t)(b * p.H + h) * (ld_chunks + 2);
     const int c = chunk0 + k;
-    if (k < 2) ca[h][k] = c < n_chunks(n) ? cf[2 + c] : 0.0;
-    else cb[h] = cf[1];
+    if (k < 2) {
+      ca[h][k] = c < n_chunks(n) ? cf[2 + c] : 0.0;
+      cm[h][k] = c < n_chunks(n) ? stats[((size_t)(b * p.H + h) * ld_chunks + c) * 6] : 0.0;
+    } else {
+      cb[h] = cf[1];
+    }
   }
   __syncthreads();
   // ---- z_base of the tile and its halo, all heads, into shared memory ----
@@ -859,7 +864,10 @@ __global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const 
     const int j = j0 - R + t;
     if (j < 0 || j >= n) continue;
     const size_t o = (size_t)(b * p.H + h) * p.ld + j;
-    tile[h][t] = log(ca[h][j / kChunk - chunk0] * P[o] + cb[h] * Wt[o] + p.eps);
+    const int k = j / kChunk - chunk0;
+    const double v = src.logit(b * p.H + h, 0, j);
+    const double pj = (v <= kMaskedLogit) ? 0.0 : exp(v - cm[h][k]);  // the bits sel_pw summed
+    tile[h][t] = log(ca[h][k] * pj + cb[h] * Wt[o] + p.eps);
   }
   __syncthreads();
   const int idx = j0 + threadIdx.x;
@@ -1648,7 +1656,7 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
   if (e == cudaSuccess)                                                                              \
     e = launch_k(sel_coef_kernel, dim3(((unsigned)slices + 7) / 8), dim3(256), 0, st, p,             \
                  (const double*)stt, cf, ldc);                                                       \
-  if (e == cudaSuccess) e = launch_k(sel_z_kernel<KH>, gz, bz, 0, st, p, (const double*)P,             \
+  if (e == cudaSuccess) e = launch_k(sel_z_kernel<KH>, gz, bz, 0, st, p, (const double*)stt,           \
                                      (const double*)Wt, (const double*)cf, ldc);
     switch (s.n_kv_heads) {
       case 1: SFI_SEL2(1) break;
