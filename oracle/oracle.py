@@ -118,6 +118,7 @@ class Oracle:
             L.orc_toy_checksum.argtypes = [C.c_void_p, C.c_uint64]
             L.orc_toy_run_request.restype = C.c_int
             L.orc_toy_run_dense.restype = C.c_int
+            L.orc_toy_capture.restype = C.c_int
 
     # ---- toy model + request loop (reference only, scheduler.cpp:213-365) ----
     @staticmethod
@@ -166,6 +167,27 @@ class Oracle:
                                         C.c_int(max_new), _ptr(tok), _ptr(lg), err, C.c_int(512))
         self._check(rc, err)
         return dict(tokens=tok, logits=lg)
+
+    def toy_capture(self, spec: dict, seed: int, tokens, allowed, pool: int = 0):
+        """The reference run_step's own slow-step capture at the last token
+        (layer 0): dict(logits [H][nJ], context [Hq*d], q [Hq*d] post-rotary,
+        k, v [n][H*d] fp32 paged rows)."""
+        ts = self._toy_spec(spec)
+        tokens = _i32(tokens)
+        allowed = _i32(allowed)
+        n, nJ = len(tokens), len(allowed)
+        H, Hq, d = spec["n_kv_heads"], spec["n_query_heads"], spec["head_dim"]
+        lg = np.zeros((H, max(nJ, 1)), np.float64)
+        ctx = np.zeros(Hq * d, np.float64)
+        q = np.zeros(Hq * d, np.float64)
+        k = np.zeros((n, H * d), np.float32)
+        v = np.zeros((n, H * d), np.float32)
+        err = C.create_string_buffer(512)
+        rc = self.lib.orc_toy_capture(C.byref(ts), C.c_uint64(seed), _ptr(tokens), C.c_int(n), C.c_int(nJ),
+                                      _ptr(allowed if nJ else _i32([0])), C.c_int(pool), _ptr(lg), _ptr(ctx),
+                                      _ptr(q), _ptr(k), _ptr(v), err, C.c_int(512))
+        self._check(rc, err)
+        return dict(logits=lg[:, :nJ].copy(), context=ctx, q=q, k=k, v=v)
 
     def _check(self, rc: int, err) -> None:
         if rc:

@@ -129,6 +129,16 @@ int orc_toy_run_request(const orc_toy_spec* spec, uint64_t seed, const int32_t* 
                         double* out_logits, int32_t* out_sel, int32_t* out_nsel, char* err, int errlen);
 int orc_toy_run_dense(const orc_toy_spec* spec, uint64_t seed, const int32_t* prompt, int plen,
                       int max_new, int32_t* out_tokens, double* out_logits, char* err, int errlen);
+/* The reference's own slow-step capture (run_step, attention.cpp:302-441):
+ * tokens[0..n-2] through dense_attention_step without capture, then the last
+ * token with CaptureSpec{window, allowed, pool, context}. Outputs (layer 0):
+ * out_logits [H][nJ] (LogitWindow values), out_ctx [Hq*d] (attention context),
+ * out_q [Hq*d] (the post-rotary query the step attended with, restated from
+ * run_step's first lines: rmsnorm, wq, apply_rope — test infrastructure),
+ * out_k / out_v [n][H*d] (the paged rows KvStore holds). */
+int orc_toy_capture(const orc_toy_spec* spec, uint64_t seed, const int32_t* tokens, int n,
+                    int nJ, const int32_t* allowed, int pool, double* out_logits, double* out_ctx,
+                    double* out_q, float* out_k, float* out_v, char* err, int errlen);
 
 #pragma GCC visibility pop
 #ifdef __cplusplus

@@ -3,6 +3,7 @@
 // /root/reference/proj/src/*.cpp into oracle/_ref/libsfi_ref.so. Nothing in
 // here re-implements reference arithmetic; every call forwards to the
 // reference's own functions (namespace sfi).
+#include <cmath>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -372,6 +373,51 @@ int orc_toy_run_dense(const orc_toy_spec* t, uint64_t seed, const int32_t* promp
       if (out_logits)
         std::copy(r.step_logits[i].begin(), r.step_logits[i].end(),
                   out_logits + static_cast<std::size_t>(i) * t->vocab_size);
+    }
+  });
+}
+
+int orc_toy_capture(const orc_toy_spec* t, uint64_t seed, const int32_t* tokens, int n, int nJ,
+                    const int32_t* allowed, int pool, double* out_logits, double* out_ctx, double* out_q,
+                    float* out_k, float* out_v, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const sfi::ModelSpec spec = toy_spec(t);
+    const sfi::ToyModel m = sfi::ToyModel::random(spec, seed);
+    sfi::KvStore store(spec);
+    sfi::CaptureSpec none;
+    for (int i = 0; i + 1 < n; ++i) sfi::dense_attention_step(m, tokens[i], store, none);
+    sfi::CaptureSpec cap;
+    cap.window = true;
+    cap.allowed.assign(allowed, allowed + nJ);
+    cap.pool = pool == 1 ? sfi::PoolMode::kMax : sfi::PoolMode::kMean;
+    cap.context = true;
+    const sfi::StepOutput so = sfi::dense_attention_step(m, tokens[n - 1], store, cap);
+    const int H = spec.n_kv_heads, d = spec.head_dim, hq = spec.n_query_heads;
+    const sfi::LogitWindow& w = (*so.attn_logits)[0];
+    for (int h = 0; h < H; ++h) std::copy(w.values[h].begin(), w.values[h].end(), out_logits + (std::size_t)h * nJ);
+    std::copy(so.attn_context[0].begin(), so.attn_context[0].end(), out_ctx);
+    // the layer-0 query of the last step: run_step's first lines (attention.cpp:29-33, 38-54, 342-349)
+    const sfi::ToyModel::LayerWeights& lw = m.layer(0);
+    const Eigen::VectorXd h0 = m.embedding().row(tokens[n - 1]).transpose();
+    const double ms = h0.squaredNorm() / static_cast<double>(h0.size());
+    const double inv = 1.0 / std::sqrt(ms + 1e-6);
+    const Eigen::VectorXd a = (h0.array() * inv * lw.ln1.array()).matrix();
+    Eigen::VectorXd q = lw.wq * a;
+    const double p = static_cast<double>(store.size() - 1);
+    for (int hh = 0; hh < hq; ++hh) {
+      double* head = q.data() + static_cast<std::ptrdiff_t>(hh) * d;
+      for (int i = 0; i < d / 2; ++i) {
+        const double theta = p * std::pow(spec.rope_base, -2.0 * i / d);
+        const double c = std::cos(theta), s = std::sin(theta);
+        const double x = head[2 * i], y = head[2 * i + 1];
+        head[2 * i] = x * c - y * s;
+        head[2 * i + 1] = x * s + y * c;
+      }
+    }
+    std::copy(q.data(), q.data() + hq * d, out_q);
+    for (int pos = 1; pos <= store.size(); ++pos) {
+      std::copy(store.key_at(0, pos), store.key_at(0, pos) + H * d, out_k + (std::size_t)(pos - 1) * H * d);
+      std::copy(store.value_at(0, pos), store.value_at(0, pos) + H * d, out_v + (std::size_t)(pos - 1) * H * d);
     }
   });
 }

@@ -38,9 +38,14 @@
 // ascending allowed list).
 // Compiled with -fmad=false (no FMA contraction). Reductions are tree-ordered
 // and the fast path rescales instead of dividing twice, so intermediates can
-// differ from the reference by a few ulps (~1e-16 relative); the indices are
-// exact whenever the K-th/(K+1)-th score gap exceeds that, measured >= 3.7e-8
-// relative and checked by tests/test_gpu_parity.py.
+// differ from the reference by a few ulps (~1e-16 relative). The index
+// contract: every score is a deterministic function of the same inputs the
+// reference's score is a function of (p from the ROW max, never a chunk max),
+// so exact ties in the reference are exact ties here and resolve the same way
+// (lower position first); strict orderings agree whenever the K-th/(K+1)-th
+// gap exceeds a few ulps — measured >= 3.7e-8 relative.
+// Checked by tests/test_gpu_parity.py and tests/test_baseline_parity.py
+// (full BASELINE layers, forced ties across statistics chunks).
 #include <cooperative_groups.h>
 
 #include <cstdlib>
@@ -639,19 +644,20 @@ __global__ void __launch_bounds__(kRefineT) sel_refine_kernel(const SelParams p)
 }
 
 // ---------------------------------------------------------------------------
-// Decode Selector, two passes (cache mode, W = 1, alpha = 1, unsharded):
-//   sel_pw_kernel  per (request, 1024-position chunk), all heads: the prior's
-//                  position factor exp(-beta u^p) (1 - u + eps)^eta once per
-//                  position (it is the same for every head), then per head
-//                  p = exp(v - m_c) with the chunk max m_c, w = (|k| + eps)^-gamma
-//                  * factor -> P, W (fp64) and the chunk's five sums -> stats.
-//   sel_z_kernel   per (request, 256 positions), all heads: row max and sums
-//                  from the chunk statistics (rescaled to the row max in chunk
-//                  order), lambda* per head, z = log(a p + b w + eps) for the tile
-//                  and its soft-NMS halo into shared memory, soft-NMS +
-//                  cross-head -> z_adj.
-// One exp + one reciprocal per (head, position) less than the three-kernel
-// path, and no z_base round trip.
+// Decode Selector, three passes (cache mode, W = 1, alpha = 1, unsharded):
+//   sel_pw_kernel   per (request, 512-position chunk, <= 4 heads): the prior's
+//                   position factor exp(-beta u^p) (1 - u + eps)^eta once per
+//                   position (the same for every head), then per head the chunk
+//                   max m_c, p = exp(v - m_c), w = (|k| + eps)^-gamma * factor -> W
+//                   (fp64) and the chunk's five sums relative to m_c -> stats.
+//   sel_coef_kernel per row: the row max M, the sums rescaled to M (chunk order),
+//                   lambda*, a = (1 - lambda) / sum p, b = lambda / sum w.
+//   sel_z_kernel    per (request, 256 positions), all heads: p = exp(v - M)
+//                   recomputed from the fp32 logits against the ROW max (equal
+//                   logits -> equal p, so exact ties are kept), z = log(a p + b w
+//                   + eps) for the tile and its soft-NMS halo in shared memory,
+//                   soft-NMS, cross-head -> z_adj.
+// No P or z_base round trip through HBM.
 constexpr int kPwT = 256;
 constexpr int kPwPer = 2;
 constexpr int kChunk = kPwT * kPwPer;  // positions per statistics chunk
@@ -771,7 +777,9 @@ __global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, doub
 
 // Per row: the row max M and the fused coefficients from the chunk statistics
 // (rescaled to M in chunk order): coef[row] = {a = (1 - lambda) / sum p,
-// b = lambda / sum w, then a * exp(m_c - M) for every chunk c}.
+// b = lambda / sum w, M}. sel_z forms p = exp(v - M) against the ROW max, as
+// row_softmax does (selector.cpp:54-74): equal logits give bit-equal p, so the
+// reference's exact ties (equal score -> lower position) survive at any distance.
 __global__ void sel_coef_kernel(const SelParams p, const double* __restrict__ stats, double* __restrict__ coef,
                                 int ld_chunks) {
   griddep_wait();
@@ -794,7 +802,6 @@ __global__ void sel_coef_kernel(const SelParams p, const double* __restrict__ st
   for (int c = lane; c < nc; c += 32) {
     const double* x = st + c * 6;
     const double e = exp(x[0] - M);
-    cf[2 + c] = e;
     s0 += x[1] * e;
     s1 += x[2];
     s2 += x[3] * (e * e);
@@ -819,13 +826,11 @@ __global__ void sel_coef_kernel(const SelParams p, const double* __restrict__ st
     lambda = (ff - fr) / denom;
     lambda = (lambda < 0.0) ? 0.0 : (p.lambda_clip < lambda) ? p.lambda_clip : lambda;
   }
-  const double a = (1.0 - lambda) * c1;
   if (lane == 0) {
-    cf[0] = a;
+    cf[0] = (1.0 - lambda) * c1;
     cf[1] = lambda * c2;
+    cf[2] = M;
   }
-  __syncwarp();
-  for (int c = lane; c < nc; c += 32) cf[2 + c] *= a;
 }
 
 template <int kH>
@@ -834,9 +839,9 @@ __global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const 
   griddep_wait();
   griddep_launch();
   __shared__ double tile[kH][kRefineT + 2 * kMaxNmsR];
-  __shared__ double ca[kH][2];  // (1 - lambda) / sum p * exp(m_c - M) for the <= 2 chunks the tile touches
-  __shared__ double cm[kH][2];  // the chunk maxima m_c (p = exp(v - m_c) is recomputed, not stored)
-  __shared__ double cb[kH];     // lambda / sum w
+  __shared__ double ca[kH];  // (1 - lambda) / sum p
+  __shared__ double cm[kH];  // the row max M (p = exp(v - M) is recomputed from the logits, not stored)
+  __shared__ double cb[kH];  // lambda / sum w
   const int b = blockIdx.y;
   const int j0 = blockIdx.x * kRefineT;
   const Src<false> src(p, b);
@@ -844,17 +849,13 @@ __global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const 
   if (j0 >= n) return;
   const int R = p.nms_radius;
   const int Hr = kH == 16 ? p.H : kH;
-  const int chunk0 = max(0, j0 - R) / kChunk;
+  (void)stats;
   if (threadIdx.x < 3 * Hr) {
     const int h = threadIdx.x / 3, k = threadIdx.x % 3;
-    const double* cf = coef + (size_t)(b * p.H + h) * (ld_chunks + 2);
-    const int c = chunk0 + k;
-    if (k < 2) {
-      ca[h][k] = c < n_chunks(n) ? cf[2 + c] : 0.0;
-      cm[h][k] = c < n_chunks(n) ? stats[((size_t)(b * p.H + h) * ld_chunks + c) * 6] : 0.0;
-    } else {
-      cb[h] = cf[1];
-    }
+    const double v = coef[(size_t)(b * p.H + h) * (ld_chunks + 2) + k];
+    if (k == 0) ca[h] = v;
+    else if (k == 1) cb[h] = v;
+    else cm[h] = v;
   }
   __syncthreads();
   // ---- z_base of the tile and its halo, all heads, into shared memory ----
@@ -864,10 +865,9 @@ __global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const 
     const int j = j0 - R + t;
     if (j < 0 || j >= n) continue;
     const size_t o = (size_t)(b * p.H + h) * p.ld + j;
-    const int k = j / kChunk - chunk0;
     const double v = src.logit(b * p.H + h, 0, j);
-    const double pj = (v <= kMaskedLogit) ? 0.0 : exp(v - cm[h][k]);  // the bits sel_pw summed
-    tile[h][t] = log(ca[h][k] * pj + cb[h] * Wt[o] + p.eps);
+    const double pj = (v <= kMaskedLogit) ? 0.0 : exp(v - cm[h]);
+    tile[h][t] = log(ca[h] * pj + cb[h] * Wt[o] + p.eps);
   }
   __syncthreads();
   const int idx = j0 + threadIdx.x;

@@ -113,6 +113,34 @@ class SfiCache:
     def fill_synthetic(self, seed: int, length: int, stream=None):
         _C.fill_synthetic(self.shape, self.cache, seed, length, self._stream(stream))
 
+    def plant_peaked(self, layer: int, q: torch.Tensor, n_planted: int = 32, scale: float = 3.0,
+                     seed: int = 0) -> torch.Tensor:
+        """SURVEY §8d "peaked" synthetic inputs: in every (request, KV head) slice,
+        n_planted positions drawn from the slice's current J (seeded) get the key
+        k = bf16(scale * q_g + N(0, 1)), g cycling over the group's query heads of
+        q fp32 [B][Hq][d]; their fp64 key norms are rewritten. Call after
+        set_lengths and fill_synthetic. Returns the planted positions int64
+        [B][H][n_planted] (1-based)."""
+        s = self.shape
+        B, H, d = s.batch, s.n_kv_heads, s.head_dim
+        G = s.n_q_heads // H
+        gen = torch.Generator(device="cpu").manual_seed(seed)
+        plen = self.prefix_len.cpu()
+        hi = torch.clamp(plen - s.n_recent, min=s.n_sink + 1)        # planted rows stay in J after a step
+        u = torch.rand(B, H, n_planted, generator=gen, dtype=torch.float64)
+        pos = (s.n_sink + 1 + (u * (hi - s.n_sink).view(B, 1, 1).double()).long()).clamp(max=hi.view(B, 1, 1))
+        g_idx = torch.arange(n_planted) % G
+        noise = torch.randn(B, H, n_planted, d, generator=gen)
+        qh = q.detach().float().cpu().view(B, H, G, d)[:, :, g_idx]   # [B][H][n][d]
+        k = (scale * qh + noise).to(torch.bfloat16)
+        dev = self.k_cache.device
+        bi = torch.arange(B).view(B, 1, 1).expand_as(pos).to(dev)
+        hi_ = torch.arange(H).view(1, H, 1).expand_as(pos).to(dev)
+        pi = (pos - 1).to(dev)
+        self.k_cache[layer][bi, hi_, pi] = k.to(dev)
+        self.key_norms[layer][bi, hi_, pi] = k.to(dev).double().pow(2).sum(-1).sqrt()
+        return pos
+
     def step_advance(self, stream=None):
         _C.step_advance(self.shape, self.cache, self._stream(stream))
 

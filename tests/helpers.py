@@ -19,12 +19,13 @@ def oracle(kind: str = "best") -> O.Oracle:
     return O.load(kind)
 
 
-def store_from_rows(orc: O.Oracle, k_rows, v_rows, Hq: int) -> O.Store:
-    """One-layer oracle KvStore from per-head rows k_rows[h][pos-1][d] (fp32)."""
+def store_from_rows(orc: O.Oracle, k_rows, v_rows, Hq: int, extra: int = 8) -> O.Store:
+    """One-layer oracle KvStore from per-head rows k_rows[h][pos-1][d] (fp32),
+    with room for `extra` more appended tokens."""
     k_rows = np.asarray(k_rows, np.float32)
     v_rows = np.asarray(v_rows, np.float32)
     H, L, d = k_rows.shape
-    st = orc.store(1, H, Hq, d, max(L, 1))
+    st = orc.store(1, H, Hq, d, max(L, 1) + extra)
     # [H][L][d] -> [L][H*d]
     st.append_many(np.transpose(k_rows, (1, 0, 2)).reshape(L, H * d),
                    np.transpose(v_rows, (1, 0, 2)).reshape(L, H * d))

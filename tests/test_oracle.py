@@ -256,3 +256,25 @@ def test_port_equals_reference_attention_random():
             pb, kb, vb = stores[1].compact(0, h)
             assert np.array_equal(pa, pb) and np.array_equal(ka, kb) and np.array_equal(va, vb)
             assert stores[0].key_norm(0, h, 17) == stores[1].key_norm(0, h, 17)
+
+
+@needs_ref
+@pytest.mark.parametrize("pool", [0, 1])
+def test_port_capture_equals_reference_run_step(pool):
+    """Pins the port's slow-step logit capture (orc_dense_capture, the oracle the
+    GPU pooled logits are checked against) to the reference's own run_step
+    capture (attention.cpp:367-409) on a toy-model step: the reference hands back
+    the window it captured, the attention context, the paged K/V and the query;
+    the port, given that K/V and query, reproduces window and context."""
+    ref, port = O.load("reference"), O.load("port")
+    spec = dict(n_layers=2, n_query_heads=8, n_kv_heads=2, head_dim=32, vocab_size=64, max_positions=256)
+    rng = np.random.default_rng(40 + pool)
+    tokens = rng.integers(5, 64, size=90)
+    allowed = np.arange(5, 90 - 16 + 1)          # J = [n_sink + 1, L - recent], contiguous in decode
+    r = ref.toy_capture(spec, 17, tokens, allowed, pool)
+    st = port.store(1, spec["n_kv_heads"], spec["n_query_heads"], spec["head_dim"], 256)
+    st.append_many(r["k"], r["v"])
+    out, lg = st.dense_capture(0, r["q"], allowed, pool)
+    assert np.abs(out - r["context"]).max() <= 1e-12 * np.abs(r["context"]).max()
+    assert np.abs(lg - r["logits"]).max() <= 1e-12 * np.abs(r["logits"]).max()
+    assert np.array_equal(lg, r["logits"]) and np.array_equal(out, r["context"])  # bit-identical in practice
