@@ -43,6 +43,9 @@ CONFIGS = {
 # batches per GPU (weak scaling); "heads" = KV-head sharding of ONE batch
 # (strong scaling, z_base all-gather in the Selector)
 SHARDING = {"c1": "dp", "c2": "dp", "c3": "heads", "c4": "seq"}
+# steps per timed window when --steps is not given (C1 256-step schedule,
+# C2 512 steps, C3/C4 64-step windows); the driver passes --steps explicitly
+DEFAULT_STEPS = {"c1": 256, "c2": 512, "c3": 64, "c4": 64}
 HEAD_DIM = 128
 T_MAX = 64
 P_TRIGGER = 1.0 / 24.0
@@ -51,6 +54,26 @@ P_TRIGGER = 1.0 / 24.0
 def metric_name(cfg_name: str) -> str:
     name, _, _, _, _, ctx = CONFIGS[cfg_name][:6]
     return f"SFI decode tokens/s ({ctx // 1024}K ctx, {name.split(',')[0]}, batch {CONFIGS[cfg_name][4]})"
+
+
+def parallelism(cfg_name: str, world: int) -> str:
+    mode = SHARDING[cfg_name] if world > 1 else "single"
+    return {"heads": f"kv-head sharded x{world} (one batch; z_base of every slow-step layer all-gathered)",
+            "seq": f"sequence sharded x{world} (LSE-merged attention partials; Selector statistics, soft-NMS "
+                   "edges and top-k candidates all-gathered)",
+            "dp": f"dp{world} (independent request batches per GPU)"}.get(mode, "1 GPU")
+
+
+def config_dict(cfg_name: str, world: int) -> dict:
+    """The workload, identical in both arms (the reference arm times the same
+    config on the host cores)."""
+    name, n_layers, Hq, H, B, ctx, ns, K, R = CONFIGS[cfg_name]
+    return {"workload": f"{name} ({cfg_name.upper()})", "layers": n_layers, "q_heads": Hq, "kv_heads": H,
+            "head_dim": HEAD_DIM, "batch": B * (world if SHARDING[cfg_name] == "dp" and world > 1 else 1),
+            "context": ctx, "n_sink": ns, "k_budget": K, "n_recent": R,
+            "schedule": f"step 0 slow; seeded triggers p=1/24; forced at t_max={T_MAX}",
+            "parallelism": parallelism(cfg_name, world),
+            "l2": "inputs larger than L2 (KV cache >= 1 GB per layer group)"}
 
 
 def schedule(n_steps: int, seed: int) -> list[bool]:
@@ -64,17 +87,6 @@ def schedule(n_steps: int, seed: int) -> list[bool]:
         since = 0 if slow else since + 1
         trig = bool(rng.random() < P_TRIGGER)
     return out
-
-
-def measured_traffic(kernel: str, cfg_name: str):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
-    --set full capture (profiles/r01/traffic.json, C2 only), else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            t = json.load(f)[kernel]
-        return t["dram_read_bytes"] + t["dram_write_bytes"] if cfg_name == "c2" else None
-    except Exception:
-        return None
 
 
 def peaks() -> dict:
@@ -142,7 +154,7 @@ class ClockSampler:
 
 class Workload:
     def __init__(self, cfg_name: str, steps_total: int, device, world: int = 1, layers: int = 0,
-                 sync_slow: bool = False):
+                 sync_slow: bool = False, inputs: str = "iid"):
         import torch
 
         import paper_2603_12038_b200 as sfi
@@ -161,7 +173,7 @@ class Workload:
         if self.mode == "heads":
             from paper_2603_12038_b200.sharded import HeadShardedSfi
 
-            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "peer") == "peer"
+            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "allgather") == "peer"
             try:  # z_base exchange in place over peer memory (CUDA IPC), else all-gather
                 self.drv = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
                                           self.K, self.R, device=device, peer=self.peer)
@@ -176,7 +188,7 @@ class Workload:
 
             # per-step (O, LSE) exchange through peer memory (CUDA IPC over NVLink,
             # sfi_peer_merge) unless SFI_SEQ_EXCHANGE=allgather or the mapping fails
-            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "peer") == "peer"
+            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "allgather") == "peer"
             try:
                 self.drv = SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx, self.ns,
                                          self.K, self.R, device=device, peer=self.peer)
@@ -215,6 +227,10 @@ class Workload:
             self.pipe = sfi.SlowStepPipeline(self.cache)
         self.cache.fill_synthetic(seed=2026 + 1, length=fill_len)
         self.set_lengths(self.ctx)
+        if inputs == "peaked" and self.mode in ("single", "dp", "heads"):
+            # 32 planted positions per (b, KV head) with k = 3 q + noise
+            for l in range(L):
+                self.cache.plant_peaked(l, self.q[l], n_planted=32, scale=3.0, seed=2026 + l)
         # initial slow step (untimed): dense + Selector + compact incl. the ring
         self.step(slow=True, rebuild_ring=True)
         t.cuda.synchronize()
@@ -298,6 +314,16 @@ class Workload:
         return (self.B * self.H * (S * 4 * HEAD_DIM * self.shard_frac() + 2 * 4 * HEAD_DIM + 8)
                 + 2 * self.B * self.Hq * HEAD_DIM * 4)
 
+    def bytes_slow_layer(self, Lcur: int) -> float:
+        """A slow-step layer's algorithmic bytes: dense KV + pooled
+        logits write (bytes_dense), the Selector's inputs (fp32 logits + fp64 norms
+        over J), the compact gather (sink + selected rows read and written, plus the
+        ring rebuild is not counted: the timed steps do not rebuild it) and the append."""
+        rl = min(self.R, Lcur - self.ns)
+        nj = (Lcur - rl - self.ns) * self.shard_frac()
+        return (self.bytes_dense(Lcur) + self.B * self.H * nj * (4 + 8)
+                + self.B * self.H * (self.ns + self.K) * 4 * HEAD_DIM * 2 + self.B * self.H * (2 * 4 * HEAD_DIM + 8))
+
     def bytes_dense(self, Lcur: int) -> float:
         rl = min(self.R, Lcur - self.ns)
         nj = Lcur - rl - self.ns
@@ -361,25 +387,22 @@ class HostIO:
 
 
 def time_kernel(wl: Workload, which: str, iters: int) -> float:
-    """Average device duration (ms) of one decode launch, CUDA events on the
-    launching stream, over `iters` launches cycling the layers."""
+    """Average device duration (ms) of one decode launch, isolated: `iters`
+    launches (cycling the layers) queued back to back between two CUDA events on
+    the launching stream, so host launch overhead is not in the figure."""
     t = wl.torch
     s = t.cuda.current_stream()
-    c = wl.cache
-    evs = []
-    for i in range(iters):
-        l = i % wl.L
-        a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-        a.record(s)
-        if which == "sparse":
-            wl.fast_kernel(l)
-        else:
-            wl.dense_kernel(l)
-        b.record(s)
-        evs.append((a, b))
+    fn = wl.fast_kernel if which == "sparse" else wl.dense_kernel
+    for l in range(min(2, wl.L)):  # warm
+        fn(l)
     t.cuda.synchronize()
-    ts = [a.elapsed_time(b) for a, b in evs]
-    return float(np.mean(ts[min(3, len(ts) - 1):]))
+    a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    a.record(s)
+    for i in range(iters):
+        fn(i % wl.L)
+    b.record(s)
+    t.cuda.synchronize()
+    return a.elapsed_time(b) / iters
 
 
 def time_graph(g, reps: int) -> float:
@@ -398,49 +421,90 @@ def time_graph(g, reps: int) -> float:
 
 
 def time_selector(wl: Workload, iters: int) -> tuple[float, float]:
+    """Selector and compact build per layer, isolated (queued back to back)."""
     t = wl.torch
     s = t.cuda.current_stream()
     c = wl.cache
-    ts, tc = [], []
-    for i in range(iters):
-        l = i % wl.L
-        a, b, e = (t.cuda.Event(enable_timing=True) for _ in range(3))
-        a.record(s)
-        wl.drv.selector(l, wl.logits, wl.params)
-        b.record(s)
-        c.compact_build(l)
-        e.record(s)
-        ts.append((a, b))
-        tc.append((b, e))
+    wl.drv.selector(0, wl.logits, wl.params)
     t.cuda.synchronize()
-    return (float(np.mean([a.elapsed_time(b) for a, b in ts[1:]])),
-            float(np.mean([a.elapsed_time(b) for a, b in tc[1:]])))
+    a, b, e = (t.cuda.Event(enable_timing=True) for _ in range(3))
+    a.record(s)
+    for i in range(iters):
+        wl.drv.selector(i % wl.L, wl.logits, wl.params)
+    b.record(s)
+    for i in range(iters):
+        c.compact_build(i % wl.L)
+    e.record(s)
+    t.cuda.synchronize()
+    return a.elapsed_time(b) / iters, b.elapsed_time(e) / iters
 
 
-def gpu_arm(args) -> dict:
+def time_dense_in_situ(wl: Workload) -> float | None:
+    """K1 as it runs inside the timed slow step: one eager asynchronous slow step
+    (dense on the main stream at the pipeline's share grid, Selector + compact of
+    the earlier layers concurrently on the aux stream), CUDA events on the main
+    stream around every dense launch; mean over layers 2.. (layer 0-1 run alone)."""
+    if wl.pipe is None:
+        return None
+    t = wl.torch
+    evs = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)) for _ in range(wl.L)]
+    wl.set_lengths(wl.ctx)
+    t.cuda.synchronize()
+    wl.drv.step_advance()
+    wl.pipe.begin()
+    for l in range(wl.L):
+        wl.pipe.layer(l, wl.q[l], wl.out[l], wl.k_new[l], wl.v_new[l], wl.params, False, dense_events=evs[l])
+    wl.pipe.end()
+    t.cuda.synchronize()
+    ts = [a.elapsed_time(b) for a, b in evs]
+    return float(np.mean(ts[2:] if len(ts) > 3 else ts))
+
+
+def traffic_for(kernel: str, cfg_name: str):
+    """DRAM bytes (read + write) per launch of `kernel` at `cfg_name` from the
+    committed ncu --set full captures (profiles/r02/traffic.json, else r01's C2
+    figures); None when no capture of that kernel at that config exists."""
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                t = json.load(f)
+        except Exception:
+            continue
+        e = t.get(cfg_name, {}).get(kernel) if cfg_name in t else (t.get(kernel) if cfg_name == "c2" else None)
+        if e:
+            return e["dram_read_bytes"] + e["dram_write_bytes"], f"profiles/{rnd}/traffic.json"
+    return None, f"no ncu capture of {kernel} at {cfg_name}"
+
+
+def _release(*objs):
+    import gc
+
+    import torch
+    for o in objs:
+        if isinstance(o, dict):
+            for g in o.values():
+                try:
+                    g.reset()
+                except Exception:
+                    pass
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
+    """One workload end to end on this rank: setup, warm-up, K timed steps (max over
+    ranks), the end-to-end variant and the per-kernel timings. `full` adds the e2e
+    and CPU-baseline legs (the headline config)."""
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group(args.backend)
-    if args.backend == "gloo":  # testing: several ranks may share one GPU
-        local %= torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    red_dev = dev if args.backend == "nccl" else torch.device("cpu")
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-    W, K = args.warmup, args.steps
+    world, rank, local, dev = ctx["world"], ctx["rank"], ctx["local"], ctx["dev"]
+    max_over_ranks = ctx["max_over_ranks"]
+    W = args.warmup
+    K = args.steps if args.steps else DEFAULT_STEPS[cfg_name]
     sched = schedule(W + K + 1, seed=2026 + 1)[1:]  # step 0 of the schedule is the setup slow step
-    wl = Workload(args.config, W + K + 8, dev, world, args.layers, args.sync_slow)
+    wl = Workload(cfg_name, W + K + 8, dev, world, args.layers, args.sync_slow, inputs=args.inputs)
     c = wl.cache
     use_graph = not args.no_graph
     graphs = {}
@@ -489,14 +553,13 @@ def gpu_arm(args) -> dict:
         dist.barrier()
     wl.drv.check_errors()
     n_slow = sum(timed)
-    tokens = wl.job_tokens * K
-    value = tokens / (ms / 1e3)
+    value = wl.job_tokens * K / (ms / 1e3)
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
-    if not args.no_e2e:
+    ge = {}
+    if full and not args.no_e2e:
         io = HostIO(wl)
-        ge = {}
         if use_graph:
             for slow in (False, True):
                 g = torch.cuda.CUDAGraph()
@@ -504,8 +567,7 @@ def gpu_arm(args) -> dict:
                     wl.step(slow, io=io)
                 ge[slow] = g
             torch.cuda.synchronize()
-        Ke = K  # the same schedule as the device-resident timing
-        sched_e = sched[W:W + Ke]
+        sched_e = sched[W:W + K]  # the same schedule as the device-resident timing
         wl.set_lengths(wl.ctx + 1)
         if world > 1:
             dist.barrier()
@@ -520,17 +582,18 @@ def gpu_arm(args) -> dict:
         b.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(a.elapsed_time(b))
-        e2e = {"value": wl.job_tokens * Ke / (ems / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": io.h2d, "d2h_bytes_per_step": io.d2h, "steps": Ke,
+        e2e = {"value": wl.job_tokens * K / (ems / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": io.h2d, "d2h_bytes_per_step": io.d2h, "steps": K,
                "copies": "pinned host <-> HBM in layer groups (" + " | ".join(str(l1 - l0) for l0, l1 in io.groups) +
                          ") on a copy stream, event-ordered with compute"}
 
     # ---- per-kernel device time (CUDA events on the launching stream) ----
     pk = peaks()
     Lcur = wl.ctx + 1
-    t_sp_iso = time_kernel(wl, "sparse", max(20, 2 * wl.L))
-    t_de = time_kernel(wl, "dense", max(8, wl.L // 2))
-    # in situ: the fast step's graph (advance + L fused launches, PDL-chained)
+    t_sp_iso = time_kernel(wl, "sparse", max(32, 2 * wl.L))
+    t_de_iso = time_kernel(wl, "dense", max(8, wl.L // 2))
+    t_de_situ = time_dense_in_situ(wl)
+    # in situ fast step: the fast step's graph (advance + L fused launches, PDL-chained)
     # replayed back to back; its launches' average duration = step time / L
     # (the advance kernel's share is charged to them: conservative)
     t_fast_step = t_slow_step = None
@@ -540,6 +603,7 @@ def gpu_arm(args) -> dict:
         wl.set_lengths(wl.ctx + 1)
         t_slow_step = time_graph(graphs[True], 3)
     t_sp = t_fast_step / wl.L if t_fast_step else t_sp_iso
+    t_de = t_de_situ if t_de_situ else t_de_iso
     # diagnostic: the same fused fast step with every layer in ONE launch (layer-batched
     # view of the cache), i.e. the kernel without the per-layer launch boundary
     t_lb = None
@@ -561,64 +625,148 @@ def gpu_arm(args) -> dict:
         except Exception:
             t_lb = None
     t_sel, t_cb = time_selector(wl, max(6, wl.L // 4))
-    bsp, bde = wl.bytes_sparse(), wl.bytes_dense(Lcur)
+    bsp, bde, bslow = wl.bytes_sparse(), wl.bytes_dense(Lcur), wl.bytes_slow_layer(Lcur)
+    hbm = pk["hbm_gbs"]
     kernels = {
         "fast_decode": {"ms": t_sp, "GB/s": bsp / t_sp / 1e6, "bytes": bsp, "isolated_ms": t_sp_iso,
+                        "isolated_frac": bsp / t_sp_iso / 1e6 / hbm,
                         "layer_batched": (None if t_lb is None else
                                           {"ms_per_layer": t_lb, "GB/s": bsp / t_lb / 1e6,
-                                           "frac": bsp / t_lb / 1e6 / pk["hbm_gbs"],
+                                           "frac": bsp / t_lb / 1e6 / hbm,
                                            "note": "diagnostic: all layers in one launch (no per-layer boundary)"}),
-                        "timing": ("fast-step graph replay / layers (in situ, PDL chain)" if t_fast_step
-                                   else "isolated launches between events")},
-        "dense_decode": {"ms": t_de, "GB/s": bde / t_de / 1e6, "bytes": bde},
-        "selector": {"ms": t_sel},
-        "compact_build": {"ms": t_cb},
+                        "timing": ("in situ: fast-step graph replay / layers (PDL chain)" if t_fast_step
+                                   else "isolated launches queued back to back")},
+        "dense_decode": {"ms": t_de, "GB/s": bde / t_de / 1e6, "bytes": bde,
+                         "isolated_ms": t_de_iso, "isolated_frac": bde / t_de_iso / 1e6 / hbm,
+                         "timing": ("in situ: the async slow step's share grid beside the Selector + compact "
+                                    "(events around each dense launch, eager step)" if t_de_situ
+                                    else "isolated full-grid launches queued back to back")},
+        "selector": {"ms": t_sel, "timing": "isolated, queued back to back"},
+        "compact_build": {"ms": t_cb, "timing": "isolated, queued back to back"},
     }
     for kk in ("fast_decode", "dense_decode"):
-        kernels[kk]["frac"] = kernels[kk]["GB/s"] / pk["hbm_gbs"]
+        kernels[kk]["frac"] = kernels[kk]["GB/s"] / hbm
     share_sp = (K - n_slow) * wl.L * t_sp
     share_de = n_slow * wl.L * t_de
     dom = "fast_decode" if share_sp >= share_de else "dense_decode"
-    roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["GB/s"], "peak": pk["hbm_gbs"],
+    traffic, tsrc = traffic_for(dom, cfg_name)
+    roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["GB/s"], "peak": hbm,
             "peak_source": pk["source"], "unit": "GB/s", "frac": kernels[dom]["frac"],
-            "traffic": measured_traffic(dom, args.config), "algorithmic_bytes": kernels[dom]["bytes"], "share_of_step": (share_sp if dom == "fast_decode" else share_de) / ms}
+            "traffic": traffic, "traffic_source": tsrc, "algorithmic_bytes": kernels[dom]["bytes"],
+            "timing": kernels[dom]["timing"], "isolated_frac": kernels[dom]["isolated_frac"],
+            "share_of_step": (share_sp if dom == "fast_decode" else share_de) / ms}
+    if t_slow_step:
+        roof["slow_step"] = {"us": t_slow_step * 1e3, "algorithmic_bytes": wl.L * bslow,
+                             "GB/s": wl.L * bslow / t_slow_step / 1e6,
+                             "frac": wl.L * bslow / t_slow_step / 1e6 / hbm,
+                             "note": "whole slow step (graph replay): dense KV + logits + Selector inputs "
+                                     "+ compact gather r/w + appends, per layer x layers"}
+    if t_fast_step:
+        roof["fast_step"] = {"us": t_fast_step * 1e3, "algorithmic_bytes": wl.L * bsp,
+                             "frac": wl.L * bsp / t_fast_step / 1e6 / hbm}
     fast_us = wl.L * (t_sp * 1e3)
     res = {
-        "metric": metric_name(args.config),
+        "metric": metric_name(cfg_name),
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True,
         "scaling": "strong" if wl.mode in ("heads", "seq") else "weak", "vs_baseline": None,
-        "dtype": "bf16 KV, fp32 accumulate; fp64 Selector", "data": "synthetic",
-        "config": {"workload": wl.name + f" ({args.config.upper()})", "layers": wl.L,
-                   "q_heads": CONFIGS[args.config][2], "kv_heads": CONFIGS[args.config][3],
-                   "kv_heads_per_gpu": wl.H, "head_dim": HEAD_DIM, "batch_per_gpu": wl.B,
-                   "context": wl.ctx, "n_sink": wl.ns, "k_budget": wl.K, "n_recent": wl.R,
-                   "schedule": f"seeded triggers p=1/24 + t_max={T_MAX}; {n_slow} slow / {K} steps",
-                   "parallelism": {
-                       "heads": f"kv-head sharded x{world} (one batch; z_base per slow-step layer exchanged via "
-                                + ("peer memory: CUDA IPC over NVLink" if getattr(wl, "peer", False) else "all-gather")
-                                + ")",
-                       "seq": f"sequence sharded x{world} (LSE-merged partials and sharded Selector stats, "
-                              "soft-NMS edges, top-k candidates exchanged via "
-                              + ("peer memory: CUDA IPC over NVLink, no collective launch" if getattr(wl, "peer", False)
-                                 else "all-gather") + ")",
-                   }.get(wl.mode, f"dp{world} (independent request batches)"),
-                   "cuda_graphs": use_graph if graph_note is None else graph_note,
-                   "slow_step": "synchronous" if wl.pipe is None else
-                                "async pipeline: dense on the main stream (1 CTA/SM), Selector + compact on an aux stream",
-                   "l2": "inputs larger than L2 (KV cache %.1f GB)" % (2 * c.sizes['kv_cache'] / 1e9)},
+        "dtype": "bf16 KV, fp32 accumulate; fp64 Selector", "data": f"synthetic ({args.inputs})",
+        "config": config_dict(cfg_name, world),
+        "run": {"kv_heads_per_gpu": wl.H, "batch_per_gpu": wl.B, "slow_steps_timed": f"{n_slow} of {K}",
+                "cuda_graphs": use_graph if graph_note is None else graph_note,
+                "slow_step": "synchronous" if wl.pipe is None else
+                             "async pipeline: dense on the main stream (share grid), Selector + compact on a "
+                             "low-priority aux stream",
+                "exchange": ("peer memory (CUDA IPC over NVLink)" if getattr(wl, "peer", False) else
+                             "NCCL all-gather" if wl.mode in ("heads", "seq") else "none"),
+                "kv_cache_gb_per_gpu": round(2 * c.sizes["kv_cache"] / 1e9, 1)},
         "slow_steps": n_slow, "fast_step_us_kernels": fast_us,
         "fast_step_us_graph": t_fast_step * 1e3 if t_fast_step else None,
         "slow_step_us_graph": t_slow_step * 1e3 if t_slow_step else None,
-        "slow_step_us_kernels": wl.L * (t_de + t_sel + t_cb) * 1e3,
+        "slow_step_us_kernels": wl.L * (t_de_iso + t_sel + t_cb) * 1e3,
         "kernels": kernels, "roofline": roof,
         "gpu_launches": sum(wl.launches(s_) for s_ in timed),
         "clocks": clk.summary(),
         "e2e": e2e,
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if full and rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_baseline(wl, sched[W:W + K], args)
+    _release(graphs, ge)
+    del wl
+    _release()
+    return res
+
+
+def _nccl_evidence() -> dict | None:
+    """NCCL's own INIT log lines of this rank (nranks, transports), when the
+    bench routed NCCL_DEBUG to a file."""
+    path = os.environ.get("SFI_NCCL_LOG")
+    if not path:
+        return None
+    import glob
+
+    lines = []
+    for fn in sorted(glob.glob(path.replace("%p", "*").replace("%h", "*"))):
+        try:
+            with open(fn) as f:
+                lines += [ln.strip() for ln in f if "nranks" in ln or "NVLS" in ln or "Init COMPLETE" in ln]
+        except OSError:
+            pass
+    return {"log_lines": lines[:12]} if lines else None
+
+
+def gpu_arm(args) -> dict:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
+        if args.backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            log = os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/sfi_bench_nccl.{os.getpid()}.%h.%p.log")
+            os.environ["SFI_NCCL_LOG"] = log
+        dist.init_process_group(args.backend)
+    if args.backend == "gloo":  # testing: several ranks may share one GPU
+        local %= torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    red_dev = dev if args.backend == "nccl" else torch.device("cpu")
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = dict(world=world, rank=rank, local=local, dev=dev, max_over_ranks=max_over_ranks)
+    primary = args.config or ("c2" if world == 1 else "c3")
+    if args.also is None:
+        also = ["c3", "c4"] if world == 1 else ["c4", "c2"]
+    else:
+        also = [x for x in args.also.split(",") if x and x != "none"]
+    also = [a for a in also if a != primary]
+    res = run_config(primary, args, ctx, full=True)
+    extra = []
+    for cfg in also:
+        try:
+            r = run_config(cfg, args, ctx, full=False)
+            extra.append({k: r[k] for k in ("metric", "value", "unit", "n_gpus", "steps", "ms_per_step", "scaling",
+                                            "slow_steps", "fast_step_us_graph", "slow_step_us_graph", "roofline",
+                                            "config", "gpu_launches")})
+        except Exception as ex:  # an extra line never costs the headline
+            extra.append({"config": cfg, "error": f"{type(ex).__name__}: {ex}"[:300]})
+            _release()
+    res["also"] = extra
+    if world > 1:
+        ev = _nccl_evidence()
+        res["nccl"] = {"nranks": world, "version": ".".join(map(str, torch.cuda.nccl.version())),
+                       "backend": args.backend, **(ev or {})}
         dist.destroy_process_group()
     return res if rank == 0 else None
 
@@ -627,48 +775,98 @@ def gpu_arm(args) -> dict:
 # CPU reference (oracle/_ref = the unmodified reference, else the port)
 
 class CpuSample:
-    """One layer of the workload on the reference CPU path: per request a
-    reference KvStore (fp32, bf16-exact values copied from the device cache),
-    the device's current selection for the compact segment, and the device's
-    pooled logits as the Selector input."""
+    """One layer of the workload on the reference CPU path, split into the
+    independent units BASELINE.md §4 names: one reference KvStore per (request,
+    KV head) (fp32, bf16-exact values; a one-head store performs exactly the
+    per-head arithmetic of attend, attention.cpp:80-113, 258-291), and one
+    run_selector call per request (cross-head couples a request's heads,
+    selector.cpp:204-230) followed by the reorganize of its heads.
+      fast unit (b, h): attention_kernel_sparse
+      slow: attention_kernel_dense per (b, h), then per b run_selector on the
+            workload's pooled logits + reorganize of its H stores."""
 
-    def __init__(self, src, data: dict):
+    def __init__(self, data: dict, threads: int):
         from oracle import oracle as O
 
         self.orc = O.load("best")
         self.kind = self.orc.kind
-        self.src = src
         self.d = data
-        self.stores = []
-        self.cur_sel = list(data["sel"])
-        B = data["B"]
-        with cf.ThreadPoolExecutor(max_workers=min(B, os.cpu_count() or 1)) as ex:
-            self.stores = list(ex.map(self._make_store, range(B)))
+        B, H = data["B"], data["H"]
+        self.units = [(b, h) for b in range(B) for h in range(H)]
+        self.cur_sel = {(b, h): data["sel"][b][h] for b, h in self.units}
+        self.pool = cf.ThreadPoolExecutor(max_workers=threads)  # persistent: no per-layer thread start-up
+        self.stores = dict(zip(self.units, self.pool.map(self._make_store, self.units)))
 
-    def _make_store(self, b):
+    def _make_store(self, bh):
+        b, h = bh
         d = self.d
-        st = self.orc.store(1, d["H"], d["Hq"], HEAD_DIM, d["L"] + 8)
-        st.append_many(d["k"][b], d["v"][b])
-        st.reorganize(0, d["sink"], d["sel"][b])
+        G, D = d["Hq"] // d["H"], HEAD_DIM
+        st = self.orc.store(1, 1, G, D, d["L"] + 8)
+        st.append_many(d["k"][b][:, h * D:(h + 1) * D], d["v"][b][:, h * D:(h + 1) * D])
+        st.reorganize(0, d["sink"], [d["sel"][b][h]])
         return st
 
-    def fast(self, b):
-        d = self.d
-        self.stores[b].attention_sparse(0, d["q"][b], d["sink"], self.cur_sel[b], d["rs"], d["rl"])
+    def _q(self, b, h):
+        G, D = self.d["Hq"] // self.d["H"], HEAD_DIM
+        return self.d["q"][b][h * G * D:(h + 1) * G * D]
 
-    def slow(self, b):
+    def fast(self, bh):
+        d = self.d
+        self.stores[bh].attention_sparse(0, self._q(*bh), d["sink"], [self.cur_sel[bh]], d["rs"], d["rl"])
+
+    def dense(self, bh):
+        self.stores[bh].attention_dense(0, self._q(*bh))
+
+    def select(self, b):
         from oracle import oracle as O
 
         d = self.d
-        st = self.stores[b]
-        st.attention_dense(0, d["q"][b])
-        sel, _ = self.orc.run_selector(d["logits"][b], np.arange(d["j0"], d["j1"] + 1),
-                                       d["norms"][b], O.make_cfg(k_budget=d["K"]))
-        st.reorganize(0, d["sink"], sel)
-        self.cur_sel[b] = sel
+        sel, _ = self.orc.run_selector(d["logits"][b], np.arange(d["j0"], d["j1"] + 1), d["norms"][b],
+                                       O.make_cfg(k_budget=d["K"]))
+        for h in range(d["H"]):
+            self.stores[(b, h)].reorganize(0, d["sink"], [sel[h]])
+            self.cur_sel[(b, h)] = sel[h]
+
+
+def time_cpu_layer(sample: CpuSample, slow: bool, threads: int) -> float:
+    """Seconds for one layer of the workload with `threads` host threads."""
+    t0 = time.perf_counter()
+    if threads == 1:
+        for u in sample.units:
+            (sample.dense if slow else sample.fast)(u)
+        if slow:
+            for b in range(sample.d["B"]):
+                sample.select(b)
+    else:
+        ex = sample.pool
+        list(ex.map(sample.dense if slow else sample.fast, sample.units))
+        if slow:
+            list(ex.map(sample.select, range(sample.d["B"])))
+    return time.perf_counter() - t0
+
+
+def host_threads() -> int:
+    """std::thread::hardware_concurrency() of this host (the CPUs this process may use)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def pooled_logits_np(k: np.ndarray, q: np.ndarray, H: int, Hq: int, j0: int, j1: int) -> np.ndarray:
+    """The workload's mean-pooled decode logits over J (attention.cpp:394-409):
+    per KV head, mean over its G query heads of q . k / sqrt(d) (input
+    preparation for the Selector, untimed)."""
+    G, D = Hq // H, HEAD_DIM
+    kh = k.reshape(k.shape[0], H, D)[j0 - 1:j1].astype(np.float64)        # [n][H][d]
+    qh = q.reshape(H, G, D)
+    lg = np.einsum("nhd,hgd->hgn", kh, qh) / np.sqrt(D)
+    return lg.mean(axis=1)
 
 
 def gather_cpu_data(wl: Workload) -> dict:
+    """Layer 0 of the running workload, read back from the device: K/V, q, the
+    current selection, the pooled logits and the key norms."""
     t = wl.torch
     c = wl.cache
     t.cuda.synchronize()
@@ -682,7 +880,7 @@ def gather_cpu_data(wl: Workload) -> dict:
     B, H, d = wl.B, wl.H, HEAD_DIM
     k = c.k_cache[0, :, :, :L].float().cpu().numpy()  # [B][H][L][d]
     v = c.v_cache[0, :, :, :L].float().cpu().numpy()
-    data = {
+    return {
         "B": B, "H": H, "Hq": wl.Hq, "L": L, "K": wl.K, "sink": list(range(1, ns + 1)),
         "rs": L - rl + 1, "rl": rl, "j0": j0, "j1": j1,
         "k": [np.ascontiguousarray(np.transpose(k[b], (1, 0, 2)).reshape(L, H * d)) for b in range(B)],
@@ -692,109 +890,204 @@ def gather_cpu_data(wl: Workload) -> dict:
         "logits": [wl.logits[b, :, : j1 - j0 + 1].double().cpu().numpy() for b in range(B)],
         "norms": [c.key_norms[0, b, :, j0 - 1:j1].cpu().numpy() for b in range(B)],
     }
-    return data
 
 
-def synth_cpu_data(cfg_name: str) -> dict:
-    """Same-shaped synthetic inputs generated on the host (numpy; bf16-exact
-    N(0,1) K/V, fp64 q), for the reference arm: no device code involved."""
+def synth_cpu_data(cfg_name: str, inputs: str = "peaked") -> dict:
+    """The workload's layer generated on the host (numpy; bf16-exact N(0,1) K/V,
+    fp64 q, 32 planted k = 3 q + noise positions per (b, KV head) when peaked),
+    for the reference arm: no device code involved. The Selector gets the
+    workload's real pooled logits over these K and q; the first selection is the
+    reference Selector's own on them."""
     name, n_layers, Hq, H, B, ctx, ns, K, R = CONFIGS[cfg_name]
     rng = np.random.default_rng(2026 + 1)
     L = ctx + 1
     rl = min(R, L - ns)
     j0, j1 = ns + 1, L - rl
-    d = HEAD_DIM
+    d, G = HEAD_DIM, Hq // H
 
     def bf16(x):
-        u = x.view(np.uint32).astype(np.uint64)
-        return (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
+        u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+        return (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32).reshape(x.shape)
 
-    ks, vs, norms, logits, sels = [], [], [], [], []
+    ks, vs, norms, logits, qs = [], [], [], [], []
     for b in range(B):
         k = bf16(rng.standard_normal((L, H * d), dtype=np.float32))
         v = bf16(rng.standard_normal((L, H * d), dtype=np.float32))
+        q = rng.standard_normal(Hq * d)
+        if inputs == "peaked":
+            kh = k.reshape(L, H, d)
+            for h in range(H):
+                pos = rng.integers(j0, j1 + 1, size=32)
+                for i, p in enumerate(pos):
+                    g = i % G
+                    kh[p - 1, h] = bf16(3.0 * q[(h * G + g) * d:(h * G + g + 1) * d].astype(np.float32)
+                                        + rng.standard_normal(d, dtype=np.float32))
         kh = k.reshape(L, H, d)
         norms.append(np.sqrt((kh[j0 - 1:j1].astype(np.float64) ** 2).sum(-1)).T.copy())
-        logits.append(rng.normal(0.0, 0.3, size=(H, j1 - j0 + 1)))
-        sels.append([np.sort(rng.choice(np.arange(j0, j1 + 1), size=min(K, j1 - j0 + 1),
-                                        replace=False)).astype(np.int32) for _ in range(H)])
+        logits.append(pooled_logits_np(k, q, H, Hq, j0, j1))
         ks.append(k)
         vs.append(v)
+        qs.append(q)
+    from oracle import oracle as O
+
+    orc = O.load("best")
+    sels = [orc.run_selector(logits[b], np.arange(j0, j1 + 1), norms[b], O.make_cfg(k_budget=K))[0]
+            for b in range(B)]
     return {"B": B, "H": H, "Hq": Hq, "L": L, "K": K, "sink": list(range(1, ns + 1)),
             "rs": L - rl + 1, "rl": rl, "j0": j0, "j1": j1, "k": ks, "v": vs,
-            "q": [rng.standard_normal(Hq * d) for _ in range(B)], "sel": sels, "logits": logits,
-            "norms": norms, "n_layers": n_layers, "name": name, "ctx": ctx}
+            "q": qs, "sel": sels, "logits": logits, "norms": norms, "n_layers": n_layers, "name": name,
+            "ctx": ctx}
 
 
-def time_cpu_layer(sample: CpuSample, slow: bool, threads: int) -> float:
-    fn = sample.slow if slow else sample.fast
-    t0 = time.perf_counter()
-    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(fn, range(sample.d["B"])))
-    return time.perf_counter() - t0
+def _median(xs):
+    return float(np.median(xs))
+
+
+def cpu_full_step(data: dict, n_layers: int, threads: int, frac_slow: float) -> dict:
+    """Un-extrapolated: every layer of one fast and one slow step actually run
+    (n_layers independent per-layer store sets over the same layer inputs; the
+    arithmetic does not depend on the values), on `threads` threads. Used where
+    it is small enough (C1: 28 layers x 8 KV heads x 8K)."""
+    samples = [CpuSample(data, threads) for _ in range(n_layers)]
+    units = [(s, u) for s in samples for u in s.units]
+    ex = samples[0].pool
+
+    def run(slow):
+        t0 = time.perf_counter()
+        list(ex.map(lambda su: (su[0].dense if slow else su[0].fast)(su[1]), units))
+        if slow:
+            list(ex.map(lambda sb: sb[0].select(sb[1]), [(s, b) for s in samples for b in range(data["B"])]))
+        return time.perf_counter() - t0
+    run(False)
+    tf = _median([run(False) for _ in range(3)])
+    ts = run(True)
+    step = frac_slow * ts + (1 - frac_slow) * tf
+    return {"value": data["B"] / step, "unit": "tokens/s", "cores": threads, "layers": n_layers,
+            "fast_step_ms": tf * 1e3, "slow_step_ms": ts * 1e3,
+            "note": f"all {n_layers} layers run (no extrapolation over layers), slow fraction {frac_slow:.3f}"}
 
 
 def cpu_baseline(wl: Workload, sched_timed: list[bool], args) -> dict:
+    """the reference CPU path on this host, on layer 0 of the same
+    workload (the device's K/V, q, selection and pooled logits), N =
+    hardware_concurrency threads over (request, KV head) units, plus the
+    single-thread figure; bench_attention protocol (1 discarded warm-up, median
+    of repeats, harness.cpp:518-551); one layer measured, extrapolated x layers at
+    the timed schedule's slow fraction."""
     data = gather_cpu_data(wl)
-    sample = CpuSample(wl, data)
-    threads = min(wl.B, os.cpu_count() or 1)
-    time_cpu_layer(sample, False, threads)  # warm-up (reference bench_attention: 1 warm-up)
-    tf = [time_cpu_layer(sample, False, threads) for _ in range(3)]
-    ts = [time_cpu_layer(sample, True, threads) for _ in range(1)]
-    t_fast, t_slow = float(np.median(tf)), float(np.median(ts))
+    N = host_threads()
+    sample = CpuSample(data, N)
+    time_cpu_layer(sample, False, N)  # warm-up
+    tf = [time_cpu_layer(sample, False, N) for _ in range(3)]
+    ts = [time_cpu_layer(sample, True, N) for _ in range(1)]
+    t_fast, t_slow = _median(tf), _median(ts)
+    tf1 = time_cpu_layer(sample, False, 1)
+    ts1 = time_cpu_layer(sample, True, 1)
     frac_slow = sum(sched_timed) / max(1, len(sched_timed))
     step_s = wl.L * (frac_slow * t_slow + (1 - frac_slow) * t_fast)
-    return {"value": wl.B / step_s, "unit": "tokens/s", "cores": threads, "kind": sample.kind,
-            "sample": (f"layer 0 of {wl.L}, all {wl.B} requests x {wl.H} KV heads at L={data['L']}: "
-                       f"fast (attention_kernel_sparse) {t_fast*1e3:.1f} ms, slow (attention_kernel_dense"
-                       f" + run_selector + reorganize) {t_slow*1e3:.1f} ms per layer; x{wl.L} layers at the "
-                       f"timed schedule's slow fraction {frac_slow:.3f}"),
-            "fast_layer_ms": t_fast * 1e3, "slow_layer_ms": t_slow * 1e3}
+    step_s1 = wl.L * (frac_slow * ts1 + (1 - frac_slow) * tf1)
+    full = cpu_full_step(data, wl.L, N, frac_slow) if wl.cfg_name == "c1" else None
+    return {"value": wl.B / step_s, "unit": "tokens/s", "cores": N, "kind": sample.kind,
+            "single_thread": {"value": wl.B / step_s1, "unit": "tokens/s", "fast_layer_ms": tf1 * 1e3,
+                              "slow_layer_ms": ts1 * 1e3},
+            "sample": (f"layer 0 of {wl.L} measured (all {wl.B} requests x {wl.H} KV heads at L={data['L']}, "
+                       f"{N} threads over {len(sample.units)} (request, KV head) units): fast "
+                       f"(attention_kernel_sparse) {t_fast*1e3:.1f} ms, slow (attention_kernel_dense + "
+                       f"run_selector + reorganize) {t_slow*1e3:.1f} ms per layer; extrapolated x{wl.L} layers "
+                       f"at the timed schedule's slow fraction {frac_slow:.3f}"),
+            "fast_layer_ms": t_fast * 1e3, "slow_layer_ms": t_slow * 1e3, "full_step_measured": full}
 
 
 def reference_arm(args) -> dict | None:
-    """--impl reference: the reference CPU implementation of the path on this
-    host's cores, same config / metric; each step a one-layer sample of the
-    workload (fast or slow per the same schedule) extrapolated to all layers."""
+    """--impl reference: the reference CPU implementation of the path (the
+    unmodified reference, oracle/_ref) on this host's cores, same config / metric
+    / schedule; every step is a one-layer sample of the workload (fast or slow
+    per the schedule, all (request, KV head) units on hardware_concurrency
+    threads) extrapolated over the layers."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
-    W, K = args.warmup, args.steps
+    cfg = args.config or ("c2" if world == 1 else "c3")
+    W = args.warmup
+    K = args.steps if args.steps else DEFAULT_STEPS[cfg]
     sched = schedule(W + K + 1, seed=2026 + 1)[1:]
-    data = synth_cpu_data(args.config)
+    data = synth_cpu_data(cfg, args.inputs)
     nl = data["n_layers"]
-    sample = CpuSample(None, data)
-    threads = min(data["B"], os.cpu_count() or 1)
+    N = host_threads()
+    sample = CpuSample(data, N)
     for i in range(W):
-        time_cpu_layer(sample, sched[i], threads)
+        time_cpu_layer(sample, sched[i], N)
     total = 0.0
+    layer_s = {True: [], False: []}
     for slow in sched[W:W + K]:
-        total += nl * time_cpu_layer(sample, slow, threads)
-    value = data["B"] * K / total
+        t = time_cpu_layer(sample, slow, N)
+        layer_s[slow].append(t)
+        total += nl * t
+    B_job = data["B"] * (world if SHARDING[cfg] == "dp" else 1)
+    value = B_job * K / total
+    tf1 = time_cpu_layer(sample, False, 1)
+    ts1 = time_cpu_layer(sample, True, 1)
+    fs = sum(sched[W:W + K]) / K
+    v1 = data["B"] / (nl * (fs * ts1 + (1 - fs) * tf1))
+    full = cpu_full_step(data, nl, N, fs) if cfg == "c1" else None
+    sample_txt = (f"each step: one layer (of {nl}) measured, all {data['B']} requests x {data['H']} KV heads "
+                  f"at L={data['L']} on {N} threads over (request, KV head) units, extrapolated x{nl}; fast = "
+                  "attention_kernel_sparse, slow = attention_kernel_dense + run_selector (workload's pooled "
+                  "logits) + reorganize")
     return {
-        "impl": "reference", "metric": metric_name(args.config),
-        "value": value, "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "impl": "reference", "metric": metric_name(cfg),
+        "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": total / K * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 KV, fp64 accumulate (reference)",
-        "data": "synthetic",
-        "config": {"workload": data["name"] + f" ({args.config.upper()})", "layers": nl,
-                   "batch_per_gpu": data["B"], "context": data["ctx"]},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": sample.kind,
-                         "sample": (f"one layer per step (of {nl}), all {data['B']} requests x "
-                                    f"{data['H']} KV heads, extrapolated x{nl}; fast = "
-                                    "attention_kernel_sparse, slow = attention_kernel_dense + "
-                                    "run_selector + reorganize")},
+        "scaling": "strong" if SHARDING[cfg] in ("heads", "seq") and world > 1 else "weak",
+        "vs_baseline": None, "dtype": "fp32 KV, fp64 accumulate (reference)",
+        "data": f"synthetic ({args.inputs})", "config": config_dict(cfg, world),
+        "measured_layer_ms": {"fast_median": _median(layer_s[False]) * 1e3 if layer_s[False] else None,
+                              "slow_median": _median(layer_s[True]) * 1e3 if layer_s[True] else None},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": N, "kind": sample.kind,
+                         "sample": sample_txt,
+                         "single_thread": {"value": v1, "unit": "tokens/s", "fast_layer_ms": tf1 * 1e3,
+                                           "slow_layer_ms": ts1 * 1e3},
+                         "full_step_measured": full},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a torchrun environment: launch N ranks of this script
+    through torch.distributed.run on this node (127.0.0.1) and return its exit code."""
+    import socket
+
+    import torch
+
+    n_dev = torch.cuda.device_count()
+    if args.gpus > n_dev and args.backend == "nccl":
+        print(f"bench.py: --gpus {args.gpus} but only {n_dev} CUDA device(s) are visible", file=sys.stderr)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    # 512 steps: SURVEY §8d's C2 workload (the seeded trigger schedule's long-run slow fraction, ~4.3%)
-    ap.add_argument("--steps", type=int, default=512)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default per config: C1 256, C2 512, C3/C4 64 — SURVEY §8d)")
     ap.add_argument("--warmup", type=int, default=8)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="headline workload (default: c2 on 1 GPU, c3 KV-head sharded on N > 1)")
+    ap.add_argument("--also", default=None,
+                    help="comma-separated extra configs timed after the headline (default: c3,c4 on 1 GPU, "
+                         "c4,c2 on N > 1; 'none' for none); reported under 'also'")
+    ap.add_argument("--inputs", default="peaked", choices=["peaked", "iid"],
+                    help="synthetic inputs: peaked = 32 planted k = 3q + noise positions per (b, KV head) "
+                         "(SURVEY §8d), iid = N(0, 1) K/V")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
@@ -806,9 +1099,11 @@ def main():
                     help="torch.distributed backend (gloo: several ranks on one GPU, testing only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     res = reference_arm(args) if args.impl == "reference" else gpu_arm(args)
     if res is not None:
-        print(json.dumps(res))
+        print(json.dumps(res), flush=True)
 
 
 if __name__ == "__main__":

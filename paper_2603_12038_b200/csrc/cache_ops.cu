@@ -8,6 +8,8 @@
 //                           clamp(L - n_sink, 0, n_recent) positions
 //   KvStore::reorganize     attention.cpp:186-217  merge(sink, selected),
 //                           strictly ascending, 1 <= p <= len, bit-exact copy
+#include <cstdio>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -311,6 +313,28 @@ __device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
   return v;
 }
 
+// Bounded wait for a peer's flag: a rank that never publishes (crashed, or a
+// schedule mismatch) ends the job loudly after kPeerTimeoutNs instead of hanging it.
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void wait_flag(const int32_t* f, int epoch) {
+  if (ld_acquire_sys(f) >= epoch) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(f) < epoch) {
+    __nanosleep(128);
+    if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+      printf("sfi peer exchange: a peer flag stayed below epoch %d for 20 s; aborting\n", epoch);
+      __trap();
+    }
+  }
+}
+
 __global__ void peer_publish_kernel(int32_t* flag) {
   griddep_wait();  // the partial producer before us on the stream has completed
   if (threadIdx.x == 0) asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(flag) : "memory");
@@ -327,7 +351,7 @@ __global__ void peer_merge_kernel(int n_parts, int rows, int D, const float* con
   if (threadIdx.x == 0) {
     const int epoch = ld_acquire_sys(my_flag);  // this rank's own publish, earlier on the stream
     for (int i = 0; i < n_parts; ++i) {
-      while (ld_acquire_sys(flags[i]) < epoch) __nanosleep(64);
+      wait_flag(flags[i], epoch);
       so[i] = o_ptrs[i];
       sl[i] = lse_ptrs[i];
     }
@@ -360,7 +384,7 @@ __global__ void peer_gather_kernel(long long words, const uint32_t* const* src, 
   __shared__ const uint32_t* s_src;
   if (threadIdx.x == 0) {
     const int epoch = ld_acquire_sys(my_flag);
-    while (ld_acquire_sys(flags[r]) < epoch) __nanosleep(64);
+    wait_flag(flags[r], epoch);
     s_src = src[r];
   }
   __syncthreads();

@@ -269,12 +269,18 @@ class SlowStepPipeline:
         self.used = [False] * self.slots
 
     def layer(self, l: int, q: torch.Tensor, out: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
-              params=None, rebuild_ring: bool = False):
+              params=None, rebuild_ring: bool = False, dense_events=None):
+        """dense_events: optional (start, end) CUDA events recorded on the main stream
+        around the dense launch (its in-situ duration beside the aux-stream work)."""
         c, main, s = self.c, self.main, l % self.slots
         if self.used[s]:
             main.wait_event(self.ev_free[s])
         c.ring_append(l, k_new, v_new)
+        if dense_events is not None:
+            dense_events[0].record(main)
         c.dense_decode_ex(l, q, out, self.logits[s], 0, share_sm=self.share_sm)
+        if dense_events is not None:
+            dense_events[1].record(main)
         self.ev_ready[s].record(main)
         with torch.cuda.stream(self.aux):
             self.aux.wait_event(self.ev_ready[s])

@@ -40,6 +40,25 @@ def all_gather_blocks(local: torch.Tensor, out: torch.Tensor, group=None) -> tor
     return out
 
 
+def agree(ok: bool, group=None, what: str = "peer-memory setup", err: str = "") -> None:
+    """Every rank votes (all_reduce MIN); raises on EVERY rank unless all succeeded,
+    so ranks fall back to the all-gather path together instead of some blocking
+    in a collective the others never enter."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
+        else torch.device("cpu")
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    if int(t.item()) != 1:
+        raise RuntimeError(f"{what} failed on at least one rank" + (f" (here: {err})" if err else ""))
+
+
+def _attempt(fn):
+    try:
+        return True, "", fn()
+    except Exception as e:  # noqa: BLE001 - reported through the vote
+        return False, f"{type(e).__name__}: {e}", None
+
+
 def _enable_peer_access(world: int) -> None:
     """Maps every visible GPU into this process's device (NVLink P2P), so IPC
     buffers opened in another device's context are addressable from kernels on
@@ -85,7 +104,7 @@ class PeerExchange:
         self.shared = dict(shared or {})  # further blocks all-gathered in place (gather())
         self.shared["_probe"] = torch.zeros(64, dtype=torch.int32, device=device)
         self._peer_views = None
-        if peers is None:
+        if peers is None:  # every step votes: no rank commits to peer memory alone
             self.connect(self._exchange_handles(group))
             self._self_test(group)
 
@@ -109,13 +128,17 @@ class PeerExchange:
     def _exchange_handles(self, group):
         from torch.multiprocessing.reductions import reduce_tensor
 
-        _enable_peer_access(self.world)
-        mine = [reduce_tensor(t) for t in self.local_views()]
+        ok, err, mine = _attempt(lambda: (_enable_peer_access(self.world),
+                                          [reduce_tensor(t) for t in self.local_views()])[1])
+        agree(ok, group, "P2P access / IPC handle export", err)
         objs = [None] * self.world
         dist.all_gather_object(objs, mine, group=group)
-        views = []
-        for r, rec in enumerate(objs):
-            views.append(self.local_views() if r == self.rank else tuple(fn(*args) for fn, args in rec))
+
+        def open_all():
+            return [self.local_views() if r == self.rank else tuple(fn(*args) for fn, args in rec)
+                    for r, rec in enumerate(objs)]
+        ok, err, views = _attempt(open_all)
+        agree(ok, group, "IPC handle import", err)
         return views
 
     def local_views(self):

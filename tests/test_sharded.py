@@ -207,3 +207,42 @@ def test_head_sharded_two_processes_one_gpu(peer):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+# ---- peer-memory setup: ranks fall back together (no split decision) ----
+
+def _agree_worker(rank, world, port, fail_rank, q):
+    try:
+        _init(rank, world, port)
+        from paper_2603_12038_b200.sharded import agree
+
+        raised = False
+        try:
+            agree(rank != fail_rank, None, "probe", "injected" if rank == fail_rank else "")
+        except RuntimeError:
+            raised = True
+        # both ranks continue with the same collective sequence afterwards (no hang)
+        t = torch.tensor([rank], dtype=torch.int32)
+        dist.all_reduce(t)
+        q.put((rank, (raised, int(t.item()))))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 0, 1])
+def test_peer_setup_vote_gloo_world2(fail_rank):
+    """sharded.agree: a step of the peer-memory setup that fails on ONE rank makes
+    every rank raise (and fall back to the all-gather path), never just that one
+    (a one-sided fallback left the other rank blocked in a collective)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, fail_rank, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    want = (fail_rank >= 0, 1)
+    assert res == {0: want, 1: want}, res
