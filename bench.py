@@ -154,7 +154,7 @@ class ClockSampler:
 
 class Workload:
     def __init__(self, cfg_name: str, steps_total: int, device, world: int = 1, layers: int = 0,
-                 sync_slow: bool = False, inputs: str = "iid"):
+                 sync_slow: bool = False, inputs: str = "iid", backend: str = "nccl"):
         import torch
 
         import paper_2603_12038_b200 as sfi
@@ -170,33 +170,38 @@ class Workload:
         self.mode = SHARDING[cfg_name] if world > 1 else "single"
         self.world = world
         fill_len = self.ctx
+        # exchange of the sharded configs (SFI_SEQ_EXCHANGE): "nccl" (default on the nccl
+        # backend) = the C ABI's in-call ncclAllGather on torch's communicator
+        # (sfi_selector_sharded_nccl / sfi_merge_partials_nccl / sfi_seq_selector_nccl);
+        # "allgather" = torch.distributed all-gathers (the gloo default); "peer" = CUDA-IPC
+        # peer memory (opt-in: only the one-GPU two-process form has run)
+        xch = os.environ.get("SFI_SEQ_EXCHANGE", "nccl" if backend == "nccl" else "allgather")
+        self.exchange = xch if world > 1 else "none"
+        self.peer = world > 1 and self.L >= 2 and xch == "peer"
+        nccl = world > 1 and xch == "nccl"
         if self.mode == "heads":
             from paper_2603_12038_b200.sharded import HeadShardedSfi
 
-            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "allgather") == "peer"
-            try:  # z_base exchange in place over peer memory (CUDA IPC), else all-gather
-                self.drv = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
-                                          self.K, self.R, device=device, peer=self.peer)
-            except Exception as e:  # pragma: no cover - depends on the box's P2P / IPC support
-                print(f"peer exchange unavailable ({e}); using all-gather", file=sys.stderr)
-                self.peer = False
-                self.drv = HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
-                                          self.K, self.R, device=device)
+            mk = lambda **kw: HeadShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,  # noqa
+                                             self.K, self.R, device=device, **kw)
+            try:
+                self.drv = mk(peer=self.peer, nccl=nccl)
+            except Exception as e:  # pragma: no cover - every rank votes in the peer setup (sharded.agree)
+                print(f"{xch} exchange unavailable ({e}); using torch all-gather", file=sys.stderr)
+                self.peer, self.exchange = False, "allgather"
+                self.drv = mk()
             self.H, self.Hq = self.drv.local_heads, self.drv.local_heads * self.G  # this rank's heads
         elif self.mode == "seq":
             from paper_2603_12038_b200.sharded import SeqShardedSfi
 
-            # per-step (O, LSE) exchange through peer memory (CUDA IPC over NVLink,
-            # sfi_peer_merge) unless SFI_SEQ_EXCHANGE=allgather or the mapping fails
-            self.peer = world > 1 and self.L >= 2 and os.environ.get("SFI_SEQ_EXCHANGE", "allgather") == "peer"
+            mk = lambda **kw: SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx,  # noqa
+                                            self.ns, self.K, self.R, device=device, **kw)
             try:
-                self.drv = SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx, self.ns,
-                                         self.K, self.R, device=device, peer=self.peer)
-            except Exception as e:  # pragma: no cover - depends on the box's P2P / IPC support
-                print(f"peer exchange unavailable ({e}); using all-gather", file=sys.stderr)
-                self.peer = False
-                self.drv = SeqShardedSfi(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ctx, self.ns,
-                                         self.K, self.R, device=device)
+                self.drv = mk(peer=self.peer, nccl=nccl)
+            except Exception as e:  # pragma: no cover
+                print(f"{xch} exchange unavailable ({e}); using torch all-gather", file=sys.stderr)
+                self.peer, self.exchange = False, "allgather"
+                self.drv = mk()
             fill_len = min(self.drv.cap, self.ctx - self.drv.base)  # this rank's positions
         else:
             self.drv = sfi.SfiCache(self.L, self.B, self.H, self.Hq, HEAD_DIM, self.Lmax, self.ns,
@@ -504,7 +509,8 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
     W = args.warmup
     K = args.steps if args.steps else DEFAULT_STEPS[cfg_name]
     sched = schedule(W + K + 1, seed=2026 + 1)[1:]  # step 0 of the schedule is the setup slow step
-    wl = Workload(cfg_name, W + K + 8, dev, world, args.layers, args.sync_slow, inputs=args.inputs)
+    wl = Workload(cfg_name, W + K + 8, dev, world, args.layers, args.sync_slow, inputs=args.inputs,
+                  backend=args.backend)
     c = wl.cache
     use_graph = not args.no_graph
     graphs = {}
@@ -677,8 +683,9 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
                 "slow_step": "synchronous" if wl.pipe is None else
                              "async pipeline: dense on the main stream (share grid), Selector + compact on a "
                              "low-priority aux stream",
-                "exchange": ("peer memory (CUDA IPC over NVLink)" if getattr(wl, "peer", False) else
-                             "NCCL all-gather" if wl.mode in ("heads", "seq") else "none"),
+                "exchange": {"nccl": "ncclAllGather in-call through the C ABI (torch's communicator)",
+                             "allgather": "torch.distributed all-gather",
+                             "peer": "peer memory (CUDA IPC over NVLink)"}.get(wl.exchange, "none"),
                 "kv_cache_gb_per_gpu": round(2 * c.sizes["kv_cache"] / 1e9, 1)},
         "slow_steps": n_slow, "fast_step_us_kernels": fast_us,
         "fast_step_us_graph": t_fast_step * 1e3 if t_fast_step else None,

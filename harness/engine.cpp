@@ -1,5 +1,6 @@
-// engine.cpp — the reference's request loop around the device hot path
-// (include/sfi_b200.hpp, "The request loop").
+// engine.cpp — END-TO-END TEST HARNESS (harness/sfi_toy.hpp, libsfi_toy.so;
+// not in the product library): the reference's request loop around the device
+// hot path.
 //
 //   run_request     scheduler.cpp:213-330   prefill + slow/fast decode loop
 //   run_dense       scheduler.cpp:332-365   dense greedy baseline
@@ -21,8 +22,9 @@
 #include <random>
 
 #include "sfi_b200.hpp"
+#include "sfi_toy.hpp"
 
-namespace sfi_b200 {
+namespace sfi {
 
 namespace {
 
@@ -264,7 +266,7 @@ StepOutput run_step(const ToyModel& model, TokenId token, KvStore& store, const 
       if (mode.select) {
         // refresh_selected for this layer: J empty -> nothing to select
         if (nJ > 0 && static_cast<int>(cap->allowed.size()) == nJ) {
-          const sfi_selector_params prm = mode.select->to_params();
+          const sfi_selector_params prm = to_params(*mode.select);
           check(sfi_selector(&dshape, &dcache, l, logits, &prm, stream));
           read_errors(store);
           (*mode.selected)[l] = read_selection(store, l);
@@ -471,7 +473,7 @@ RequestResult run_request(const ToyModel& model, const std::vector<TokenId>& pro
         continue;
       }
       float* d = capture_window(store, l, q_rows[l], allowed, prompt_len - 1 - rows + 1, cfg.pool);
-      const sfi_selector_params prm = cfg.to_params();
+      const sfi_selector_params prm = to_params(cfg);
       check(sfi_selector_window(&store.device().shape(), &store.device().cache(), l, d, rows, &prm, store.stream()));
       read_errors(store);
       state.per_layer[l].selected = read_selection(store, l);
@@ -569,4 +571,4 @@ DenseResult run_dense(const ToyModel& model, const std::vector<TokenId>& prompt,
   return result;
 }
 
-}  // namespace sfi_b200
+}  // namespace sfi

@@ -321,6 +321,38 @@ SFI_API int sfi_seq_selector_pick(const sfi_shape* shape, const sfi_cache* cache
                                   const int32_t* cand_pos_all, int32_t pos_base, int32_t pos_end,
                                   void* scratch, void* stream);
 
+/* ---- Multi-GPU over an NCCL communicator (SURVEY §8b "a multi-GPU variant
+ * taking an NCCL communicator", §8e) -----------------------------------------
+ * `nccl_comm` is an ncclComm_t (ncclCommInitRank, or the communicator of
+ * torch's ProcessGroupNCCL) of the n_shards ranks; every call enqueues its
+ * kernels and the ncclAllGather calls on `stream`, no host sync (graph
+ * capturable). NCCL is resolved at run time from the process (the library
+ * that created the communicator); SFI_ERR_UNSUPPORTED when none is loaded.
+ *   sfi_selector_sharded_nccl  C3 KV-head sharding: sfi_selector_fuse, the
+ *       z_base all-gather into z_all [n_shards][B][H][max_positions] fp64,
+ *       sfi_selector_finish (cross-head over all heads, top-k of own heads) —
+ *       indices bit-identical to the unsharded Selector (cross-head coupling,
+ *       selector.cpp:204-230).
+ *   sfi_merge_partials_nccl    C4 sequence sharding: all-gather of this rank's
+ *       (O, LSE) partials (o_part [rows][head_dim], lse_part [rows]) into
+ *       o_all / lse_all, then sfi_merge_partials in rank order.
+ *   sfi_seq_selector_nccl      C4: the sharded Selector's three exchanges (row
+ *       statistics, soft-NMS edges, top-k candidates) and the global pick;
+ *       scratch of sfi_seq_selector_nccl_scratch_bytes. */
+SFI_API int sfi_selector_sharded_nccl(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                      const float* pooled_logits, const sfi_selector_params* params,
+                                      void* nccl_comm, int32_t n_shards, int32_t shard, double* z_all, void* stream);
+SFI_API int sfi_merge_partials_nccl(int32_t n_parts, int32_t rows, int32_t head_dim, const float* o_part,
+                                    const float* lse_part, float* o_all, float* lse_all, float* out,
+                                    void* nccl_comm, void* stream);
+SFI_API size_t sfi_seq_selector_nccl_scratch_bytes(const sfi_shape* shape, const sfi_selector_params* params,
+                                                   int32_t n_shards);
+SFI_API int sfi_seq_selector_nccl(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
+                                  const float* pooled_logits, const sfi_selector_params* params,
+                                  const int32_t* j_off, const int32_t* n_glob, int32_t pos_base, int32_t pos_end,
+                                  void* nccl_comm, int32_t n_shards, void* scratch, size_t scratch_bytes,
+                                  void* stream);
+
 /* run_selector on explicit device arrays (the reference-facing form,
  * selector.cpp:254-299): H heads, a W x n window per head over an arbitrary
  * ascending allowed list. logits fp64 [H][W][n], norms fp64 [H][n] (CacheStats
@@ -338,6 +370,31 @@ SFI_API int sfi_selector_explicit(int32_t H, int32_t W, int32_t n, int32_t k_bud
  * rows fp64 [rows][n] over allowed int32 [n]; sel int32 [rows][k], n_sel [rows]. */
 SFI_API int sfi_select_top_k(int32_t rows, int32_t n, int32_t k, const double* scores,
                              const int32_t* allowed, int32_t* sel, int32_t* n_sel, void* stream);
+
+/* Selector stages, one at a time (the reference's stage API: evidence_from_window
+ * selector.cpp:96-127, prior_from_stats :129-160, fuse :162-185, z = log(s+eps)
+ * :270-276, refine_soft_nms :187-202, refine_cross_head :204-230, normalize
+ * distribution.cpp:41-60). Device arrays, fp64, one row per head:
+ *   EVIDENCE    a = logit window [H][W*n]            -> out = f [H][n]
+ *   PRIOR       a = key norms [H][n], b = u(j) [n]    -> out = r [H][n]
+ *   NORMALIZE   a = weights [H][n]                   -> out [H][n]
+ *   FUSE        a = f [H][n], b = r [H][n]           -> out = s [H][n], out2 = lambda* [H]
+ *   Z_BASE      a = s [H][n]                         -> out = log(s + eps)
+ *   SOFT_NMS    a = z [H][n] (rank-order rows)       -> out [H][n]
+ *   CROSS_HEAD  a = z [H][n]                         -> out [H][n]
+ * head_err [H] int32 (EVIDENCE / PRIOR / NORMALIZE): 0, or the sfi_status of
+ * the head's first failure in the reference's check order; the caller zeroes
+ * it and reads it after the stream. Stream-ordered, no host sync. */
+#define SFI_STAGE_EVIDENCE 0
+#define SFI_STAGE_PRIOR 1
+#define SFI_STAGE_NORMALIZE 2
+#define SFI_STAGE_FUSE 3
+#define SFI_STAGE_Z_BASE 4
+#define SFI_STAGE_SOFT_NMS 5
+#define SFI_STAGE_CROSS_HEAD 6
+SFI_API int sfi_selector_stage(int32_t stage, int32_t H, int32_t W, int32_t n, const double* a, const double* b,
+                               const sfi_selector_params* params, double* out, double* out2, int32_t* head_err,
+                               void* stream);
 
 /* Debug: after sfi_selector, copies the fp64 stage arrays z_base and z_adj
  * (selector.cpp:270-297) of request b into host buffers [n_kv_heads][n_J]. */

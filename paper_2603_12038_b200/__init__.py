@@ -5,16 +5,23 @@ re-implemented on sm_100a: every hot-path call below launches the CUDA kernels
 in ``libsfi_b200.so`` through the C ABI (include/sfi_b200.h). There is no CPU
 fallback: importing this package fails loudly when the extension is missing.
 
-Reference-named operators (hot path):
-    run_selector, select_top_k, make_cache_stats, KvStore,
-    attention_kernel_dense, attention_kernel_sparse, dense_capture
-Host-side scheduler bookkeeping (integer logic, scheduler.cpp):
-    init_decode_state, compute_allowed, next_step_type,
-    fast_step_update, slow_step_update, flop_model
-Request loop around the device path (scheduler.cpp:213-365), with the
-reference's toy decoder as the activation source:
-    ToyModel, run_request, run_dense, argmax_token
-Batched device API (production / bench): SfiCache (torch-allocated buffers).
+Reference names (``sfi._sfi``):
+    Selector: run_selector, evidence_from_window, prior_from_stats, fuse,
+        refine_soft_nms, refine_cross_head, select_top_k, make_cache_stats,
+        normalize, validate_distribution, ScoreDistribution, FusedScore
+        (every stage on the device)
+    KV / attention: KvStore, attention_kernel_dense, attention_kernel_sparse
+    Config: SelectorConfig, TriggerConfig, CacheLimits, Config, default_config,
+        load_config_file, save_config_file
+    Scheduler bookkeeping (host integer logic, scheduler.cpp): init_decode_state,
+        compute_allowed, next_step_type, fast_step_update, slow_step_update,
+        flop_model, StepRecord
+B200 additions: dense_capture (the slow-step capture as an operator),
+SfiCache (batched device API over torch-allocated buffers, the production /
+bench path), SlowStepPipeline, sharded.HeadShardedSfi / SeqShardedSfi.
+The reference's toy decoder and request loop (ToyModel, run_request,
+run_dense) are end-to-end TEST HARNESS code, in the separate ``harness``
+package (harness/libsfi_toy.so), not in this library.
 """
 from __future__ import annotations
 
@@ -37,40 +44,49 @@ from ._sfi_b200 import (  # noqa: F401,E402
     Config,
     DecodeState,
     DenseCapture,
+    FusedScore,
     KernelStats,
     KvStore,
     LogitWindow,
     ModelSpec,
     PoolMode,
-    RequestResult,
-    RunOptions,
+    RefinedScores,
+    ScoreDistribution,
     SelectorConfig,
     SelectorParams,
-    SelectorStages,
+    SelectorTrace,
     SfiError,
     SparseState,
     StepCause,
     StepRecord,
     SupportSet,
-    ToyModel,
     TriggerConfig,
-    argmax_token,
     attention_kernel_dense,
     attention_kernel_sparse,
     compute_allowed,
     default_config,
     dense_capture,
+    dot,
+    evidence_from_window,
     fast_step_update,
     flop_model,
+    fuse,
     init_decode_state,
+    load_config_file,
     make_cache_stats,
     next_step_type,
-    run_dense,
-    run_request,
+    normalize,
+    prior_from_stats,
+    refine_cross_head,
+    refine_soft_nms,
     run_selector,
-    run_selector_stages,
+    same_support,
+    save_config_file,
     select_top_k,
     slow_step_update,
+    squared_norm,
+    step_record_to_json,
+    validate_distribution,
 )
 
 LIBRARY_PATH = _os.path.join(_HERE, "libsfi_b200.so")
@@ -85,13 +101,13 @@ def __getattr__(name):
 
 
 __all__ = [
-    "CacheLimits", "CacheStats", "CompactSegment", "Config", "DecodeState", "DenseCapture",
-    "KernelStats", "KvStore", "LogitWindow", "ModelSpec", "PoolMode", "SelectorConfig",
-    "SelectorParams", "SelectorStages", "SfiError", "SparseState", "SupportSet", "TriggerConfig",
-    "attention_kernel_dense", "attention_kernel_sparse", "compute_allowed", "default_config",
-    "dense_capture", "fast_step_update", "flop_model", "init_decode_state", "make_cache_stats",
-    "next_step_type", "run_selector", "run_selector_stages", "select_top_k", "slow_step_update",
-    "SfiCache", "SlowStepPipeline", "LIBRARY_PATH",
-    "ToyModel", "StepCause", "StepRecord", "RunOptions", "RequestResult", "run_request", "run_dense",
-    "argmax_token",
+    "CacheLimits", "CacheStats", "CompactSegment", "Config", "DecodeState", "DenseCapture", "FusedScore",
+    "KernelStats", "KvStore", "LogitWindow", "ModelSpec", "PoolMode", "RefinedScores", "ScoreDistribution",
+    "SelectorConfig", "SelectorParams", "SelectorTrace", "SfiError", "SparseState", "StepCause", "StepRecord",
+    "SupportSet", "TriggerConfig", "attention_kernel_dense", "attention_kernel_sparse", "compute_allowed",
+    "default_config", "dense_capture", "dot", "evidence_from_window", "fast_step_update", "flop_model", "fuse",
+    "init_decode_state", "load_config_file", "make_cache_stats", "next_step_type", "normalize",
+    "prior_from_stats", "refine_cross_head", "refine_soft_nms", "run_selector", "same_support",
+    "save_config_file", "select_top_k", "slow_step_update", "squared_norm", "step_record_to_json",
+    "validate_distribution", "SfiCache", "SlowStepPipeline", "LIBRARY_PATH",
 ]

@@ -1,8 +1,12 @@
 """In-tree build of the sm_100a extension.
 
   libsfi_b200.so       C ABI (include/sfi_b200.h) + C++ host API
-                       (include/sfi_b200.hpp) + all CUDA kernels, cudart static
+                       (include/sfi/*.hpp, namespace sfi) + all CUDA kernels,
+                       cudart static
   _sfi_b200*.so        pybind11 module over the C++ host API (rpath $ORIGIN)
+  harness/libsfi_toy.so, harness/_sfi_toy*.so
+                       END-TO-END TEST HARNESS (not product): the toy decoder
+                       + request loop (harness/engine.cpp) over libsfi_b200.so
 
 Every CUDA translation unit is compiled with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo``; selector.cu also gets
@@ -28,9 +32,14 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                  "-I" + INC, "-I" + CSRC]
+HARNESS = os.path.join(ROOT, "harness")
+TOY_LIB = os.path.join(HARNESS, "libsfi_toy.so")
+TOY_EXT = os.path.join(HARNESS, "_sfi_toy" + sysconfig.get_config_var("EXT_SUFFIX"))
 CU = ["decode.cu", "fast_decode.cu", "capture.cu", "cache_ops.cu", "selector.cu", "capi.cu"]
-CPP = ["host.cpp", "engine.cpp"]
+CPP = ["host.cpp"]
 HEADERS = [os.path.join(INC, h) for h in ("sfi_b200.h", "sfi_b200.hpp")] + [
+    os.path.join(INC, "sfi", h) for h in ("attention.hpp", "config.hpp", "distribution.hpp", "error.hpp",
+                                          "scheduler.hpp", "selector.hpp")] + [
     os.path.join(CSRC, h) for h in ("common.cuh", "kernels.h")]
 
 
@@ -53,9 +62,11 @@ def _compile(src: str) -> str:
     obj = os.path.join(OBJ, src + ".o")
     if _newer(obj, [path] + HEADERS):
         extra = ["-fmad=false"] if src == "selector.cu" else []
-        if src == "engine.cpp":  # the toy model's fp64 host math: no contraction, as in the reference build
-            extra = ["-Xcompiler", "-ffp-contract=off"]
-        _run([NVCC] + COMMON + extra + ["-c", path, "-o", obj])
+        cmd = [NVCC] + COMMON + extra + ["-c", path, "-o", obj]
+        if src.endswith(".cpp"):  # the host API is C++20 (std::span, as the reference's headers)
+            cmd = [NVCC] + ARCH + ["-O3", "-std=c++20", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+                                   "-I" + INC, "-I" + CSRC, "-c", path, "-o", obj]
+        _run(cmd)
     return obj
 
 
@@ -66,14 +77,26 @@ def build(verbose: bool = False) -> str:
     if _newer(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs +
              ["-Xlinker", "--exclude-libs,ALL"])
+    import pybind11
+    py_inc = ["-I" + pybind11.get_include(), "-I" + sysconfig.get_paths()["include"], "-I" + INC]
     bsrc = os.path.join(CSRC, "bindings.cpp")
     if _newer(EXT, [bsrc, LIB] + HEADERS):
-        import pybind11
-        _run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-fvisibility=hidden",
-              "-I" + pybind11.get_include(), "-I" + sysconfig.get_paths()["include"], "-I" + INC,
-              bsrc, "-o", EXT, "-L" + PKG, "-lsfi_b200", "-Wl,-rpath,$ORIGIN"])
+        _run(["g++", "-O2", "-std=c++20", "-shared", "-fPIC", "-fvisibility=hidden"] + py_inc +
+             [bsrc, "-o", EXT, "-L" + PKG, "-lsfi_b200", "-Wl,-rpath,$ORIGIN"])
+    # test harness: the toy decoder + request loop over the product library
+    esrc, tsrc, thdr = (os.path.join(HARNESS, f) for f in ("engine.cpp", "toy_bindings.cpp", "sfi_toy.hpp"))
+    cuda_inc = "-I" + os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")
+    if _newer(TOY_LIB, [esrc, thdr, LIB] + HEADERS):
+        # the toy model's fp64 host math: no contraction, as in the reference build
+        _run(["g++", "-O2", "-std=c++20", "-shared", "-fPIC", "-ffp-contract=off", "-I" + INC, "-I" + HARNESS,
+              cuda_inc, esrc, "-o", TOY_LIB, "-L" + PKG, "-lsfi_b200", "-Wl,-rpath,$ORIGIN/../paper_2603_12038_b200",
+              "-L" + os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64"), "-lcudart"])
+    if _newer(TOY_EXT, [tsrc, thdr, TOY_LIB] + HEADERS):
+        _run(["g++", "-O2", "-std=c++20", "-shared", "-fPIC", "-fvisibility=hidden"] + py_inc +
+             ["-I" + HARNESS, tsrc, "-o", TOY_EXT, "-L" + HARNESS, "-lsfi_toy", "-L" + PKG, "-lsfi_b200",
+              "-Wl,-rpath,$ORIGIN", "-Wl,-rpath,$ORIGIN/../paper_2603_12038_b200"])
     if verbose:
-        print("built", LIB, EXT)
+        print("built", LIB, EXT, TOY_LIB, TOY_EXT)
     return EXT
 
 

@@ -1,7 +1,9 @@
 // bindings.cpp — pybind11 module `_sfi_b200`: the reference's `_sfi` names
 // (proj/bindings/module.cpp:29-247, python/sfi/__init__.py) for the hot-path
-// operators, backed by the B200 host API, plus the batched device API (the
-// C ABI one-to-one, taking raw device pointers and a cudaStream_t handle).
+// operators, backed by the B200 host API (namespace sfi), plus the batched
+// device API (the C ABI one-to-one, taking raw device pointers and a
+// cudaStream_t handle). The toy decoder / request loop bindings live in the
+// test harness module (harness/toy_bindings.cpp -> _sfi_toy).
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
@@ -11,7 +13,7 @@
 #include "sfi_b200.hpp"
 
 namespace py = pybind11;
-using namespace sfi_b200;
+using namespace sfi;
 
 namespace {
 
@@ -88,6 +90,28 @@ PYBIND11_MODULE(_sfi_b200, m) {
       .def_readwrite("limits", &Config::limits)
       .def("validate", &Config::validate);
   m.def("default_config", &default_config);
+  m.def("load_config_file", &load_config_file, py::arg("path"));
+  m.def("save_config_file", &save_config_file, py::arg("config"), py::arg("path"));
+
+  // distribution.hpp:31-58
+  py::class_<ScoreDistribution>(m, "ScoreDistribution")
+      .def(py::init<>())
+      .def(py::init([](std::vector<Pos> support, std::vector<double> mass) {
+             ScoreDistribution d;
+             d.support = std::move(support);
+             d.mass = std::move(mass);
+             return d;
+           }),
+           py::arg("support"), py::arg("mass"))
+      .def_readwrite("support", &ScoreDistribution::support)
+      .def_readwrite("mass", &ScoreDistribution::mass);
+  m.def("validate_distribution", &validate_distribution);
+  m.def("normalize", [](const std::vector<Pos>& support, const std::vector<double>& weights) {
+    return normalize(support, weights);
+  });
+  m.def("dot", &dot);
+  m.def("squared_norm", &squared_norm);
+  m.def("same_support", &same_support);
 
   py::class_<LogitWindow>(m, "LogitWindow")
       .def(py::init<>())
@@ -104,26 +128,42 @@ PYBIND11_MODULE(_sfi_b200, m) {
   m.def("make_cache_stats", &make_cache_stats, py::arg("key_norms"), py::arg("allowed"),
         py::arg("epsilon") = 1e-8);
 
-  py::class_<SelectorStages>(m, "SelectorStages")
+  // selector.hpp:57-130: every stage on the device
+  py::class_<FusedScore>(m, "FusedScore")
+      .def_readonly("evidence", &FusedScore::evidence)
+      .def_readonly("prior", &FusedScore::prior)
+      .def_readonly("lambda_star", &FusedScore::lambda_star)
+      .def_readonly("fused", &FusedScore::fused);
+  py::class_<RefinedScores>(m, "RefinedScores")
+      .def_readonly("base", &RefinedScores::base)
+      .def_readonly("after_nms", &RefinedScores::after_nms)
+      .def_readonly("after_cross", &RefinedScores::after_cross);
+  py::class_<SelectorTrace>(m, "SelectorTrace")
       .def(py::init<>())
-      .def_readonly("base", &SelectorStages::base)
-      .def_readonly("after_cross", &SelectorStages::after_cross);
-
+      .def_readwrite("capture_stages", &SelectorTrace::capture_stages)
+      .def_readwrite("capture_debug", &SelectorTrace::capture_debug)
+      .def_readonly("elementary_ops", &SelectorTrace::elementary_ops)
+      .def_readonly("stages", &SelectorTrace::stages)
+      .def_readonly("fusion", &SelectorTrace::fusion)
+      .def_readonly("debug_lines", &SelectorTrace::debug_lines);
+  m.def("evidence_from_window",
+        [](const LogitWindow& w, const SelectorConfig& cfg) { return evidence_from_window(w, cfg); });
+  m.def("prior_from_stats", [](const CacheStats& stats, const std::vector<Pos>& allowed,
+                               const SelectorConfig& cfg) { return prior_from_stats(stats, allowed, cfg); });
+  m.def("fuse", [](const ScoreDistribution& f, const ScoreDistribution& r, const SelectorConfig& cfg) {
+    return fuse(f, r, cfg);
+  });
+  m.def("refine_soft_nms", [](const std::vector<double>& z, const SelectorConfig& cfg) { return refine_soft_nms(z, cfg); });
+  m.def("refine_cross_head", [](const std::vector<std::vector<double>>& z, const SelectorConfig& cfg) {
+    return refine_cross_head(z, cfg);
+  });
   m.def("select_top_k", &select_top_k, py::arg("scores"), py::arg("allowed"), py::arg("k"));
   m.def(
       "run_selector",
-      [](const LogitWindow& w, const CacheStats& stats, const SelectorConfig& cfg) {
-        return run_selector(w, stats, cfg);
+      [](const LogitWindow& w, const CacheStats& stats, const SelectorConfig& cfg, SelectorTrace* trace) {
+        return run_selector(w, stats, cfg, trace);
       },
-      py::arg("window"), py::arg("stats"), py::arg("config"));
-  m.def(
-      "run_selector_stages",
-      [](const LogitWindow& w, const CacheStats& stats, const SelectorConfig& cfg) {
-        SelectorStages st;
-        auto sel = run_selector(w, stats, cfg, &st);
-        return py::make_tuple(sel, st);
-      },
-      py::arg("window"), py::arg("stats"), py::arg("config"));
+      py::arg("window"), py::arg("stats"), py::arg("config"), py::arg("trace") = nullptr);
 
   py::class_<ModelSpec>(m, "ModelSpec")
       .def(py::init<>())
@@ -176,11 +216,19 @@ PYBIND11_MODULE(_sfi_b200, m) {
            "host fp32 pointers [n_layers][count][H*d]")
       .def("key_row", &KvStore::key_row)
       .def("value_row", &KvStore::value_row)
+      .def("key_at", &KvStore::key_row, "H*d values (copy of the view key_at returns)")
+      .def("value_at", &KvStore::value_row)
+      .def("set_access_trace", &KvStore::set_access_trace)
+      .def("access_trace", [](KvStore& s) {
+        py::list out;
+        for (const auto& a : s.access_trace()) out.append(py::make_tuple(a.layer, a.head, a.slot));
+        return out;
+      })
       .def("key_norm", &KvStore::key_norm)
       .def("reorganize", &KvStore::reorganize)
       .def("compact_valid", &KvStore::compact_valid)
       .def("compact_matches", &KvStore::compact_matches)
-      .def("compact", &KvStore::compact)
+      .def("compact", &KvStore::compact, py::return_value_policy::copy)
       .def("recent_tail", &KvStore::recent_tail);
 
   m.def("attention_kernel_dense",
@@ -224,58 +272,20 @@ PYBIND11_MODULE(_sfi_b200, m) {
         py::arg("limits"));
   m.def("flop_model", &flop_model, py::arg("prefix_len"), py::arg("support"), py::arg("slow_fraction"));
 
-  // ---- request loop around the device path (engine.cpp; scheduler.hpp:79-135) ----
-  py::class_<ToyModel>(m, "ToyModel")
-      .def_static("random", &ToyModel::random, py::arg("spec"), py::arg("seed"))
-      .def("spec", &ToyModel::spec)
-      .def("weight_checksum", [](const ToyModel& t) {
-        // order-fixed sum over every weight (identity check against the reference's ToyModel::random)
-        double acc = 0.0;
-        auto add = [&](const std::vector<double>& v) { for (double x : v) acc += x; };
-        add(t.embedding().v);
-        for (int l = 0; l < t.spec().n_layers; ++l) {
-          const auto& lw = t.layer(l);
-          for (const auto* w : {&lw.wq, &lw.wk, &lw.wv, &lw.wo, &lw.w_gate, &lw.w_up, &lw.w_down}) add(w->v);
-        }
-        add(t.lm_head().v);
-        return acc;
-      });
   py::enum_<StepCause>(m, "StepCause")
       .value("initial", StepCause::kInitial)
       .value("trigger", StepCause::kTrigger)
       .value("forced", StepCause::kForced)
       .value("none", StepCause::kNone);
   py::class_<StepRecord>(m, "StepRecord")
-      .def_readonly("t", &StepRecord::t)
-      .def_readonly("slow", &StepRecord::slow)
-      .def_readonly("cause", &StepRecord::cause)
-      .def_readonly("support_size", &StepRecord::support_size)
-      .def_readonly("allowed_size", &StepRecord::allowed_size)
-      .def_readonly("prefix_len", &StepRecord::prefix_len);
-  py::class_<RunOptions>(m, "RunOptions")
       .def(py::init<>())
-      .def_readwrite("collect_logits", &RunOptions::collect_logits)
-      .def_readwrite("capture_selected", &RunOptions::capture_selected);
-  py::class_<RequestResult>(m, "RequestResult")
-      .def_readonly("tokens", &RequestResult::tokens)
-      .def_readonly("log", &RequestResult::log)
-      .def_readonly("step_logits", &RequestResult::step_logits)
-      .def_readonly("total_flops", &RequestResult::total_flops)
-      .def_readonly("total_kv_reads", &RequestResult::total_kv_reads)
-      .def_readonly("dense_equiv_reads", &RequestResult::dense_equiv_reads)
-      .def_readonly("fast_retention", &RequestResult::fast_retention)
-      .def_readonly("selected_per_step", &RequestResult::selected_per_step);
-  py::class_<DenseResult>(m, "DenseResult")
-      .def_readonly("tokens", &DenseResult::tokens)
-      .def_readonly("step_logits", &DenseResult::step_logits)
-      .def_readonly("total_kv_reads", &DenseResult::total_kv_reads)
-      .def_readonly("total_flops", &DenseResult::total_flops);
-  m.def("argmax_token", &argmax_token, py::arg("logits"));
-  m.def("run_request", &run_request, py::arg("model"), py::arg("prompt"), py::arg("limits"), py::arg("trigger"),
-        py::arg("selector"), py::arg("max_new"), py::arg("opts") = RunOptions{},
-        py::call_guard<py::gil_scoped_release>());
-  m.def("run_dense", &run_dense, py::arg("model"), py::arg("prompt"), py::arg("max_new"),
-        py::call_guard<py::gil_scoped_release>());
+      .def_readwrite("t", &StepRecord::t)
+      .def_readwrite("slow", &StepRecord::slow)
+      .def_readwrite("cause", &StepRecord::cause)
+      .def_readwrite("support_size", &StepRecord::support_size)
+      .def_readwrite("allowed_size", &StepRecord::allowed_size)
+      .def_readwrite("prefix_len", &StepRecord::prefix_len);
+  m.def("step_record_to_json", &step_record_to_json);
 
   // ---- batched device API: the C ABI one-to-one --------------------------
   py::class_<sfi_shape>(m, "Shape")
@@ -312,7 +322,7 @@ PYBIND11_MODULE(_sfi_b200, m) {
 #undef PTR_FIELD
 
   py::class_<sfi_selector_params>(m, "SelectorParams")
-      .def(py::init([](const SelectorConfig& c) { return c.to_params(); }), py::arg("config") = SelectorConfig{});
+      .def(py::init([](const SelectorConfig& c) { return to_params(c); }), py::arg("config") = SelectorConfig{});
 
   m.def("version", &sfi_version);
   m.def("last_launch_count", &sfi_last_launch_count);
@@ -457,6 +467,32 @@ PYBIND11_MODULE(_sfi_b200, m) {
                               std::uintptr_t z_all, int n_shards, int shard, std::uintptr_t stream) {
     check(sfi_selector_finish(&s, &c, layer, &prm, static_cast<const double*>(vp(z_all)), n_shards, shard,
                               vp(stream)));
+  });
+  // multi-GPU entry points over an NCCL communicator (ncclComm_t as an integer)
+  m.def("selector_sharded_nccl", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
+                                    const sfi_selector_params& prm, std::uintptr_t comm, int n_shards, int shard,
+                                    std::uintptr_t z_all, std::uintptr_t stream) {
+    check(sfi_selector_sharded_nccl(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm, vp(comm), n_shards,
+                                    shard, static_cast<double*>(vp(z_all)), vp(stream)));
+  });
+  m.def("merge_partials_nccl", [](int n_parts, int rows, int d, std::uintptr_t o, std::uintptr_t lse,
+                                  std::uintptr_t o_all, std::uintptr_t lse_all, std::uintptr_t out,
+                                  std::uintptr_t comm, std::uintptr_t stream) {
+    check(sfi_merge_partials_nccl(n_parts, rows, d, static_cast<const float*>(vp(o)),
+                                  static_cast<const float*>(vp(lse)), static_cast<float*>(vp(o_all)),
+                                  static_cast<float*>(vp(lse_all)), static_cast<float*>(vp(out)), vp(comm),
+                                  vp(stream)));
+  });
+  m.def("seq_selector_nccl_scratch_bytes", [](const sfi_shape& s, const sfi_selector_params& prm, int n_shards) {
+    return sfi_seq_selector_nccl_scratch_bytes(&s, &prm, n_shards);
+  });
+  m.def("seq_selector_nccl", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
+                                const sfi_selector_params& prm, std::uintptr_t j_off, std::uintptr_t n_glob,
+                                int pos_base, int pos_end, std::uintptr_t comm, int n_shards, std::uintptr_t scratch,
+                                size_t scratch_bytes, std::uintptr_t stream) {
+    check(sfi_seq_selector_nccl(&s, &c, layer, static_cast<const float*>(vp(logits)), &prm,
+                                static_cast<const int32_t*>(vp(j_off)), static_cast<const int32_t*>(vp(n_glob)),
+                                pos_base, pos_end, vp(comm), n_shards, vp(scratch), scratch_bytes, vp(stream)));
   });
   m.def("selector", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t logits,
                        const sfi_selector_params& prm, std::uintptr_t stream) {

@@ -3,6 +3,7 @@
 // status codes and a thread-local error message. No exceptions cross it.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -799,6 +800,25 @@ SFI_API int sfi_select_top_k(int32_t rows, int32_t n, int32_t k, const double* s
   return SFI_OK;
 }
 
+SFI_API int sfi_selector_stage(int32_t stage, int32_t H, int32_t W, int32_t n, const double* a, const double* b,
+                               const sfi_selector_params* prm, double* out, double* out2, int32_t* head_err,
+                               void* stream) {
+  g_launches = 0;
+  if (stage < SFI_STAGE_EVIDENCE || stage > SFI_STAGE_CROSS_HEAD)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "selector_stage: unknown stage");
+  if (H < 0 || n < 0 || (stage == SFI_STAGE_EVIDENCE && W < 1))
+    return fail(SFI_ERR_INVALID_ARGUMENT, "selector_stage: bad shape");
+  if (H == 0 || n == 0) return SFI_OK;
+  const bool needs_b = stage == SFI_STAGE_PRIOR || stage == SFI_STAGE_FUSE;
+  const bool needs_err = stage <= SFI_STAGE_NORMALIZE;
+  if (!a || !out || !prm || (needs_b && !b) || (needs_err && !head_err))
+    return fail(SFI_ERR_INVALID_ARGUMENT, "selector_stage: null argument");
+  SFI_CUDA(sfi_impl::launch_selector_stage(stage, H, W, n, a, b, *prm, out, out2, head_err, (cudaStream_t)stream),
+           "sfi_selector_stage");
+  g_launches = 1;
+  return SFI_OK;
+}
+
 SFI_API int sfi_selector_stages(const sfi_shape* s, const sfi_cache* c, int32_t b, double* z_base,
                                 double* z_adj, int32_t n_j, void* stream) {
   int rc = validate(s);
@@ -888,3 +908,154 @@ SFI_API int sfi_fill_synthetic(const sfi_shape* s, const sfi_cache* c, uint64_t 
 }
 
 }  // extern "C"
+
+// ---- multi-GPU entry points over an NCCL communicator ----
+// The exchange of each sharded step, done in-call on `stream`: the caller
+// passes an ncclComm_t (from ncclCommInitRank, or torch's ProcessGroupNCCL
+// communicator). NCCL is resolved at run time from the process — the library
+// that created the communicator (RTLD_DEFAULT), else libnccl.so.2 — so
+// libsfi_b200.so carries no link-time NCCL dependency and never mixes two NCCL
+// builds in one process.
+namespace {
+
+using NcclAllGather = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
+using NcclErrStr = const char* (*)(int);
+constexpr int kNcclInt32 = 2, kNcclFloat32 = 7, kNcclFloat64 = 8;  // ncclDataType_t (nccl.h)
+
+struct NcclApi {
+  NcclAllGather all_gather = nullptr;
+  NcclErrStr err_str = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* f = dlsym(RTLD_DEFAULT, "ncclAllGather");
+    void* e = dlsym(RTLD_DEFAULT, "ncclGetErrorString");
+    if (!f) {
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (h) {
+        f = dlsym(h, "ncclAllGather");
+        e = dlsym(h, "ncclGetErrorString");
+      }
+    }
+    a.all_gather = reinterpret_cast<NcclAllGather>(f);
+    a.err_str = reinterpret_cast<NcclErrStr>(e);
+    return a;
+  }();
+  return api;
+}
+
+int nccl_gather(const void* send, void* recv, size_t count, int dtype, void* comm, void* stream, const char* what) {
+  const NcclApi& api = nccl_api();
+  if (!api.all_gather) return fail(SFI_ERR_UNSUPPORTED, std::string(what) + ": NCCL is not available in this process");
+  const int r = api.all_gather(send, recv, count, dtype, comm, (cudaStream_t)stream);
+  if (r != 0)
+    return fail(SFI_ERR_CUDA, std::string(what) + ": ncclAllGather failed: " + (api.err_str ? api.err_str(r) : "?"));
+  return SFI_OK;
+}
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+SFI_API int sfi_selector_sharded_nccl(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* logits,
+                                      const sfi_selector_params* prm, void* comm, int32_t n_shards, int32_t shard,
+                                      double* z_all, void* stream) {
+  if (!comm || !z_all) return fail(SFI_ERR_INVALID_ARGUMENT, "selector_sharded_nccl: null communicator or z_all");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "selector_sharded_nccl: bad shard index");
+  const double* z = nullptr;
+  size_t bytes = 0;
+  int rc = sfi_selector_fuse(s, c, layer, logits, prm, &z, &bytes, stream);
+  if (rc) return rc;
+  const int nl = g_launches;
+  if ((rc = nccl_gather(z, z_all, bytes / sizeof(double), kNcclFloat64, comm, stream, "selector_sharded_nccl")))
+    return rc;
+  rc = sfi_selector_finish(s, c, layer, prm, z_all, n_shards, shard, stream);
+  g_launches += nl;
+  return rc;
+}
+
+SFI_API int sfi_merge_partials_nccl(int32_t n_parts, int32_t rows, int32_t head_dim, const float* o_part,
+                                    const float* lse_part, float* o_all, float* lse_all, float* out, void* comm,
+                                    void* stream) {
+  if (!comm || !o_part || !lse_part || !o_all || !lse_all || !out)
+    return fail(SFI_ERR_INVALID_ARGUMENT, "merge_partials_nccl: null argument");
+  int rc = nccl_gather(o_part, o_all, (size_t)rows * head_dim, kNcclFloat32, comm, stream, "merge_partials_nccl");
+  if (rc || (rc = nccl_gather(lse_part, lse_all, (size_t)rows, kNcclFloat32, comm, stream, "merge_partials_nccl")))
+    return rc;
+  return sfi_merge_partials(n_parts, rows, head_dim, o_all, lse_all, out, stream);
+}
+
+namespace {
+struct SeqNcclScratch {
+  double *row_stats, *stats_all, *edges, *edges_all, *cand_score, *cand_score_all;
+  int32_t *cand_pos, *cand_pos_all;
+  void* pick;
+  size_t bytes;
+};
+SeqNcclScratch seq_nccl_layout(const sfi_shape* s, const sfi_selector_params* prm, int32_t P, void* base) {
+  const size_t rows = (size_t)s->batch * s->n_kv_heads, K = (size_t)std::max(s->k_budget, 1);
+  const size_t ne = (size_t)sfi_seq_edges_doubles(s, prm);
+  uint8_t* p = static_cast<uint8_t*>(base);
+  SeqNcclScratch x{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    void* q = p ? p + off : nullptr;
+    off += al256(bytes);
+    return q;
+  };
+  x.row_stats = static_cast<double*>(take(rows * 6 * 8));
+  x.stats_all = static_cast<double*>(take(P * rows * 6 * 8));
+  x.edges = static_cast<double*>(take(ne * 8));
+  x.edges_all = static_cast<double*>(take(P * ne * 8));
+  x.cand_score = static_cast<double*>(take(rows * K * 8));
+  x.cand_score_all = static_cast<double*>(take(P * rows * K * 8));
+  x.cand_pos = static_cast<int32_t*>(take(rows * K * 4));
+  x.cand_pos_all = static_cast<int32_t*>(take(P * rows * K * 4));
+  x.pick = take(sfi_seq_pick_scratch_bytes(s, P));
+  x.bytes = off;
+  return x;
+}
+}  // namespace
+
+SFI_API size_t sfi_seq_selector_nccl_scratch_bytes(const sfi_shape* s, const sfi_selector_params* prm,
+                                                   int32_t n_shards) {
+  if (!s || !prm || n_shards < 1) return 0;
+  return seq_nccl_layout(s, prm, n_shards, nullptr).bytes;
+}
+
+SFI_API int sfi_seq_selector_nccl(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* logits,
+                                  const sfi_selector_params* prm, const int32_t* j_off, const int32_t* n_glob,
+                                  int32_t pos_base, int32_t pos_end, void* comm, int32_t n_shards, void* scratch,
+                                  size_t scratch_bytes, void* stream) {
+  if (!comm || !scratch || !prm) return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_nccl: null argument");
+  const SeqNcclScratch x = seq_nccl_layout(s, prm, n_shards, scratch);
+  if (scratch_bytes < x.bytes) return fail(SFI_ERR_INVALID_ARGUMENT, "seq_selector_nccl: scratch too small");
+  const size_t rows = (size_t)s->batch * s->n_kv_heads, K = (size_t)std::max(s->k_budget, 1);
+  const size_t ne = (size_t)sfi_seq_edges_doubles(s, prm);
+  int launches = 0, rc;
+  // row statistics -> global max / sums; soft-NMS edges; top-k candidates -> global pick
+  if ((rc = sfi_seq_selector_stats(s, c, layer, logits, prm, j_off, n_glob, 1, x.row_stats, x.stats_all, n_shards,
+                                   x.edges, stream)))
+    return rc;
+  launches += g_launches;
+  if ((rc = nccl_gather(x.row_stats, x.stats_all, rows * 6, kNcclFloat64, comm, stream, "seq_selector_nccl"))) return rc;
+  if ((rc = sfi_seq_selector_stats(s, c, layer, logits, prm, j_off, n_glob, 3, x.row_stats, x.stats_all, n_shards,
+                                   x.edges, stream)))
+    return rc;
+  launches += g_launches;
+  if ((rc = nccl_gather(x.edges, x.edges_all, ne, kNcclFloat64, comm, stream, "seq_selector_nccl"))) return rc;
+  if ((rc = sfi_seq_selector_finish(s, c, layer, prm, j_off, n_glob, x.edges_all, n_shards, pos_base, x.cand_score,
+                                    x.cand_pos, stream)))
+    return rc;
+  launches += g_launches;
+  if ((rc = nccl_gather(x.cand_score, x.cand_score_all, rows * K, kNcclFloat64, comm, stream, "seq_selector_nccl")) ||
+      (rc = nccl_gather(x.cand_pos, x.cand_pos_all, rows * K, kNcclInt32, comm, stream, "seq_selector_nccl")))
+    return rc;
+  rc = sfi_seq_selector_pick(s, c, layer, n_shards, x.cand_score_all, x.cand_pos_all, pos_base, pos_end, x.pick,
+                             stream);
+  g_launches += launches;
+  return rc;
+}

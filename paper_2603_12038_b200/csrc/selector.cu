@@ -1817,3 +1817,239 @@ cudaError_t launch_topk_explicit(int rows, int n, int K, const double* scores, c
 }
 
 }  // namespace sfi_impl
+
+// ---------------------------------------------------------------------------
+// Reference-facing Selector stages (selector.hpp:84-122, distribution.cpp:
+// 41-60): one CTA per head row, deterministic block reductions, the
+// reference's formulas in its operation order (the stage API is the
+// reference's debugging / composition surface; the decode hot path uses the
+// fused kernels above). Per-head errors land in head_err[h] (0 = ok, else the
+// sfi_status code of the FIRST failure in the reference's check order).
+namespace sfi_impl {
+namespace {
+
+constexpr int kStageT = 256;
+
+template <typename Op>
+__device__ __forceinline__ double stage_reduce(double v, double* red, Op op) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();  // red may still be read by the previous call
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double acc = red[0];
+  for (int w = 1; w < kStageT / 32; ++w) acc = op(acc, red[w]);
+  return acc;
+}
+
+struct StageArgs {
+  int H, W, n;
+  const double* a;
+  const double* b;
+  double* out;
+  double* out2;
+  int32_t* head_err;
+  double alpha, gamma, beta, p_curve, eta, lambda_clip, alpha_soft, alpha_cross, temperature, eps;
+  int nms_radius;
+};
+
+// normalize(weights) of one row in place (distribution.cpp:41-60); false on error
+__device__ bool stage_normalize_row(const double* w, double* out, int n, double* red, int32_t* err) {
+  bool bad = false;
+  double s = 0.0;
+  for (int j = threadIdx.x; j < n; j += kStageT) {
+    const double x = w[j];
+    if (!isfinite(x) || x < 0.0) bad = true;
+    s += x;
+  }
+  const double anybad = stage_reduce(bad ? 1.0 : 0.0, red, OpMax{});
+  if (anybad > 0.0) {
+    if (threadIdx.x == 0) *err = SFI_ERR_NON_FINITE_INPUT;
+    return false;
+  }
+  const double sum = stage_reduce(s, red, OpSum{});
+  if (sum <= 0.0) {
+    if (threadIdx.x == 0) *err = SFI_ERR_EMPTY_SUPPORT;
+    return false;
+  }
+  for (int j = threadIdx.x; j < n; j += kStageT) out[j] = w[j] / sum;
+  return true;
+}
+
+// evidence_from_window (selector.cpp:54-74, 96-127): per window row softmax
+// (finite check, max from kMaskedLogit, masked -> 0, sum, divide), power mean
+// over the rows, inverse power map, normalize.
+__global__ void __launch_bounds__(kStageT) stage_evidence_kernel(const StageArgs p) {
+  __shared__ double red[kStageT / 32];
+  const int h = blockIdx.x, n = p.n;
+  double* mu = p.out + (size_t)h * n;
+  for (int row = 0; row < p.W; ++row) {
+    const double* v = p.a + ((size_t)h * p.W + row) * n;
+    bool bad = false;
+    double m = kMaskedLogit;
+    for (int j = threadIdx.x; j < n; j += kStageT) {
+      const double x = v[j];
+      if (!isfinite(x)) bad = true;
+      else m = smax(m, x);
+    }
+    if (stage_reduce(bad ? 1.0 : 0.0, red, OpMax{}) > 0.0) {
+      if (threadIdx.x == 0) p.head_err[h] = SFI_ERR_NON_FINITE_INPUT;
+      return;
+    }
+    const double M = stage_reduce(m, red, OpMax{});
+    double s = 0.0;
+    for (int j = threadIdx.x; j < n; j += kStageT) s += (v[j] <= kMaskedLogit) ? 0.0 : exp(v[j] - M);
+    const double sum = stage_reduce(s, red, OpSum{});
+    if (sum <= 0.0) {
+      if (threadIdx.x == 0) p.head_err[h] = SFI_ERR_EMPTY_SUPPORT;
+      return;
+    }
+    for (int j = threadIdx.x; j < n; j += kStageT) {
+      const double pj = ((v[j] <= kMaskedLogit) ? 0.0 : exp(v[j] - M)) / sum;
+      mu[j] = (row == 0 ? 0.0 : mu[j]) + pow_ref(pj, p.alpha);
+    }
+  }
+  const double inv_w = 1.0 / (double)p.W;
+  const double inv_a = 1.0 / p.alpha;
+  for (int j = threadIdx.x; j < n; j += kStageT) mu[j] = pow_ref(mu[j] * inv_w, inv_a);
+  __syncthreads();
+  stage_normalize_row(mu, mu, n, red, p.head_err + h);
+}
+
+// prior_from_stats (selector.cpp:129-160): a = key norms [H][n], b = u(j) [n]
+__global__ void __launch_bounds__(kStageT) stage_prior_kernel(const StageArgs p) {
+  __shared__ double red[kStageT / 32];
+  const int h = blockIdx.x, n = p.n;
+  const double* nm = p.a + (size_t)h * n;
+  double* w = p.out + (size_t)h * n;
+  bool bad = false;
+  for (int j = threadIdx.x; j < n; j += kStageT) {
+    const double x = nm[j];
+    if (!isfinite(x) || x < 0.0) {
+      bad = true;
+      continue;
+    }
+    const double u = p.b[j];
+    const double pi_kn = pow_ref(x + p.eps, -p.gamma);
+    const double pi_pos = exp(-p.beta * pow_ref(u, p.p_curve)) * pow_ref(1.0 - u + p.eps, p.eta);
+    w[j] = pi_kn * pi_pos;
+  }
+  if (stage_reduce(bad ? 1.0 : 0.0, red, OpMax{}) > 0.0) {
+    if (threadIdx.x == 0) p.head_err[h] = SFI_ERR_NON_FINITE_INPUT;
+    return;
+  }
+  stage_normalize_row(w, w, n, red, p.head_err + h);
+}
+
+__global__ void __launch_bounds__(kStageT) stage_normalize_kernel(const StageArgs p) {
+  __shared__ double red[kStageT / 32];
+  const int h = blockIdx.x;
+  stage_normalize_row(p.a + (size_t)h * p.n, p.out + (size_t)h * p.n, p.n, red, p.head_err + h);
+}
+
+// fuse (selector.cpp:162-185): |f|^2, f.r, |r|^2, lambda*, s; out2[h] = lambda*
+__global__ void __launch_bounds__(kStageT) stage_fuse_kernel(const StageArgs p) {
+  __shared__ double red[kStageT / 32];
+  const int h = blockIdx.x, n = p.n;
+  const double* f = p.a + (size_t)h * n;
+  const double* r = p.b + (size_t)h * n;
+  double sff = 0.0, sfr = 0.0, srr = 0.0;
+  for (int j = threadIdx.x; j < n; j += kStageT) {
+    sff += f[j] * f[j];
+    sfr += f[j] * r[j];
+    srr += r[j] * r[j];
+  }
+  const double ff = stage_reduce(sff, red, OpSum{});
+  const double fr = stage_reduce(sfr, red, OpSum{});
+  const double rr = stage_reduce(srr, red, OpSum{});
+  const double denom = ff - 2.0 * fr + rr;
+  double lambda = 0.0;
+  if (fabs(denom) >= p.eps) {
+    lambda = (ff - fr) / denom;
+    lambda = (lambda < 0.0) ? 0.0 : (p.lambda_clip < lambda) ? p.lambda_clip : lambda;
+  }
+  if (threadIdx.x == 0 && p.out2) p.out2[h] = lambda;
+  double* s = p.out + (size_t)h * n;
+  for (int j = threadIdx.x; j < n; j += kStageT) s[j] = (1.0 - lambda) * f[j] + lambda * r[j];
+}
+
+// z = log(s + eps) (selector.cpp:270-276), elementwise over [H][n]
+__global__ void stage_zbase_kernel(const StageArgs p) {
+  const size_t total = (size_t)p.H * p.n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
+    p.out[i] = log(p.a[i] + p.eps);
+}
+
+// refine_soft_nms (selector.cpp:187-202) per row, rank-order window
+__global__ void stage_soft_nms_kernel(const StageArgs p) {
+  const size_t total = (size_t)p.H * p.n;
+  const int n = p.n, R = p.nms_radius;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const double* z = p.a + (i / n) * n;
+    const int j = (int)(i % n);
+    const int lo = max(0, j - R), hi = min(n - 1, j + R);
+    double m = z[j];
+    for (int k = lo; k <= hi; ++k) m = smax(m, z[k]);
+    p.out[i] = z[j] - p.alpha_soft * (m - z[j]);
+  }
+}
+
+// refine_cross_head (selector.cpp:204-230) per position, heads in order
+__global__ void stage_cross_head_kernel(const StageArgs p) {
+  const int n = p.n, H = p.H;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double mx = p.a[j];
+    for (int h = 1; h < H; ++h) mx = smax(mx, p.a[(size_t)h * n + j]);
+    double sum = 0.0;
+    for (int h = 0; h < H; ++h) sum += exp((p.a[(size_t)h * n + j] - mx) / p.temperature);
+    for (int h = 0; h < H; ++h) {
+      const double z = p.a[(size_t)h * n + j];
+      const double r = exp((z - mx) / p.temperature) / sum;
+      p.out[(size_t)h * n + j] = z + p.alpha_cross * log(smax(r, p.eps));
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_selector_stage(int stage, int H, int W, int n, const double* a, const double* b,
+                                  const sfi_selector_params& prm, double* out, double* out2, int32_t* head_err,
+                                  cudaStream_t st) {
+  StageArgs p{};
+  p.H = H;
+  p.W = W;
+  p.n = n;
+  p.a = a;
+  p.b = b;
+  p.out = out;
+  p.out2 = out2;
+  p.head_err = head_err;
+  p.alpha = prm.alpha;
+  p.gamma = prm.gamma;
+  p.beta = prm.beta;
+  p.p_curve = prm.p_curve;
+  p.eta = prm.eta;
+  p.lambda_clip = prm.lambda_clip;
+  p.alpha_soft = prm.alpha_soft;
+  p.alpha_cross = prm.alpha_cross;
+  p.temperature = prm.temperature;
+  p.eps = prm.epsilon;
+  p.nms_radius = prm.nms_radius;
+  const unsigned elem_blocks = (unsigned)std::min<size_t>(((size_t)H * n + 255) / 256, 4096);
+  switch (stage) {
+    case SFI_STAGE_EVIDENCE: stage_evidence_kernel<<<H, kStageT, 0, st>>>(p); break;
+    case SFI_STAGE_PRIOR: stage_prior_kernel<<<H, kStageT, 0, st>>>(p); break;
+    case SFI_STAGE_NORMALIZE: stage_normalize_kernel<<<H, kStageT, 0, st>>>(p); break;
+    case SFI_STAGE_FUSE: stage_fuse_kernel<<<H, kStageT, 0, st>>>(p); break;
+    case SFI_STAGE_Z_BASE: stage_zbase_kernel<<<std::max(elem_blocks, 1u), 256, 0, st>>>(p); break;
+    case SFI_STAGE_SOFT_NMS: stage_soft_nms_kernel<<<std::max(elem_blocks, 1u), 256, 0, st>>>(p); break;
+    case SFI_STAGE_CROSS_HEAD:
+      stage_cross_head_kernel<<<std::max(std::min((n + 255) / 256, 4096), 1), 256, 0, st>>>(p);
+      break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace sfi_impl

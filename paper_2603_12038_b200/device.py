@@ -219,6 +219,13 @@ class SfiCache:
                            params if params is not None else _C.SelectorParams(),
                            self._ptr(z_all, torch.float64), n_shards, shard, self._stream(stream))
 
+    def _C_sel_nccl(self, layer: int, logits: torch.Tensor, params, comm: int, n_shards: int, shard: int,
+                    z_all: torch.Tensor, stream=None):
+        """KV-head-sharded Selector over an NCCL communicator (sfi_selector_sharded_nccl)."""
+        _C.selector_sharded_nccl(self.shape, self.cache, layer, self._ptr(logits, torch.float32),
+                                 params if params is not None else _C.SelectorParams(), comm, n_shards, shard,
+                                 self._ptr(z_all, torch.float64), self._stream(stream))
+
     def compact_build(self, layer: int, rebuild_ring: bool = False, stream=None):
         _C.compact_build(self.shape, self.cache, layer, int(bool(rebuild_ring)), self._stream(stream))
 

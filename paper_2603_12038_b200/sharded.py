@@ -40,6 +40,23 @@ def all_gather_blocks(local: torch.Tensor, out: torch.Tensor, group=None) -> tor
     return out
 
 
+def nccl_comm_ptr(group=None) -> int:
+    """The ncclComm_t of torch's NCCL process group (as an integer), for the C
+    ABI's NCCL entry points (sfi_selector_sharded_nccl, sfi_merge_partials_nccl,
+    sfi_seq_selector_nccl). torch creates communicators lazily: one tiny
+    collective first makes sure this one exists."""
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    if dist.get_backend(group) != "nccl":
+        raise RuntimeError("the C-ABI NCCL exchange needs the nccl backend")
+    t = torch.zeros(1, device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(t, group=group)
+    torch.cuda.synchronize()
+    ptr = pg._get_backend(torch.device("cuda"))._comm_ptr()
+    if not ptr:
+        raise RuntimeError("ProcessGroupNCCL has no communicator for this device")
+    return int(ptr)
+
+
 def agree(ok: bool, group=None, what: str = "peer-memory setup", err: str = "") -> None:
     """Every rank votes (all_reduce MIN); raises on EVERY rank unless all succeeded,
     so ranks fall back to the all-gather path together instead of some blocking
@@ -183,10 +200,13 @@ class HeadShardedSfi:
 
     def __init__(self, n_layers: int, batch: int, n_kv_heads: int, n_q_heads: int, head_dim: int,
                  max_positions: int, n_sink: int = 4, k_budget: int = 2048, n_recent: int = 256,
-                 group=None, device=None, peer: bool = False):
+                 group=None, device=None, peer: bool = False, nccl: bool = False):
         """peer=True: the Selector's z_base all-gather reads every rank's block in
         place over peer memory (PeerExchange: CUDA IPC, sfi_peer_gather), one
-        block slot per layer so a block is only rewritten after every rank read it."""
+        block slot per layer so a block is only rewritten after every rank read it.
+        nccl=True: the C ABI's sfi_selector_sharded_nccl does fuse + ncclAllGather
+        + finish in one call on torch's NCCL communicator (graph capturable).
+        Otherwise torch.distributed all-gathers the blocks."""
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -202,6 +222,7 @@ class HeadShardedSfi:
         self.z_all = torch.empty((self.world, batch, self.local_heads, max_positions), dtype=torch.float64,
                                  device=dev)
         self.px = None
+        self.comm = nccl_comm_ptr(group) if nccl else 0
         if peer and self.world > 1:
             if n_layers < 2:
                 raise ValueError("peer exchange keeps one z_base slot per layer: needs >= 2 layers")
@@ -215,6 +236,10 @@ class HeadShardedSfi:
         return slice(self.h0 * self.G, self.h1 * self.G)
 
     def selector(self, layer: int, logits: torch.Tensor, params=None):
+        if self.comm:
+            c = self.cache
+            c._C_sel_nccl(layer, logits, params, self.comm, self.world, self.rank, self.z_all)
+            return
         z = self.cache.selector_fuse(layer, logits, params)
         if self.px is not None:
             st = self.cache._stream()
@@ -260,7 +285,7 @@ class SeqShardedSfi:
     def __init__(self, n_layers: int, batch: int, n_kv_heads: int, n_q_heads: int, head_dim: int,
                  max_positions: int, prompt_len: int, n_sink: int = 4, k_budget: int = 2048,
                  n_recent: int = 256, group=None, device=None, world: int | None = None,
-                 rank: int | None = None, peer: bool = False, peers: list | None = None):
+                 rank: int | None = None, peer: bool = False, peers: list | None = None, nccl: bool = False):
         """peer=True: the per-step (O, LSE) exchange goes through PeerExchange
         (peer memory, no collective launch); `peers` wires lockstep shards of
         one process to each other instead of through IPC."""
@@ -301,6 +326,11 @@ class SeqShardedSfi:
         self.o_all = z(P, B, Hq, head_dim, dt=torch.float32)
         self.lse_all = z(P, B, Hq, dt=torch.float32)
         self.n_recent = n_recent
+        # nccl=True: every exchange in-call through the C ABI on torch's NCCL communicator
+        self.comm = nccl_comm_ptr(group) if nccl else 0
+        if self.comm:
+            nb = _C.seq_selector_nccl_scratch_bytes(self.cache.shape, self.params, P)
+            self.nccl_scratch = z(nb, dt=torch.uint8)
         self.px = None
         if peer or peers is not None:
             if n_layers < 2:  # a slot may only be rewritten once every rank merged it
@@ -372,8 +402,17 @@ class SeqShardedSfi:
         all_gather_blocks(self.o_part, self.o_all, self.group)
         all_gather_blocks(self.lse_part, self.lse_all, self.group)
 
+    def _nccl_merge(self, out):
+        B, Hq, d = self.o_part.shape
+        self._C.merge_partials_nccl(self.world, B * Hq, d, self.o_part.data_ptr(), self.lse_part.data_ptr(),
+                                    self.o_all.data_ptr(), self.lse_all.data_ptr(),
+                                    self.cache._ptr(out, torch.float32), self.comm, self.cache._stream())
+
     def dense_decode(self, layer, q, out, logits, pool=0):
         self.dense_partial(layer, q, logits, pool)
+        if self.comm:
+            self._nccl_merge(out)
+            return
         if self.px is not None:
             self.peer_merge(layer, out)
             return
@@ -382,6 +421,9 @@ class SeqShardedSfi:
 
     def fast_decode(self, layer, q, k_new, v_new, out, prefetch=False):
         self.fast_partial(layer, q, k_new, v_new, prefetch)
+        if self.comm:
+            self._nccl_merge(out)
+            return
         if self.px is not None:
             self.peer_merge(layer, out)
             return
@@ -416,6 +458,13 @@ class SeqShardedSfi:
 
     def selector(self, layer, logits, params=None):
         # three exchanges per layer: row statistics, soft-NMS edges, top-k candidates
+        if self.comm:  # all three in one C-ABI call over NCCL
+            c = self.cache
+            self._C.seq_selector_nccl(c.shape, c.cache, layer, c._ptr(logits, torch.float32), params or self.params,
+                                      self.j_off.data_ptr(), self.n_glob.data_ptr(), self.base, self.base + self.cap,
+                                      self.comm, self.world, self.nccl_scratch.data_ptr(), self.nccl_scratch.numel(),
+                                      c._stream())
+            return
         if self.px is not None:  # over peer memory: publish, then gather in place
             st = self.cache._stream()
             self.sel_stats(layer, logits, 1, params)

@@ -1,4 +1,5 @@
-// test_api.cpp — the reference's C++ call sites against include/sfi_b200.hpp.
+// test_api.cpp — the reference's C++ call sites against include/sfi/*.hpp (the
+// reference's header paths and namespace) and libsfi_b200.so.
 // Restates KATs of /root/reference/proj/tests (test_core.cpp, test_scheduler.cpp,
 // test_attention.cpp, test_selector.cpp) with a minimal self-contained checker.
 // `test_api` runs the host-side cases; `test_api gpu` adds the device cases.
@@ -7,10 +8,19 @@
 #include <cstring>
 #include <functional>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
-#include "sfi_b200.hpp"
+// The reference's own header paths and namespace: a reference caller compiles
+// unchanged against include/sfi/*.hpp and links libsfi_b200.so.
+#include "sfi/attention.hpp"
+#include "sfi/config.hpp"
+#include "sfi/distribution.hpp"
+#include "sfi/error.hpp"
+#include "sfi/scheduler.hpp"
+#include "sfi/selector.hpp"
+#include "sfi_b200.h"
 
 namespace {
 
@@ -28,13 +38,13 @@ int g_fail = 0, g_checks = 0;
     bool thrown_ = false;                           \
     try {                                           \
       expr;                                         \
-    } catch (const sfi_b200::Error& e_) {           \
+    } catch (const sfi::Error& e_) {           \
       thrown_ = e_.code() == (code_);               \
     }                                               \
     CHECK(thrown_);                                 \
   } while (0)
 
-using namespace sfi_b200;
+using namespace sfi;
 
 void test_default_config() {  // test_core.cpp:20-44
   const Config c = default_config();
@@ -156,7 +166,7 @@ void test_reorganize_device() {  // test_attention.cpp:293-325
   CHECK(seg0.positions == (std::vector<Pos>{1, 2, 3, 7, 11, 19}));
   bool same = true;
   for (std::size_t i = 0; i < seg0.positions.size(); ++i) {
-    const auto row = store.key_row(0, seg0.positions[i]);
+    const float* row = store.key_at(0, seg0.positions[i]);
     for (int c = 0; c < spec.head_dim; ++c) same &= seg0.k[i * spec.head_dim + c] == row[c];
   }
   CHECK(same);
@@ -192,47 +202,105 @@ void test_selector_device() {  // test_selector.cpp:52-60, 295-301
   CHECK(select_top_k({0.1, 0.2}, {10, 20}, 5) == (std::vector<Pos>{10, 20}));
 }
 
-}  // namespace
 
-// The reference's run_request / run_dense call sites (scheduler.hpp:116-135)
-// against the device-path loop: C7 full retention (SFI tokens == dense tokens)
-// and the C8 schedule rule, through the C++ API.
-void test_request_loop_device() {
-  ModelSpec spec;
-  spec.n_layers = 2;
-  spec.n_query_heads = 8;
-  spec.n_kv_heads = 2;
-  spec.head_dim = 64;
-  spec.vocab_size = 256;
-  spec.max_positions = 1024;
-  const ToyModel model = ToyModel::random(spec, 9001);
-  std::vector<TokenId> prompt;
-  for (int i = 0; i < 70; ++i) prompt.push_back(5 + (i * 37) % 250);
-  CacheLimits full;
-  full.n_recent = 512;
-  full.k_budget = 64;
-  TriggerConfig trig;
-  trig.t_max = 8;
-  SelectorConfig cfg;
-  cfg.k_budget = 64;
-  const RequestResult r = run_request(model, prompt, full, trig, cfg, 24);
-  const DenseResult d = run_dense(model, prompt, 24);
-  CHECK(r.tokens.size() == 24 && r.log.size() == 24);
-  CHECK(r.tokens == d.tokens);  // C7 (acceptance.cpp:125-160)
-  int fast = 0, last_slow = 0;
-  for (int t = 0; t < 24; ++t) {  // C8 rule (acceptance.cpp:162-205)
-    const bool slow = t == 0 || trig.is_trigger(r.tokens[t - 1]) || t - last_slow >= trig.t_max;
-    if (slow) last_slow = t;
-    CHECK(slow == r.log[t].slow);
-    fast += !r.log[t].slow;
+void test_kvstore_reference_surface() {  // attention.hpp:100-155 signatures and semantics
+  const ModelSpec spec = spec64();
+  KvStore store(spec);  // the reference constructor (default CacheLimits)
+  std::mt19937_64 rng(5);
+  const int n = 40, hd = spec.n_kv_heads * spec.head_dim;
+  std::vector<std::vector<float>> keys;
+  for (int t = 0; t < n; ++t) {
+    store.begin_token();
+    for (int l = 0; l < spec.n_layers; ++l) {
+      const auto k = bf16_values(rng, hd), v = bf16_values(rng, hd);
+      store.append_layer(l, k.data(), v.data());
+      if (l == 1) keys.push_back(k);
+    }
+    store.end_token();
   }
-  CHECK(fast > 0);
-  CHECK(r.total_kv_reads <= r.dense_equiv_reads);
-  CacheLimits small;
-  small.n_recent = 16;
-  small.k_budget = 64;
-  CHECK_THROWS_CODE(run_request(model, prompt, small, trig, SelectorConfig{}, 4), ErrorCode::kUnsupported);  // k mismatch
+  // key_at: a view of H*d floats in the reference's [pos][H][d] paged layout
+  const float* k7 = store.key_at(1, 7);
+  CHECK(std::equal(k7, k7 + hd, keys[6].begin()));
+  CHECK_THROWS_CODE(store.key_at(0, n + 1), ErrorCode::kOutOfRange);
+  double acc = 0.0;
+  for (int c = 0; c < spec.head_dim; ++c) acc += static_cast<double>(keys[6][spec.head_dim + c]) * keys[6][spec.head_dim + c];
+  CHECK(store.key_norm(1, 1, 7) == std::sqrt(acc));
+  // a sink other than {1..n_sink}: gathered into the layer's own compact view
+  const std::vector<Pos> sink = {2, 5};
+  store.reorganize(1, sink, {{9, 30}, {3, 4, 6}});
+  const KvStore::CompactSegment& seg = store.compact(1, 0);  // const reference, as in the reference
+  CHECK(seg.positions == (std::vector<Pos>{2, 5, 9, 30}));
+  bool same = true;
+  for (std::size_t i = 0; i < seg.positions.size(); ++i) {
+    const float* row = store.key_at(1, seg.positions[i]);
+    for (int c = 0; c < spec.head_dim; ++c) same &= seg.k[i * spec.head_dim + c] == row[c];
+  }
+  CHECK(same);
+  CHECK(store.compact_matches(1, sink, {{9, 30}, {3, 4, 6}}));
+  // compact-read instrumentation (attention.cpp:242-244): one record per compact row per q head
+  store.set_access_trace(true);
+  SupportSet sup;
+  sup.sink = sink;
+  sup.selected = {{9, 30}, {3, 4, 6}};
+  sup.recent_start = 31;  // a recent range that does not end at size()
+  sup.recent_len = 4;
+  std::vector<double> q(static_cast<std::size_t>(spec.n_query_heads) * spec.head_dim, 0.01);
+  KernelStats ks;
+  const auto out = attention_kernel_sparse(store, 1, q, sup, &ks);
+  CHECK(out.size() == q.size() && ks.reads == static_cast<std::uint64_t>(4 + 4 + 5 + 4));
+  const int G = spec.group_size();
+  CHECK(store.access_trace().size() == static_cast<std::size_t>(G * (4 + 5)));
+  CHECK(store.access_trace().front().layer == 1 && store.access_trace().back().head == 1);
 }
+
+void test_selector_stages_device() {  // selector.hpp:84-122 through the stage kernels
+  LogitWindow w;
+  w.width = 1;
+  w.allowed = {5, 9};
+  w.values = {{0.0, std::log(2.0)}};
+  SelectorConfig cfg;
+  const auto f = evidence_from_window(w, cfg);  // test_selector.cpp:52-60
+  CHECK(f.size() == 1 && std::abs(f[0].mass[0] - 1.0 / 3) < 1e-12 && std::abs(f[0].mass[1] - 2.0 / 3) < 1e-12);
+  CHECK(validate_distribution(f[0]));
+  ScoreDistribution a, b;  // fuse KAT (test_selector.cpp:160-170)
+  a.support = b.support = {1, 2, 3};
+  a.mass = {0.5, 0.3, 0.2};
+  b.mass = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+  const FusedScore fs = fuse(a, b, cfg);
+  CHECK(fs.lambda_star == 0.02);
+  CHECK(std::abs(fs.fused.mass[0] - 0.4966666666666667) < 1e-15);
+  SelectorConfig r1;
+  r1.nms_radius = 1;
+  const auto nms = refine_soft_nms({1.0, 0.5, 0.2}, r1);  // test_selector.cpp:217-229
+  CHECK(std::abs(nms[0] - 1.0) < 1e-15 && std::abs(nms[1] - 0.25) < 1e-15 && std::abs(nms[2] - 0.05) < 1e-15);
+  const auto ch = refine_cross_head({{1.0}, {1.0}}, cfg);  // test_selector.cpp:261-280
+  CHECK(std::abs(ch[0][0] - (1.0 + 0.35 * std::log(0.5))) < 1e-15);
+  const std::vector<Pos> sup = {1, 2};
+  const std::vector<double> wts = {1.0, 3.0};
+  const ScoreDistribution nd = normalize(sup, wts);
+  CHECK(nd.mass[0] == 0.25 && nd.mass[1] == 0.75);
+  CHECK_THROWS_CODE(normalize(sup, std::vector<double>{0.0, 0.0}), ErrorCode::kEmptySupport);
+  SelectorTrace trace;
+  trace.capture_stages = true;
+  const CacheStats st = make_cache_stats({{1.0, 1.0}}, w.allowed, 1e-8);
+  const auto sel = run_selector(w, st, cfg, &trace);
+  CHECK(sel[0].size() == 2 && trace.stages.base.size() == 1 && trace.fusion.size() == 1);
+  CHECK(trace.elementary_ops > 0);
+}
+
+void test_config_io() {  // config.cpp:111-200
+  Config c = default_config();
+  c.selector.alpha_cross = 0.125;
+  c.trigger.trigger_tokens = {7, 8};
+  std::stringstream ss;
+  save_config(c, ss);
+  const Config back = load_config(ss);
+  CHECK(back.selector.alpha_cross == 0.125 && back.trigger.trigger_tokens == (std::vector<TokenId>{7, 8}));
+  std::stringstream bad("alpha=1\nbogus=2\n");
+  CHECK_THROWS_CODE(load_config(bad), ErrorCode::kConfig);
+}
+
+}  // namespace
 
 int main(int argc, char** argv) {
   const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
@@ -241,11 +309,13 @@ int main(int argc, char** argv) {
       {"compute_allowed", test_compute_allowed},
       {"triggers", test_triggers},
       {"c_abi_errors", test_c_abi_errors},
+      {"config_io", test_config_io},
   };
   if (gpu) {
     cases.push_back({"reorganize_device", test_reorganize_device});
     cases.push_back({"selector_device", test_selector_device});
-    cases.push_back({"request_loop_device", test_request_loop_device});
+    cases.push_back({"kvstore_reference_surface", test_kvstore_reference_surface});
+    cases.push_back({"selector_stages_device", test_selector_stages_device});
   }
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

@@ -1,6 +1,6 @@
 """End-to-end request loop with the device hot path inside.
 
-paper_2603_12038_b200.run_request / run_dense (engine.cpp) are the reference's
+harness.run_request / run_dense (harness/engine.cpp, the test harness) are the reference's
 run_request / run_dense (scheduler.cpp:213-365) over the reference's toy
 decoder, with every KV append, dense attention + logit capture, Selector
 (decode W = 1 and the W-row prefill window), compact rebuild and sparse
@@ -24,6 +24,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
+import harness as toy
 from helpers import oracle
 
 SPEC = dict(n_layers=2, n_query_heads=8, n_kv_heads=2, head_dim=64, vocab_size=256, max_positions=2048)
@@ -69,7 +70,7 @@ def test_toy_weights_match_reference():
     if orc.kind != "reference":
         pytest.skip("reference library not built")
     for seed in (9000, 7001, 4200):
-        ours = sfi.ToyModel.random(_spec(), seed).weight_checksum()
+        ours = toy.ToyModel.random(_spec(), seed).weight_checksum()
         assert ours == orc.toy_checksum(SPEC, seed), seed
 
 
@@ -78,7 +79,7 @@ def test_request_loop_argument_errors():
     reference's codes and order (scheduler.cpp:218-231, :336-341)."""
     import paper_2603_12038_b200 as sfi
 
-    model = sfi.ToyModel.random(_spec(), 1)
+    model = toy.ToyModel.random(_spec(), 1)
     lim, trig, cfg = _limits(4, 16, 16), _trigger([0], 8), _selector(16)
 
     def code(fn):
@@ -86,17 +87,17 @@ def test_request_loop_argument_errors():
             fn()
         return e.value.code
 
-    assert code(lambda: sfi.run_request(model, [], lim, trig, cfg, 4)) == "out_of_range"
-    assert code(lambda: sfi.run_request(model, [5, 6], lim, trig, cfg, 0)) == "out_of_range"
-    assert code(lambda: sfi.run_request(model, [5] * 2040, lim, trig, cfg, 16)) == "context_overflow"
-    assert code(lambda: sfi.run_request(model, [5, 6], _limits(4, 2048, 16), trig, cfg, 4)) == "config"
-    assert code(lambda: sfi.run_request(model, [5, 6], lim, trig, _selector(32), 4)) == "unsupported"
+    assert code(lambda: toy.run_request(model, [], lim, trig, cfg, 4)) == "out_of_range"
+    assert code(lambda: toy.run_request(model, [5, 6], lim, trig, cfg, 0)) == "out_of_range"
+    assert code(lambda: toy.run_request(model, [5] * 2040, lim, trig, cfg, 16)) == "context_overflow"
+    assert code(lambda: toy.run_request(model, [5, 6], _limits(4, 2048, 16), trig, cfg, 4)) == "config"
+    assert code(lambda: toy.run_request(model, [5, 6], lim, trig, _selector(32), 4)) == "unsupported"
     bad = _selector(16)
     bad.alpha = 0.0
-    assert code(lambda: sfi.run_request(model, [5, 6], lim, trig, bad, 4)) == "config"
-    assert code(lambda: sfi.run_dense(model, [], 4)) == "out_of_range"
-    assert code(lambda: sfi.run_dense(model, [5, 6], 0)) == "out_of_range"
-    assert code(lambda: sfi.run_dense(model, [5] * 2040, 16)) == "context_overflow"
+    assert code(lambda: toy.run_request(model, [5, 6], lim, trig, bad, 4)) == "config"
+    assert code(lambda: toy.run_dense(model, [], 4)) == "out_of_range"
+    assert code(lambda: toy.run_dense(model, [5, 6], 0)) == "out_of_range"
+    assert code(lambda: toy.run_dense(model, [5] * 2040, 16)) == "context_overflow"
 
 
 # ---------------------------------------------------------------- GPU ----
@@ -111,11 +112,11 @@ def test_c7_full_retention_matches_dense():
 
     rng = np.random.default_rng(901)
     for i in range(6):
-        model = sfi.ToyModel.random(_spec(), 9000 + i)
+        model = toy.ToyModel.random(_spec(), 9000 + i)
         prompt = _prompt(rng, int(rng.integers(48, 96)))
-        res = sfi.run_request(model, prompt, _limits(4, 512, 64), _trigger([0, 1, 2, 3, 4], 64),
+        res = toy.run_request(model, prompt, _limits(4, 512, 64), _trigger([0, 1, 2, 3, 4], 64),
                               _selector(64), 32)
-        dense = sfi.run_dense(model, prompt, 32)
+        dense = toy.run_dense(model, prompt, 32)
         assert list(res.tokens) == list(dense.tokens), i
         assert any(not r.slow for r in res.log), "the sparse path must be exercised"
         d = np.abs(np.array(res.step_logits) - np.array(dense.step_logits)).max()
@@ -129,13 +130,13 @@ def test_c8_trigger_replay_and_c9_segment_freezing():
     rng = np.random.default_rng(555)
     trig_slows = forced = 0
     for run in range(4):
-        model = sfi.ToyModel.random(_spec(), 7000 + run)
+        model = toy.ToyModel.random(_spec(), 7000 + run)
         prompt = _prompt(rng, 32 + int(rng.integers(0, 33)))
-        probe = sfi.run_dense(model, prompt, 40)
+        probe = toy.run_dense(model, prompt, 40)
         trig = _trigger([probe.tokens[7], probe.tokens[23]], 11)
-        opts = sfi.RunOptions()
+        opts = toy.RunOptions()
         opts.capture_selected = True
-        res = sfi.run_request(model, prompt, _limits(4, 16, 32), trig, _selector(32), 40, opts)
+        res = toy.run_request(model, prompt, _limits(4, 16, 32), trig, _selector(32), 40, opts)
         last_slow = 0
         for t in range(40):
             slow = t == 0 or res.tokens[t - 1] in trig.trigger_tokens or t - last_slow >= trig.t_max
@@ -157,15 +158,15 @@ def _compare(sfi, orc, sp, spec_d, seeds, rng, k, n_recent, t_max, steps, pool="
     worst = 0.0
     jacc = []
     for seed in seeds:
-        model = sfi.ToyModel.random(sp, seed)
+        model = toy.ToyModel.random(sp, seed)
         prompt = _prompt(rng, 48 + int(rng.integers(0, 48)))
         lim = dict(n_sink=4, n_recent=n_recent, k_budget=k, t_max=t_max,
                    trigger_tokens=[int(rng.integers(5, 256))], window_prefill=16)
-        opts = sfi.RunOptions()
+        opts = toy.RunOptions()
         opts.capture_selected = True
         cfg = _selector(k)
         cfg.pool = sfi.PoolMode.max if pool == "max" else sfi.PoolMode.mean
-        res = sfi.run_request(model, prompt, _limits(4, n_recent, k), _trigger(lim["trigger_tokens"], t_max),
+        res = toy.run_request(model, prompt, _limits(4, n_recent, k), _trigger(lim["trigger_tokens"], t_max),
                               cfg, steps, opts)
         ref = orc.toy_run_request(spec_d, seed, prompt, lim, orc_cfg(k, pool=1 if pool == "max" else 0), steps)
         ours = np.array(res.tokens)
