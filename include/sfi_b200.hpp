@@ -7,7 +7,8 @@
 // and relinks against libsfi_b200.so unchanged. Every hot-path call launches
 // the sm_100a kernels through the C ABI (sfi_b200.h); there is no CPU
 // fallback. B200 extensions (DeviceCache, dense_capture, KvStore prefill /
-// device accessors, check) live beside them in namespace sfi.
+// device accessors, check, the DecodeExecutor of sfi/decode.hpp) live beside
+// them in namespace sfi.
 //
 // `sfi_b200` is kept as an alias of `sfi` for existing callers.
 #pragma once
@@ -15,6 +16,7 @@
 #include "sfi_b200.h"
 #include "sfi/attention.hpp"
 #include "sfi/config.hpp"
+#include "sfi/decode.hpp"
 #include "sfi/distribution.hpp"
 #include "sfi/error.hpp"
 #include "sfi/scheduler.hpp"

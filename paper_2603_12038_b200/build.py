@@ -36,9 +36,9 @@ HARNESS = os.path.join(ROOT, "harness")
 TOY_LIB = os.path.join(HARNESS, "libsfi_toy.so")
 TOY_EXT = os.path.join(HARNESS, "_sfi_toy" + sysconfig.get_config_var("EXT_SUFFIX"))
 CU = ["decode.cu", "fast_decode.cu", "capture.cu", "cache_ops.cu", "selector.cu", "capi.cu"]
-CPP = ["host.cpp"]
+CPP = ["host.cpp", "executor.cpp"]
 HEADERS = [os.path.join(INC, h) for h in ("sfi_b200.h", "sfi_b200.hpp")] + [
-    os.path.join(INC, "sfi", h) for h in ("attention.hpp", "config.hpp", "distribution.hpp", "error.hpp",
+    os.path.join(INC, "sfi", h) for h in ("attention.hpp", "config.hpp", "decode.hpp", "distribution.hpp", "error.hpp",
                                           "scheduler.hpp", "selector.hpp")] + [
     os.path.join(CSRC, h) for h in ("common.cuh", "kernels.h")]
 

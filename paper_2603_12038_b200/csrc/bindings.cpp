@@ -324,6 +324,43 @@ PYBIND11_MODULE(_sfi_b200, m) {
   py::class_<sfi_selector_params>(m, "SelectorParams")
       .def(py::init([](const SelectorConfig& c) { return to_params(c); }), py::arg("config") = SelectorConfig{});
 
+  // ---- the C++ decode executor (sfi/decode.hpp): async slow step + graph-captured steps ----
+  py::class_<DecodeExecutor>(m, "DecodeExecutor")
+      .def(py::init([](const sfi_shape& s, const sfi_cache& c, std::uintptr_t stream, const SelectorConfig& cfg,
+                       int slots, bool share_sm, std::uintptr_t logits_ring) {
+             return std::make_unique<DecodeExecutor>(s, c, vp(stream), cfg, slots, share_sm,
+                                                     static_cast<float*>(vp(logits_ring)));
+           }),
+           py::arg("shape"), py::arg("cache"), py::arg("stream"), py::arg("selector") = SelectorConfig{},
+           py::arg("slots") = 4, py::arg("share_sm") = true, py::arg("logits_ring") = 0)
+      .def("step",
+           [](DecodeExecutor& x, bool slow, std::uintptr_t q, std::uintptr_t k, std::uintptr_t v, std::uintptr_t out,
+              size_t sq, size_t skv, size_t so, bool rebuild_ring, std::vector<std::uintptr_t> wait_before,
+              std::vector<std::uintptr_t> record_after, bool capture, std::uintptr_t origin) {
+             StepBuffers io;
+             io.q = static_cast<const float*>(vp(q));
+             io.k_new = vp(k);
+             io.v_new = vp(v);
+             io.out = static_cast<float*>(vp(out));
+             io.layer_stride_q = sq;
+             io.layer_stride_kv = skv;
+             io.layer_stride_out = so;
+             StepHooks hooks;
+             for (auto e : wait_before) hooks.wait_before.push_back(vp(e));
+             for (auto e : record_after) hooks.record_after.push_back(vp(e));
+             const StepHooks* hp = (wait_before.empty() && record_after.empty()) ? nullptr : &hooks;
+             if (capture) x.capture(slow, io, rebuild_ring, hp);
+             else x.step(slow, io, rebuild_ring, hp, vp(origin));
+           },
+           py::arg("slow"), py::arg("q"), py::arg("k_new"), py::arg("v_new"), py::arg("out"), py::arg("stride_q") = 0,
+           py::arg("stride_kv") = 0, py::arg("stride_out") = 0, py::arg("rebuild_ring") = false,
+           py::arg("wait_before") = std::vector<std::uintptr_t>{}, py::arg("record_after") = std::vector<std::uintptr_t>{},
+           py::arg("capture") = false, py::arg("origin") = 0)
+      .def("replay", &DecodeExecutor::replay, py::arg("slow"))
+      .def("captured", &DecodeExecutor::captured, py::arg("slow"))
+      .def("logits_slot", [](const DecodeExecutor& x, int l) { return reinterpret_cast<std::uintptr_t>(x.logits_slot(l)); })
+      .def("launches_per_step", &DecodeExecutor::launches_per_step, py::arg("slow"));
+
   m.def("version", &sfi_version);
   m.def("last_launch_count", &sfi_last_launch_count);
   m.def("buffer_sizes", [](const sfi_shape& s) {

@@ -298,3 +298,57 @@ class SlowStepPipeline:
 
     def end(self):
         self.main.wait_stream(self.aux)  # join: the next fast step reads the new compact rows
+
+
+class StepExecutor:
+    """The C++ decode executor (include/sfi/decode.hpp, executor.cpp) over one
+    SfiCache: whole decode steps of all layers — fast (advance + one fused K4
+    launch per layer) or slow (the layer-wise asynchronous pipeline: dense on a
+    high-priority main stream, Selector + compact on a lowest-priority aux
+    stream through a `slots`-deep pooled-logit ring, one completion barrier) —
+    enqueued from C++, capturable once per kind into a CUDA graph (node
+    priorities kept) and replayed with no host work.
+
+    q, out: fp32 [L][B][Hq][d]; k_new, v_new: bf16 [L][B][H][d] (views with any
+    per-layer stride, e.g. rows of one packed [L][q | k | v] buffer)."""
+
+    def __init__(self, cache: SfiCache, selector=None, slots: int = 4, share_sm: bool = True, stream=None):
+        self.c = cache
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=cache.k_cache.device)
+        s = cache.shape
+        self.logits = torch.zeros((slots, s.batch, s.n_kv_heads, s.max_positions), dtype=torch.float32,
+                                  device=cache.k_cache.device)
+        self.x = _C.DecodeExecutor(cache.shape, cache.cache, self.stream.cuda_stream,
+                                   selector if selector is not None else _C.SelectorConfig(), slots, share_sm,
+                                   self.logits.data_ptr())
+
+    @staticmethod
+    def _stride(t: torch.Tensor) -> int:
+        return t.stride(0) * t.element_size()
+
+    def _args(self, q, k_new, v_new, out):
+        for t in (q, k_new, v_new, out):
+            if not t.is_cuda or not t[0].is_contiguous():
+                raise ValueError("step buffers: CUDA tensors with contiguous layers")
+        return (q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(), self._stride(q),
+                self._stride(k_new), self._stride(out))
+
+    def step(self, slow: bool, q, k_new, v_new, out, rebuild_ring: bool = False, wait_before=(), record_after=(),
+             origin=None):
+        """Enqueue one step after the work on `origin` (a torch stream; default: the
+        executor's stream). wait_before / record_after: per-layer torch.cuda.Events."""
+        if k_new.stride(0) * k_new.element_size() != self._stride(v_new):
+            raise ValueError("k_new / v_new layer strides differ")
+        self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring,
+                    [e.cuda_event for e in wait_before], [e.cuda_event for e in record_after], False,
+                    0 if origin is None else origin.cuda_stream)
+
+    def capture(self, slow: bool, q, k_new, v_new, out, rebuild_ring: bool = False):
+        self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring, [], [], True, 0)
+
+    def replay(self, slow: bool):
+        self.x.replay(slow)
+
+    def logits_slot(self, layer: int) -> torch.Tensor:
+        """Layer `layer`'s pooled logits after a slow step (until layer + slots reuses the slot)."""
+        return self.logits[layer % self.logits.shape[0]]
