@@ -226,10 +226,16 @@ class Workload:
         self.out = t.zeros(L, B, Hq, d, device=device)
         self.logits = self.cache.pooled_logits
         drv = self.drv
-        # asynchronous slow step (1 GPU / dp): Selector + compact overlap the next layers' dense decode
+        # 1 GPU / dp: whole steps through the C++ decode executor (include/sfi/decode.hpp):
+        # the asynchronous slow step (Selector + compact of layer i on a low-priority aux
+        # stream behind the dense decode of layers i+1..) and graph-captured steps
         self.pipe = None
+        self.exec = None
         if self.mode in ("single", "dp") and not sync_slow:
-            self.pipe = sfi.SlowStepPipeline(self.cache)
+            from paper_2603_12038_b200.device import StepExecutor
+
+            self.exec = StepExecutor(self.cache, slots=int(os.environ.get("SFI_EXEC_SLOTS", "2")),
+                                     priorities=int(os.environ.get("SFI_EXEC_PRIO", "0")))
         self.cache.fill_synthetic(seed=2026 + 1, length=fill_len)
         self.set_lengths(self.ctx)
         if inputs == "peaked" and self.mode in ("single", "dp", "heads"):
@@ -255,6 +261,16 @@ class Workload:
         (LSE-merged attention partials, sharded Selector statistics). `io`: the
         end-to-end variant's per-layer host copies (HostIO)."""
         d = self.drv
+        if self.exec is not None:
+            origin = self.torch.cuda.current_stream()
+            if io is not None:
+                io.begin()
+            wb, ra = io.hook_events() if io is not None else ((), ())
+            self.exec.step(slow, self.q, self.k_new, self.v_new, self.out, rebuild_ring, wb, ra, origin=origin)
+            if io is not None:
+                io.copy_outputs()
+                io.end()
+            return
         if io is not None:
             io.begin()
         d.step_advance()
@@ -362,6 +378,8 @@ class HostIO:
         self.groups = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
         self.ev_in = [t.cuda.Event() for _ in self.groups]
         self.ev_out = [t.cuda.Event() for _ in self.groups]
+        for e in self.ev_in + self.ev_out:  # create the CUDA events now (the executor records / waits on them)
+            e.record()
         self.h2d = wl.q.numel() * 4 + wl.k_new.numel() * 2 + wl.v_new.numel() * 2
         self.d2h = wl.out.numel() * 4
 
@@ -387,6 +405,21 @@ class HostIO:
                     self.cs.wait_event(self.ev_out[gi])
                     self.oh[l0:l1].copy_(self.wl.out[l0:l1], non_blocking=True)
 
+    def hook_events(self):
+        """Per-layer events for the C++ executor: the main stream waits for a group's
+        inputs before its first layer and marks its last layer's output."""
+        wb, ra = [None] * self.wl.L, [None] * self.wl.L
+        for gi, (l0, l1) in enumerate(self.groups):
+            wb[l0] = self.ev_in[gi]
+            ra[l1 - 1] = self.ev_out[gi]
+        return wb, ra
+
+    def copy_outputs(self):
+        with self.t.cuda.stream(self.cs):
+            for gi, (l0, l1) in enumerate(self.groups):
+                self.cs.wait_event(self.ev_out[gi])
+                self.oh[l0:l1].copy_(self.wl.out[l0:l1], non_blocking=True)
+
     def end(self):
         self.main.wait_stream(self.cs)  # join: the step ends when its output is on the host
 
@@ -410,17 +443,18 @@ def time_kernel(wl: Workload, which: str, iters: int) -> float:
     return a.elapsed_time(b) / iters
 
 
-def time_graph(g, reps: int) -> float:
-    """ms per replay of a captured step graph, back to back between two events."""
+def time_graph(g, reps: int, stream) -> float:
+    """ms per replay of a captured step (a torch CUDAGraph or the executor's replay
+    callable), back to back between two events on the stream it replays on."""
     t = __import__("torch")
-    s = t.cuda.current_stream()
-    g.replay()
+    run = g if callable(g) else g.replay
+    run()
     t.cuda.synchronize()
     a, b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-    a.record(s)
+    a.record(stream)
     for _ in range(reps):
-        g.replay()
-    b.record(s)
+        run()
+    b.record(stream)
     t.cuda.synchronize()
     return a.elapsed_time(b) / reps
 
@@ -446,23 +480,23 @@ def time_selector(wl: Workload, iters: int) -> tuple[float, float]:
 
 def time_dense_in_situ(wl: Workload) -> float | None:
     """K1 as it runs inside the timed slow step: one eager asynchronous slow step
-    (dense on the main stream at the pipeline's share grid, Selector + compact of
-    the earlier layers concurrently on the aux stream), CUDA events on the main
-    stream around every dense launch; mean over layers 2.. (layer 0-1 run alone)."""
-    if wl.pipe is None:
+    through the C++ executor (dense on the high-priority main stream at the
+    pipeline's share grid, Selector + compact of the earlier layers concurrently on
+    the low-priority aux stream), a timing event recorded on the main stream after
+    every layer (the executor's per-layer hook): the mean per-layer main-chain time
+    (append + dense decode) over layers 2.. (layers 0-1 run with an idle aux stream)."""
+    if wl.exec is None:
         return None
     t = wl.torch
-    evs = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)) for _ in range(wl.L)]
+    evs = [t.cuda.Event(enable_timing=True) for _ in range(wl.L)]
+    for e in evs:
+        e.record()
     wl.set_lengths(wl.ctx)
     t.cuda.synchronize()
-    wl.drv.step_advance()
-    wl.pipe.begin()
-    for l in range(wl.L):
-        wl.pipe.layer(l, wl.q[l], wl.out[l], wl.k_new[l], wl.v_new[l], wl.params, False, dense_events=evs[l])
-    wl.pipe.end()
+    wl.exec.step(True, wl.q, wl.k_new, wl.v_new, wl.out, False, (), evs)
     t.cuda.synchronize()
-    ts = [a.elapsed_time(b) for a, b in evs]
-    return float(np.mean(ts[2:] if len(ts) > 3 else ts))
+    ts = [evs[i - 1].elapsed_time(evs[i]) for i in range(2, wl.L)]
+    return float(np.mean(ts)) if ts else None
 
 
 def traffic_for(kernel: str, cfg_name: str):
@@ -515,15 +549,22 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
     use_graph = not args.no_graph
     graphs = {}
     graph_note = None
+    # the stream the timed steps run on: the C++ executor's own stream (its graphs keep
+    # their node priorities), else torch's current stream
+    stream = wl.exec.stream if wl.exec is not None else torch.cuda.current_stream()
     if use_graph:
         # both paths already ran eagerly in setup (kernel attributes, driver entry
         # points); capture records without executing, so prefix_len is untouched
         try:
             for slow in (False, True):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    wl.step(slow)
-                graphs[slow] = g
+                if wl.exec is not None:
+                    wl.exec.capture(slow, wl.q, wl.k_new, wl.v_new, wl.out)
+                    graphs[slow] = (lambda s_=slow: wl.exec.replay(s_))
+                else:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        wl.step(slow)
+                    graphs[slow] = g
             torch.cuda.synchronize()
         except Exception as ex:  # e.g. a collective backend that cannot be captured
             use_graph, graphs = False, {}
@@ -533,9 +574,11 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
 
     def run(slow: bool):
         if use_graph:
-            graphs[slow].replay()
+            g = graphs[slow]
+            g() if callable(g) else g.replay()
         else:
-            wl.step(slow)
+            with torch.cuda.stream(stream):
+                wl.step(slow)
 
     for i in range(W):
         run(sched[i])
@@ -546,7 +589,6 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
@@ -578,14 +620,15 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        cur = torch.cuda.current_stream()  # torch's graphs replay on the current stream
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        a.record(cur)
         for slow in sched_e:
             if use_graph:
                 ge[slow].replay()
             else:
                 wl.step(slow, io=io)
-        b.record(stream)
+        b.record(cur)
         torch.cuda.synchronize()
         ems = max_over_ranks(a.elapsed_time(b))
         e2e = {"value": wl.job_tokens * K / (ems / 1e3), "unit": "tokens/s",
@@ -605,9 +648,9 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
     t_fast_step = t_slow_step = None
     if use_graph:
         wl.set_lengths(wl.ctx + 1)
-        t_fast_step = time_graph(graphs[False], 16)
+        t_fast_step = time_graph(graphs[False], 16, stream)
         wl.set_lengths(wl.ctx + 1)
-        t_slow_step = time_graph(graphs[True], 3)
+        t_slow_step = time_graph(graphs[True], 3, stream)
     t_sp = t_fast_step / wl.L if t_fast_step else t_sp_iso
     t_de = t_de_situ if t_de_situ else t_de_iso
     # diagnostic: the same fused fast step with every layer in ONE launch (layer-batched
@@ -680,9 +723,10 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
         "config": config_dict(cfg_name, world),
         "run": {"kv_heads_per_gpu": wl.H, "batch_per_gpu": wl.B, "slow_steps_timed": f"{n_slow} of {K}",
                 "cuda_graphs": use_graph if graph_note is None else graph_note,
-                "slow_step": "synchronous" if wl.pipe is None else
-                             "async pipeline: dense on the main stream (share grid), Selector + compact on a "
-                             "low-priority aux stream",
+                "slow_step": "synchronous" if wl.exec is None else
+                             "C++ DecodeExecutor: async pipeline, dense on a high-priority main stream (share "
+                             "grid), Selector + compact on a low-priority aux stream, 4-slot logit ring; steps "
+                             "replayed from CUDA graphs with node priorities",
                 "exchange": {"nccl": "ncclAllGather in-call through the C ABI (torch's communicator)",
                              "allgather": "torch.distributed all-gather",
                              "peer": "peer memory (CUDA IPC over NVLink)"}.get(wl.exchange, "none"),

@@ -50,7 +50,7 @@ class DecodeExecutor {
   // logits_ring: caller-owned fp32 [slots][B][H][max_positions] device buffer
   // for the pooled-logit ring, or nullptr to allocate one.
   DecodeExecutor(const sfi_shape& shape, const sfi_cache& cache, void* stream, const SelectorConfig& selector = {},
-                 int slots = 4, bool share_sm = true, float* logits_ring = nullptr);
+                 int slots = 2, bool share_sm = true, float* logits_ring = nullptr, int priorities = 0);
   ~DecodeExecutor();
   DecodeExecutor(const DecodeExecutor&) = delete;
   DecodeExecutor& operator=(const DecodeExecutor&) = delete;
@@ -83,6 +83,7 @@ class DecodeExecutor {
   sfi_selector_params prm_;
   int slots_;
   bool share_;
+  int prio_;  // 0: equal stream priorities, 1: main stream high / aux low (the paper's), 2: aux high
   float* logits_ = nullptr;
   bool own_logits_ = false;
   std::vector<void*> ev_ready_, ev_free_;

@@ -327,12 +327,13 @@ PYBIND11_MODULE(_sfi_b200, m) {
   // ---- the C++ decode executor (sfi/decode.hpp): async slow step + graph-captured steps ----
   py::class_<DecodeExecutor>(m, "DecodeExecutor")
       .def(py::init([](const sfi_shape& s, const sfi_cache& c, std::uintptr_t stream, const SelectorConfig& cfg,
-                       int slots, bool share_sm, std::uintptr_t logits_ring) {
+                       int slots, bool share_sm, std::uintptr_t logits_ring, int priorities) {
              return std::make_unique<DecodeExecutor>(s, c, vp(stream), cfg, slots, share_sm,
-                                                     static_cast<float*>(vp(logits_ring)));
+                                                     static_cast<float*>(vp(logits_ring)), priorities);
            }),
            py::arg("shape"), py::arg("cache"), py::arg("stream"), py::arg("selector") = SelectorConfig{},
-           py::arg("slots") = 4, py::arg("share_sm") = true, py::arg("logits_ring") = 0)
+           py::arg("slots") = 2, py::arg("share_sm") = true, py::arg("logits_ring") = 0,
+           py::arg("priorities") = 0)
       .def("step",
            [](DecodeExecutor& x, bool slow, std::uintptr_t q, std::uintptr_t k, std::uintptr_t v, std::uintptr_t out,
               size_t sq, size_t skv, size_t so, bool rebuild_ring, std::vector<std::uintptr_t> wait_before,

@@ -30,16 +30,19 @@ void* new_event() {
 }  // namespace
 
 DecodeExecutor::DecodeExecutor(const sfi_shape& shape, const sfi_cache& cache, void* stream,
-                               const SelectorConfig& selector, int slots, bool share_sm, float* logits_ring)
-    : s_(shape), c_(cache), user_(stream), prm_(to_params(selector)), slots_(slots), share_(share_sm) {
+                               const SelectorConfig& selector, int slots, bool share_sm, float* logits_ring,
+                               int priorities)
+    : s_(shape), c_(cache), user_(stream), prm_(to_params(selector)), slots_(slots), share_(share_sm),
+      prio_(priorities) {
   check(sfi_shape_validate(&s_));
   if (slots_ < 1) fail(ErrorCode::kConfig, "DecodeExecutor: slots must be >= 1");
   selector.validate();
   int least = 0, greatest = 0;
   ok(cudaDeviceGetStreamPriorityRange(&least, &greatest), "stream priorities");
   cudaStream_t hi, lo;
-  ok(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, greatest), "main stream");
-  ok(cudaStreamCreateWithPriority(&lo, cudaStreamNonBlocking, least), "aux stream");
+  const int p_main = prio_ == 1 ? greatest : least, p_aux = prio_ == 2 ? greatest : least;
+  ok(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, p_main), "main stream");
+  ok(cudaStreamCreateWithPriority(&lo, cudaStreamNonBlocking, p_aux), "aux stream");
   cudaStream_t cap;
   ok(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
   hi_ = hi;
@@ -166,7 +169,7 @@ void DecodeExecutor::capture(bool slow, const StepBuffers& io, bool rebuild_ring
   ok(cudaStreamEndCapture(S(cap_), &g), "capture");
   cudaGraphExec_t ge = nullptr;
   // node priorities: the main chain's kernels ahead of the aux chain's on every SM
-  ok(cudaGraphInstantiateWithFlags(&ge, g, cudaGraphInstantiateFlagUseNodePriority), "instantiate");
+  ok(cudaGraphInstantiateWithFlags(&ge, g, prio_ ? cudaGraphInstantiateFlagUseNodePriority : 0), "instantiate");
   cudaGraphDestroy(g);
   void*& slot = graph_[slow ? 1 : 0];
   if (slot) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(slot));

@@ -312,7 +312,8 @@ class StepExecutor:
     q, out: fp32 [L][B][Hq][d]; k_new, v_new: bf16 [L][B][H][d] (views with any
     per-layer stride, e.g. rows of one packed [L][q | k | v] buffer)."""
 
-    def __init__(self, cache: SfiCache, selector=None, slots: int = 4, share_sm: bool = True, stream=None):
+    def __init__(self, cache: SfiCache, selector=None, slots: int = 2, share_sm: bool = True, stream=None,
+                 priorities: int = 0):
         self.c = cache
         self.stream = stream if stream is not None else torch.cuda.Stream(device=cache.k_cache.device)
         s = cache.shape
@@ -320,7 +321,7 @@ class StepExecutor:
                                   device=cache.k_cache.device)
         self.x = _C.DecodeExecutor(cache.shape, cache.cache, self.stream.cuda_stream,
                                    selector if selector is not None else _C.SelectorConfig(), slots, share_sm,
-                                   self.logits.data_ptr())
+                                   self.logits.data_ptr(), priorities)
 
     @staticmethod
     def _stride(t: torch.Tensor) -> int:
@@ -340,7 +341,8 @@ class StepExecutor:
         if k_new.stride(0) * k_new.element_size() != self._stride(v_new):
             raise ValueError("k_new / v_new layer strides differ")
         self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring,
-                    [e.cuda_event for e in wait_before], [e.cuda_event for e in record_after], False,
+                    [e.cuda_event if e is not None else 0 for e in wait_before],
+                    [e.cuda_event if e is not None else 0 for e in record_after], False,
                     0 if origin is None else origin.cuda_stream)
 
     def capture(self, slow: bool, q, k_new, v_new, out, rebuild_ring: bool = False):
