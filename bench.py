@@ -459,6 +459,36 @@ def time_graph(g, reps: int, stream) -> float:
     return a.elapsed_time(b) / reps
 
 
+def fast_grid(wl: Workload) -> int:
+    """CTAs of one fused fast-step launch (fast_decode.cu fast_cluster_size)."""
+    slices, c = wl.B * wl.H, 1
+    while c < 8 and slices * c <= 148:
+        c *= 2
+    if c == 8 and slices * 32 <= 148:
+        c = 16
+    return slices * c
+
+
+def launch_floor_ms(wl: Workload) -> float | None:
+    """Per-layer launch floor of the fast step: a CUDA graph of 1 + L empty
+    kernels (sfi_launch_floor) with the fused fast step's PDL protocol and grid,
+    replayed back to back; ms per launch."""
+    import paper_2603_12038_b200 as sfi
+
+    t = wl.torch
+    try:
+        g = t.cuda.CUDAGraph()
+        s = t.cuda.Stream()
+        with t.cuda.stream(s):
+            sfi._C.launch_floor(2, fast_grid(wl), s.cuda_stream)  # warm
+        t.cuda.synchronize()
+        with t.cuda.graph(g):
+            sfi._C.launch_floor(1 + wl.L, fast_grid(wl), t.cuda.current_stream().cuda_stream)
+        return time_graph(g, 16, t.cuda.current_stream()) / (1 + wl.L)
+    except Exception:
+        return None
+
+
 def time_selector(wl: Workload, iters: int) -> tuple[float, float]:
     """Selector and compact build per layer, isolated (queued back to back)."""
     t = wl.torch
@@ -713,6 +743,12 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
     if t_fast_step:
         roof["fast_step"] = {"us": t_fast_step * 1e3, "algorithmic_bytes": wl.L * bsp,
                              "frac": wl.L * bsp / t_fast_step / 1e6 / hbm}
+        fl = launch_floor_ms(wl)
+        if fl:
+            roof["fast_step"].update({
+                "launch_floor_us_per_layer": fl * 1e3, "us_per_layer": t_sp * 1e3,
+                "vs_launch_floor": t_sp / fl,
+                "floor_note": "graph of 1 + L empty kernels with the fast step's PDL protocol and grid"})
     fast_us = wl.L * (t_sp * 1e3)
     res = {
         "metric": metric_name(cfg_name),

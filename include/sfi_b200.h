@@ -353,6 +353,11 @@ SFI_API int sfi_seq_selector_nccl(const sfi_shape* shape, const sfi_cache* cache
                                   void* nccl_comm, int32_t n_shards, void* scratch, size_t scratch_bytes,
                                   void* stream);
 
+/* Measurement aid: n_launches empty kernels of `grid` CTAs with the fused fast
+ * step's programmatic-dependent-launch protocol, back to back on `stream` — the
+ * per-layer launch floor a one-launch-per-layer fast step cannot go below. */
+SFI_API int sfi_launch_floor(int32_t n_launches, int32_t grid, void* stream);
+
 /* run_selector on explicit device arrays (the reference-facing form,
  * selector.cpp:254-299): H heads, a W x n window per head over an arbitrary
  * ascending allowed list. logits fp64 [H][W][n], norms fp64 [H][n] (CacheStats

@@ -362,6 +362,7 @@ PYBIND11_MODULE(_sfi_b200, m) {
       .def("logits_slot", [](const DecodeExecutor& x, int l) { return reinterpret_cast<std::uintptr_t>(x.logits_slot(l)); })
       .def("launches_per_step", &DecodeExecutor::launches_per_step, py::arg("slow"));
 
+  m.def("launch_floor", [](int n, int grid, std::uintptr_t stream) { check(sfi_launch_floor(n, grid, vp(stream))); });
   m.def("version", &sfi_version);
   m.def("last_launch_count", &sfi_last_launch_count);
   m.def("buffer_sizes", [](const sfi_shape& s) {

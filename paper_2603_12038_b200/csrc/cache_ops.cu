@@ -511,4 +511,21 @@ cudaError_t launch_fill_synthetic(const sfi_shape& s, const sfi_cache& c, uint64
   return cudaGetLastError();
 }
 
+namespace {
+// The per-layer launch floor: an empty kernel with the fused fast step's PDL
+// protocol (wait for the predecessor, release the successor) and grid size.
+__global__ void floor_kernel(int) {
+  griddep_wait();
+  griddep_launch();
+}
+}  // namespace
+
+cudaError_t launch_floor(int n, int grid, cudaStream_t st) {
+  for (int i = 0; i < n; ++i) {
+    const cudaError_t e = launch_k(floor_kernel, dim3(grid), dim3(32), 0, st, i);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace sfi_impl

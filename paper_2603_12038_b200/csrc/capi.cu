@@ -1059,3 +1059,11 @@ SFI_API int sfi_seq_selector_nccl(const sfi_shape* s, const sfi_cache* c, int32_
   g_launches += launches;
   return rc;
 }
+
+SFI_API int sfi_launch_floor(int32_t n_launches, int32_t grid, void* stream) {
+  g_launches = 0;
+  if (n_launches < 0 || grid < 1) return fail(SFI_ERR_INVALID_ARGUMENT, "launch_floor: bad arguments");
+  SFI_CUDA(sfi_impl::launch_floor(n_launches, grid, (cudaStream_t)stream), "sfi_launch_floor");
+  g_launches = n_launches;
+  return SFI_OK;
+}

@@ -125,6 +125,7 @@ cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* l
                                      const sfi_selector_params& prm, double* sa, double* sb,
                                      int32_t* sel, int32_t* n_sel, uint32_t* err, cudaStream_t st,
                                      int* launches);
+cudaError_t launch_floor(int n, int grid, cudaStream_t st);
 cudaError_t launch_selector_stage(int stage, int H, int W, int n, const double* a, const double* b,
                                   const sfi_selector_params& prm, double* out, double* out2, int32_t* head_err,
                                   cudaStream_t st);
