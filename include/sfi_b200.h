@@ -176,6 +176,11 @@ SFI_API int sfi_dense_decode(const sfi_shape* shape, const sfi_cache* cache, int
  * layer's Selector in the asynchronous slow-step pipeline — run at the same
  * time on the rest. */
 #define SFI_DENSE_SHARE_SM 2
+/* Kernel choice for the dense decode (default: SFI_DENSE_TC env, else mma.sync):
+ * SFI_DENSE_TC = the tcgen05/TMEM kernel (D = 128, G in {4, 8, 16}),
+ * SFI_DENSE_MMA = the mma.sync kernel. */
+#define SFI_DENSE_TC 4
+#define SFI_DENSE_MMA 8
 SFI_API int sfi_dense_decode_ex(const sfi_shape* shape, const sfi_cache* cache, int32_t layer,
                                 const float* q, float* out, float* lse, float* pooled_logits,
                                 int32_t pool_mode, int32_t flags, void* stream);

@@ -411,6 +411,8 @@ PYBIND11_MODULE(_sfi_b200, m) {
                               static_cast<float*>(vp(lse)), static_cast<float*>(vp(logits)), pool, flags, vp(stream)));
   });
   m.attr("DENSE_SHARE_SM") = SFI_DENSE_SHARE_SM;
+  m.attr("DENSE_TC") = SFI_DENSE_TC;
+  m.attr("DENSE_MMA") = SFI_DENSE_MMA;
   m.def("fast_decode", [](const sfi_shape& s, const sfi_cache& c, int layer, std::uintptr_t q,
                           std::uintptr_t k, std::uintptr_t v, std::uintptr_t out, int flags,
                           std::uintptr_t stream) {

@@ -100,13 +100,13 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// 2D bf16 view [rows][D] with 64-column x 64-row boxes, 128-byte swizzle.
-int make_tmap(CUtensorMap* m, void* base, uint64_t rows, int D) {
+// 2D bf16 view [rows][D] with 64-column x box_rows boxes, 128-byte swizzle.
+int make_tmap(CUtensorMap* m, void* base, uint64_t rows, int D, uint32_t box_rows = 64) {
   EncodeFn fn = encode_fn();
   if (!fn) return fail(SFI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {(cuuint64_t)D, rows};
   const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t box[2] = {64, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -195,7 +195,30 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
              "trace");
     g_trace_ctas = ctas;
   }
-  SFI_CUDA(sfi_impl::launch_decode(p, tk, tv, D, group_of(*s), ctas, (cudaStream_t)stream),
+  // K1 on tcgen05: dense, D = 128, G in {4, 8, 16}; one CTA per SM
+  static const int env_tc = [] {
+    const char* e = std::getenv("SFI_DENSE_TC");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int G = group_of(*s);
+  const bool want_tc = (flags & SFI_DENSE_TC) ? true : (flags & SFI_DENSE_MMA) ? false : env_tc > 0;
+  if (!sparse && D == 128 && (G == 4 || G == 8 || G == 16) && want_tc) {
+    CUtensorMap tk2, tv2;
+    if ((rc = make_tmap(&tk2, c->k_cache, slices * rows_per, D, 128))) return rc;
+    if ((rc = make_tmap(&tv2, c->v_cache, slices * rows_per, D, 128))) return rc;
+    static const int env_tc_share = [] {
+      const char* e = std::getenv("SFI_DENSE_TC_SHARE_PERMILLE");
+      return e ? std::atoi(e) : 750;
+    }();
+    const int share_tc = (flags & SFI_DENSE_SHARE_SM) ? env_tc_share : 1000;
+    int tc_ctas = std::max(1, std::min(num_sms() * share_tc / 1000,
+                                       sfi_impl::decode_tc_tiles_upper(s->max_positions) * s->batch * s->n_kv_heads));
+    if (env_ctas > 0) tc_ctas = std::min(env_ctas, num_sms());
+    SFI_CUDA(sfi_impl::launch_decode_tc(p, tk2, tv2, G, tc_ctas, (cudaStream_t)stream), "sfi_dense_decode (tcgen05)");
+    g_launches = 1;
+    return SFI_OK;
+  }
+  SFI_CUDA(sfi_impl::launch_decode(p, tk, tv, D, G, ctas, (cudaStream_t)stream),
            sparse ? "sfi_sparse_decode" : "sfi_dense_decode");
   g_launches = 1;
   return SFI_OK;
@@ -619,7 +642,8 @@ SFI_API int sfi_seq_lengths(const sfi_shape* s, const sfi_cache* c, int32_t* g_p
 
 SFI_API int sfi_dense_decode_ex(const sfi_shape* s, const sfi_cache* c, int32_t layer, const float* q, float* out,
                                 float* lse, float* pooled_logits, int32_t pool_mode, int32_t flags, void* stream) {
-  if (flags & ~SFI_DENSE_SHARE_SM) return fail(SFI_ERR_INVALID_ARGUMENT, "dense_decode_ex: unknown flags");
+  if (flags & ~(SFI_DENSE_SHARE_SM | SFI_DENSE_TC | SFI_DENSE_MMA))
+    return fail(SFI_ERR_INVALID_ARGUMENT, "dense_decode_ex: unknown flags");
   return decode_common(s, c, layer, q, out, pooled_logits, pool_mode, false, stream, lse, flags);
 }
 

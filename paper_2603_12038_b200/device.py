@@ -160,13 +160,15 @@ class SfiCache:
                         self._stream(stream))
 
     def dense_decode_ex(self, layer: int, q: torch.Tensor, out: torch.Tensor, logits: torch.Tensor | None = None,
-                        pool: int = 0, share_sm: bool = False, lse: torch.Tensor | None = None, stream=None):
-        """dense_decode with options: share_sm = one CTA per SM (room for concurrent
-        kernels on another stream); lse = natural-log sum-exp per q head."""
+                        pool: int = 0, share_sm: bool = False, lse: torch.Tensor | None = None, stream=None,
+                        kernel: str | None = None):
+        """dense_decode with options: share_sm = leave SM slots to concurrent kernels on
+        another stream; lse = natural-log sum-exp per q head; kernel = "tc" (tcgen05 /
+        TMEM) or "mma" (mma.sync), default the SFI_DENSE_TC environment choice."""
+        flags = (_C.DENSE_SHARE_SM if share_sm else 0) | {None: 0, "tc": _C.DENSE_TC, "mma": _C.DENSE_MMA}[kernel]
         _C.dense_decode_ex(self.shape, self.cache, layer, self._ptr(q, torch.float32),
                            self._ptr(out, torch.float32), self._ptr(lse, torch.float32),
-                           self._ptr(logits, torch.float32), pool, _C.DENSE_SHARE_SM if share_sm else 0,
-                           self._stream(stream))
+                           self._ptr(logits, torch.float32), pool, flags, self._stream(stream))
 
     def sparse_decode(self, layer: int, q: torch.Tensor, out: torch.Tensor, stream=None):
         _C.sparse_decode(self.shape, self.cache, layer, self._ptr(q, torch.float32),
