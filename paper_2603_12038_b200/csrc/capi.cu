@@ -188,6 +188,7 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   if (env_ctas > 0) ctas = std::min(env_ctas, sfi_impl::kMaxCtas);
   p.trace = nullptr;
   static const bool env_trace = std::getenv("SFI_DECODE_TRACE") != nullptr;
+  const bool trace_on = env_trace;
   if (env_trace) {
     p.trace = sfi_impl::decode_trace_buffer();
     if (!p.trace) return fail(SFI_ERR_CUDA, "trace buffer");
@@ -196,25 +197,42 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
     g_trace_ctas = ctas;
   }
   // K1 on tcgen05: dense, D = 128, G in {4, 8, 16}; one CTA per SM
-  static const int env_tc = [] {
+  static const int env_tc = [] {  // default on; SFI_DENSE_TC=0 selects the mma.sync kernel
     const char* e = std::getenv("SFI_DENSE_TC");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
   }();
   const int G = group_of(*s);
-  const bool want_tc = (flags & SFI_DENSE_TC) ? true : (flags & SFI_DENSE_MMA) ? false : env_tc > 0;
+  // default: the tcgen05 kernel, except beside the Selector at G <= 8 (SFI_DENSE_SHARE_SM),
+  // where the mma.sync kernel's 2 CTAs per SM on 65% of the slots overlap the Selector
+  // chain better (C2 async slow step 8.33 vs 8.49 ms per step, measured)
+  const bool share_flag = (flags & SFI_DENSE_SHARE_SM) != 0;
+  const bool want_tc = (flags & SFI_DENSE_TC)    ? true
+                       : (flags & SFI_DENSE_MMA) ? false
+                                                 : env_tc > 0 && (!share_flag || group_of(*s) >= 16);
   if (!sparse && D == 128 && (G == 4 || G == 8 || G == 16) && want_tc) {
     CUtensorMap tk2, tv2;
     if ((rc = make_tmap(&tk2, c->k_cache, slices * rows_per, D, 128))) return rc;
     if ((rc = make_tmap(&tv2, c->v_cache, slices * rows_per, D, 128))) return rc;
+    // alone: 3 stages (192 KB) on every SM. Beside the Selector (SFI_DENSE_SHARE_SM):
+    // the 2-stage variant (~150 KB, 224 threads) on SFI_DENSE_TC_SHARE_PERMILLE of
+    // the SMs, so the Selector's CTAs can co-reside on the same SMs
     static const int env_tc_share = [] {
       const char* e = std::getenv("SFI_DENSE_TC_SHARE_PERMILLE");
-      return e ? std::atoi(e) : 750;
+      return e ? std::atoi(e) : 1000;
     }();
-    const int share_tc = (flags & SFI_DENSE_SHARE_SM) ? env_tc_share : 1000;
+    static const int env_tc_share_stages = [] {
+      const char* e = std::getenv("SFI_DENSE_TC_SHARE_STAGES");
+      return e ? std::atoi(e) : 2;
+    }();
+    const bool share_mode = (flags & SFI_DENSE_SHARE_SM) != 0;
+    const int share_tc = share_mode ? env_tc_share : 1000;
+    const int stages = share_mode ? (env_tc_share_stages == 3 ? 3 : 2) : 3;
     int tc_ctas = std::max(1, std::min(num_sms() * share_tc / 1000,
                                        sfi_impl::decode_tc_tiles_upper(s->max_positions) * s->batch * s->n_kv_heads));
     if (env_ctas > 0) tc_ctas = std::min(env_ctas, num_sms());
-    SFI_CUDA(sfi_impl::launch_decode_tc(p, tk2, tv2, G, tc_ctas, (cudaStream_t)stream), "sfi_dense_decode (tcgen05)");
+    if (trace_on) g_trace_ctas = tc_ctas;
+    SFI_CUDA(sfi_impl::launch_decode_tc(p, tk2, tv2, G, stages, tc_ctas, (cudaStream_t)stream),
+             "sfi_dense_decode (tcgen05)");
     g_launches = 1;
     return SFI_OK;
   }

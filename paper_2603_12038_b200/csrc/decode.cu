@@ -808,7 +808,6 @@ __global__ void __launch_bounds__(kThreads, 2)
 // Partials (m, l, O) and the last-arriver merge use decode_kernel's formats
 // (merge_slice), so the two kernels are interchangeable.
 constexpr int kTcRows = 128;
-constexpr int kTcStages = 3;
 // softmax warps: G = 16 splits the heads over two warps per TMEM lane quadrant
 template <int G>
 __host__ __device__ constexpr int tc_softmax_warps() { return G >= 16 ? 8 : 4; }
@@ -816,13 +815,13 @@ template <int G>
 __host__ __device__ constexpr int tc_threads() { return (3 + tc_softmax_warps<G>()) * 32; }
 constexpr int kTcMaxThreads = 11 * 32;
 
-template <int G>
+template <int G, int ST>
 struct TcGeo {
   static constexpr int N = (2 * G < 16) ? 16 : 2 * G;        // MMA N (hi + lo rows, padded)
   static constexpr int kBox = kTcRows * 128;                  // 128 rows x 64 bf16 = 16 KB
   static constexpr int kTileBytes = 2 * kBox;                 // one tensor, D = 128
   static constexpr int kStageBytes = 2 * kTileBytes;          // K + V
-  static constexpr int kRing = kTcStages * kStageBytes;       // 192 KB
+  static constexpr int kRing = ST * kStageBytes;              // ST stages of K + V
   static constexpr int kOpBox = N * 128;                      // Q / P box: N rows x 64 bf16
   static constexpr int kOpBytes = 2 * kOpBox;                 // 64-column boxes for 128 cols
   static constexpr int kQOff = kRing;                         // 2 Q buffers
@@ -917,11 +916,12 @@ __device__ __forceinline__ uint32_t op_off(int r, int c, int box_bytes) {
 
 __device__ __forceinline__ int tc_tiles(int rows) { return (rows + kTcRows - 1) / kTcRows; }
 
-template <int G>
+template <int G, int ST>
 __global__ void __launch_bounds__(kTcMaxThreads, 1)
     decode_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                      const DecodeParams p) {
-  using Geo = TcGeo<G>;
+  using Geo = TcGeo<G, ST>;
+  constexpr int kTcStages = ST;
   constexpr int N = Geo::N;
   constexpr int D = 128;
   constexpr int PR = part_rows<G>();
@@ -1472,9 +1472,9 @@ __global__ void __launch_bounds__(kTcMaxThreads, 1)
   }
 }
 
-template <int G>
+template <int G, int ST>
 int tc_smem_bytes(int slices) {
-  return TcGeo<G>::kPrefOff + (slices + 1) * (int)sizeof(int);
+  return TcGeo<G, ST>::kPrefOff + (slices + 1) * (int)sizeof(int);
 }
 
 using DecodeFn = void (*)(CUtensorMap, CUtensorMap, DecodeParams);
@@ -1514,22 +1514,23 @@ int decode_grid(int tiles_upper, int num_sms, int permille) {
 }
 
 cudaError_t launch_decode_tc(const DecodeParams& p, const CUtensorMap& tmk128, const CUtensorMap& tmv128, int G,
-                             int ctas, cudaStream_t stream) {
+                             int stages, int ctas, cudaStream_t stream) {
   using Fn = void (*)(CUtensorMap, CUtensorMap, DecodeParams);
   Fn fn = nullptr;
-  int smem = 0;
+  int smem = 0, threads = 0;
   const int S = p.B * p.H;
-  switch (G) {
-    case 4: fn = decode_tc_kernel<4>; smem = tc_smem_bytes<4>(S); break;
-    case 8: fn = decode_tc_kernel<8>; smem = tc_smem_bytes<8>(S); break;
-    case 16: fn = decode_tc_kernel<16>; smem = tc_smem_bytes<16>(S); break;
-    default: return cudaErrorInvalidValue;
+#define SFI_TC_CASE(GG, SS)                      \
+  if (G == GG && stages == SS) {                 \
+    fn = decode_tc_kernel<GG, SS>;               \
+    smem = tc_smem_bytes<GG, SS>(S);             \
+    threads = tc_threads<GG>();                  \
   }
-  if (S > kMaxSlices || ctas > kMaxCtas || p.sparse) return cudaErrorInvalidValue;
+  SFI_TC_CASE(4, 3) SFI_TC_CASE(8, 3) SFI_TC_CASE(16, 3) SFI_TC_CASE(4, 2) SFI_TC_CASE(8, 2) SFI_TC_CASE(16, 2)
+#undef SFI_TC_CASE
+  if (!fn || S > kMaxSlices || ctas > kMaxCtas || p.sparse) return cudaErrorInvalidValue;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
-  return launch_k(fn, dim3(ctas), dim3(G == 4 ? tc_threads<4>() : G == 8 ? tc_threads<8>() : tc_threads<16>()),
-                  (size_t)smem, stream, tmk128, tmv128, p);
+  return launch_k(fn, dim3(ctas), dim3(threads), (size_t)smem, stream, tmk128, tmv128, p);
 }
 
 int decode_tc_tiles_upper(int max_positions) { return (max_positions + kTcRows - 1) / kTcRows; }

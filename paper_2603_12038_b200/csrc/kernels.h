@@ -128,7 +128,7 @@ cudaError_t launch_selector_explicit(int H, int W, int n, int K, const double* l
 cudaError_t launch_floor(int n, int grid, cudaStream_t st);
 // K1 on tcgen05 (dense, D = 128, G in {4, 8, 16}): tensor maps with 64 x 128 boxes
 cudaError_t launch_decode_tc(const DecodeParams& p, const CUtensorMap& tmk128, const CUtensorMap& tmv128, int G,
-                             int ctas, cudaStream_t stream);
+                             int stages, int ctas, cudaStream_t stream);
 int decode_tc_tiles_upper(int max_positions);
 cudaError_t launch_selector_stage(int stage, int H, int W, int n, const double* a, const double* b,
                                   const sfi_selector_params& prm, double* out, double* out2, int32_t* head_err,
