@@ -363,6 +363,15 @@ long long* decode_trace_buffer() {
 // rows of one stream-K partial: 8, or 16 for GQA group 16 (decode.cu part_rows)
 static size_t part_rows(const sfi_shape& s) { return group_of(s) > 8 ? 16 : 8; }
 
+// long-row top-k buffers (selector.cu sel_bt_*), only when |J| can exceed the
+// single-CTA top-k: [rows][65536] bin counts, [rows][max_positions] listed
+// indices, [rows][8] row state, [rows][64][2] segment counts / offsets
+size_t bt_bytes(const sfi_shape& s) {
+  if (s.max_positions <= kTopkCtaMaxPositions) return 0;
+  const size_t rows = (size_t)s.batch * s.n_kv_heads;
+  return rows * (65536 * 4 + (size_t)s.max_positions * 4 + 8 * 4 + 64 * 2 * 4);
+}
+
 size_t workspace_bytes(const sfi_shape& s) {
   const size_t slices = (size_t)s.batch * s.n_kv_heads;
   size_t b = 0;
@@ -373,6 +382,7 @@ size_t workspace_bytes(const sfi_shape& s) {
   // two-pass decode Selector: [rows][chunks][6] statistics + [rows][chunks + 2] coefficients
   b += align_up(slices * (size_t)(7 * ((s.max_positions + 511) / 512) + 2) * sizeof(double));
   b += align_up((size_t)s.n_layers * slices * 2 * sizeof(int32_t));  // fast-decode tile-claim counters
+  b += align_up(bt_bytes(s));                                          // long-row top-k (C3 / C4)
   return b;
 }
 
@@ -395,6 +405,8 @@ Workspace carve_workspace(const sfi_shape& s, void* base) {
   w.sel.stats = reinterpret_cast<double*>(p);
   p += align_up(slices * (size_t)(7 * ((s.max_positions + 511) / 512) + 2) * sizeof(double));
   w.steal = reinterpret_cast<int32_t*>(p);
+  p += align_up((size_t)s.n_layers * slices * 2 * sizeof(int32_t));
+  w.sel.bt = bt_bytes(s) ? p : nullptr;
   return w;
 }
 

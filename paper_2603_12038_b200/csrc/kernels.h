@@ -112,7 +112,9 @@ struct SelectorScratch {
   double* b;      // [B*H][Lmax]  w -> r -> z_adj
   double* c;      // [B*H][Lmax]  prior weights w (two-pass decode Selector)
   double* stats;  // [B*H][ceil(Lmax / 512)][6] chunk statistics, then [B*H][chunks + 2] coefficients
+  void* bt = nullptr;  // long-row top-k buffers (null when Lmax <= kTopkCtaMaxPositions)
 };
+constexpr int kTopkCtaMaxPositions = 48 * 1024;  // rows up to this length: the single-CTA top-k
 // phases: 1 = fuse (z_base into scr.a), 2 = refine + top-k; z_all != null:
 // head-sharded finish over the all-gathered z_base of n_shards shards
 cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, const float* logits,

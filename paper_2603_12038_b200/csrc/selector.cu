@@ -111,6 +111,9 @@ struct SelParams {
   double* edges;            // [rows][2R+2] (phase 3 out): first R, last R z_base values, j_off, n
   const double* edges_all;  // [n_shards][rows][2R+2] all-gathered edges (refine halo)
   int n_shards;
+  // long-row top-k: sel_z adds every z_adj to a per-row value histogram
+  uint32_t* bt_hist;        // [rows][kBtBins] or null
+  double bt_zlo, bt_scale;  // bin = clamp((z - zlo) * scale)
 };
 
 // Row geometry: n = |J|, j_min, position of index j, u(j).
@@ -542,6 +545,13 @@ __device__ __forceinline__ double halo(const SelParams& p, int row, int g, int R
 
 // refine_cross_head (selector.cpp:204-230) at one position over the Hr heads in
 // head order, then z_adj of this shard's heads -> sb
+constexpr int kBtBins = 65536;
+// monotonic (non-decreasing) value -> bin map of z_adj: equal z, equal bin
+__device__ __forceinline__ int bt_bin(double z, double zlo, double scale) {
+  const double t = (z - zlo) * scale;
+  return t <= 0.0 ? 0 : (t >= (double)(kBtBins - 1) ? kBtBins - 1 : (int)t);
+}
+
 template <int kH>
 __device__ __forceinline__ void cross_head_store(const SelParams& p, int b, int idx, const double (&zn)[kH],
                                                  int Hr) {
@@ -567,7 +577,10 @@ __device__ __forceinline__ void cross_head_store(const SelParams& p, int b, int 
   for (int h = 0; h < kH; ++h)
     if (h < Hr && h >= p.h_off && h < p.h_off + p.H) {  // this shard's heads only
       const double lr = (e[h] >= floor_e) ? (x[h] - ls) : le;
-      p.sb[(size_t)(b * p.H + h - p.h_off) * p.ld + idx] = zn[h] + p.alpha_cross * lr;
+      const double z = zn[h] + p.alpha_cross * lr;
+      const size_t row = (size_t)(b * p.H + h - p.h_off);
+      p.sb[row * p.ld + idx] = z;
+      if (p.bt_hist) atomicAdd(&p.bt_hist[row * kBtBins + bt_bin(z, p.bt_zlo, p.bt_scale)], 1u);
     }
 }
 
@@ -1154,7 +1167,7 @@ __global__ void __launch_bounds__(kT)
 // and the full 64-bit key is read back only for elements that tie with the
 // threshold on the high word. Same output contract as sel_topk_kernel.
 constexpr int kTopkCtaT = 1024;
-constexpr int kTopkCtaMax = 48 * 1024;
+constexpr int kTopkCtaMax = kTopkCtaMaxPositions;
 
 template <bool kExp>
 __global__ void __launch_bounds__(kTopkCtaT) sel_topk_cta_kernel(const SelParams p) {
@@ -1485,6 +1498,330 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
 }
 
 // ---------------------------------------------------------------------------
+// Top-k of long rows (|J| > kTopkCtaMax: C3 131K, C4 262K), rows x segments
+// wide instead of one 8-CTA cluster per row. sel_z has added every z_adj to a
+// per-row histogram of kBtBins value bins over [zlo, zhi], the bounds z_adj
+// can take (z_base in [log eps, log(1 + eps)], lowered by at most
+// (alpha_soft + alpha_cross) |log eps|); the bin map is monotonic, so
+//   sel_bt_thresh  (row)           the bin b* holding the K-th largest key; keys in
+//                                  higher bins are selected (histogram zeroed after)
+//   sel_bt_scan    (segment, row)  per segment: count of keys above b*; keys in b* listed
+//   sel_bt_pick    (row)           the exact threshold (key, index) among the listed keys
+//                                  (bitonic sort in shared memory, radix select beyond)
+//                                  and each segment's output offset
+//   sel_bt_emit    (segment, row)  the selected positions, ascending
+// Same output contract as sel_topk_kernel (score desc, position asc; ties by position).
+constexpr int kBtSmemCand = 2048;
+constexpr int kBtMaxSeg = 64;
+
+struct BtBuf {
+  uint32_t* hist;  // [rows][kBtBins]
+  int32_t* cand;   // [rows][Lmax] listed indices
+  int32_t* meta;   // [rows][8]: b*, above, need, listed, Tk hi, Tk lo, Ti, mode (1: n <= K / empty)
+  int32_t* seg;    // [rows][kBtMaxSeg][2]: count above b*, output offset
+  int P;           // segments per row
+};
+
+__host__ __device__ __forceinline__ int bt_seg_start(int s, int n, int P) { return (int)(((long long)s * n) / P); }
+
+template <int kT, typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* wsum, T& total) {
+  constexpr int kW = kT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < kW ? wsum[lane] : T(0);
+    T wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kW) wsum[lane] = wi - w;
+    if (lane == kW - 1) wsum[kW] = wi;
+  }
+  __syncthreads();
+  total = wsum[kW];
+  const T r = wsum[warp] + inc - v;
+  __syncthreads();
+  return r;
+}
+
+constexpr int kBtT = 1024;
+
+__global__ void __launch_bounds__(kBtT) sel_bt_thresh_kernel(const SelParams p, const BtBuf bt) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ uint32_t wsum[33];
+  const int row = blockIdx.x;
+  const Src<false> src(p, row / p.H);
+  const int n = src.n, K = p.K;
+  int32_t* m = bt.meta + (size_t)row * 8;
+  uint32_t* h = bt.hist + (size_t)row * kBtBins;
+  constexpr int kPer = kBtBins / kBtT;  // 64 bins per thread, descending across threads
+  const int hi_bin = kBtBins - kPer * threadIdx.x;  // bins [hi_bin - kPer, hi_bin)
+  uint32_t cnt = 0;
+  if (n > K && K > 0)
+    for (int k = 1; k <= kPer; ++k) cnt += h[hi_bin - k];
+  uint32_t total;
+  const uint32_t before = block_excl_scan<kBtT>(cnt, wsum, total);
+  if (n > K && K > 0 && before < (uint32_t)K && before + cnt >= (uint32_t)K) {
+    uint32_t c = before;
+    for (int k = 1; k <= kPer; ++k) {
+      const uint32_t v = h[hi_bin - k];
+      if (c + v >= (uint32_t)K) {
+        m[0] = hi_bin - k;
+        m[1] = (int32_t)c;
+        m[2] = K - (int32_t)c;
+        break;
+      }
+      c += v;
+    }
+  }
+  if (threadIdx.x == 0) {
+    m[3] = 0;
+    m[7] = (n > K && K > 0) ? 0 : 1;
+  }
+  __syncthreads();
+  for (int k = 1; k <= kPer; ++k) h[hi_bin - k] = 0u;  // zero at rest for the next call
+}
+
+constexpr int kBtScanT = 256;
+
+__global__ void __launch_bounds__(kBtScanT) sel_bt_scan_kernel(const SelParams p, const BtBuf bt) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ uint32_t wsum[33];
+  const int seg = blockIdx.x, row = blockIdx.y;
+  int32_t* m = bt.meta + (size_t)row * 8;
+  if (m[7]) return;
+  const Src<false> src(p, row / p.H);
+  const int n = src.n;
+  const int s0 = bt_seg_start(seg, n, bt.P), s1 = bt_seg_start(seg + 1, n, bt.P);
+  const int bstar = m[0];
+  const double* z = p.sb + (size_t)row * p.ld;
+  int32_t* cand = bt.cand + (size_t)row * p.Lmax;
+  uint32_t cnt = 0;
+  for (int i0 = s0 + threadIdx.x; i0 < s1; i0 += 4 * kBtScanT) {
+    double zv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) zv[u] = (i0 + u * kBtScanT < s1) ? z[i0 + u * kBtScanT] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * kBtScanT;
+      if (i >= s1) break;
+      const int bn = bt_bin(zv[u], p.bt_zlo, p.bt_scale);
+      if (bn > bstar) ++cnt;
+      else if (bn == bstar) cand[atomicAdd(&m[3], 1)] = i;
+    }
+  }
+  uint32_t total;
+  block_excl_scan<kBtScanT>(cnt, wsum, total);
+  if (threadIdx.x == 0) bt.seg[((size_t)row * kBtMaxSeg + seg) * 2] = (int32_t)total;
+}
+
+// (key desc, index asc) ordering of listed elements
+__device__ __forceinline__ bool bt_before(unsigned long long ka, int ia, unsigned long long kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, const BtBuf bt) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ unsigned long long sk[kBtSmemCand];
+  __shared__ int si[kBtSmemCand];
+  __shared__ uint32_t hist[256];
+  __shared__ int segcnt[kBtMaxSeg];
+  __shared__ unsigned long long s_tk;
+  __shared__ int s_ti, s_gt;
+  const int row = blockIdx.x;
+  int32_t* m = bt.meta + (size_t)row * 8;
+  if (m[7]) return;
+  const Src<false> src(p, row / p.H);
+  const int n = src.n;
+  const int listed = m[3], need = m[2];
+  const double* z = p.sb + (size_t)row * p.ld;
+  const int32_t* cand = bt.cand + (size_t)row * p.Lmax;
+  if (threadIdx.x < kBtMaxSeg) segcnt[threadIdx.x] = 0;
+  if (listed <= kBtSmemCand) {
+    // bitonic sort of the listed (key, index) pairs, padded to a power of two
+    int np2 = 1;
+    while (np2 < listed) np2 <<= 1;
+    for (int i = threadIdx.x; i < np2; i += kBtT) {
+      if (i < listed) {
+        sk[i] = okey(z[cand[i]]);
+        si[i] = cand[i];
+      } else {
+        sk[i] = 0ull;
+        si[i] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= np2; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < np2; i += kBtT) {
+          const int ij = i ^ j;
+          if (ij > i) {
+            const bool up = (i & k) == 0;  // this run sorted "before" first
+            const bool swap = up ? bt_before(sk[ij], si[ij], sk[i], si[i]) : bt_before(sk[i], si[i], sk[ij], si[ij]);
+            if (swap) {
+              const unsigned long long tk = sk[i];
+              sk[i] = sk[ij];
+              sk[ij] = tk;
+              const int ti = si[i];
+              si[i] = si[ij];
+              si[ij] = ti;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    if (threadIdx.x == 0) {
+      s_tk = sk[need - 1];
+      s_ti = si[need - 1];
+    }
+  } else {
+    // radix select over the listed keys in global memory: the need-th largest key
+    // Tk (8-bit digits), then the (need - #(> Tk))-th smallest index among key == Tk
+    unsigned long long prefix = 0ull, pmask = 0ull;
+    int rem = need;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += kBtT) hist[i] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < listed; i += kBtT) {
+        const unsigned long long k = okey(z[cand[i]]);
+        if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int c = 0, d = 255;
+        for (; d > 0; --d) {
+          if (c + (int)hist[d] >= rem) break;
+          c += (int)hist[d];
+        }
+        s_gt = c;
+        s_tk = (unsigned long long)d;
+      }
+      __syncthreads();
+      rem -= s_gt;
+      prefix |= s_tk << shift;
+      pmask |= 255ull << shift;
+      __syncthreads();
+    }
+    // index among the rem-th smallest with key == prefix
+    uint32_t iprefix = 0u, imask = 0u;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += kBtT) hist[i] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < listed; i += kBtT) {
+        const int ix = cand[i];
+        if (okey(z[ix]) == prefix && ((uint32_t)ix & imask) == iprefix) atomicAdd(&hist[((uint32_t)ix >> shift) & 255], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int c = 0, d = 0;
+        for (; d < 255; ++d) {
+          if (c + (int)hist[d] >= rem) break;
+          c += (int)hist[d];
+        }
+        s_gt = c;
+        s_ti = d;
+      }
+      __syncthreads();
+      rem -= s_gt;
+      iprefix |= (uint32_t)s_ti << shift;
+      imask |= 255u << shift;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      s_tk = prefix;
+      s_ti = (int)iprefix;
+    }
+  }
+  __syncthreads();
+  const unsigned long long Tk = s_tk;
+  const int Ti = s_ti;
+  // selected listed elements per segment
+  for (int i = threadIdx.x; i < listed; i += kBtT) {
+    const int ix = cand[i];
+    const unsigned long long k = okey(z[ix]);
+    if (!bt_before(Tk, Ti, k, ix)) {  // (k, ix) at or before the threshold element
+      int sgi = (int)(((long long)ix * bt.P) / n);
+      while (sgi + 1 < bt.P && bt_seg_start(sgi + 1, n, bt.P) <= ix) ++sgi;
+      while (sgi > 0 && bt_seg_start(sgi, n, bt.P) > ix) --sgi;
+      atomicAdd(&segcnt[sgi], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int sg = 0; sg < bt.P; ++sg) {
+      int32_t* e = bt.seg + ((size_t)row * kBtMaxSeg + sg) * 2;
+      const int c = e[0] + segcnt[sg];
+      e[1] = off;
+      off += c;
+    }
+    m[4] = (int32_t)(Tk >> 32);
+    m[5] = (int32_t)(Tk & 0xffffffffull);
+    m[6] = Ti;
+  }
+}
+
+__global__ void __launch_bounds__(kBtScanT) sel_bt_emit_kernel(const SelParams p, const BtBuf bt) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ uint32_t wsum[33];
+  const int seg = blockIdx.x, row = blockIdx.y;
+  const int32_t* m = bt.meta + (size_t)row * 8;
+  const Src<false> src(p, row / p.H);
+  const int n = src.n, K = p.K;
+  int32_t* out = p.sel + (size_t)row * K;
+  const int s0 = bt_seg_start(seg, n, bt.P), s1 = bt_seg_start(seg + 1, n, bt.P);
+  if (m[7]) {  // empty J, K = 0, or |J| <= K: all of J (selector.cpp:238-239)
+    if (n > 0 && K > 0)
+      for (int i = s0 + threadIdx.x; i < s1; i += kBtScanT) out[i] = src.pos(i);
+    if (seg == 0 && threadIdx.x == 0) p.n_sel[row] = (n > 0 && K > 0) ? n : 0;
+    return;
+  }
+  const int bstar = m[0];
+  const unsigned long long Tk = ((unsigned long long)(uint32_t)m[4] << 32) | (uint32_t)m[5];
+  const int Ti = m[6];
+  const double* z = p.sb + (size_t)row * p.ld;
+  const int len = s1 - s0;
+  const int E = (len + kBtScanT - 1) / kBtScanT;
+  const int e0 = s0 + threadIdx.x * E, e1 = min(s1, e0 + E);
+  auto sel = [&](int i) {
+    const double zi = z[i];
+    const int bn = bt_bin(zi, p.bt_zlo, p.bt_scale);
+    if (bn != bstar) return bn > bstar;
+    return !bt_before(Tk, Ti, okey(zi), i);
+  };
+  uint32_t cnt = 0;
+  for (int i = e0; i < e1; ++i) cnt += sel(i) ? 1u : 0u;
+  uint32_t total;
+  const uint32_t before = block_excl_scan<kBtScanT>(cnt, wsum, total);
+  int o = bt.seg[((size_t)row * kBtMaxSeg + seg) * 2 + 1] + (int)before;
+  for (int i = e0; i < e1; ++i)
+    if (sel(i)) out[o++] = src.pos(i);
+  if (seg == 0 && threadIdx.x == 0) p.n_sel[row] = K;
+}
+
+cudaError_t launch_bt_topk(const SelParams& p, const BtBuf& bt, int rows, cudaStream_t st) {
+  cudaError_t e = launch_k(sel_bt_thresh_kernel, dim3(rows), dim3(kBtT), 0, st, p, bt);
+  if (e == cudaSuccess) e = launch_k(sel_bt_scan_kernel, dim3(bt.P, rows), dim3(kBtScanT), 0, st, p, bt);
+  if (e == cudaSuccess) e = launch_k(sel_bt_pick_kernel, dim3(rows), dim3(kBtT), 0, st, p, bt);
+  if (e == cudaSuccess) e = launch_k(sel_bt_emit_kernel, dim3(bt.P, rows), dim3(kBtScanT), 0, st, p, bt);
+  return e;
+}
+
+// ---------------------------------------------------------------------------
 // Sequence sharding (C4): candidates of the local top-k, then the global pick.
 
 // (z_adj score, global position) of this shard's local top-k; -inf / 0 pads
@@ -1644,6 +1981,26 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
     cudaError_t e;
     const bool small_pw = (size_t)ldc * s.batch * ((s.n_kv_heads + kPwHeads - 1) / kPwHeads) < 128;
     const bool def_exp = p.gamma == 1.0 && p.p_curve == 2.0 && p.eta == 0.5;
+    // long rows: the rows x segments top-k over sel_z's value histogram
+    static const bool force_cluster = std::getenv("SFI_TOPK_CLUSTER") != nullptr;
+    const bool use_bt = scr.bt != nullptr && s.max_positions > kTopkCtaMax && !force_cluster &&
+                        p.alpha_soft >= 0.0 && p.alpha_cross >= 0.0;
+    BtBuf bt{};
+    if (use_bt) {
+      uint8_t* w = static_cast<uint8_t*>(scr.bt);
+      bt.hist = reinterpret_cast<uint32_t*>(w);
+      w += slices * kBtBins * 4;
+      bt.cand = reinterpret_cast<int32_t*>(w);
+      w += slices * (size_t)s.max_positions * 4;
+      bt.meta = reinterpret_cast<int32_t*>(w);
+      w += slices * 8 * 4;
+      bt.seg = reinterpret_cast<int32_t*>(w);
+      bt.P = (int)std::max<size_t>(1, std::min<size_t>(kBtMaxSeg, (296 + slices - 1) / slices));
+      p.bt_hist = bt.hist;
+      // z_adj in [log(eps) (1 + alpha_soft + alpha_cross), log(1 + eps)] (margins of 1)
+      p.bt_zlo = std::log(p.eps) * (1.0 + p.alpha_soft + p.alpha_cross) - 1.0;
+      p.bt_scale = (double)(kBtBins - 1) / (std::log1p(p.eps) + 1.0 - p.bt_zlo);
+    }
 #define SFI_SEL2(KH)                                                                             \
   e = small_pw ? (def_exp ? launch_k(sel_pw_kernel<KH, 1, true>, dim3(ldc, s.batch, KH == 16 ? s.n_kv_heads : KH), \
                                      ba, 0, st, p, P, Wt, stt, ldc)                                  \
@@ -1668,6 +2025,10 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
 #undef SFI_SEL2
     if (e != cudaSuccess) return e;
     if (launches) *launches += 3;
+    if (use_bt) {
+      if (launches) *launches += 3;  // 4 kernels instead of one
+      return launch_bt_topk(p, bt, (int)slices, st);
+    }
     return launch_topk<false>(p, (int)slices, s.max_positions, st);
   }
   return run3<false>(p, (int)slices, s.max_positions, s.batch, st, launches, phases);

@@ -257,3 +257,39 @@ def test_forced_cluster_topk(force):
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "ok" in r.stdout
+
+
+@pytest.mark.parametrize("refine", [False, True])
+def test_long_row_topk_exact_ties(refine):
+    """The long-row top-k (|J| > 48K: value histogram + listed threshold bin, rows x
+    segments) with massive exact ties straddling the K-th place (quantized logits
+    repeated in every chunk, lambda_clip = 0): indices equal the reference's."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2603_12038_b200 import SelectorConfig, SelectorParams, SfiCache
+
+    B, H, Hq, ctx, ns, K, R = 1, 4, 8, 60000, 4, 2048, 64
+    c = SfiCache(1, B, H, Hq, 128, ctx + 8, ns, K, R)
+    c.fill_synthetic(seed=6, length=ctx)
+    c.set_lengths([ctx], [ns])
+    rng = np.random.default_rng(9)
+    base = np.round(rng.normal(0, 1, size=(H, 512)) * 2) / 2
+    lg = np.tile(base, (1, (ctx + 8 + 511) // 512))[:, :ctx + 8]
+    logits = torch.from_numpy(np.broadcast_to(lg, (B, H, ctx + 8)).astype(np.float32).copy()).cuda()
+    cfg = SelectorConfig()
+    cfg.k_budget = K
+    kw = dict(lambda_clip=0.0) if refine else dict(lambda_clip=0.0, alpha_soft=0.0, alpha_cross=0.0)
+    for k_, v_ in kw.items():
+        setattr(cfg, k_, v_)
+    c.selector(0, logits, SelectorParams(cfg))
+    torch.cuda.synchronize()
+    c.check_errors()
+    L, rl = int(c.prefix_len[0]), int(c.recent_len[0])
+    j0, j1 = ns + 1, L - rl
+    vals = logits[0, :, :j1 - j0 + 1].double().cpu().numpy()
+    norms = c.key_norms[0, 0, :, j0 - 1:j1].cpu().numpy()
+    want, _ = oracle().run_selector(vals, np.arange(j0, j1 + 1), norms, O.make_cfg(k_budget=K, **kw))
+    for h in range(H):
+        got = c.sel[0, 0, h, :int(c.n_sel[0, 0, h])].cpu().numpy()
+        assert np.array_equal(got, want[h]), h
