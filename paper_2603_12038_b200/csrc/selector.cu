@@ -580,7 +580,12 @@ __device__ __forceinline__ void cross_head_store(const SelParams& p, int b, int 
       const double z = zn[h] + p.alpha_cross * lr;
       const size_t row = (size_t)(b * p.H + h - p.h_off);
       p.sb[row * p.ld + idx] = z;
-      if (p.bt_hist) atomicAdd(&p.bt_hist[row * kBtBins + bt_bin(z, p.bt_zlo, p.bt_scale)], 1u);
+      if (p.bt_hist) {  // warp-aggregated: lanes with the same bin add once
+        const int bn = bt_bin(z, p.bt_zlo, p.bt_scale);
+        const unsigned act = __activemask();
+        const unsigned same = __match_any_sync(act, bn);
+        if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&p.bt_hist[row * kBtBins + bn], (uint32_t)__popc(same));
+      }
     }
 }
 
@@ -1559,38 +1564,71 @@ constexpr int kBtT = 1024;
 __global__ void __launch_bounds__(kBtT) sel_bt_thresh_kernel(const SelParams p, const BtBuf bt) {
   griddep_wait();
   griddep_launch();
+  // 1024 chunks of 64 bins, chunk c = bins [kBtBins - 64 (c + 1), kBtBins - 64 c) (descending);
+  // warp w sums chunks 32 w .. 32 w + 31 with coalesced 256-byte reads
+  __shared__ uint32_t csum[kBtT];
   __shared__ uint32_t wsum[33];
+  __shared__ int s_c;
+  __shared__ uint32_t s_before;
   const int row = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Src<false> src(p, row / p.H);
   const int n = src.n, K = p.K;
   int32_t* m = bt.meta + (size_t)row * 8;
   uint32_t* h = bt.hist + (size_t)row * kBtBins;
-  constexpr int kPer = kBtBins / kBtT;  // 64 bins per thread, descending across threads
-  const int hi_bin = kBtBins - kPer * threadIdx.x;  // bins [hi_bin - kPer, hi_bin)
-  uint32_t cnt = 0;
-  if (n > K && K > 0)
-    for (int k = 1; k <= kPer; ++k) cnt += h[hi_bin - k];
+  const bool active = n > K && K > 0;
+  if (active) {
+    uint2 v[32];  // all 32 loads in flight before any reduction
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = __ldcg(reinterpret_cast<const uint2*>(h + kBtBins - 64 * (warp * 32 + k + 1)) + lane);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      uint32_t x = v[k].x + v[k].y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == k) csum[warp * 32 + k] = x;
+    }
+  } else {
+    csum[threadIdx.x] = 0u;
+  }
+  __syncthreads();
+  const uint32_t mine = csum[threadIdx.x];
   uint32_t total;
-  const uint32_t before = block_excl_scan<kBtT>(cnt, wsum, total);
-  if (n > K && K > 0 && before < (uint32_t)K && before + cnt >= (uint32_t)K) {
-    uint32_t c = before;
-    for (int k = 1; k <= kPer; ++k) {
-      const uint32_t v = h[hi_bin - k];
-      if (c + v >= (uint32_t)K) {
-        m[0] = hi_bin - k;
-        m[1] = (int32_t)c;
-        m[2] = K - (int32_t)c;
-        break;
-      }
-      c += v;
+  const uint32_t before = block_excl_scan<kBtT>(mine, wsum, total);
+  if (active && before < (uint32_t)K && before + mine >= (uint32_t)K) {
+    s_c = threadIdx.x;
+    s_before = before;
+  }
+  __syncthreads();
+  if (active && warp == 0) {  // the 64 bins of chunk s_c, descending: lane pairs, warp prefix
+    const int c = s_c;
+    const int top = kBtBins - 64 * c;  // bins [top - 64, top)
+    const uint32_t v1 = h[top - 1 - 2 * lane], v2 = h[top - 2 - 2 * lane];
+    uint32_t inc = v1 + v2;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t ex = s_before + inc - v1 - v2;  // keys in bins above this lane's pair
+    const bool hit1 = ex < (uint32_t)K && ex + v1 >= (uint32_t)K;
+    const bool hit2 = !hit1 && ex + v1 < (uint32_t)K && ex + v1 + v2 >= (uint32_t)K;
+    if (hit1) {
+      m[0] = top - 1 - 2 * lane;
+      m[1] = (int32_t)ex;
+      m[2] = K - (int32_t)ex;
+    } else if (hit2) {
+      m[0] = top - 2 - 2 * lane;
+      m[1] = (int32_t)(ex + v1);
+      m[2] = K - (int32_t)(ex + v1);
     }
   }
   if (threadIdx.x == 0) {
     m[3] = 0;
-    m[7] = (n > K && K > 0) ? 0 : 1;
+    m[7] = active ? 0 : 1;
   }
   __syncthreads();
-  for (int k = 1; k <= kPer; ++k) h[hi_bin - k] = 0u;  // zero at rest for the next call
+  for (int i = threadIdx.x; i < kBtBins / 4; i += kBtT) reinterpret_cast<uint4*>(h)[i] = make_uint4(0, 0, 0, 0);
 }
 
 constexpr int kBtScanT = 256;
@@ -1774,11 +1812,15 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
   }
 }
 
+constexpr int kBtEmitTiles = 32;  // 256-key tiles per segment held in registers (flags)
+
 __global__ void __launch_bounds__(kBtScanT) sel_bt_emit_kernel(const SelParams p, const BtBuf bt) {
   griddep_wait();
   griddep_launch();
-  __shared__ uint32_t wsum[33];
+  constexpr int kW = kBtScanT / 32;
+  __shared__ int wcnt[kBtEmitTiles * kW + 1];
   const int seg = blockIdx.x, row = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* m = bt.meta + (size_t)row * 8;
   const Src<false> src(p, row / p.H);
   const int n = src.n, K = p.K;
@@ -1794,22 +1836,57 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_emit_kernel(const SelParams p
   const unsigned long long Tk = ((unsigned long long)(uint32_t)m[4] << 32) | (uint32_t)m[5];
   const int Ti = m[6];
   const double* z = p.sb + (size_t)row * p.ld;
-  const int len = s1 - s0;
-  const int E = (len + kBtScanT - 1) / kBtScanT;
-  const int e0 = s0 + threadIdx.x * E, e1 = min(s1, e0 + E);
-  auto sel = [&](int i) {
-    const double zi = z[i];
-    const int bn = bt_bin(zi, p.bt_zlo, p.bt_scale);
-    if (bn != bstar) return bn > bstar;
-    return !bt_before(Tk, Ti, okey(zi), i);
-  };
-  uint32_t cnt = 0;
-  for (int i = e0; i < e1; ++i) cnt += sel(i) ? 1u : 0u;
-  uint32_t total;
-  const uint32_t before = block_excl_scan<kBtScanT>(cnt, wsum, total);
-  int o = bt.seg[((size_t)row * kBtMaxSeg + seg) * 2 + 1] + (int)before;
-  for (int i = e0; i < e1; ++i)
-    if (sel(i)) out[o++] = src.pos(i);
+  int o_base = bt.seg[((size_t)row * kBtMaxSeg + seg) * 2 + 1];
+  // rounds of up to kBtEmitTiles tiles: flags in a register bitmask, counts per (tile, warp)
+  for (int r0 = s0; r0 < s1; r0 += kBtEmitTiles * kBtScanT) {
+    double zv[kBtEmitTiles];
+#pragma unroll
+    for (int u = 0; u < kBtEmitTiles; ++u) {
+      const int i = r0 + u * kBtScanT + threadIdx.x;
+      zv[u] = i < s1 ? z[i] : 0.0;
+    }
+    uint32_t flags = 0u;
+#pragma unroll
+    for (int u = 0; u < kBtEmitTiles; ++u) {
+      const int i = r0 + u * kBtScanT + threadIdx.x;
+      bool f = false;
+      if (i < s1) {
+        const int bn = bt_bin(zv[u], p.bt_zlo, p.bt_scale);
+        f = bn != bstar ? bn > bstar : !bt_before(Tk, Ti, okey(zv[u]), i);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wcnt[u * kW + warp] = __popc(bal);
+      flags |= (f ? 1u : 0u) << u;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive prefix over (tile, warp) in position order
+      int carry = 0;
+      for (int b0 = 0; b0 < kBtEmitTiles * kW; b0 += 32) {
+        const int v = wcnt[b0 + lane];
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        wcnt[b0 + lane] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) wcnt[kBtEmitTiles * kW] = carry;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kBtEmitTiles; ++u) {
+      const bool f = (flags >> u) & 1u;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (f) {
+        const int i = r0 + u * kBtScanT + threadIdx.x;
+        out[o_base + wcnt[u * kW + warp] + __popc(bal & ((1u << lane) - 1u))] = src.pos(i);
+      }
+    }
+    o_base += wcnt[kBtEmitTiles * kW];
+    __syncthreads();
+  }
   if (seg == 0 && threadIdx.x == 0) p.n_sel[row] = K;
 }
 
