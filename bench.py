@@ -760,9 +760,9 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
         "run": {"kv_heads_per_gpu": wl.H, "batch_per_gpu": wl.B, "slow_steps_timed": f"{n_slow} of {K}",
                 "cuda_graphs": use_graph if graph_note is None else graph_note,
                 "slow_step": "synchronous" if wl.exec is None else
-                             "C++ DecodeExecutor: async pipeline, dense on a high-priority main stream (share "
-                             "grid), Selector + compact on a low-priority aux stream, 4-slot logit ring; steps "
-                             "replayed from CUDA graphs with node priorities",
+                             f"C++ DecodeExecutor: async pipeline, dense on the main stream (share grid), Selector + "
+                             f"compact on an aux stream, {wl.exec.logits.shape[0]}-slot logit ring; steps "
+                             f"replayed from CUDA graphs",
                 "exchange": {"nccl": "ncclAllGather in-call through the C ABI (torch's communicator)",
                              "allgather": "torch.distributed all-gather",
                              "peer": "peer memory (CUDA IPC over NVLink)"}.get(wl.exchange, "none"),
