@@ -545,6 +545,120 @@ def traffic_for(kernel: str, cfg_name: str):
     return None, f"no ncu capture of {kernel} at {cfg_name}"
 
 
+# C5 (BASELINE configs[4]): long-CoT generation, 2K prefill + 32K generated tokens on
+# Qwen3-8B attention shapes, batch 8; SFI (K = 2048) across the generation vs full-KV
+# dense decode; the refresh budget t_max swept through the seeded schedule's slow fraction
+C5 = dict(layers=36, q_heads=32, kv_heads=8, batch=8, prefill=2048, generated=32768, n_sink=4, k_budget=2048,
+          n_recent=256)
+C5_TMAX = (16, 32, 64, 128)
+
+
+def c5_slow_fraction(t_max: int, steps: int, seed: int = 2031) -> float:
+    """Slow steps / steps of the seeded schedule over a whole generation (step 0 slow;
+    triggers Bernoulli(1/24), forced at t_max; scheduler.cpp:93-99)."""
+    rng = np.random.default_rng(seed)
+    since, trig, n = 0, True, 0
+    for _ in range(steps):
+        slow = trig or since + 1 >= t_max
+        n += slow
+        since = 0 if slow else since + 1
+        trig = bool(rng.random() < P_TRIGGER)
+    return n / steps
+
+
+def run_c5(dev) -> dict:
+    """The C5 line: per context point of the generation (2K, 10K, 18K, 26K, 34K) the
+    executor's fast and slow steps and a full-KV dense step (append + K1 over the
+    whole cache, every layer) are replayed from CUDA graphs; a schedule's time per
+    token is (1 - f) fast + f slow, averaged over the generation (trapezoid in
+    context). scripts/sweep_c5.py sweeps K as well."""
+    import torch
+
+    import paper_2603_12038_b200 as sfi
+    from paper_2603_12038_b200.device import StepExecutor
+
+    c5 = C5
+    L, Hq, H, B, d = c5["layers"], c5["q_heads"], c5["kv_heads"], c5["batch"], HEAD_DIM
+    ns, K, R = c5["n_sink"], c5["k_budget"], c5["n_recent"]
+    ctxs = [c5["prefill"] + i * c5["generated"] // 4 for i in range(5)]
+    cache = sfi.SfiCache(L, B, H, Hq, d, ctxs[-1] + 64, ns, K, R, device=dev)
+    cache.fill_synthetic(seed=2031, length=ctxs[-1])
+    g = torch.Generator().manual_seed(2031)
+    q = torch.randn(L, B, Hq, d, generator=g).to(dev)
+    kn = torch.randn(L, B, H, d, generator=g).bfloat16().to(dev)
+    vn = torch.randn(L, B, H, d, generator=g).bfloat16().to(dev)
+    out = torch.zeros(L, B, Hq, d, device=dev)
+    x = StepExecutor(cache, slots=2)
+    st = x.stream
+    fast_ms, slow_ms, dense_ms = {}, {}, {}
+
+    def at(ctx):
+        cache.set_lengths([ctx] * B, [ns] * B)
+        torch.cuda.synchronize()
+
+    for ctx in ctxs:
+        at(ctx)
+        x.step(True, q, kn, vn, out, rebuild_ring=True)  # selection + compact cache at this context
+        x.step(False, q, kn, vn, out)
+        st.synchronize()
+        at(ctx)
+        x.capture(False, q, kn, vn, out)
+        x.capture(True, q, kn, vn, out)
+        at(ctx)
+        fast_ms[ctx] = time_graph(lambda: x.replay(False), 8, st)
+        at(ctx)
+        slow_ms[ctx] = time_graph(lambda: x.replay(True), 3, st)
+        cache.check_errors()
+    gd = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        at(ctxs[0])
+
+        def dense_step():
+            cache.step_advance()
+            for l in range(L):
+                cache.ring_append(l, kn[l], vn[l])
+                cache.dense_decode(l, q[l], out[l])
+
+        dense_step()  # eager once (kernel attributes), then capture
+        st.synchronize()
+        with torch.cuda.graph(gd, stream=st):
+            dense_step()
+    for ctx in ctxs:
+        at(ctx)
+        with torch.cuda.stream(st):  # a torch graph replays on the current stream
+            dense_ms[ctx] = time_graph(gd, 3, st)
+    cache.check_errors()
+
+    def gen_avg(per):  # mean ms per step over a generation uniform in context
+        ys = [per[c] for c in ctxs]
+        return float(np.trapezoid(ys, ctxs) / (ctxs[-1] - ctxs[0]))
+
+    dense_avg = gen_avg(dense_ms)
+    rows = []
+    for t in C5_TMAX:
+        f = c5_slow_fraction(t, c5["generated"])
+        avg = gen_avg({c: (1 - f) * fast_ms[c] + f * slow_ms[c] for c in ctxs})
+        rows.append({"t_max": t, "slow_fraction": round(f, 4), "tokens_per_s": B / (avg / 1e3),
+                     "speedup_vs_full_kv": dense_avg / avg})
+    head = next(r for r in rows if r["t_max"] == T_MAX)
+    del x, cache
+    _release()
+    return {"metric": f"SFI decode tokens/s (C5 long-CoT: {c5['prefill'] // 1024}K prefill + "
+                      f"{c5['generated'] // 1024}K generated, Qwen3-8B-shaped attention, batch {B})",
+            "value": head["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1, "higher_is_better": True,
+            "full_kv_dense_tokens_per_s": B / (dense_avg / 1e3), "speedup_vs_full_kv": head["speedup_vs_full_kv"],
+            "t_max": T_MAX, "sweep": rows,
+            "per_context_ms": {str(c): {"fast": fast_ms[c], "slow": slow_ms[c], "full_kv_dense": dense_ms[c]}
+                               for c in ctxs},
+            "config": {"workload": "Qwen3-8B-shaped attention, long-CoT generation (C5)", "layers": L,
+                       "q_heads": Hq, "kv_heads": H, "head_dim": d, "batch": B, "prefill": c5["prefill"],
+                       "generated": c5["generated"], "n_sink": ns, "k_budget": K, "n_recent": R,
+                       "contexts": ctxs},
+            "timing": "CUDA-graph replays of the executor's fast / slow steps and of a full-KV dense step at each "
+                      "context point (CUDA events on the replay stream); the schedule mixes them by its seeded slow "
+                      "fraction over the 32K generated tokens; per-K sweep: scripts/sweep_c5.py"}
+
+
 def _release(*objs):
     import gc
 
@@ -834,7 +948,7 @@ def gpu_arm(args) -> dict:
     ctx = dict(world=world, rank=rank, local=local, dev=dev, max_over_ranks=max_over_ranks)
     primary = args.config or ("c2" if world == 1 else "c3")
     if args.also is None:
-        also = ["c3", "c4"] if world == 1 else ["c4", "c2"]
+        also = ["c3", "c4", "c5"] if world == 1 else ["c4", "c2"]
     else:
         also = [x for x in args.also.split(",") if x and x != "none"]
     also = [a for a in also if a != primary]
@@ -842,6 +956,10 @@ def gpu_arm(args) -> dict:
     extra = []
     for cfg in also:
         try:
+            if cfg == "c5":
+                if world == 1:
+                    extra.append(run_c5(dev))
+                continue
             r = run_config(cfg, args, ctx, full=False)
             extra.append({k: r[k] for k in ("metric", "value", "unit", "n_gpus", "steps", "ms_per_step", "scaling",
                                             "slow_steps", "fast_step_us_graph", "slow_step_us_graph", "roofline",
@@ -1170,7 +1288,7 @@ def main():
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="headline workload (default: c2 on 1 GPU, c3 KV-head sharded on N > 1)")
     ap.add_argument("--also", default=None,
-                    help="comma-separated extra configs timed after the headline (default: c3,c4 on 1 GPU, "
+                    help="comma-separated extra configs timed after the headline (default: c3,c4,c5 on 1 GPU, "
                          "c4,c2 on N > 1; 'none' for none); reported under 'also'")
     ap.add_argument("--inputs", default="peaked", choices=["peaked", "iid"],
                     help="synthetic inputs: peaked = 32 planted k = 3q + noise positions per (b, KV head) "

@@ -64,6 +64,7 @@ __global__ void append_kernel(const AppendParams p) {
   const int c = threadIdx.x;
   const int L = p.prefix_len[b];
   const int row = p.block_mode ? (L + i) : (L - 1);
+  if (!p.block_mode && overflow_raised(p.err)) return;
   if (row < 0 || row >= p.Lmax) {
     if (c == 0) raise_error(p.err, p.block_mode ? SFI_ERR_CONTEXT_OVERFLOW : SFI_ERR_OUT_OF_RANGE);
     return;

@@ -363,11 +363,10 @@ long long* decode_trace_buffer() {
 // rows of one stream-K partial: 8, or 16 for GQA group 16 (decode.cu part_rows)
 static size_t part_rows(const sfi_shape& s) { return group_of(s) > 8 ? 16 : 8; }
 
-// long-row top-k buffers (selector.cu sel_bt_*), only when |J| can exceed the
-// single-CTA top-k: [rows][65536] bin counts, [rows][max_positions] listed
+// long-row top-k buffers (selector.cu sel_bt_*; the default when |J| can exceed the
+// single-CTA top-k, SFI_TOPK_BT=1 for every length): [rows][65536 + 1024] bin and chunk counts, [rows][max_positions] listed
 // indices, [rows][8] row state, [rows][64][2] segment counts / offsets
 size_t bt_bytes(const sfi_shape& s) {
-  if (s.max_positions <= kTopkCtaMaxPositions) return 0;
   const size_t rows = (size_t)s.batch * s.n_kv_heads;
   return rows * (65536 * 4 + (size_t)s.max_positions * 4 + 8 * 4 + 64 * 2 * 4);
 }

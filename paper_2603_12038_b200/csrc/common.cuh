@@ -18,6 +18,12 @@ constexpr float kLazyMax = 8.f;
 __device__ __forceinline__ void raise_error(uint32_t* flags, int code) {
   if (flags) atomicOr(flags, 1u << code);
 }
+// A context overflow raised by this step's advance (advance_kernel / seq_lengths_kernel)
+// freezes the cache: the current token's append is skipped until the host clears the
+// flags, so the last valid row is never overwritten.
+__device__ __forceinline__ bool overflow_raised(const uint32_t* flags) {
+  return flags && ((*(const volatile uint32_t*)flags >> SFI_ERR_CONTEXT_OVERFLOW) & 1u);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

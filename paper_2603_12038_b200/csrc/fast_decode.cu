@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 #pragma unroll
     for (int c = 0; c < kC; ++c) vv[c] = 0.f;
-    const bool mine = rank == 0 && ok && fused;
+    const bool mine = rank == 0 && ok && fused && !overflow_raised(p.err);
     if (rank == 0 && !ok && lane == 0)
       raise_error(p.err, (rl < 1 && fused) || L < 1 || L > p.Lmax ? SFI_ERR_OUT_OF_RANGE : SFI_ERR_CONFIG);
     if (mine) {

@@ -112,7 +112,7 @@ struct SelectorScratch {
   double* b;      // [B*H][Lmax]  w -> r -> z_adj
   double* c;      // [B*H][Lmax]  prior weights w (two-pass decode Selector)
   double* stats;  // [B*H][ceil(Lmax / 512)][6] chunk statistics, then [B*H][chunks + 2] coefficients
-  void* bt = nullptr;  // long-row top-k buffers (null when Lmax <= kTopkCtaMaxPositions)
+  void* bt = nullptr;  // long-row top-k buffers (sel_bt_*)
 };
 constexpr int kTopkCtaMaxPositions = 48 * 1024;  // rows up to this length: the single-CTA top-k
 // phases: 1 = fuse (z_base into scr.a), 2 = refine + top-k; z_all != null:

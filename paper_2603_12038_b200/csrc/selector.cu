@@ -546,6 +546,7 @@ __device__ __forceinline__ double halo(const SelParams& p, int row, int g, int R
 // refine_cross_head (selector.cpp:204-230) at one position over the Hr heads in
 // head order, then z_adj of this shard's heads -> sb
 constexpr int kBtBins = 65536;
+constexpr int kBtRow = kBtBins;  // histogram words per row
 // monotonic (non-decreasing) value -> bin map of z_adj: equal z, equal bin
 __device__ __forceinline__ int bt_bin(double z, double zlo, double scale) {
   const double t = (z - zlo) * scale;
@@ -584,7 +585,7 @@ __device__ __forceinline__ void cross_head_store(const SelParams& p, int b, int 
         const int bn = bt_bin(z, p.bt_zlo, p.bt_scale);
         const unsigned act = __activemask();
         const unsigned same = __match_any_sync(act, bn);
-        if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&p.bt_hist[row * kBtBins + bn], (uint32_t)__popc(same));
+        if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&p.bt_hist[row * kBtRow + bn], (uint32_t)__popc(same));
       }
     }
 }
@@ -1560,50 +1561,75 @@ __device__ __forceinline__ T block_excl_scan(T v, T* wsum, T& total) {
 }
 
 constexpr int kBtT = 1024;
+constexpr int kBtThCS = 8;                      // thresh: CTAs per row (one cluster)
+constexpr int kBtThT = 256;
+constexpr int kBtChunks = kBtBins / 64;         // 64-bin chunks per row
+constexpr int kBtThChunks = kBtChunks / kBtThCS;  // chunks per CTA
 
-__global__ void __launch_bounds__(kBtT) sel_bt_thresh_kernel(const SelParams p, const BtBuf bt) {
+// The bin b* holding the K-th largest key of a row: one 8-CTA cluster per row.
+// Chunk c = bins [kBtBins - 64 (c + 1), kBtBins - 64 c) (descending); CTA r sums
+// chunks [r kBtThChunks, (r + 1) kBtThChunks) with coalesced 256-byte reads (16
+// per warp in flight), rank 0 scans all chunk sums over DSMEM, then resolves the
+// 64 bins of the chunk holding the K-th key.
+__global__ void __cluster_dims__(kBtThCS, 1, 1) __launch_bounds__(kBtThT)
+    sel_bt_thresh_kernel(const SelParams p, const BtBuf bt) {
   griddep_wait();
   griddep_launch();
-  // 1024 chunks of 64 bins, chunk c = bins [kBtBins - 64 (c + 1), kBtBins - 64 c) (descending);
-  // warp w sums chunks 32 w .. 32 w + 31 with coalesced 256-byte reads
-  __shared__ uint32_t csum[kBtT];
+  __shared__ uint32_t csum[kBtThChunks];
   __shared__ uint32_t wsum[33];
   __shared__ int s_c;
   __shared__ uint32_t s_before;
-  const int row = blockIdx.x;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Src<false> src(p, row / p.H);
   const int n = src.n, K = p.K;
   int32_t* m = bt.meta + (size_t)row * 8;
-  uint32_t* h = bt.hist + (size_t)row * kBtBins;
+  const uint32_t* h = bt.hist + (size_t)row * kBtRow;
   const bool active = n > K && K > 0;
+  constexpr int kPerWarp = kBtThChunks / (kBtThT / 32);
+  static_assert(kPerWarp == 16, "16 chunk reads in flight per lane");
   if (active) {
-    uint2 v[32];  // all 32 loads in flight before any reduction
+    uint2 v[kPerWarp];
+    const int c0 = rank * kBtThChunks + warp * kPerWarp;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = __ldcg(reinterpret_cast<const uint2*>(h + kBtBins - 64 * (warp * 32 + k + 1)) + lane);
+    for (int k = 0; k < kPerWarp; ++k) v[k] = __ldcg(reinterpret_cast<const uint2*>(h + kBtBins - 64 * (c0 + k + 1)) + lane);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
+    for (int k = 0; k < kPerWarp; ++k) {
       uint32_t x = v[k].x + v[k].y;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == k) csum[warp * 32 + k] = x;
+      if (lane == k) csum[warp * kPerWarp + k] = x;
     }
-  } else {
-    csum[threadIdx.x] = 0u;
   }
-  __syncthreads();
-  const uint32_t mine = csum[threadIdx.x];
-  uint32_t total;
-  const uint32_t before = block_excl_scan<kBtT>(mine, wsum, total);
-  if (active && before < (uint32_t)K && before + mine >= (uint32_t)K) {
-    s_c = threadIdx.x;
-    s_before = before;
+  cl.sync();  // every CTA's chunk sums visible cluster-wide
+  if (rank == 0 && active) {
+    // thread t owns chunks 4t .. 4t + 3 (kBtChunks = 4 x kBtThT), read over DSMEM
+    static_assert(kBtChunks == 4 * kBtThT, "four chunk sums per thread");
+    const int c0 = 4 * threadIdx.x;
+    const uint32_t* rs = cl.map_shared_rank(csum, c0 / kBtThChunks);
+    uint32_t a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = rs[(c0 % kBtThChunks) + k];
+    const uint32_t mine = a[0] + a[1] + a[2] + a[3];
+    uint32_t total;
+    uint32_t before = block_excl_scan<kBtThT>(mine, wsum, total);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (before < (uint32_t)K && before + a[k] >= (uint32_t)K) {
+        s_c = c0 + k;
+        s_before = before;
+      }
+      before += a[k];
+    }
   }
-  __syncthreads();
+  cl.sync();  // rank 0 done reading the peers' sums
+  if (rank != 0) return;
   if (active && warp == 0) {  // the 64 bins of chunk s_c, descending: lane pairs, warp prefix
     const int c = s_c;
     const int top = kBtBins - 64 * c;  // bins [top - 64, top)
-    const uint32_t v1 = h[top - 1 - 2 * lane], v2 = h[top - 2 - 2 * lane];
+    const uint32_t v1 = __ldcg(h + top - 1 - 2 * lane), v2 = __ldcg(h + top - 2 - 2 * lane);
     uint32_t inc = v1 + v2;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1627,8 +1653,7 @@ __global__ void __launch_bounds__(kBtT) sel_bt_thresh_kernel(const SelParams p, 
     m[3] = 0;
     m[7] = active ? 0 : 1;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kBtBins / 4; i += kBtT) reinterpret_cast<uint4*>(h)[i] = make_uint4(0, 0, 0, 0);
+  // the histogram is zeroed by sel_bt_scan (every segment CTA clears its share)
 }
 
 constexpr int kBtScanT = 256;
@@ -1638,6 +1663,11 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_scan_kernel(const SelParams p
   griddep_launch();
   __shared__ uint32_t wsum[33];
   const int seg = blockIdx.x, row = blockIdx.y;
+  {  // clear this segment's share of the row's histogram for the next Selector call
+    uint4* h4 = reinterpret_cast<uint4*>(bt.hist + (size_t)row * kBtRow);
+    const int w0 = bt_seg_start(seg, kBtRow / 4, bt.P), w1 = bt_seg_start(seg + 1, kBtRow / 4, bt.P);
+    for (int i = w0 + threadIdx.x; i < w1; i += kBtScanT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   int32_t* m = bt.meta + (size_t)row * 8;
   if (m[7]) return;
   const Src<false> src(p, row / p.H);
@@ -1798,17 +1828,26 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int off = 0;
-    for (int sg = 0; sg < bt.P; ++sg) {
-      int32_t* e = bt.seg + ((size_t)row * kBtMaxSeg + sg) * 2;
-      const int c = e[0] + segcnt[sg];
-      e[1] = off;
-      off += c;
+  static_assert(kBtMaxSeg == 64, "two lanes' segments per thread of warp 0");
+  if (threadIdx.x < 32) {  // segment output offsets: exclusive prefix of (above b*) + (selected listed)
+    int32_t* e = bt.seg + (size_t)row * kBtMaxSeg * 2;
+    const int s0 = 2 * threadIdx.x, s1 = s0 + 1;
+    const int c0 = s0 < bt.P ? e[2 * s0] + segcnt[s0] : 0;
+    const int c1 = s1 < bt.P ? e[2 * s1] + segcnt[s1] : 0;
+    int inc = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if ((int)threadIdx.x >= o) inc += y;
     }
-    m[4] = (int32_t)(Tk >> 32);
-    m[5] = (int32_t)(Tk & 0xffffffffull);
-    m[6] = Ti;
+    const int ex = inc - c0 - c1;
+    if (s0 < bt.P) e[2 * s0 + 1] = ex;
+    if (s1 < bt.P) e[2 * s1 + 1] = ex + c0;
+    if (threadIdx.x == 0) {
+      m[4] = (int32_t)(Tk >> 32);
+      m[5] = (int32_t)(Tk & 0xffffffffull);
+      m[6] = Ti;
+    }
   }
 }
 
@@ -1891,7 +1930,7 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_emit_kernel(const SelParams p
 }
 
 cudaError_t launch_bt_topk(const SelParams& p, const BtBuf& bt, int rows, cudaStream_t st) {
-  cudaError_t e = launch_k(sel_bt_thresh_kernel, dim3(rows), dim3(kBtT), 0, st, p, bt);
+  cudaError_t e = launch_k(sel_bt_thresh_kernel, dim3(kBtThCS, rows), dim3(kBtThT), 0, st, p, bt);
   if (e == cudaSuccess) e = launch_k(sel_bt_scan_kernel, dim3(bt.P, rows), dim3(kBtScanT), 0, st, p, bt);
   if (e == cudaSuccess) e = launch_k(sel_bt_pick_kernel, dim3(rows), dim3(kBtT), 0, st, p, bt);
   if (e == cudaSuccess) e = launch_k(sel_bt_emit_kernel, dim3(bt.P, rows), dim3(kBtScanT), 0, st, p, bt);
@@ -2060,13 +2099,15 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
     const bool def_exp = p.gamma == 1.0 && p.p_curve == 2.0 && p.eta == 0.5;
     // long rows: the rows x segments top-k over sel_z's value histogram
     static const bool force_cluster = std::getenv("SFI_TOPK_CLUSTER") != nullptr;
-    const bool use_bt = scr.bt != nullptr && s.max_positions > kTopkCtaMax && !force_cluster &&
+    static const int bt_env = std::getenv("SFI_TOPK_BT") ? std::atoi(std::getenv("SFI_TOPK_BT")) : -1;
+    const bool bt_len = bt_env < 0 ? s.max_positions > kTopkCtaMax : bt_env > 0;
+    const bool use_bt = scr.bt != nullptr && bt_len && !force_cluster &&
                         p.alpha_soft >= 0.0 && p.alpha_cross >= 0.0;
     BtBuf bt{};
     if (use_bt) {
       uint8_t* w = static_cast<uint8_t*>(scr.bt);
       bt.hist = reinterpret_cast<uint32_t*>(w);
-      w += slices * kBtBins * 4;
+      w += slices * kBtRow * 4;
       bt.cand = reinterpret_cast<int32_t*>(w);
       w += slices * (size_t)s.max_positions * 4;
       bt.meta = reinterpret_cast<int32_t*>(w);

@@ -305,11 +305,12 @@ class SlowStepPipeline:
 class StepExecutor:
     """The C++ decode executor (include/sfi/decode.hpp, executor.cpp) over one
     SfiCache: whole decode steps of all layers — fast (advance + one fused K4
-    launch per layer) or slow (the layer-wise asynchronous pipeline: dense on a
-    high-priority main stream, Selector + compact on a lowest-priority aux
-    stream through a `slots`-deep pooled-logit ring, one completion barrier) —
-    enqueued from C++, capturable once per kind into a CUDA graph (node
-    priorities kept) and replayed with no host work.
+    launch per layer) or slow (the layer-wise asynchronous pipeline: dense on the
+    main stream, Selector + compact on an aux stream through a `slots`-deep
+    pooled-logit ring, one completion barrier; `priorities=1` makes the main
+    stream high- and the aux stream lowest-priority, kept as graph node
+    priorities — measured slower) — enqueued from C++, capturable
+    once per kind into a CUDA graph and replayed with no host work.
 
     q, out: fp32 [L][B][Hq][d]; k_new, v_new: bf16 [L][B][H][d] (views with any
     per-layer stride, e.g. rows of one packed [L][q | k | v] buffer)."""

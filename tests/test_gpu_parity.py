@@ -526,3 +526,42 @@ def test_prefill_capture_and_window_selector(pool):
         for h in range(H):
             ns_ = int(c.n_sel[0, b, h])
             assert np.array_equal(c.sel[0, b, h, :ns_].cpu().numpy(), want_sel[h]), (b, h)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ["ring_append", "fast_decode"])
+def test_context_overflow_freezes_cache(path):
+    """An advance past max_positions raises SFI_ERR_CONTEXT_OVERFLOW and the
+    current token's append is skipped (ring_append and the fused fast step), so
+    the last valid row, its ring slot and norm are not overwritten."""
+    import torch
+
+    from paper_2603_12038_b200 import SelectorParams, SfiCache
+
+    Lmax, H, Hq, d = 600, 2, 8, 128
+    c = SfiCache(1, 1, H, Hq, d, Lmax, 4, 64, 32)
+    c.fill_synthetic(seed=5, length=Lmax)
+    c.set_lengths([Lmax], [4])
+    g = torch.Generator().manual_seed(3)
+    q = torch.randn(1, Hq, d, generator=g).cuda()
+    out = torch.zeros_like(q)
+    logits = torch.zeros_like(c.pooled_logits)
+    c.dense_decode(0, q, out, logits, 0)
+    c.selector(0, logits, SelectorParams())
+    c.compact_build(0, rebuild_ring=True)
+    torch.cuda.synchronize()
+    c.check_errors()
+    snap = [t.clone() for t in (c.k_cache, c.v_cache, c.ck, c.cv, c.key_norms)]
+    kn = torch.randn(1, H, d, generator=g).bfloat16().cuda()
+    vn = torch.randn(1, H, d, generator=g).bfloat16().cuda()
+    c.step_advance()
+    if path == "ring_append":
+        c.ring_append(0, kn, vn)
+    else:
+        c.fast_decode(0, q, kn, vn, out)
+    torch.cuda.synchronize()
+    rc, flags, _ = c.read_errors()
+    assert rc and flags & (1 << 9), hex(flags)
+    assert int(c.prefix_len[0]) == Lmax
+    for a, b in zip(snap, (c.k_cache, c.v_cache, c.ck, c.cv, c.key_norms)):
+        assert torch.equal(a, b)
