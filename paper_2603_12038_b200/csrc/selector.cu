@@ -1246,24 +1246,11 @@ __global__ void __launch_bounds__(kTopkCtaT) sel_topk_cta_kernel(const SelParams
   int above = 0;
   bool resolved = false;
   unsigned long long T = 0;
+  // keys with high word in the current range: all n at first, then the count of
+  // the digit bucket each radix pass narrows the range to
+  int cnt_range = n;
   while (true) {
     // candidate shortcut (also the exit once the high word is pinned)
-    int cnt_range;
-    {
-      // count of keys with high word in the current range (cheap smem pass)
-      int c = 0;
-      for (int i = threadIdx.x; i < n; i += kTopkCtaT) {
-        const uint32_t h = shi[i];
-        c += (h >= lo && (bits >= 32 || ((h - lo) >> bits) == 0u));
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      __syncthreads();
-      if (lane == 0) wred[warp][0] = (uint32_t)c;
-      __syncthreads();
-      cnt_range = 0;
-      for (int w = 0; w < kW; ++w) cnt_range += (int)wred[w][0];
-    }
     if (cnt_range <= kCandCap) {
       if (threadIdx.x == 0) s_ncand = 0;
       __syncthreads();
@@ -1338,6 +1325,7 @@ __global__ void __launch_bounds__(kTopkCtaT) sel_topk_cta_kernel(const SelParams
     above += s_cum;
     lo += (uint32_t)s_tb << shift;
     bits = shift;
+    cnt_range = s_cnt;
     __syncthreads();
   }
   if (!resolved) {
