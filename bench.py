@@ -443,10 +443,13 @@ def time_kernel(wl: Workload, which: str, iters: int) -> float:
     return a.elapsed_time(b) / iters
 
 
-def time_graph(g, reps: int, stream) -> float:
+def time_graph(g, reps: int, stream=None) -> float:
     """ms per replay of a captured step (a torch CUDAGraph or the executor's replay
-    callable), back to back between two events on the stream it replays on."""
+    callable), back to back between two events on the stream it replays on
+    (default: the current stream)."""
     t = __import__("torch")
+    if stream is None:
+        stream = t.cuda.current_stream()
     run = g if callable(g) else g.replay
     run()
     t.cuda.synchronize()

@@ -10,7 +10,7 @@ contexts spanning the generation; a (K, t_max) schedule's time per token is
 (triggers Bernoulli(1/24), forced at t_max; scheduler.cpp:93-99), averaged over
 the generation (trapezoid over the context points). Synthetic bf16 KV, batch 8.
 
-    python scripts/sweep_c5.py [--batch 8] [--out profiles/r01/c5_sweep.json]
+    python scripts/sweep_c5.py [--batch 8] [--out profiles/r02/c5_sweep.json]
 """
 from __future__ import annotations
 
@@ -53,13 +53,13 @@ def graph(fn):
 
 
 def replay_ms(g, reps):
-    return bench.time_graph(g, reps)
+    return bench.time_graph(g, reps, torch.cuda.current_stream())
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=8)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "c5_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02", "c5_sweep.json"))
     args = ap.parse_args()
     B = args.batch
     dev = torch.device("cuda", 0)
