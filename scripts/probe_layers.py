@@ -11,7 +11,7 @@ import bench  # noqa: E402
 import paper_2603_12038_b200 as sfi  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-wl = bench.Workload(cfg, 200, torch.device("cuda", 0))
+wl = bench.Workload(cfg, 200, torch.device("cuda", 0), sync_slow=True)  # per-layer launches from Python
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g):
     wl.step(False)
