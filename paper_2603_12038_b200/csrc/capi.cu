@@ -175,10 +175,11 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
     const char* e = std::getenv("SFI_DENSE_SHARE_PERMILLE");
     return e ? std::atoi(e) : 0;
   }();
-  // G = 16: the dense decode is consumer-latency-bound and wants every CTA slot
-  // (C4 async slow step 21.4 -> 20.2 ms); G <= 8 streams at HBM speed with 65%
-  const int share = (env_share > 0 && env_share <= 1000) ? env_share
-                    : (s->n_q_heads / s->n_kv_heads >= 16 ? 1000 : 650);
+  // measured optimum of the async slow step per group size (profiles/r02/share_sweep.txt,
+  // 3 repeats each): G = 4 (C2) 67.5% of the 2-CTA slots (8.23 vs 8.37 ms at 65%),
+  // G = 8 (C3) 75% (27.9 vs 30.4 ms); G = 16 (C4) takes the tcgen05 kernel on every SM
+  const int Gq = s->n_q_heads / s->n_kv_heads;
+  const int share = (env_share > 0 && env_share <= 1000) ? env_share : (Gq >= 16 ? 1000 : Gq >= 8 ? 750 : 675);
   int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms(),
                                    (flags & SFI_DENSE_SHARE_SM) ? share : 875);
   static const int env_ctas = [] {
@@ -205,24 +206,28 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   // default: the tcgen05 kernel, except beside the Selector at G <= 8 (SFI_DENSE_SHARE_SM),
   // where the mma.sync kernel's 2 CTAs per SM on 65% of the slots overlap the Selector
   // chain better (C2 async slow step 8.33 vs 8.49 ms per step, measured)
+  static const int env_tc_share_g = [] {  // smallest group that takes tcgen05 beside the Selector
+    const char* e = std::getenv("SFI_DENSE_TC_SHARE_G");
+    return e ? std::atoi(e) : 16;
+  }();
   const bool share_flag = (flags & SFI_DENSE_SHARE_SM) != 0;
   const bool want_tc = (flags & SFI_DENSE_TC)    ? true
                        : (flags & SFI_DENSE_MMA) ? false
-                                                 : env_tc > 0 && (!share_flag || group_of(*s) >= 16);
+                                                 : env_tc > 0 && (!share_flag || group_of(*s) >= env_tc_share_g);
   if (!sparse && D == 128 && (G == 4 || G == 8 || G == 16) && want_tc) {
     CUtensorMap tk2, tv2;
     if ((rc = make_tmap(&tk2, c->k_cache, slices * rows_per, D, 128))) return rc;
     if ((rc = make_tmap(&tv2, c->v_cache, slices * rows_per, D, 128))) return rc;
     // alone: 3 stages (192 KB) on every SM. Beside the Selector (SFI_DENSE_SHARE_SM):
-    // the 2-stage variant (~150 KB, 224 threads) on SFI_DENSE_TC_SHARE_PERMILLE of
-    // the SMs, so the Selector's CTAs can co-reside on the same SMs
+    // SFI_DENSE_TC_SHARE_PERMILLE of the SMs with SFI_DENSE_TC_SHARE_STAGES stages
+    // (default 3; 2 stages, ~150 KB, let Selector CTAs co-reside but measured slower)
     static const int env_tc_share = [] {
       const char* e = std::getenv("SFI_DENSE_TC_SHARE_PERMILLE");
       return e ? std::atoi(e) : 1000;
     }();
-    static const int env_tc_share_stages = [] {
+    static const int env_tc_share_stages = [] {  // C4: 3 stages 14.5 vs 2 stages 15.4 ms per slow step
       const char* e = std::getenv("SFI_DENSE_TC_SHARE_STAGES");
-      return e ? std::atoi(e) : 2;
+      return e ? std::atoi(e) : 3;
     }();
     const bool share_mode = (flags & SFI_DENSE_SHARE_SM) != 0;
     const int share_tc = share_mode ? env_tc_share : 1000;
