@@ -569,20 +569,21 @@ def c5_slow_fraction(t_max: int, steps: int, seed: int = 2031) -> float:
     return n / steps
 
 
-def run_c5(dev) -> dict:
+def run_c5(dev, k_budget: int | None = None, batch: int | None = None, dense: bool = True) -> dict:
     """The C5 line: per context point of the generation (2K, 10K, 18K, 26K, 34K) the
     executor's fast and slow steps and a full-KV dense step (append + K1 over the
     whole cache, every layer) are replayed from CUDA graphs; a schedule's time per
     token is (1 - f) fast + f slow, averaged over the generation (trapezoid in
-    context). scripts/sweep_c5.py sweeps K as well."""
+    context). scripts/sweep_c5.py calls it per (K, batch)."""
     import torch
 
     import paper_2603_12038_b200 as sfi
     from paper_2603_12038_b200.device import StepExecutor
 
     c5 = C5
-    L, Hq, H, B, d = c5["layers"], c5["q_heads"], c5["kv_heads"], c5["batch"], HEAD_DIM
-    ns, K, R = c5["n_sink"], c5["k_budget"], c5["n_recent"]
+    L, Hq, H, d = c5["layers"], c5["q_heads"], c5["kv_heads"], HEAD_DIM
+    B = batch or c5["batch"]
+    ns, K, R = c5["n_sink"], k_budget or c5["k_budget"], c5["n_recent"]
     ctxs = [c5["prefill"] + i * c5["generated"] // 4 for i in range(5)]
     cache = sfi.SfiCache(L, B, H, Hq, d, ctxs[-1] + 64, ns, K, R, device=dev)
     cache.fill_synthetic(seed=2031, length=ctxs[-1])
@@ -612,46 +613,48 @@ def run_c5(dev) -> dict:
         at(ctx)
         slow_ms[ctx] = time_graph(lambda: x.replay(True), 3, st)
         cache.check_errors()
-    gd = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(st):
-        at(ctxs[0])
+    if dense:
+        gd = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st):
+            at(ctxs[0])
 
-        def dense_step():
-            cache.step_advance()
-            for l in range(L):
-                cache.ring_append(l, kn[l], vn[l])
-                cache.dense_decode(l, q[l], out[l])
+            def dense_step():
+                cache.step_advance()
+                for l in range(L):
+                    cache.ring_append(l, kn[l], vn[l])
+                    cache.dense_decode(l, q[l], out[l])
 
-        dense_step()  # eager once (kernel attributes), then capture
-        st.synchronize()
-        with torch.cuda.graph(gd, stream=st):
-            dense_step()
-    for ctx in ctxs:
-        at(ctx)
-        with torch.cuda.stream(st):  # a torch graph replays on the current stream
-            dense_ms[ctx] = time_graph(gd, 3, st)
-    cache.check_errors()
+            dense_step()  # eager once (kernel attributes), then capture
+            st.synchronize()
+            with torch.cuda.graph(gd, stream=st):
+                dense_step()
+        for ctx in ctxs:
+            at(ctx)
+            with torch.cuda.stream(st):  # a torch graph replays on the current stream
+                dense_ms[ctx] = time_graph(gd, 3, st)
+        cache.check_errors()
 
     def gen_avg(per):  # mean ms per step over a generation uniform in context
         ys = [per[c] for c in ctxs]
         return float(np.trapezoid(ys, ctxs) / (ctxs[-1] - ctxs[0]))
 
-    dense_avg = gen_avg(dense_ms)
+    dense_avg = gen_avg(dense_ms) if dense else None
     rows = []
     for t in C5_TMAX:
         f = c5_slow_fraction(t, c5["generated"])
         avg = gen_avg({c: (1 - f) * fast_ms[c] + f * slow_ms[c] for c in ctxs})
         rows.append({"t_max": t, "slow_fraction": round(f, 4), "tokens_per_s": B / (avg / 1e3),
-                     "speedup_vs_full_kv": dense_avg / avg})
+                     "speedup_vs_full_kv": dense_avg / avg if dense else None})
     head = next(r for r in rows if r["t_max"] == T_MAX)
     del x, cache
     _release()
     return {"metric": f"SFI decode tokens/s (C5 long-CoT: {c5['prefill'] // 1024}K prefill + "
                       f"{c5['generated'] // 1024}K generated, Qwen3-8B-shaped attention, batch {B})",
             "value": head["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1, "higher_is_better": True,
-            "full_kv_dense_tokens_per_s": B / (dense_avg / 1e3), "speedup_vs_full_kv": head["speedup_vs_full_kv"],
+            "full_kv_dense_tokens_per_s": B / (dense_avg / 1e3) if dense else None,
+            "speedup_vs_full_kv": head["speedup_vs_full_kv"],
             "t_max": T_MAX, "sweep": rows,
-            "per_context_ms": {str(c): {"fast": fast_ms[c], "slow": slow_ms[c], "full_kv_dense": dense_ms[c]}
+            "per_context_ms": {str(c): {"fast": fast_ms[c], "slow": slow_ms[c], "full_kv_dense": dense_ms.get(c)}
                                for c in ctxs},
             "config": {"workload": "Qwen3-8B-shaped attention, long-CoT generation (C5)", "layers": L,
                        "q_heads": Hq, "kv_heads": H, "head_dim": d, "batch": B, "prefill": c5["prefill"],
