@@ -511,25 +511,28 @@ def time_selector(wl: Workload, iters: int) -> tuple[float, float]:
     return a.elapsed_time(b) / iters, b.elapsed_time(e) / iters
 
 
-def time_dense_in_situ(wl: Workload) -> float | None:
+def time_dense_in_situ(wl: Workload) -> tuple[float | None, float | None]:
     """K1 as it runs inside the timed slow step: one eager asynchronous slow step
-    through the C++ executor (dense on the high-priority main stream at the
-    pipeline's share grid, Selector + compact of the earlier layers concurrently on
-    the low-priority aux stream), a timing event recorded on the main stream after
-    every layer (the executor's per-layer hook): the mean per-layer main-chain time
-    (append + dense decode) over layers 2.. (layers 0-1 run with an idle aux stream)."""
+    through the C++ executor (dense on the main stream at the pipeline's share grid,
+    Selector + compact of the earlier layers concurrently on the aux stream), with
+    the executor's per-layer hooks recording events on the main stream right before
+    each dense launch and right after it. Returns (mean dense launch duration, mean
+    per-layer main-chain period incl. the ring append and the logit-slot waits),
+    both over layers 2.. (layers 0-1 run with an idle aux stream)."""
     if wl.exec is None:
-        return None
+        return None, None
     t = wl.torch
-    evs = [t.cuda.Event(enable_timing=True) for _ in range(wl.L)]
-    for e in evs:
+    before = [t.cuda.Event(enable_timing=True) for _ in range(wl.L)]
+    after = [t.cuda.Event(enable_timing=True) for _ in range(wl.L)]
+    for e in before + after:
         e.record()
     wl.set_lengths(wl.ctx)
     t.cuda.synchronize()
-    wl.exec.step(True, wl.q, wl.k_new, wl.v_new, wl.out, False, (), evs)
+    wl.exec.step(True, wl.q, wl.k_new, wl.v_new, wl.out, False, (), after, record_before_attention=before)
     t.cuda.synchronize()
-    ts = [evs[i - 1].elapsed_time(evs[i]) for i in range(2, wl.L)]
-    return float(np.mean(ts)) if ts else None
+    launch = [before[i].elapsed_time(after[i]) for i in range(2, wl.L)]
+    period = [after[i - 1].elapsed_time(after[i]) for i in range(2, wl.L)]
+    return (float(np.mean(launch)), float(np.mean(period))) if launch else (None, None)
 
 
 def traffic_for(kernel: str, cfg_name: str):
@@ -791,7 +794,7 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
     Lcur = wl.ctx + 1
     t_sp_iso = time_kernel(wl, "sparse", max(32, 2 * wl.L))
     t_de_iso = time_kernel(wl, "dense", max(8, wl.L // 2))
-    t_de_situ = time_dense_in_situ(wl)
+    t_de_situ, t_de_period = time_dense_in_situ(wl)
     # in situ fast step: the fast step's graph (advance + L fused launches, PDL-chained)
     # replayed back to back; its launches' average duration = step time / L
     # (the advance kernel's share is charged to them: conservative)
@@ -837,9 +840,11 @@ def run_config(cfg_name: str, args, ctx: dict, full: bool) -> dict:
                                    else "isolated launches queued back to back")},
         "dense_decode": {"ms": t_de, "GB/s": bde / t_de / 1e6, "bytes": bde,
                          "isolated_ms": t_de_iso, "isolated_frac": bde / t_de_iso / 1e6 / hbm,
+                         "main_chain_period_ms": t_de_period,
                          "timing": ("in situ: the async slow step's share grid beside the Selector + compact "
-                                    "(events around each dense launch, eager step)" if t_de_situ
-                                    else "isolated full-grid launches queued back to back")},
+                                    "(events on the main stream right before and after each dense launch, eager "
+                                    "step; main_chain_period_ms adds the ring append and the logit-slot waits)"
+                                    if t_de_situ else "isolated full-grid launches queued back to back")},
         "selector": {"ms": t_sel, "timing": "isolated, queued back to back"},
         "compact_build": {"ms": t_cb, "timing": "isolated, queued back to back"},
     }

@@ -41,6 +41,10 @@ struct StepBuffers {  // device pointers, all layers packed
 struct StepHooks {  // optional per-layer events (cudaEvent_t), size n_layers or empty
   std::vector<void*> wait_before;  // the main stream waits on [l] before layer l
   std::vector<void*> record_after; // recorded on the main stream after layer l's output is written
+  // recorded on the main stream right before layer l's attention kernel (after the
+  // logit-slot wait and the ring append of a slow step): with record_after it brackets
+  // the attention launch alone, as it runs beside the aux stream's Selector
+  std::vector<void*> record_before_attention;
 };
 
 class DecodeExecutor {

@@ -337,7 +337,8 @@ PYBIND11_MODULE(_sfi_b200, m) {
       .def("step",
            [](DecodeExecutor& x, bool slow, std::uintptr_t q, std::uintptr_t k, std::uintptr_t v, std::uintptr_t out,
               size_t sq, size_t skv, size_t so, bool rebuild_ring, std::vector<std::uintptr_t> wait_before,
-              std::vector<std::uintptr_t> record_after, bool capture, std::uintptr_t origin) {
+              std::vector<std::uintptr_t> record_after, bool capture, std::uintptr_t origin,
+              std::vector<std::uintptr_t> record_before_attention) {
              StepBuffers io;
              io.q = static_cast<const float*>(vp(q));
              io.k_new = vp(k);
@@ -349,14 +350,17 @@ PYBIND11_MODULE(_sfi_b200, m) {
              StepHooks hooks;
              for (auto e : wait_before) hooks.wait_before.push_back(vp(e));
              for (auto e : record_after) hooks.record_after.push_back(vp(e));
-             const StepHooks* hp = (wait_before.empty() && record_after.empty()) ? nullptr : &hooks;
+             for (auto e : record_before_attention) hooks.record_before_attention.push_back(vp(e));
+             const StepHooks* hp =
+                 (wait_before.empty() && record_after.empty() && record_before_attention.empty()) ? nullptr : &hooks;
              if (capture) x.capture(slow, io, rebuild_ring, hp);
              else x.step(slow, io, rebuild_ring, hp, vp(origin));
            },
            py::arg("slow"), py::arg("q"), py::arg("k_new"), py::arg("v_new"), py::arg("out"), py::arg("stride_q") = 0,
            py::arg("stride_kv") = 0, py::arg("stride_out") = 0, py::arg("rebuild_ring") = false,
            py::arg("wait_before") = std::vector<std::uintptr_t>{}, py::arg("record_after") = std::vector<std::uintptr_t>{},
-           py::arg("capture") = false, py::arg("origin") = 0)
+           py::arg("capture") = false, py::arg("origin") = 0,
+           py::arg("record_before_attention") = std::vector<std::uintptr_t>{})
       .def("replay", &DecodeExecutor::replay, py::arg("slow"))
       .def("captured", &DecodeExecutor::captured, py::arg("slow"))
       .def("logits_slot", [](const DecodeExecutor& x, int l) { return reinterpret_cast<std::uintptr_t>(x.logits_slot(l)); })

@@ -107,7 +107,8 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
   const int L = s_.n_layers;
   if (!io.q || !io.k_new || !io.v_new || !io.out) fail(ErrorCode::kOutOfRange, "DecodeExecutor: null step buffer");
   if (hooks && ((!hooks->wait_before.empty() && (int)hooks->wait_before.size() != L) ||
-                (!hooks->record_after.empty() && (int)hooks->record_after.size() != L)))
+                (!hooks->record_after.empty() && (int)hooks->record_after.size() != L) ||
+                (!hooks->record_before_attention.empty() && (int)hooks->record_before_attention.size() != L)))
     fail(ErrorCode::kSupportMismatch, "DecodeExecutor: one hook event per layer");
   // fork: the main (high-priority) stream continues the origin stream
   ok(cudaEventRecord(E(ev_fork_), S(origin)), "fork");
@@ -126,15 +127,21 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
     layer_io(io, l, &q, &k, &v, &out);
     if (hooks && !hooks->wait_before.empty() && hooks->wait_before[l])
       ok(cudaStreamWaitEvent(S(hi_), E(hooks->wait_before[l]), 0), "hook");
+    auto mark_attention = [&] {
+      if (hooks && !hooks->record_before_attention.empty() && hooks->record_before_attention[l])
+        ok(cudaEventRecord(E(hooks->record_before_attention[l]), S(hi_)), "hook");
+    };
     if (!slow) {
       // ONE launch: append fused with the sparse decode; the compact rows of layer l
       // are not written by the preceding kernel, so they stream before the PDL wait
+      mark_attention();
       check(sfi_fast_decode(&s_, &c_, l, q, k, v, out, SFI_FAST_PREFETCH, hi_));
     } else {
       const int sl = l % slots_;
       float* lg = logits_ + (size_t)sl * slot_elems;
       if (used[sl]) ok(cudaStreamWaitEvent(S(hi_), E(ev_free_[sl]), 0), "slot");
       check(sfi_ring_append(&s_, &c_, l, k, v, hi_));
+      mark_attention();
       check(sfi_dense_decode_ex(&s_, &c_, l, q, out, nullptr, lg, SFI_POOL_MEAN, share_ ? SFI_DENSE_SHARE_SM : 0,
                                 hi_));
       ok(cudaEventRecord(E(ev_ready_[sl]), S(hi_)), "slot ready");

@@ -338,15 +338,16 @@ class StepExecutor:
                 self._stride(k_new), self._stride(out))
 
     def step(self, slow: bool, q, k_new, v_new, out, rebuild_ring: bool = False, wait_before=(), record_after=(),
-             origin=None):
+             origin=None, record_before_attention=()):
         """Enqueue one step after the work on `origin` (a torch stream; default: the
-        executor's stream). wait_before / record_after: per-layer torch.cuda.Events."""
+        executor's stream). wait_before / record_after / record_before_attention:
+        per-layer torch.cuda.Events (the last two bracket each layer's attention
+        launch on the main stream)."""
         if k_new.stride(0) * k_new.element_size() != self._stride(v_new):
             raise ValueError("k_new / v_new layer strides differ")
-        self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring,
-                    [e.cuda_event if e is not None else 0 for e in wait_before],
-                    [e.cuda_event if e is not None else 0 for e in record_after], False,
-                    0 if origin is None else origin.cuda_stream)
+        ev = lambda es: [e.cuda_event if e is not None else 0 for e in es]  # noqa: E731
+        self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring, ev(wait_before), ev(record_after), False,
+                    0 if origin is None else origin.cuda_stream, ev(record_before_attention))
 
     def capture(self, slow: bool, q, k_new, v_new, out, rebuild_ring: bool = False):
         self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring, [], [], True, 0)
