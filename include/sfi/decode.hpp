@@ -45,6 +45,9 @@ struct StepHooks {  // optional per-layer events (cudaEvent_t), size n_layers or
   // logit-slot wait and the ring append of a slow step): with record_after it brackets
   // the attention launch alone, as it runs beside the aux stream's Selector
   std::vector<void*> record_before_attention;
+  // slow steps, recorded on the aux stream: before layer l's Selector (after its
+  // logits are ready), after the Selector, after the compact rebuild
+  std::vector<void*> aux_begin, aux_selected, aux_end;
 };
 
 class DecodeExecutor {

@@ -338,7 +338,7 @@ PYBIND11_MODULE(_sfi_b200, m) {
            [](DecodeExecutor& x, bool slow, std::uintptr_t q, std::uintptr_t k, std::uintptr_t v, std::uintptr_t out,
               size_t sq, size_t skv, size_t so, bool rebuild_ring, std::vector<std::uintptr_t> wait_before,
               std::vector<std::uintptr_t> record_after, bool capture, std::uintptr_t origin,
-              std::vector<std::uintptr_t> record_before_attention) {
+              std::vector<std::uintptr_t> record_before_attention, std::vector<std::uintptr_t> aux_events) {
              StepBuffers io;
              io.q = static_cast<const float*>(vp(q));
              io.k_new = vp(k);
@@ -351,8 +351,20 @@ PYBIND11_MODULE(_sfi_b200, m) {
              for (auto e : wait_before) hooks.wait_before.push_back(vp(e));
              for (auto e : record_after) hooks.record_after.push_back(vp(e));
              for (auto e : record_before_attention) hooks.record_before_attention.push_back(vp(e));
-             const StepHooks* hp =
-                 (wait_before.empty() && record_after.empty() && record_before_attention.empty()) ? nullptr : &hooks;
+             // aux_events: [3][L] flattened (aux_begin, aux_selected, aux_end)
+             if (!aux_events.empty()) {
+               if (aux_events.size() % 3) throw std::invalid_argument("aux_events: 3 x n_layers events");
+               const size_t L = aux_events.size() / 3;
+               for (size_t i = 0; i < L; ++i) {
+                 hooks.aux_begin.push_back(vp(aux_events[i]));
+                 hooks.aux_selected.push_back(vp(aux_events[L + i]));
+                 hooks.aux_end.push_back(vp(aux_events[2 * L + i]));
+               }
+             }
+             const StepHooks* hp = (wait_before.empty() && record_after.empty() && record_before_attention.empty() &&
+                                    aux_events.empty())
+                                       ? nullptr
+                                       : &hooks;
              if (capture) x.capture(slow, io, rebuild_ring, hp);
              else x.step(slow, io, rebuild_ring, hp, vp(origin));
            },
@@ -360,7 +372,8 @@ PYBIND11_MODULE(_sfi_b200, m) {
            py::arg("stride_kv") = 0, py::arg("stride_out") = 0, py::arg("rebuild_ring") = false,
            py::arg("wait_before") = std::vector<std::uintptr_t>{}, py::arg("record_after") = std::vector<std::uintptr_t>{},
            py::arg("capture") = false, py::arg("origin") = 0,
-           py::arg("record_before_attention") = std::vector<std::uintptr_t>{})
+           py::arg("record_before_attention") = std::vector<std::uintptr_t>{},
+           py::arg("aux_events") = std::vector<std::uintptr_t>{})
       .def("replay", &DecodeExecutor::replay, py::arg("slow"))
       .def("captured", &DecodeExecutor::captured, py::arg("slow"))
       .def("logits_slot", [](const DecodeExecutor& x, int l) { return reinterpret_cast<std::uintptr_t>(x.logits_slot(l)); })

@@ -108,7 +108,10 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
   if (!io.q || !io.k_new || !io.v_new || !io.out) fail(ErrorCode::kOutOfRange, "DecodeExecutor: null step buffer");
   if (hooks && ((!hooks->wait_before.empty() && (int)hooks->wait_before.size() != L) ||
                 (!hooks->record_after.empty() && (int)hooks->record_after.size() != L) ||
-                (!hooks->record_before_attention.empty() && (int)hooks->record_before_attention.size() != L)))
+                (!hooks->record_before_attention.empty() && (int)hooks->record_before_attention.size() != L) ||
+                (!hooks->aux_begin.empty() && (int)hooks->aux_begin.size() != L) ||
+                (!hooks->aux_selected.empty() && (int)hooks->aux_selected.size() != L) ||
+                (!hooks->aux_end.empty() && (int)hooks->aux_end.size() != L)))
     fail(ErrorCode::kSupportMismatch, "DecodeExecutor: one hook event per layer");
   // fork: the main (high-priority) stream continues the origin stream
   ok(cudaEventRecord(E(ev_fork_), S(origin)), "fork");
@@ -146,8 +149,15 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
                                 hi_));
       ok(cudaEventRecord(E(ev_ready_[sl]), S(hi_)), "slot ready");
       ok(cudaStreamWaitEvent(S(lo_), E(ev_ready_[sl]), 0), "slot ready");
+      auto mark_aux = [&](std::vector<void*> StepHooks::*evs) {
+        if (hooks && !(hooks->*evs).empty() && (hooks->*evs)[l])
+          ok(cudaEventRecord(E((hooks->*evs)[l]), S(lo_)), "hook");
+      };
+      mark_aux(&StepHooks::aux_begin);
       check(sfi_selector(&s_, &c_, l, lg, &prm_, lo_));
+      mark_aux(&StepHooks::aux_selected);
       check(sfi_compact_build(&s_, &c_, l, rebuild_ring ? 1 : 0, lo_));
+      mark_aux(&StepHooks::aux_end);
       ok(cudaEventRecord(E(ev_free_[sl]), S(lo_)), "slot free");
       used[sl] = true;
     }

@@ -338,16 +338,19 @@ class StepExecutor:
                 self._stride(k_new), self._stride(out))
 
     def step(self, slow: bool, q, k_new, v_new, out, rebuild_ring: bool = False, wait_before=(), record_after=(),
-             origin=None, record_before_attention=()):
+             origin=None, record_before_attention=(), aux_events=((), (), ())):
         """Enqueue one step after the work on `origin` (a torch stream; default: the
         executor's stream). wait_before / record_after / record_before_attention:
         per-layer torch.cuda.Events (the last two bracket each layer's attention
-        launch on the main stream)."""
+        launch on the main stream); aux_events: three per-layer lists recorded on the
+        aux stream of a slow step (before the Selector, after it, after the compact
+        rebuild)."""
         if k_new.stride(0) * k_new.element_size() != self._stride(v_new):
             raise ValueError("k_new / v_new layer strides differ")
         ev = lambda es: [e.cuda_event if e is not None else 0 for e in es]  # noqa: E731
         self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring, ev(wait_before), ev(record_after), False,
-                    0 if origin is None else origin.cuda_stream, ev(record_before_attention))
+                    0 if origin is None else origin.cuda_stream, ev(record_before_attention),
+                    [x for es in aux_events for x in ev(es)])
 
     def capture(self, slow: bool, q, k_new, v_new, out, rebuild_ring: bool = False):
         self.x.step(slow, *self._args(q, k_new, v_new, out), rebuild_ring, [], [], True, 0)
