@@ -373,7 +373,7 @@ static size_t part_rows(const sfi_shape& s) { return group_of(s) > 8 ? 16 : 8; }
 // indices, [rows][8] row state, [rows][64][2] segment counts / offsets
 size_t bt_bytes(const sfi_shape& s) {
   const size_t rows = (size_t)s.batch * s.n_kv_heads;
-  return rows * (65536 * 4 + (size_t)s.max_positions * 4 + 8 * 4 + 64 * 2 * 4);
+  return rows * (65536 * 4 + (size_t)s.max_positions * 4 + 16 * 4 + 64 * 2 * 4);
 }
 
 size_t workspace_bytes(const sfi_shape& s) {

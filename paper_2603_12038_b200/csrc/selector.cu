@@ -1497,21 +1497,25 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
 // per-row histogram of kBtBins value bins over [zlo, zhi], the bounds z_adj
 // can take (z_base in [log eps, log(1 + eps)], lowered by at most
 // (alpha_soft + alpha_cross) |log eps|); the bin map is monotonic, so
-//   sel_bt_thresh  (row)           the bin b* holding the K-th largest key; keys in
-//                                  higher bins are selected (histogram zeroed after)
-//   sel_bt_scan    (segment, row)  per segment: count of keys above b*; keys in b* listed
-//   sel_bt_pick    (row)           the exact threshold (key, index) among the listed keys
+//   sel_bt_thresh  (8-CTA cluster  the bin b* holding the K-th largest key; keys in
+//                   per row)       higher bins are selected
+//   sel_bt_scan    (segment, row)  per segment: count of keys above b*; keys in b* listed;
+//                                  the segment's share of the histogram cleared; the last
+//                                  segment CTA of a row to arrive then picks the
+//                                  exact threshold (key, index) among the listed keys
 //                                  (bitonic sort in shared memory, radix select beyond)
 //                                  and each segment's output offset
 //   sel_bt_emit    (segment, row)  the selected positions, ascending
 // Same output contract as sel_topk_kernel (score desc, position asc; ties by position).
 constexpr int kBtSmemCand = 2048;
+constexpr int kBtMeta = 16;  // row state words
 constexpr int kBtMaxSeg = 64;
 
 struct BtBuf {
   uint32_t* hist;  // [rows][kBtBins]
   int32_t* cand;   // [rows][Lmax] listed indices
-  int32_t* meta;   // [rows][8]: b*, above, need, listed, Tk hi, Tk lo, Ti, mode (1: n <= K / empty)
+  int32_t* meta;   // [rows][kBtMeta]: b*, above, need, listed, Tk hi, Tk lo, Ti, mode (1: n <= K / empty),
+                   //   scan arrivals
   int32_t* seg;    // [rows][kBtMaxSeg][2]: count above b*, output offset
   int P;           // segments per row
 };
@@ -1573,7 +1577,7 @@ __global__ void __cluster_dims__(kBtThCS, 1, 1) __launch_bounds__(kBtThT)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Src<false> src(p, row / p.H);
   const int n = src.n, K = p.K;
-  int32_t* m = bt.meta + (size_t)row * 8;
+  int32_t* m = bt.meta + (size_t)row * kBtMeta;
   const uint32_t* h = bt.hist + (size_t)row * kBtRow;
   const bool active = n > K && K > 0;
   constexpr int kPerWarp = kBtThChunks / (kBtThT / 32);
@@ -1646,6 +1650,9 @@ __global__ void __cluster_dims__(kBtThCS, 1, 1) __launch_bounds__(kBtThT)
 
 constexpr int kBtScanT = 256;
 
+template <int kT>
+__device__ __forceinline__ void bt_pick_row(const SelParams& p, const BtBuf& bt, int row);
+
 __global__ void __launch_bounds__(kBtScanT) sel_bt_scan_kernel(const SelParams p, const BtBuf bt) {
   griddep_wait();
   griddep_launch();
@@ -1656,7 +1663,7 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_scan_kernel(const SelParams p
     const int w0 = bt_seg_start(seg, kBtRow / 4, bt.P), w1 = bt_seg_start(seg + 1, kBtRow / 4, bt.P);
     for (int i = w0 + threadIdx.x; i < w1; i += kBtScanT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
-  int32_t* m = bt.meta + (size_t)row * 8;
+  int32_t* m = bt.meta + (size_t)row * kBtMeta;
   if (m[7]) return;
   const Src<false> src(p, row / p.H);
   const int n = src.n;
@@ -1680,7 +1687,17 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_scan_kernel(const SelParams p
   }
   uint32_t total;
   block_excl_scan<kBtScanT>(cnt, wsum, total);
-  if (threadIdx.x == 0) bt.seg[((size_t)row * kBtMaxSeg + seg) * 2] = (int32_t)total;
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    bt.seg[((size_t)row * kBtMaxSeg + seg) * 2] = (int32_t)total;
+    __threadfence();  // this CTA's count and listed keys before its arrival
+    s_last = atomicAdd(&m[8], 1) == bt.P - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();  // every segment's count and listed keys are visible
+  bt_pick_row<kBtScanT>(p, bt, row);
+  if (threadIdx.x == 0) m[8] = 0;  // arrivals reset for the next call
 }
 
 // (key desc, index asc) ordering of listed elements
@@ -1688,21 +1705,20 @@ __device__ __forceinline__ bool bt_before(unsigned long long ka, int ia, unsigne
   return ka > kb || (ka == kb && ia < ib);
 }
 
-__global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, const BtBuf bt) {
-  griddep_wait();
-  griddep_launch();
+// The exact threshold (key, index) among a row's listed keys and every segment's
+// output offset; run by the last scan CTA of the row to arrive (kT threads).
+template <int kT>
+__device__ __forceinline__ void bt_pick_row(const SelParams& p, const BtBuf& bt, int row) {
   __shared__ unsigned long long sk[kBtSmemCand];
   __shared__ int si[kBtSmemCand];
   __shared__ uint32_t hist[256];
   __shared__ int segcnt[kBtMaxSeg];
   __shared__ unsigned long long s_tk;
   __shared__ int s_ti, s_gt;
-  const int row = blockIdx.x;
-  int32_t* m = bt.meta + (size_t)row * 8;
-  if (m[7]) return;
+  int32_t* m = bt.meta + (size_t)row * kBtMeta;
   const Src<false> src(p, row / p.H);
   const int n = src.n;
-  const int listed = m[3], need = m[2];
+  const int listed = __ldcg(&m[3]), need = m[2];
   const double* z = p.sb + (size_t)row * p.ld;
   const int32_t* cand = bt.cand + (size_t)row * p.Lmax;
   if (threadIdx.x < kBtMaxSeg) segcnt[threadIdx.x] = 0;
@@ -1710,10 +1726,10 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
     // bitonic sort of the listed (key, index) pairs, padded to a power of two
     int np2 = 1;
     while (np2 < listed) np2 <<= 1;
-    for (int i = threadIdx.x; i < np2; i += kBtT) {
+    for (int i = threadIdx.x; i < np2; i += kT) {
       if (i < listed) {
-        sk[i] = okey(z[cand[i]]);
-        si[i] = cand[i];
+        sk[i] = okey(__ldcg(&z[__ldcg(&cand[i])]));
+        si[i] = __ldcg(&cand[i]);
       } else {
         sk[i] = 0ull;
         si[i] = 0x7fffffff;
@@ -1722,7 +1738,7 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
     __syncthreads();
     for (int k = 2; k <= np2; k <<= 1)
       for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < np2; i += kBtT) {
+        for (int i = threadIdx.x; i < np2; i += kT) {
           const int ij = i ^ j;
           if (ij > i) {
             const bool up = (i & k) == 0;  // this run sorted "before" first
@@ -1749,10 +1765,10 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
     unsigned long long prefix = 0ull, pmask = 0ull;
     int rem = need;
     for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int i = threadIdx.x; i < 256; i += kBtT) hist[i] = 0u;
+      for (int i = threadIdx.x; i < 256; i += kT) hist[i] = 0u;
       __syncthreads();
-      for (int i = threadIdx.x; i < listed; i += kBtT) {
-        const unsigned long long k = okey(z[cand[i]]);
+      for (int i = threadIdx.x; i < listed; i += kT) {
+        const unsigned long long k = okey(__ldcg(&z[__ldcg(&cand[i])]));
         if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1u);
       }
       __syncthreads();
@@ -1774,11 +1790,11 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
     // index among the rem-th smallest with key == prefix
     uint32_t iprefix = 0u, imask = 0u;
     for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = threadIdx.x; i < 256; i += kBtT) hist[i] = 0u;
+      for (int i = threadIdx.x; i < 256; i += kT) hist[i] = 0u;
       __syncthreads();
-      for (int i = threadIdx.x; i < listed; i += kBtT) {
-        const int ix = cand[i];
-        if (okey(z[ix]) == prefix && ((uint32_t)ix & imask) == iprefix) atomicAdd(&hist[((uint32_t)ix >> shift) & 255], 1u);
+      for (int i = threadIdx.x; i < listed; i += kT) {
+        const int ix = __ldcg(&cand[i]);
+        if (okey(__ldcg(&z[ix])) == prefix && ((uint32_t)ix & imask) == iprefix) atomicAdd(&hist[((uint32_t)ix >> shift) & 255], 1u);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -1805,9 +1821,9 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
   const unsigned long long Tk = s_tk;
   const int Ti = s_ti;
   // selected listed elements per segment
-  for (int i = threadIdx.x; i < listed; i += kBtT) {
-    const int ix = cand[i];
-    const unsigned long long k = okey(z[ix]);
+  for (int i = threadIdx.x; i < listed; i += kT) {
+    const int ix = __ldcg(&cand[i]);
+    const unsigned long long k = okey(__ldcg(&z[ix]));
     if (!bt_before(Tk, Ti, k, ix)) {  // (k, ix) at or before the threshold element
       int sgi = (int)(((long long)ix * bt.P) / n);
       while (sgi + 1 < bt.P && bt_seg_start(sgi + 1, n, bt.P) <= ix) ++sgi;
@@ -1820,8 +1836,8 @@ __global__ void __launch_bounds__(kBtT) sel_bt_pick_kernel(const SelParams p, co
   if (threadIdx.x < 32) {  // segment output offsets: exclusive prefix of (above b*) + (selected listed)
     int32_t* e = bt.seg + (size_t)row * kBtMaxSeg * 2;
     const int s0 = 2 * threadIdx.x, s1 = s0 + 1;
-    const int c0 = s0 < bt.P ? e[2 * s0] + segcnt[s0] : 0;
-    const int c1 = s1 < bt.P ? e[2 * s1] + segcnt[s1] : 0;
+    const int c0 = s0 < bt.P ? __ldcg(&e[2 * s0]) + segcnt[s0] : 0;
+    const int c1 = s1 < bt.P ? __ldcg(&e[2 * s1]) + segcnt[s1] : 0;
     int inc = c0 + c1;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1848,7 +1864,7 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_emit_kernel(const SelParams p
   __shared__ int wcnt[kBtEmitTiles * kW + 1];
   const int seg = blockIdx.x, row = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* m = bt.meta + (size_t)row * 8;
+  const int32_t* m = bt.meta + (size_t)row * kBtMeta;
   const Src<false> src(p, row / p.H);
   const int n = src.n, K = p.K;
   int32_t* out = p.sel + (size_t)row * K;
@@ -1920,7 +1936,6 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_emit_kernel(const SelParams p
 cudaError_t launch_bt_topk(const SelParams& p, const BtBuf& bt, int rows, cudaStream_t st) {
   cudaError_t e = launch_k(sel_bt_thresh_kernel, dim3(kBtThCS, rows), dim3(kBtThT), 0, st, p, bt);
   if (e == cudaSuccess) e = launch_k(sel_bt_scan_kernel, dim3(bt.P, rows), dim3(kBtScanT), 0, st, p, bt);
-  if (e == cudaSuccess) e = launch_k(sel_bt_pick_kernel, dim3(rows), dim3(kBtT), 0, st, p, bt);
   if (e == cudaSuccess) e = launch_k(sel_bt_emit_kernel, dim3(bt.P, rows), dim3(kBtScanT), 0, st, p, bt);
   return e;
 }
@@ -2099,7 +2114,7 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
       bt.cand = reinterpret_cast<int32_t*>(w);
       w += slices * (size_t)s.max_positions * 4;
       bt.meta = reinterpret_cast<int32_t*>(w);
-      w += slices * 8 * 4;
+      w += slices * kBtMeta * 4;
       bt.seg = reinterpret_cast<int32_t*>(w);
       bt.P = (int)std::max<size_t>(1, std::min<size_t>(kBtMaxSeg, (296 + slices - 1) / slices));
       p.bt_hist = bt.hist;
