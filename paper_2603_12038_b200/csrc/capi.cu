@@ -177,7 +177,7 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   }();
   // measured optimum of the async slow step per group size (profiles/r02/share_sweep.txt,
   // 3 repeats each): G = 4 (C2) 67.5% of the 2-CTA slots (8.23 vs 8.37 ms at 65%),
-  // G = 8 (C3) 75% (27.9 vs 30.4 ms); G = 16 (C4) takes the tcgen05 kernel on every SM
+  // G = 8 (C3) 75% (27.9 vs 30.4 ms); G = 16 (C4) takes the tcgen05 kernel on 77.5% of the SMs
   const int Gq = s->n_q_heads / s->n_kv_heads;
   const int share = (env_share > 0 && env_share <= 1000) ? env_share : (Gq >= 16 ? 1000 : Gq >= 8 ? 750 : 675);
   int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms(),
@@ -221,9 +221,9 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
     // alone: 3 stages (192 KB) on every SM. Beside the Selector (SFI_DENSE_SHARE_SM):
     // SFI_DENSE_TC_SHARE_PERMILLE of the SMs with SFI_DENSE_TC_SHARE_STAGES stages
     // (default 3; 2 stages, ~150 KB, let Selector CTAs co-reside but measured slower)
-    static const int env_tc_share = [] {
+    static const int env_tc_share = [] {  // C4: 775 permille 13.8 vs 14.9 ms per slow step on every SM
       const char* e = std::getenv("SFI_DENSE_TC_SHARE_PERMILLE");
-      return e ? std::atoi(e) : 1000;
+      return e ? std::atoi(e) : 775;
     }();
     static const int env_tc_share_stages = [] {  // C4: 3 stages 14.5 vs 2 stages 15.4 ms per slow step
       const char* e = std::getenv("SFI_DENSE_TC_SHARE_STAGES");
