@@ -177,9 +177,11 @@ int decode_common(const sfi_shape* s, const sfi_cache* c, int layer, const float
   }();
   // measured optimum of the async slow step per group size (profiles/r02/share_sweep.txt,
   // 3 repeats each): G = 4 (C2) 67.5% of the 2-CTA slots (8.23 vs 8.37 ms at 65%),
-  // G = 8 (C3) 75% (27.9 vs 30.4 ms); G = 16 (C4) takes the tcgen05 kernel on 77.5% of the SMs
+  // G = 8 (C3) 75% (27.9 vs 30.4 ms), G = 2 (C1) 50% (1.02 vs 1.04 ms); G = 16 (C4) takes
+  // the tcgen05 kernel on 77.5% of the SMs
   const int Gq = s->n_q_heads / s->n_kv_heads;
-  const int share = (env_share > 0 && env_share <= 1000) ? env_share : (Gq >= 16 ? 1000 : Gq >= 8 ? 750 : 675);
+  const int share = (env_share > 0 && env_share <= 1000) ? env_share
+                    : (Gq >= 16 ? 1000 : Gq >= 8 ? 750 : Gq >= 4 ? 675 : 500);
   int ctas = sfi_impl::decode_grid(per_slice * s->batch * s->n_kv_heads, num_sms(),
                                    (flags & SFI_DENSE_SHARE_SM) ? share : 875);
   static const int env_ctas = [] {
