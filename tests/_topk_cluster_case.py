@@ -1,7 +1,8 @@
 """Child process of tests/test_baseline_parity.py::test_forced_cluster_topk.
 
 SFI_TOPK_CLUSTER (read once per process by the Selector's top-k launcher) forces
-the cluster top-k: =1 the 8-CTA variant, =4 the 4-CTA one, for every row length.
+the cluster top-k: =1 the 8-CTA variant, =4 the 4-CTA one, for every row length;
+SFI_TOPK_BT=1 forces the rows x segments histogram top-k (sel_bt_*) instead.
 Runs the device Selector in cache mode at |J| ~ 5K (keys in shared memory) and
 ~100K (4-CTA: 25K keys per CTA > the 22K shared-memory cap, so global keys) and
 compares the indices with the reference run_selector. Prints "ok".
@@ -25,7 +26,7 @@ def main() -> None:
     from oracle import oracle as O
     from paper_2603_12038_b200 import SelectorParams, SfiCache
 
-    assert os.environ.get("SFI_TOPK_CLUSTER") in ("1", "4")
+    assert os.environ.get("SFI_TOPK_CLUSTER") in ("1", "4") or os.environ.get("SFI_TOPK_BT") == "1"
     for B, H, Hq, lens, K in [(2, 4, 16, [5300, 4100], 700), (1, 8, 32, [100_400], 2048)]:
         c = SfiCache(1, B, H, Hq, 128, max(lens) + 8, 4, K, 256)
         c.fill_synthetic(seed=max(lens), length=max(lens))

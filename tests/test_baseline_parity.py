@@ -247,12 +247,14 @@ def test_selector_exact_ties_across_chunks(refine):
 
 # ---- the cluster top-k variants forced at small sizes (SFI_TOPK_CLUSTER) ----
 
-@pytest.mark.parametrize("force", ["1", "4"])
+@pytest.mark.parametrize("force", ["cluster=1", "cluster=4", "bt=1"])
 def test_forced_cluster_topk(force):
-    """The cluster top-k is chosen per process from SFI_TOPK_CLUSTER: run the
-    Selector parity check in a child with it forced (8-CTA or 4-CTA clusters,
-    shared-memory keys at |J| = 5K, global keys at |J| = 100K with 4 CTAs)."""
-    env = dict(os.environ, SFI_TOPK_CLUSTER=force)
+    """The top-k variant is chosen per process from the environment: run the
+    Selector parity check in a child with it forced — SFI_TOPK_CLUSTER (8-CTA or
+    4-CTA clusters, shared-memory keys at |J| = 5K, global keys at |J| = 100K with
+    4 CTAs) or SFI_TOPK_BT (the long-row histogram top-k at both lengths)."""
+    kind, val = force.split("=")
+    env = dict(os.environ, **{"SFI_TOPK_CLUSTER" if kind == "cluster" else "SFI_TOPK_BT": val})
     r = subprocess.run([sys.executable, os.path.join(HERE, "_topk_cluster_case.py")], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
