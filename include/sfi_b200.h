@@ -144,8 +144,10 @@ SFI_API int sfi_set_lengths(const sfi_shape* shape, const sfi_cache* cache,
 
 /* prefix_len[b] += 1 for every request: opens the next decode step
  * (KvStore::begin_token attention.cpp:128-134; fast/slow_step_update
- * scheduler.cpp:101-131) and slides recent_len[b] by the SFI rule. Sets
- * SFI_ERR_CONTEXT_OVERFLOW past max_positions. */
+ * scheduler.cpp:101-131) and slides recent_len[b] by the SFI rule. Past
+ * max_positions it sets SFI_ERR_CONTEXT_OVERFLOW and leaves prefix_len; until the
+ * flags are read, sfi_ring_append and the fused sfi_fast_decode skip the append
+ * (no valid row is overwritten). */
 SFI_API int sfi_step_advance(const sfi_shape* shape, const sfi_cache* cache, void* stream);
 
 /* Appends the current token (row prefix_len[b]-1) of `layer`:
