@@ -1688,11 +1688,10 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_scan_kernel(const SelParams p
   uint32_t total;
   block_excl_scan<kBtScanT>(cnt, wsum, total);
   __shared__ int s_last;
-  if (threadIdx.x == 0) {
-    bt.seg[((size_t)row * kBtMaxSeg + seg) * 2] = (int32_t)total;
-    __threadfence();  // this CTA's count and listed keys before its arrival
-    s_last = atomicAdd(&m[8], 1) == bt.P - 1;
-  }
+  if (threadIdx.x == 0) bt.seg[((size_t)row * kBtMaxSeg + seg) * 2] = (int32_t)total;
+  __threadfence();  // every thread: its listed keys (thread 0: the count) before the arrival
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&m[8], 1) == bt.P - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();  // every segment's count and listed keys are visible
