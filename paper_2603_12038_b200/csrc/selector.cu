@@ -693,6 +693,14 @@ __global__ void __launch_bounds__(kPwT, 4) sel_pw_kernel(const SelParams p, doub
                                                       int ld_chunks) {
   griddep_wait();  // PDL: logits come from the preceding dense decode
   griddep_launch();
+  if (p.bt_hist) {  // long-row top-k: clear this CTA's share of the histograms sel_z fills next
+    const size_t words = (size_t)p.B * p.H * kBtRow / 4;
+    const size_t nb = (size_t)gridDim.x * gridDim.y * gridDim.z;
+    const size_t cta = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const size_t w0 = words * cta / nb, w1 = words * (cta + 1) / nb;
+    uint4* h4 = reinterpret_cast<uint4*>(p.bt_hist);
+    for (size_t i = w0 + threadIdx.x; i < w1; i += blockDim.x) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   constexpr int kH = kHT < kHC ? kHT : kHC;  // heads of this CTA
   constexpr int kW = kPwT / 32;
   __shared__ double red[kW][kH][5];
@@ -1500,8 +1508,7 @@ cudaError_t launch_topk(const SelParams& p, int rows, int n_max, cudaStream_t st
 //   sel_bt_thresh  (8-CTA cluster  the bin b* holding the K-th largest key; keys in
 //                   per row)       higher bins are selected
 //   sel_bt_scan    (segment, row)  per segment: count of keys above b*; keys in b* listed;
-//                                  the segment's share of the histogram cleared; the last
-//                                  segment CTA of a row to arrive then picks the
+//                                  the last segment CTA of a row to arrive then picks the
 //                                  exact threshold (key, index) among the listed keys
 //                                  (bitonic sort in shared memory, radix select beyond)
 //                                  and each segment's output offset
@@ -1644,8 +1651,9 @@ __global__ void __cluster_dims__(kBtThCS, 1, 1) __launch_bounds__(kBtThT)
   if (threadIdx.x == 0) {
     m[3] = 0;
     m[7] = active ? 0 : 1;
+    m[8] = 0;  // scan arrivals (also reset by the picking CTA; here in case a call was cut short)
   }
-  // the histogram is zeroed by sel_bt_scan (every segment CTA clears its share)
+  // the histograms are cleared by sel_pw at the start of every Selector call
 }
 
 constexpr int kBtScanT = 256;
@@ -1658,11 +1666,6 @@ __global__ void __launch_bounds__(kBtScanT) sel_bt_scan_kernel(const SelParams p
   griddep_launch();
   __shared__ uint32_t wsum[33];
   const int seg = blockIdx.x, row = blockIdx.y;
-  {  // clear this segment's share of the row's histogram for the next Selector call
-    uint4* h4 = reinterpret_cast<uint4*>(bt.hist + (size_t)row * kBtRow);
-    const int w0 = bt_seg_start(seg, kBtRow / 4, bt.P), w1 = bt_seg_start(seg + 1, kBtRow / 4, bt.P);
-    for (int i = w0 + threadIdx.x; i < w1; i += kBtScanT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
-  }
   int32_t* m = bt.meta + (size_t)row * kBtMeta;
   if (m[7]) return;
   const Src<false> src(p, row / p.H);
