@@ -581,12 +581,8 @@ __device__ __forceinline__ void cross_head_store(const SelParams& p, int b, int 
       const double z = zn[h] + p.alpha_cross * lr;
       const size_t row = (size_t)(b * p.H + h - p.h_off);
       p.sb[row * p.ld + idx] = z;
-      if (p.bt_hist) {  // warp-aggregated: lanes with the same bin add once
-        const int bn = bt_bin(z, p.bt_zlo, p.bt_scale);
-        const unsigned act = __activemask();
-        const unsigned same = __match_any_sync(act, bn);
-        if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&p.bt_hist[row * kBtRow + bn], (uint32_t)__popc(same));
-      }
+      if (p.bt_hist)  // one fire-and-forget RED per key (a warp-aggregated match_any version: C3 Selector 186 vs 174 us)
+        atomicAdd(&p.bt_hist[row * kBtRow + bt_bin(z, p.bt_zlo, p.bt_scale)], 1u);
     }
 }
 
