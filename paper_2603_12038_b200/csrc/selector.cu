@@ -856,6 +856,76 @@ __global__ void sel_coef_kernel(const SelParams p, const double* __restrict__ st
   }
 }
 
+// The same per row for long rows (C3, C4: 256-512 chunks): one 256-thread CTA per row,
+// threads own chunks c = t + 256 k; warp trees then the 8 warps in order (fixed order).
+__global__ void __launch_bounds__(256) sel_coef_wide_kernel(const SelParams p, const double* __restrict__ stats,
+                                                            double* __restrict__ coef, int ld_chunks) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ double red[8][5];
+  __shared__ double sM;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x;
+  const Src<false> src(p, row / p.H);
+  const int n = src.n;
+  if (n <= 0) return;
+  const double* st = stats + (size_t)row * ld_chunks * 6;
+  double* cf = coef + (size_t)row * (ld_chunks + 2);
+  const int nc = n_chunks(n);
+  double M = kMaskedLogit;
+  for (int c = threadIdx.x; c < nc; c += 256) M = smax(M, st[c * 6]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = smax(M, __shfl_xor_sync(0xffffffffu, M, o));
+  if (lane == 0) red[warp][0] = M;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0][0];
+    for (int w = 1; w < 8; ++w) m = smax(m, red[w][0]);
+    sM = m;
+  }
+  __syncthreads();
+  M = sM;
+  double x5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int c = threadIdx.x; c < nc; c += 256) {
+    const double* x = st + c * 6;
+    const double e = exp(x[0] - M);
+    x5[0] += x[1] * e;
+    x5[1] += x[2];
+    x5[2] += x[3] * (e * e);
+    x5[3] += x[4] * e;
+    x5[4] += x[5];
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x5[k] += __shfl_xor_sync(0xffffffffu, x5[k], o);
+  }
+  __syncthreads();  // red reused
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) red[warp][k] = x5[k];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double s[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    s[k] = red[0][k];
+    for (int w = 1; w < 8; ++w) s[k] += red[w][k];
+  }
+  if (s[0] <= 0.0 || s[1] <= 0.0) raise_error(p.err, SFI_ERR_EMPTY_SUPPORT);
+  const double c1 = 1.0 / s[0], c2 = 1.0 / s[1];
+  const double ff = s[2] * c1 * c1, fr = s[3] * c1 * c2, rr = s[4] * c2 * c2;
+  const double denom = ff - 2.0 * fr + rr;
+  double lambda = 0.0;
+  if (fabs(denom) >= p.eps) {
+    lambda = (ff - fr) / denom;
+    lambda = (lambda < 0.0) ? 0.0 : (p.lambda_clip < lambda) ? p.lambda_clip : lambda;
+  }
+  cf[0] = (1.0 - lambda) * c1;
+  cf[1] = lambda * c2;
+  cf[2] = M;
+}
+
 template <int kH>
 __global__ void __launch_bounds__(kRefineT, kH <= 8 ? 4 : 2) sel_z_kernel(const SelParams p, const double* stats, const double* Wt,
                                                          const double* coef, int ld_chunks) {
@@ -2130,8 +2200,10 @@ cudaError_t launch_selector(const sfi_shape& s, const sfi_cache& c, int layer, c
                           : launch_k(sel_pw_kernel<KH>, dim3(ldc, s.batch, (KH + kPwHeads - 1) / kPwHeads), ba, 0, \
                                      st, p, P, Wt, stt, ldc));                                       \
   if (e == cudaSuccess)                                                                              \
-    e = launch_k(sel_coef_kernel, dim3(((unsigned)slices + 7) / 8), dim3(256), 0, st, p,             \
-                 (const double*)stt, cf, ldc);                                                       \
+    e = ldc > 128 ? launch_k(sel_coef_wide_kernel, dim3((unsigned)slices), dim3(256), 0, st, p,        \
+                             (const double*)stt, cf, ldc)                                            \
+                  : launch_k(sel_coef_kernel, dim3(((unsigned)slices + 7) / 8), dim3(256), 0, st, p,  \
+                             (const double*)stt, cf, ldc);                                           \
   if (e == cudaSuccess) e = launch_k(sel_z_kernel<KH>, gz, bz, 0, st, p, (const double*)stt,           \
                                      (const double*)Wt, (const double*)cf, ldc);
     switch (s.n_kv_heads) {
