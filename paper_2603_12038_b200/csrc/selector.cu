@@ -1625,7 +1625,6 @@ __device__ __forceinline__ T block_excl_scan(T v, T* wsum, T& total) {
   return r;
 }
 
-constexpr int kBtT = 1024;
 constexpr int kBtThCS = 8;                      // thresh: CTAs per row (one cluster)
 constexpr int kBtThT = 256;
 constexpr int kBtChunks = kBtBins / 64;         // 64-bin chunks per row
