@@ -227,8 +227,8 @@ class Workload:
         self.logits = self.cache.pooled_logits
         drv = self.drv
         # 1 GPU / dp: whole steps through the C++ decode executor (include/sfi/decode.hpp):
-        # the asynchronous slow step (Selector + compact of layer i on a low-priority aux
-        # stream behind the dense decode of layers i+1..) and graph-captured steps
+        # the asynchronous slow step (Selector + compact of layer i on an aux stream behind
+        # the dense decode of layers i+1..) and graph-captured steps
         self.pipe = None
         self.exec = None
         if self.mode in ("single", "dp") and not sync_slow:

@@ -7,17 +7,17 @@
 //     sink and recent lengths per request, rewritten on the device once per
 //     step and read by every kernel of the step) + one fused K4 launch per
 //     layer (append + sparse attention), PDL-chained.
-//   slow step: the layer-wise asynchronous pipeline. A high-priority main
-//     stream runs append + dense decode (K1, share grid) of layer 0..L-1; as
-//     soon as layer i's pooled logits exist, a lowest-priority aux stream runs
-//     the Selector (K2) and compact rebuild (K3) of layer i from ring slot
-//     i % R; layer i + R's dense decode waits for slot i's release event; a
-//     single completion barrier joins the streams at the end of the step.
+//   slow step: the layer-wise asynchronous pipeline. A main stream runs
+//     append + dense decode (K1, share grid) of layer 0..L-1; as soon as layer
+//     i's pooled logits exist, an aux stream runs the Selector (K2) and compact
+//     rebuild (K3) of layer i from ring slot i % R; layer i + R's dense decode
+//     waits for slot i's release event; a single completion barrier joins the
+//     streams at the end of the step. Stream priorities (main high, aux lowest,
+//     kept as graph node priorities) are opt-in: measured slower.
 //
 // Per-layer hooks (optional CUDA events) let a caller overlap host<->device
 // copies of the step's inputs / outputs with its layers. A step can be
-// captured once into a CUDA graph (instantiated with node priorities) and
-// replayed; the descriptor lives in device memory, so a replay needs no host
+// captured once into a CUDA graph and replayed; the descriptor lives in device memory, so a replay needs no host
 // work at all.
 #pragma once
 

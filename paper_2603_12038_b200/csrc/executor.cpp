@@ -113,7 +113,7 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
                 (!hooks->aux_selected.empty() && (int)hooks->aux_selected.size() != L) ||
                 (!hooks->aux_end.empty() && (int)hooks->aux_end.size() != L)))
     fail(ErrorCode::kSupportMismatch, "DecodeExecutor: one hook event per layer");
-  // fork: the main (high-priority) stream continues the origin stream
+  // fork: the main stream continues the origin stream
   ok(cudaEventRecord(E(ev_fork_), S(origin)), "fork");
   ok(cudaStreamWaitEvent(S(hi_), E(ev_fork_), 0), "fork");
   check(sfi_step_advance(&s_, &c_, hi_));  // the step's packed length descriptor, once
