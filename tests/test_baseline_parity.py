@@ -295,3 +295,41 @@ def test_long_row_topk_exact_ties(refine):
     for h in range(H):
         got = c.sel[0, 0, h, :int(c.n_sel[0, 0, h])].cpu().numpy()
         assert np.array_equal(got, want[h]), h
+
+
+def test_long_row_topk_ragged_batch():
+    """The long-row top-k over a ragged batch (rows of different |J| in one launch,
+    one row with |J| <= K that takes all of J, one empty J) on peaked inputs: every
+    row's indices equal the reference's run_selector on the device's logits."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2603_12038_b200 import SelectorParams, SfiCache
+
+    H, Hq, ns, K, R = 2, 8, 4, 2048, 64
+    lens = [70000, 49500, 1900, 40]
+    B = len(lens)
+    c = SfiCache(1, B, H, Hq, 128, max(lens) + 8, ns, K, R)
+    c.fill_synthetic(seed=12, length=max(lens))
+    c.set_lengths(lens, [ns] * B)
+    q = torch.randn(B, Hq, 128, generator=torch.Generator().manual_seed(12)).cuda()
+    c.plant_peaked(0, q, n_planted=32, scale=3.0, seed=12)
+    out = torch.zeros_like(q)
+    logits = torch.zeros_like(c.pooled_logits)
+    c.dense_decode(0, q, out, logits, 0)
+    c.selector(0, logits, SelectorParams())
+    torch.cuda.synchronize()
+    c.check_errors()
+    ref = oracle()
+    for b in range(B):
+        L, rl = int(c.prefix_len[b]), int(c.recent_len[b])
+        j0, j1 = ns + 1, L - rl
+        if j1 < j0:  # empty J: no selection
+            assert all(int(c.n_sel[0, b, h]) == 0 for h in range(H)), b
+            continue
+        vals = logits[b, :, :j1 - j0 + 1].double().cpu().numpy()
+        norms = c.key_norms[0, b, :, j0 - 1:j1].cpu().numpy()
+        want, _ = ref.run_selector(vals, np.arange(j0, j1 + 1), norms, O.make_cfg(k_budget=K))
+        for h in range(H):
+            got = c.sel[0, b, h, :int(c.n_sel[0, b, h])].cpu().numpy()
+            assert np.array_equal(got, want[h]), (b, h)
