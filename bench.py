@@ -465,6 +465,9 @@ def time_graph(g, reps: int, stream=None) -> float:
 def fast_grid(wl: Workload) -> int:
     """CTAs of one fused fast-step launch (fast_decode.cu fast_cluster_size)."""
     slices, c = wl.B * wl.H, 1
+    tiles = -(-wl.R // 64) + -(-(wl.ns + wl.K) // 64)
+    if 2 <= tiles <= 16 and slices * tiles <= 2 * 148:  # small slices: one tile per CTA
+        return slices * tiles
     while c < 8 and slices * c <= 148:
         c *= 2
     if c == 8 and slices * 32 <= 148:

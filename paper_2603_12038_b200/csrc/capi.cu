@@ -310,7 +310,8 @@ int fast_common(const sfi_shape* s, const sfi_cache* c, int layer, const float* 
     const char* e = std::getenv("SFI_FAST_CLUSTER");
     return e ? std::atoi(e) : 0;
   }();
-  int C = sfi_impl::fast_cluster_size(s->batch * s->n_kv_heads, num_sms());
+  const int fast_tiles = (s->n_recent + 63) / 64 + (s->n_sink + s->k_budget + 63) / 64;
+  int C = sfi_impl::fast_cluster_size(s->batch * s->n_kv_heads, num_sms(), fast_tiles);
   if (env_c >= 1 && env_c <= 16) C = env_c;
   p.trace = nullptr;
   static const bool env_trace = std::getenv("SFI_DECODE_TRACE") != nullptr;

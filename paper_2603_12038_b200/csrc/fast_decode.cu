@@ -746,7 +746,10 @@ FastFn pick(int G) {
 // CTAs per slice: the largest power of two that keeps the grid within the two
 // CTA slots of every SM, up to 8 (portable clusters); up to 16 (non-portable)
 // when the slices are so few that 8 per slice would leave most SMs idle.
-int fast_cluster_size(int slices, int num_sms) {
+int fast_cluster_size(int slices, int num_sms, int tiles) {
+  // small slices (C1: 10 tiles of the compact layout): one tile per CTA when every
+  // slice's tiles fit as CTAs at 2 per SM (C1 fast step 123 -> 111 us per step)
+  if (tiles >= 2 && tiles <= 16 && slices * tiles <= 2 * num_sms) return tiles;
   int c = 1;
   while (c < 8 && slices * c * 2 <= 2 * num_sms) c *= 2;
   if (c == 8 && slices * 32 <= num_sms) c = 16;

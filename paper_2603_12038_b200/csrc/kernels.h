@@ -91,7 +91,7 @@ struct FastParams {
   float* lse;                     // [B][Hq] partial mode (sequence shards): LSE out, empty allowed
   int32_t* steal;                 // [layers][B][H][2] tile-claim / done counters (null: static split)
 };
-int fast_cluster_size(int slices, int num_sms);
+int fast_cluster_size(int slices, int num_sms, int tiles);  // tiles: 64-row tiles of one compact slice
 cudaError_t launch_fast_decode(const FastParams& p, const CUtensorMap& tmk, const CUtensorMap& tmv, int D,
                                int G, int C, cudaStream_t stream);
 
