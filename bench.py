@@ -962,7 +962,7 @@ def gpu_arm(args) -> dict:
     ctx = dict(world=world, rank=rank, local=local, dev=dev, max_over_ranks=max_over_ranks)
     primary = args.config or ("c2" if world == 1 else "c3")
     if args.also is None:
-        also = ["c3", "c4", "c5"] if world == 1 else ["c4", "c2"]
+        also = ["c3", "c4", "c1", "c5"] if world == 1 else ["c4", "c2"]
     else:
         also = [x for x in args.also.split(",") if x and x != "none"]
     also = [a for a in also if a != primary]
@@ -1302,7 +1302,7 @@ def main():
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="headline workload (default: c2 on 1 GPU, c3 KV-head sharded on N > 1)")
     ap.add_argument("--also", default=None,
-                    help="comma-separated extra configs timed after the headline (default: c3,c4,c5 on 1 GPU, "
+                    help="comma-separated extra configs timed after the headline (default: c3,c4,c1,c5 on 1 GPU, "
                          "c4,c2 on N > 1; 'none' for none); reported under 'also'")
     ap.add_argument("--inputs", default="peaked", choices=["peaked", "iid"],
                     help="synthetic inputs: peaked = 32 planted k = 3q + noise positions per (b, KV head) "
