@@ -1510,7 +1510,11 @@ int decode_smem_bytes(int D, int G, int slices) {
 }
 
 int decode_grid(int tiles_upper, int num_sms, int permille) {
-  return std::max(1, std::min(2 * num_sms * permille / 1000, tiles_upper));
+  // at least ~8 tiles per CTA: small problems (C1, 33.8 MB per launch) lose more to
+  // the stream-K merges of many thin CTAs than they gain in parallelism
+  // (C1 K1 alone 24.0 -> 18.8 us, beside the Selector 27.9 -> 23.1 us)
+  const int cap = std::max(num_sms / 2, (tiles_upper + 7) / 8);
+  return std::max(1, std::min({2 * num_sms * permille / 1000, tiles_upper, cap}));
 }
 
 cudaError_t launch_decode_tc(const DecodeParams& p, const CUtensorMap& tmk128, const CUtensorMap& tmv128, int G,
