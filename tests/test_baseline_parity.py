@@ -333,3 +333,40 @@ def test_long_row_topk_ragged_batch():
         for h in range(H):
             got = c.sel[0, b, h, :int(c.n_sel[0, b, h])].cpu().numpy()
             assert np.array_equal(got, want[h]), (b, h)
+
+
+def test_long_row_topk_nondefault_config():
+    """The long-row top-k with a non-default Selector config (stronger soft-NMS and
+    cross-head terms, temperature != 1, radius 3, wider lambda clip, other prior
+    exponent): the histogram's value range follows alpha_soft / alpha_cross, and
+    the indices equal the reference's."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2603_12038_b200 import SelectorConfig, SelectorParams, SfiCache
+
+    B, H, Hq, ctx, ns, K, R = 1, 4, 16, 66000, 4, 1500, 128
+    c = SfiCache(1, B, H, Hq, 128, ctx + 8, ns, K, R)
+    c.fill_synthetic(seed=21, length=ctx)
+    c.set_lengths([ctx], [ns])
+    q = torch.randn(B, Hq, 128, generator=torch.Generator().manual_seed(21)).cuda()
+    c.plant_peaked(0, q, n_planted=32, scale=3.0, seed=21)
+    out = torch.zeros_like(q)
+    logits = torch.zeros_like(c.pooled_logits)
+    c.dense_decode(0, q, out, logits, 0)
+    kw = dict(alpha_soft=0.8, alpha_cross=0.6, temperature=0.7, nms_radius=3, lambda_clip=0.05, beta=2.0)
+    cfg = SelectorConfig()
+    cfg.k_budget = K
+    for k_, v_ in kw.items():
+        setattr(cfg, k_, v_)
+    c.selector(0, logits, SelectorParams(cfg))
+    torch.cuda.synchronize()
+    c.check_errors()
+    L, rl = int(c.prefix_len[0]), int(c.recent_len[0])
+    j0, j1 = ns + 1, L - rl
+    vals = logits[0, :, :j1 - j0 + 1].double().cpu().numpy()
+    norms = c.key_norms[0, 0, :, j0 - 1:j1].cpu().numpy()
+    want, _ = oracle().run_selector(vals, np.arange(j0, j1 + 1), norms, O.make_cfg(k_budget=K, **kw))
+    for h in range(H):
+        got = c.sel[0, 0, h, :int(c.n_sel[0, 0, h])].cpu().numpy()
+        assert np.array_equal(got, want[h]), h
