@@ -32,6 +32,11 @@
 //                     ordered cluster scan emits the selected positions
 //                     ascending with the reference tie rule (equal scores ->
 //                     lower position).
+// The production decode path (cache mode, W = 1, alpha = 1, unsharded) instead
+// runs sel_pw (chunk statistics + prior weights) -> sel_coef (row max M,
+// lambda*, coefficients) -> sel_z (z_base, soft-NMS, cross-head -> z_adj) and
+// then the single-CTA top-k (|J| <= 48K: sel_topk_cta_kernel) or, for long
+// rows, the rows x segments histogram top-k (sel_bt_thresh / scan / emit).
 // Inputs come either from the device cache (production: fp32 pooled logits
 // over the contiguous J_b, cached fp64 key norms) or from explicit arrays
 // (reference-facing run_selector: fp64 W x |J| windows over an arbitrary
