@@ -84,8 +84,14 @@ class DecodeExecutor {
   sfi_shape s_;
   sfi_cache c_;
   void* user_;
-  void* hi_ = nullptr;  // cudaStream_t, greatest priority
-  void* lo_ = nullptr;  // cudaStream_t, least priority
+  void* hi_ = nullptr;  // cudaStream_t: the main chain (append + dense decode)
+  void* lo_ = nullptr;  // cudaStream_t: the aux chain (Selector + compact)
+  // SFI_EXEC_AUX_STREAMS=2: odd layers' Selector + compact on a second aux stream with
+  // their own Selector scratch (a copy of the cache descriptor over a second workspace)
+  void* lo2_ = nullptr;
+  sfi_cache c2_{};
+  void* ws2_ = nullptr;
+  void* ev_aux2_done_ = nullptr;
   void* cap_ = nullptr; // cudaStream_t the graphs are captured from (never the legacy default stream)
   sfi_selector_params prm_;
   int slots_;

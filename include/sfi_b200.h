@@ -101,7 +101,7 @@ typedef struct {
   int32_t* recent_len; /* [batch] recent window length; sfi_step_advance keeps it at
                           clamp(L_b - n_sink_b, 0, n_recent) (scheduler.cpp:45-51) */
   uint32_t* error_flags;
-  void* workspace; /* >= sfi_workspace_bytes(shape); must be zeroed once at allocation */
+  void* workspace; /* >= sfi_sizes.workspace (sfi_buffer_sizes); must be zeroed once at allocation */
   size_t workspace_bytes;
 } sfi_cache;
 

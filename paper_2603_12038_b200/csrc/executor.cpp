@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "sfi/attention.hpp"
@@ -63,6 +64,21 @@ DecodeExecutor::DecodeExecutor(const sfi_shape& shape, const sfi_cache& cache, v
   ev_fork_ = new_event();
   ev_join_ = new_event();
   ev_aux_done_ = new_event();
+  const char* env_aux = std::getenv("SFI_EXEC_AUX_STREAMS");
+  if (env_aux && std::atoi(env_aux) >= 2) {
+    cudaStream_t lo2;
+    ok(cudaStreamCreateWithPriority(&lo2, cudaStreamNonBlocking, p_aux), "aux stream 2");
+    lo2_ = lo2;
+    sfi_sizes sz{};
+    check(sfi_buffer_sizes(&s_, &sz));
+    const size_t wb = sz.workspace;
+    ok(cudaMalloc(&ws2_, wb), "second workspace");
+    ok(cudaMemset(ws2_, 0, wb), "second workspace");
+    c2_ = c_;
+    c2_.workspace = ws2_;
+    c2_.workspace_bytes = wb;
+    ev_aux2_done_ = new_event();
+  }
 }
 
 DecodeExecutor::~DecodeExecutor() {
@@ -72,6 +88,11 @@ DecodeExecutor::~DecodeExecutor() {
   for (void* e : ev_free_) cudaEventDestroy(E(e));
   for (void* e : {ev_fork_, ev_join_, ev_aux_done_}) cudaEventDestroy(E(e));
   if (own_logits_) cudaFree(logits_);
+  if (lo2_) {
+    cudaEventDestroy(E(ev_aux2_done_));
+    cudaStreamDestroy(S(lo2_));
+    cudaFree(ws2_);
+  }
   cudaStreamDestroy(S(hi_));
   cudaStreamDestroy(S(lo_));
   cudaStreamDestroy(S(cap_));
@@ -120,6 +141,7 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
   if (slow) {
     ok(cudaEventRecord(E(ev_fork_), S(hi_)), "fork aux");
     ok(cudaStreamWaitEvent(S(lo_), E(ev_fork_), 0), "fork aux");
+    if (lo2_) ok(cudaStreamWaitEvent(S(lo2_), E(ev_fork_), 0), "fork aux 2");
   }
   std::vector<bool> used(slots_, false);
   const size_t slot_elems = (size_t)s_.batch * s_.n_kv_heads * s_.max_positions;
@@ -148,17 +170,20 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
       check(sfi_dense_decode_ex(&s_, &c_, l, q, out, nullptr, lg, SFI_POOL_MEAN, share_ ? SFI_DENSE_SHARE_SM : 0,
                                 hi_));
       ok(cudaEventRecord(E(ev_ready_[sl]), S(hi_)), "slot ready");
-      ok(cudaStreamWaitEvent(S(lo_), E(ev_ready_[sl]), 0), "slot ready");
+      const bool second = lo2_ && (l & 1);
+      void* aux = second ? lo2_ : lo_;
+      const sfi_cache* cs = second ? &c2_ : &c_;
+      ok(cudaStreamWaitEvent(S(aux), E(ev_ready_[sl]), 0), "slot ready");
       auto mark_aux = [&](std::vector<void*> StepHooks::*evs) {
         if (hooks && !(hooks->*evs).empty() && (hooks->*evs)[l])
-          ok(cudaEventRecord(E((hooks->*evs)[l]), S(lo_)), "hook");
+          ok(cudaEventRecord(E((hooks->*evs)[l]), S(aux)), "hook");
       };
       mark_aux(&StepHooks::aux_begin);
-      check(sfi_selector(&s_, &c_, l, lg, &prm_, lo_));
+      check(sfi_selector(&s_, cs, l, lg, &prm_, aux));
       mark_aux(&StepHooks::aux_selected);
-      check(sfi_compact_build(&s_, &c_, l, rebuild_ring ? 1 : 0, lo_));
+      check(sfi_compact_build(&s_, cs, l, rebuild_ring ? 1 : 0, aux));
       mark_aux(&StepHooks::aux_end);
-      ok(cudaEventRecord(E(ev_free_[sl]), S(lo_)), "slot free");
+      ok(cudaEventRecord(E(ev_free_[sl]), S(aux)), "slot free");
       used[sl] = true;
     }
     if (hooks && !hooks->record_after.empty() && hooks->record_after[l])
@@ -167,6 +192,10 @@ void DecodeExecutor::enqueue(void* origin, bool slow, const StepBuffers& io, boo
   if (slow) {  // the single completion barrier: the next fast step reads the new compact rows
     ok(cudaEventRecord(E(ev_aux_done_), S(lo_)), "join aux");
     ok(cudaStreamWaitEvent(S(hi_), E(ev_aux_done_), 0), "join aux");
+    if (lo2_) {
+      ok(cudaEventRecord(E(ev_aux2_done_), S(lo2_)), "join aux 2");
+      ok(cudaStreamWaitEvent(S(hi_), E(ev_aux2_done_), 0), "join aux 2");
+    }
   }
   ok(cudaEventRecord(E(ev_join_), S(hi_)), "join");
   ok(cudaStreamWaitEvent(S(origin), E(ev_join_), 0), "join");
